@@ -1,0 +1,102 @@
+/* weldgpu.h -- C ABI of libweldgpu.so, the B200 executor under the Weld IR's
+ * data-parallel core (`for(vector, builders, func)` + the five builders).
+ *
+ * The reference (weldmill, pure Python) has no native boundary: its executor
+ * seam is the module function
+ *     weldmill.engine.evaluate(e, env, config, externs) -> (Value, EvalStats)
+ *     /root/reference/pkg/src/weldmill/engine/run.py:1008-1074
+ * imported by name at api.py:23 and called at api.py:374.  The Python package
+ * paper_1709_06416_b200 keeps that exact signature and binds this library
+ * with ctypes.  Each entry point below says which
+ * reference code path it replaces.
+ *
+ * Conventions: every function returns 0 on success, -1 on failure with the
+ * message available from wg_last_error() (thread-local).  Device addresses
+ * are plain uint64_t; no exceptions cross the ABI; no torch types.
+ */
+#ifndef WELDGPU_H
+#define WELDGPU_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- process / device ------------------------------------------------- */
+const char* wg_last_error(void);
+int wg_version(void);
+int wg_device_count(int* n);
+/* Replaces the per-evaluate worker pool set-up (_Pool, run.py:261-284): one
+ * device and one non-blocking stream per process. */
+int wg_init(int device);
+int wg_sm_count(int* n);
+int wg_stream(uint64_t* stream);
+int wg_sync(void);
+
+/* ---- columnar buffer manager (replaces Python lists + _Runtime.alloc,
+ *      run.py:184-228, builders.py:59-106) --------------------------------- */
+int wg_alloc(uint64_t bytes, uint64_t* dptr);
+int wg_free(uint64_t dptr);
+int wg_mem_stats(uint64_t* live, uint64_t* peak);
+int wg_mem_reset_peak(void);
+int wg_memset(uint64_t dptr, int value, uint64_t bytes);
+int wg_h2d(uint64_t dst, const void* src, uint64_t bytes);
+int wg_d2h(void* dst, uint64_t src, uint64_t bytes);
+int wg_d2h_async(void* dst, uint64_t src, uint64_t bytes);
+int wg_d2d(uint64_t dst, uint64_t src, uint64_t bytes);
+int wg_host_alloc(uint64_t bytes, void** p);
+int wg_host_free(void* p);
+int wg_host_register(void* p, uint64_t bytes);
+int wg_host_unregister(void* p);
+
+/* ---- runtime errors (replaces the EvalError raises inside the loop body,
+ *      run.py:411-425, 693-710; builders.py:413-417) ------------------------ */
+int wg_error_ptr(uint64_t* p);
+int wg_read_error(int64_t* code, int64_t* info);
+
+/* ---- loop compilation and launch (replaces _compile_inner/_compile_for,
+ *      run.py:560-983: the closure network becomes one NVRTC-compiled
+ *      sm_100a kernel per fused outer `for`) -------------------------------- */
+int wg_compile(const char* src, const char* name, int nheaders, const char* const* header_srcs,
+               const char* const* header_names, int nopts, const char* const* opts, uint64_t* module_out,
+               char* log_buf, uint64_t log_cap);
+int wg_compile_check(const char* src, const char* name, int nheaders, const char* const* header_srcs,
+                     const char* const* header_names, int nopts, const char* const* opts, uint64_t* cubin_bytes,
+                     char* log_buf, uint64_t log_cap);
+int wg_module_function(uint64_t module, const char* name, uint64_t* fn);
+int wg_occupancy(uint64_t fn, int block, int dyn_smem, int* blocks_per_sm);
+int wg_launch(uint64_t fn, uint32_t grid, uint32_t block, uint32_t dyn_smem, const void* params,
+              uint64_t params_size);
+
+/* ---- builder result() helpers ------------------------------------------
+ * dictmerger table init/compaction: DictMergerState.result, builders.py:380-392
+ * order_key transform + stable sort: order_key builders.py:496-507, ToVec
+ *   run.py:737-747, Sort run.py:723-735
+ * run starts: GroupBuilderState.result, builders.py:478-493 */
+int wg_table_init(uint64_t table, uint64_t nslots, int slot_words, const uint64_t* pattern);
+int wg_table_compact(uint64_t table, uint64_t nslots, int slot_words, int mode, const uint64_t* out_words, int nout,
+                     uint64_t* count_out);
+int wg_order_key(uint64_t src, int kind, uint64_t n, uint64_t perm, uint64_t dst);
+int wg_iota_u32(uint64_t dst, uint64_t n);
+int wg_sort_pairs(uint64_t keys_in, uint64_t vals_in, uint64_t keys_out, uint64_t vals_out, uint64_t n, int begin_bit,
+                  int end_bit);
+int wg_gather(uint64_t src, uint64_t perm, uint64_t dst, uint64_t n, int width);
+int wg_narrow(uint64_t src, uint64_t dst, int width, uint64_t n);
+int wg_widen(uint64_t src, uint64_t dst, int width, uint64_t n);
+int wg_run_starts(const uint64_t* key_words, int kw, uint64_t n, uint64_t starts_out, uint64_t* nruns);
+
+/* ---- synthetic inputs and measurement (bench.py; no reference analogue) -- */
+int wg_gen_column(uint64_t dst, uint64_t n, uint64_t row0, int dist, int width, uint64_t seed, uint64_t col,
+                  int64_t lo, uint64_t span, double flo, double fhi, double div, int ncat, const double* cum,
+                  const int64_t* vals);
+int wg_mul_inplace_f64(uint64_t a, uint64_t b, uint64_t n);
+int wg_flush_l2(uint64_t buf, uint64_t bytes, uint32_t salt);
+int wg_event_create(uint64_t* ev);
+int wg_event_record(uint64_t ev);
+int wg_event_elapsed_ms(uint64_t start, uint64_t stop, float* ms);
+int wg_event_destroy(uint64_t ev);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WELDGPU_H */

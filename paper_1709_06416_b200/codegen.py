@@ -1,0 +1,1338 @@
+"""Lower one fused outer ``for`` loop to an sm_100a CUDA kernel.
+
+Replaces the reference's closure compiler and loop runner
+(/root/reference/pkg/src/weldmill/engine/run.py:560-983): instead of one
+Python closure per IR node executed per row, the loop body becomes straight
+C++ inside a hand-written kernel skeleton, compiled once by NVRTC.
+
+Kernel skeleton (one CTA = 256 threads; a tile = 256 x ITEMS iterations,
+each thread owning ITEMS *consecutive* iterations so every column is read
+with 16-byte vector loads):
+
+  * static schedule  -- grid-stride over tiles with a persistent grid of
+    (#SM x occupancy) CTAs; used when no builder needs ordered output.
+  * scan schedule    -- tiles claimed through an atomic counter; each tile
+    runs the body once to *count* appends per thread (phase A, which also
+    performs every order-insensitive merge), computes the tile's output
+    offset with a block scan + single-pass decoupled look-back, then runs
+    the body again to *store* appends (phase B).  Column values stay in
+    registers between the phases, so HBM traffic is read-once.
+
+Per builder (reference state classes in engine/builders.py):
+  merger      (:286-328) per-thread register fold -> block tree fold ->
+              per-CTA partial -> last CTA folds partials in fixed order
+  vecbuilder  (:231-283) DIRECT(k) when every path merges exactly k values
+              (out[i*k + c], vector stores); otherwise SCAN(M) above
+  groupbuilder(:453-493) appended {key, value} pairs in iteration order;
+              result() stable-sorts by key (builders_dev.py)
+  dictmerger  (:331-392) open-addressing table in HBM, key claim by CAS,
+              per-field atomic fold; shared-memory privatised table for
+              low-cardinality keys (strategy local/shared)
+  vecmerger   (:395-450) bounds-checked atomic fold at index; shared-memory
+              privatised bins when they fit (strategy local/shared)
+"""
+from __future__ import annotations
+
+import math
+import struct as _struct
+from dataclasses import dataclass, field
+
+from . import _ref  # noqa: F401
+from weldmill.expr import (
+    BinaryOp, BitSelect, Broadcast, CastScalar, ExternCall, FieldAccess, For, Ident, If, Lambda, Len, Let,
+    Literal, Lookup, MakeStruct, MakeVector, Merge, NewBuilder, Result, UnaryOp,
+)
+
+from .irtypes import (
+    BOOL, CTYPE, F32, F64, FLOAT_KINDS, I32, I64, INT_KINDS, OPCODE, OPSTRUCT, SIZE, STYPE, Builder, DeviceUnsupported,
+    DictMerger, GroupBuilder, Merger, Scalar, Simd, Struct, Vec, VecBuilder, VecMerger, identity_value,
+    internal_identity, leaves,
+)
+
+W = 4  # SIMD_WIDTH (types.py:15)
+BLOCK = 256
+
+# Extern names recognised as device intrinsics (the reference resolves
+# `call(name, ...)` through a host registry, run.py:832-846).
+EXTERN_F64 = {
+    "exp": "exp", "log": "log", "sqrt": "sqrt", "erf": "erf", "erfc": "erfc", "sin": "sin", "cos": "cos",
+    "tan": "tan", "tanh": "tanh", "sinh": "sinh", "cosh": "cosh", "asin": "asin", "acos": "acos",
+    "atan": "atan", "fabs": "fabs", "log1p": "log1p", "expm1": "expm1", "log2": "log2", "log10": "log10",
+    "cbrt": "cbrt", "exp2": "exp2", "atan2": "atan2", "pow": "pow", "hypot": "hypot", "copysign": "copysign",
+    "fmod": "fmod",
+}
+
+
+# ---------------------------------------------------------------------------
+# Values during code generation
+
+
+class S:
+    """A scalar C expression of an IR scalar kind."""
+    __slots__ = ("c", "kind")
+
+    def __init__(self, c, kind):
+        self.c = c
+        self.kind = kind
+
+
+class T:
+    """A struct value: tuple of field values."""
+    __slots__ = ("items",)
+
+    def __init__(self, items):
+        self.items = list(items)
+
+
+class Lanes:
+    """A simd value: W lane scalars."""
+    __slots__ = ("lanes", "kind")
+
+    def __init__(self, lanes, kind):
+        self.lanes = list(lanes)
+        self.kind = kind
+
+
+class VRef:
+    """A loop-invariant device vector visible inside the body."""
+    __slots__ = ("cols", "n", "elem")
+
+    def __init__(self, cols, n, elem):
+        self.cols = cols  # C pointer expressions, one per leaf
+        self.n = n        # C expression for the length
+        self.elem = elem
+
+
+class SVec:
+    """A small vector literal built inside the body (registers)."""
+    __slots__ = ("items", "elem")
+
+    def __init__(self, items, elem):
+        self.items = list(items)
+        self.elem = elem
+
+
+class BRef:
+    """A reference to a builder (outer, by id) or a body-local merger."""
+    __slots__ = ("b",)
+
+    def __init__(self, b):
+        self.b = b
+
+
+class BTuple:
+    __slots__ = ("items",)
+
+    def __init__(self, items):
+        self.items = list(items)
+
+
+# ---------------------------------------------------------------------------
+# Loop specification handed over by the executor
+
+
+@dataclass
+class IterSpec:
+    elem: object          # element IR type (flat)
+    simd: bool
+    strided: bool         # explicit start/stride window (non-contiguous)
+    kinds: list = field(default_factory=list)
+
+
+@dataclass(eq=False)
+class BSpec:
+    """One outer builder as seen by the kernel."""
+    bid: int
+    kind: object                  # weldmill BuilderKind
+    mode: str = ""                # vec/group: direct | scan | none ; dict/vecm: global | smem
+    k: int = 0                    # direct: appends per iteration; scan: max appends per iteration
+    extra: dict = field(default_factory=dict)
+
+
+@dataclass
+class Param:
+    name: str
+    ctype: str
+    key: tuple
+
+
+@dataclass
+class KernelPlan:
+    source: str
+    name: str
+    params: list
+    schedule: str                 # static | scan
+    items: int
+    block: int
+    smem: int
+    builders: list
+    scan_bids: list
+    merger_bids: list
+    key: str = ""
+
+
+def _hex_f64(v):
+    b = _struct.unpack("<Q", _struct.pack("<d", v))[0]
+    return f"__longlong_as_double(0x{b:016x}LL)"
+
+
+def _hex_f32(v):
+    b = _struct.unpack("<I", _struct.pack("<f", v))[0]
+    return f"__int_as_float(0x{b:08x})"
+
+
+def c_literal(kind, v):
+    if kind == BOOL:
+        return "true" if v else "false"
+    if kind == I64:
+        return f"((i64)0x{v & 0xFFFFFFFFFFFFFFFF:016x}ULL)"
+    if kind == I32:
+        return f"((i32)0x{v & 0xFFFFFFFF:08x}U)"
+    if kind == F64:
+        return _hex_f64(float(v))
+    return _hex_f32(float(v))
+
+
+def key_layout(kinds):
+    """Pack key leaves into 64-bit words: list of (word, shift, width)."""
+    out = []
+    word, pos = 0, 0
+    for k in kinds:
+        w = 64 if SIZE[k] == 8 else (32 if SIZE[k] == 4 else 8)
+        if pos + w > 64:
+            word += 1
+            pos = 0
+        out.append((word, pos, w))
+        pos += w
+    return out, word + 1
+
+
+# ---------------------------------------------------------------------------
+
+
+class Gen:
+    def __init__(self, loop: For, iters, bstruct, captures, externs, strategy, items=None):
+        self.loop = loop
+        self.iters = iters
+        self.bstruct = bstruct      # nested tuple/BSpec mirroring the builders value
+        self.captures = captures    # name -> (IR type, runtime value)
+        self.externs = externs
+        self.strategy = strategy
+        self.params = []
+        self.pnames = set()
+        self.lines = []
+        self.ind = 1
+        self.ntmp = 0
+        self.phase = "A"
+        self.local_mergers = []
+        self.bspecs = []
+        self._collect(bstruct)
+        self.items = items
+
+    # -- helpers -----------------------------------------------------------
+    def _collect(self, bs):
+        if isinstance(bs, BSpec):
+            self.bspecs.append(bs)
+        else:
+            for x in bs:
+                self._collect(x)
+
+    def param(self, name, ctype, key):
+        if name not in self.pnames:
+            self.pnames.add(name)
+            self.params.append(Param(name, ctype, key))
+        return f"p.{name}"
+
+    def emit(self, line):
+        self.lines.append("  " * self.ind + line)
+
+    def tmp(self, prefix="t"):
+        self.ntmp += 1
+        return f"{prefix}{self.ntmp}"
+
+    def let(self, kind, expr):
+        name = self.tmp()
+        self.emit(f"const {CTYPE[kind]} {name} = {expr};")
+        return S(name, kind)
+
+    # -- expressions -------------------------------------------------------
+    def ex(self, e, env):
+        m = getattr(self, "ex_" + type(e).__name__, None)
+        if m is None:
+            raise DeviceUnsupported(f"{type(e).__name__} inside a loop body is not lowered to the device")
+        return m(e, env)
+
+    def ex_Literal(self, e, env):
+        kind = e.ty.kind
+        v = e.value
+        if kind == F32:
+            from .irtypes import f32_round
+            v = f32_round(float(v))
+        return S(c_literal(kind, v), kind)
+
+    def ex_Ident(self, e, env):
+        if e.name in env:
+            return env[e.name]
+        raise DeviceUnsupported(f"unbound name {e.name!r} in loop body")
+
+    def ex_Let(self, e, env):
+        v = self.ex(e.value, env)
+        env2 = dict(env)
+        env2[e.name] = v
+        return self.ex(e.body, env2)
+
+    def ex_MakeStruct(self, e, env):
+        vals = [self.ex(x, env) for x in e.items]
+        if any(isinstance(v, (BRef, BTuple)) for v in vals):
+            return BTuple(vals)
+        return T(vals)
+
+    def ex_FieldAccess(self, e, env):
+        b = self.ex(e.base, env)
+        if isinstance(b, (T, BTuple)):
+            return b.items[e.ordinal]
+        raise DeviceUnsupported("field access on a non-struct value")
+
+    def ex_MakeVector(self, e, env):
+        return SVec([self.ex(x, env) for x in e.items], e.ty.elem)
+
+    def ex_Broadcast(self, e, env):
+        v = self.ex(e.value, env)
+        return Lanes([S(v.c, v.kind)] * W, v.kind)
+
+    def _binop_c(self, op, kind, a, b):
+        if op in ("==", "!=", "<", "<=", ">", ">="):
+            return f"({a} {op} {b})"
+        if kind == BOOL:
+            if op == "&":
+                return f"({a} && {b})"
+            if op == "|":
+                return f"({a} || {b})"
+            raise DeviceUnsupported(f"operator {op} over bool")
+        if kind in INT_KINDS:
+            sfx = "i64" if kind == I64 else "i32"
+            if op in ("+", "-", "*"):
+                return f"wg_{ {'+': 'add', '-': 'sub', '*': 'mul'}[op]}_{sfx}({a}, {b})"
+            if op == "/":
+                return f"wg_div_{sfx}({a}, {b}, p.err)"
+            if op == "%":
+                return f"wg_rem_{sfx}({a}, {b}, p.err)"
+            if op in ("&", "|"):
+                return f"(({CTYPE[kind]})({a} {op} {b}))"
+            if op in ("min", "max"):
+                return f"wg_{op}_{sfx}({a}, {b})"
+        else:
+            sfx = "f64" if kind == F64 else "f32"
+            if op in ("+", "-", "*", "/"):
+                return f"({a} {op} {b})"
+            if op == "%":
+                return f"wg_rem_{sfx}({a}, {b})"
+            if op in ("min", "max"):
+                return f"wg_{op}_{sfx}({a}, {b})"
+        raise DeviceUnsupported(f"operator {op} over {kind}")
+
+    def ex_BinaryOp(self, e, env):
+        op = e.op
+        if op in ("&&", "||"):
+            a = self.ex(e.lhs, env)
+            name = self.tmp()
+            self.emit(f"bool {name} = {a.c};")
+            self.emit(f"if ({'' if op == '&&' else '!'}{name}) {{")
+            self.ind += 1
+            b = self.ex(e.rhs, env)
+            self.emit(f"{name} = {b.c};")
+            self.ind -= 1
+            self.emit("}")
+            return S(name, BOOL)
+        a = self.ex(e.lhs, env)
+        b = self.ex(e.rhs, env)
+        lt = e.lhs.ty
+        if isinstance(lt, Simd):
+            rk = BOOL if op in ("==", "!=", "<", "<=", ">", ">=") else lt.kind
+            return Lanes([self.let(rk, self._binop_c(op, lt.kind, x.c, y.c)) for x, y in zip(a.lanes, b.lanes)], rk)
+        rk = BOOL if op in ("==", "!=", "<", "<=", ">", ">=") else lt.kind
+        return self.let(rk, self._binop_c(op, lt.kind, a.c, b.c))
+
+    def ex_UnaryOp(self, e, env):
+        v = self.ex(e.operand, env)
+        t = e.operand.ty
+
+        def one(x, kind):
+            if e.op == "!":
+                return self.let(BOOL, f"(!{x.c})")
+            if kind in FLOAT_KINDS:
+                return self.let(kind, f"(-{x.c})")
+            return self.let(kind, f"wg_neg_{'i64' if kind == I64 else 'i32'}({x.c})")
+
+        if isinstance(t, Simd):
+            return Lanes([one(x, t.kind) for x in v.lanes], t.kind)
+        return one(v, t.kind)
+
+    def _cast_c(self, src, dst, a):
+        if src == dst:
+            return a
+        if dst in INT_KINDS:
+            d = "i64" if dst == I64 else "i32"
+            if src == F64:
+                return f"wg_f64_to_{d}({a})"
+            if src == F32:
+                return f"wg_f32_to_{d}({a})"
+            if src == BOOL:
+                return f"(({CTYPE[dst]})({a} ? 1 : 0))"
+            if dst == I32:
+                return f"((i32)(u32)(u64)({a}))"
+            return f"((i64)({a}))"
+        if dst == F64:
+            if src == BOOL:
+                return f"({a} ? 1.0 : 0.0)"
+            return f"((double)({a}))"
+        if dst == F32:
+            if src == BOOL:
+                return f"({a} ? 1.0f : 0.0f)"
+            if src == I64:
+                return f"wg_i64_to_f32({a})"
+            if src == I32:
+                return f"((float)(double)({a}))"
+            return f"((float)({a}))"
+        raise DeviceUnsupported(f"cast {src} -> {dst}")
+
+    def ex_CastScalar(self, e, env):
+        v = self.ex(e.value, env)
+        src = e.value.ty
+        if isinstance(src, Simd):
+            return Lanes([self.let(e.kind, self._cast_c(src.kind, e.kind, x.c)) for x in v.lanes], e.kind)
+        return self.let(e.kind, self._cast_c(src.kind, e.kind, v.c))
+
+    def ex_ExternCall(self, e, env):
+        if e.name not in self.externs:
+            from weldmill.errors import ExternCallUnknown
+            raise ExternCallUnknown(f"no extern function {e.name!r} registered")
+        fn = EXTERN_F64.get(e.name)
+        if fn is None:
+            from weldmill.errors import ExternCallUnknown
+            raise ExternCallUnknown(f"extern {e.name!r} has no device implementation")
+        args = [self.ex(a, env) for a in e.args]
+        rk = e.ty.kind
+        cargs = ", ".join(f"(double)({a.c})" for a in args)
+        if rk == F64:
+            return self.let(F64, f"{fn}({cargs})")
+        if rk == F32:
+            return self.let(F32, f"((float){fn}({cargs}))")
+        raise DeviceUnsupported(f"extern {e.name} returning {rk}")
+
+    def _select(self, c, a, b):
+        if isinstance(a, S):
+            return self.let(a.kind, f"({c} ? {a.c} : {b.c})")
+        if isinstance(a, T):
+            return T([self._select(c, x, y) for x, y in zip(a.items, b.items)])
+        if isinstance(a, Lanes):
+            return Lanes([self._select(c, x, y) for x, y in zip(a.lanes, b.lanes)], a.kind)
+        raise DeviceUnsupported("select over non-scalar values")
+
+    def ex_BitSelect(self, e, env):
+        c = self.ex(e.cond, env)
+        a = self.ex(e.on_true, env)
+        b = self.ex(e.on_false, env)
+        if isinstance(c, Lanes):
+            return Lanes([self.let(a.kind, f"({ci.c} ? {x.c} : {y.c})")
+                          for ci, x, y in zip(c.lanes, a.lanes, b.lanes)], a.kind)
+        return self._select(c.c, a, b)
+
+    def _declare_like(self, v, ty):
+        """Declare mutable temps shaped like IR type ty."""
+        if isinstance(ty, Scalar):
+            n = self.tmp()
+            self.emit(f"{CTYPE[ty.kind]} {n} = {c_literal(ty.kind, 0)};")
+            return S(n, ty.kind)
+        if isinstance(ty, Struct):
+            return T([self._declare_like(None, f) for f in ty.fields])
+        if isinstance(ty, Simd):
+            return Lanes([self._declare_like(None, Scalar(ty.kind)) for _ in range(W)], ty.kind)
+        raise DeviceUnsupported(f"conditional value of type {ty}")
+
+    def _assign(self, dst, src):
+        if isinstance(dst, S):
+            self.emit(f"{dst.c} = {src.c};")
+        elif isinstance(dst, T):
+            for d, s in zip(dst.items, src.items):
+                self._assign(d, s)
+        else:
+            for d, s in zip(dst.lanes, src.lanes):
+                self._assign(d, s)
+
+    def ex_If(self, e, env):
+        c = self.ex(e.cond, env)
+        if isinstance(e.ty, Builder) or _is_builder_struct(e.ty):
+            self.emit(f"if ({c.c}) {{")
+            self.ind += 1
+            r = self.ex(e.on_true, env)
+            self.ind -= 1
+            self.emit("} else {")
+            self.ind += 1
+            self.ex(e.on_false, env)
+            self.ind -= 1
+            self.emit("}")
+            return r
+        out = self._declare_like(None, e.ty)
+        self.emit(f"if ({c.c}) {{")
+        self.ind += 1
+        self._assign(out, self.ex(e.on_true, env))
+        self.ind -= 1
+        self.emit("} else {")
+        self.ind += 1
+        self._assign(out, self.ex(e.on_false, env))
+        self.ind -= 1
+        self.emit("}")
+        return out
+
+    def ex_Len(self, e, env):
+        v = self.ex(e.coll, env)
+        if isinstance(v, VRef):
+            return S(v.n, I64)
+        if isinstance(v, SVec):
+            return S(c_literal(I64, len(v.items)), I64)
+        raise DeviceUnsupported("len() of this value inside a loop body")
+
+    def _load_elem(self, vref, idx_c):
+        ks = leaves(vref.elem)
+        vals = []
+        for col, k in zip(vref.cols, ks):
+            ld = f"{col}[{idx_c}]"
+            vals.append(self.let(k, f"({ld} != 0)" if k == BOOL else ld))
+        return _shape(vref.elem, vals)
+
+    def ex_Lookup(self, e, env):
+        coll = self.ex(e.coll, env)
+        idx = self.ex(e.index, env)
+        if isinstance(coll, VRef):
+            ty = coll.elem
+            out = self._declare_like(None, ty)
+            ix = idx.c
+            self.emit(f"if ((u64)({ix}) >= (u64)({coll.n})) {{ wg_raise(p.err, WG_ERR_LOOKUP_OOB, {ix}); }} else {{")
+            self.ind += 1
+            self._assign(out, self._load_elem(coll, ix))
+            self.ind -= 1
+            self.emit("}")
+            return out
+        if isinstance(coll, SVec):
+            out = self._declare_like(None, coll.elem)
+            self.emit(f"switch ({idx.c}) {{")
+            for j, item in enumerate(coll.items):
+                self.emit(f"case {j}: {{")
+                self.ind += 1
+                self._assign(out, item)
+                self.emit("break; }")
+                self.ind -= 1
+            self.emit(f"default: wg_raise(p.err, WG_ERR_LOOKUP_OOB, {idx.c});")
+            self.emit("}")
+            return out
+        raise DeviceUnsupported("lookup into this collection inside a loop body (dict probes are not lowered yet)")
+
+    # -- builders ------------------------------------------------------------
+    def ex_NewBuilder(self, e, env):
+        kind = e.kind
+        if isinstance(kind, Merger):
+            lm = _LocalMerger(self, kind)
+            self.local_mergers.append(lm)
+            return BRef(lm)
+        raise DeviceUnsupported(f"{kind} created inside a loop body")
+
+    def ex_Result(self, e, env):
+        b = self.ex(e.builder, env)
+        if isinstance(b, BRef) and isinstance(b.b, _LocalMerger):
+            return b.b.result()
+        raise DeviceUnsupported("result() of an outer builder inside a loop body")
+
+    def ex_Merge(self, e, env):
+        bref = self.ex(e.builder, env)
+        v = self.ex(e.value, env)
+        if not isinstance(bref, BRef):
+            raise DeviceUnsupported("merge into a non-builder")
+        b = bref.b
+        if isinstance(b, _LocalMerger):
+            b.merge(v)
+        else:
+            self.merge(b, v, e.value.ty)
+        return bref
+
+    def ex_For(self, e, env):
+        """A loop nested in the body: runs sequentially per thread (the
+        reference runs nested loops inside the parent's chunk, run.py:952-956)."""
+        datas = [self.ex(it.data, env) for it in e.iters]
+        for it in e.iters:
+            if it.simd:
+                raise DeviceUnsupported("simditer in a nested loop")
+        bval = self.ex(e.builders, env)
+        lam = e.func
+        if not isinstance(lam, Lambda):
+            raise DeviceUnsupported("nested loop body must be a lambda")
+        pb, pi, px = (p.name for p in lam.params)
+        if all(isinstance(d, SVec) for d in datas):
+            if any(it.start is not None for it in e.iters):
+                raise DeviceUnsupported("windowed iteration over a vector literal")
+            n = len(datas[0].items)
+            if any(len(d.items) != n for d in datas):
+                from weldmill.errors import ZipLengthMismatch
+                raise ZipLengthMismatch("zipped iterations disagree")
+            for j in range(n):
+                elem = datas[0].items[j] if len(datas) == 1 else T([d.items[j] for d in datas])
+                env2 = dict(env)
+                env2.update({pb: bval, pi: S(c_literal(I64, j), I64), px: elem})
+                self.ex(lam.body, env2)
+            return bval
+        if all(isinstance(d, VRef) for d in datas):
+            if self._counts_outer(lam.body, env, {pb: bval}):
+                raise DeviceUnsupported("appends inside a data-dependent nested loop (two-pass sizing not lowered)")
+            cnt = self.tmp("n")
+            starts, strides = [], []
+            for k, (it, d) in enumerate(zip(e.iters, datas)):
+                if it.start is not None:
+                    s = self.ex(it.start, env).c
+                    en = self.ex(it.end, env).c
+                    st = self.ex(it.stride, env).c
+                    self.emit(f"if (!({st} >= 1 && 0 <= {s} && {s} <= {en} && {en} <= {d.n})) "
+                              f"wg_raise(p.err, WG_ERR_LOOKUP_OOB, {s});")
+                    c = f"(({st} >= 1 && 0 <= {s} && {s} <= {en} && {en} <= {d.n}) ? (({en} - {s} + {st} - 1) / {st}) : 0)"
+                else:
+                    s, st, c = "0", "1", d.n
+                starts.append(s)
+                strides.append(st)
+                if k == 0:
+                    self.emit(f"const i64 {cnt} = {c};")
+                else:
+                    self.emit(f"if ({c} != {cnt}) wg_raise(p.err, WG_ERR_INTERNAL, 0);")
+            j = self.tmp("j")
+            self.emit(f"for (i64 {j} = 0; {j} < {cnt}; ++{j}) {{")
+            self.ind += 1
+            elems = [self._load_elem(d, f"({s} + {j} * {st})") for d, s, st in zip(datas, starts, strides)]
+            elem = elems[0] if len(elems) == 1 else T(elems)
+            env2 = dict(env)
+            env2.update({pb: bval, pi: S(j, I64), px: elem})
+            self.ex(lam.body, env2)
+            self.ind -= 1
+            self.emit("}")
+            return bval
+        raise DeviceUnsupported("nested loop over this kind of vector")
+
+    def _counts_outer(self, body, env, benv):
+        try:
+            cnt = merge_counts(body, {**_benv_from(env), **benv})
+        except DeviceUnsupported:
+            return True
+        return any(mx > 0 for b, (mn, mx) in cnt.items() if isinstance(b, BSpec)
+                   and isinstance(b.kind, (VecBuilder, GroupBuilder)))
+
+    # -- outer builder merges ----------------------------------------------
+    def merge(self, b: BSpec, v, vty):
+        kind = b.kind
+        if isinstance(v, Lanes):
+            for lane in v.lanes:
+                self.merge(b, lane, Scalar(v.kind))
+            return
+        if isinstance(kind, Merger):
+            if self.phase != "A":
+                return
+            vals = _flat(v)
+            ks = leaves(kind.elem)
+            for f, (x, k) in enumerate(zip(vals, ks)):
+                self.emit(f"m{b.bid}_{f} = {OPSTRUCT[kind.op]}<{CTYPE[k]}>::f(m{b.bid}_{f}, {x.c});")
+            self.emit(f"m{b.bid}_h = 1;")
+            return
+        if isinstance(kind, (VecBuilder, GroupBuilder)):
+            vals = _flat(v)
+            ks = b.extra["kinds"]
+            if b.mode == "direct":
+                if self.phase != "A":
+                    return
+                if b.extra.get("buffered"):
+                    for f, (x, k) in enumerate(zip(vals, ks)):
+                        val = f"(u8)({x.c})" if k == BOOL else x.c
+                        self.emit(f"o{b.bid}_{f}[j * {b.k} + c{b.bid}] = {val};")
+                else:
+                    for f, (x, k) in enumerate(zip(vals, ks)):
+                        val = f"(u8)({x.c})" if k == BOOL else x.c
+                        col = self.param(f"a{b.bid}_{f}", f"{STYPE[k]}*", ("b", b.bid, "col", f))
+                        self.emit(f"{col}[li * {b.k} + c{b.bid}] = {val};")
+                self.emit(f"c{b.bid} += 1;")
+                return
+            if b.mode == "scan":
+                if self.phase == "A":
+                    self.emit(f"cnt{b.bid} += 1;")
+                else:
+                    for f, (x, k) in enumerate(zip(vals, ks)):
+                        val = f"(u8)({x.c})" if k == BOOL else x.c
+                        col = self.param(f"a{b.bid}_{f}", f"{STYPE[k]}*", ("b", b.bid, "col", f))
+                        self.emit(f"{col}[wpos{b.bid}] = {val};")
+                    self.emit(f"wpos{b.bid} += 1;")
+                return
+            raise DeviceUnsupported(f"appender mode {b.mode}")
+        if isinstance(kind, DictMerger):
+            if self.phase != "A":
+                return
+            self._dict_merge(b, v)
+            return
+        if isinstance(kind, VecMerger):
+            if self.phase != "A":
+                return
+            idx, val = v.items
+            vals = _flat(val)
+            ks = leaves(kind.elem)
+            n = self.param(f"v{b.bid}_len", "i64", ("b", b.bid, "len"))
+            self.emit(f"if ((u64)({idx.c}) >= (u64)({n})) {{ wg_raise(p.err, WG_ERR_VECMERGER_OOB, {idx.c}); }} else {{")
+            self.ind += 1
+            opc = OPCODE[kind.op]
+            for f, (x, k) in enumerate(zip(vals, ks)):
+                if b.mode == "smem":
+                    self.emit(f"wg_smem_fold<{opc}, {CTYPE[k]}>((({CTYPE[k]}*)(s_vm{b.bid} + {f} * {b.extra['nbins']})) + {idx.c}, {x.c});")
+                else:
+                    col = self.param(f"v{b.bid}_{f}", f"{CTYPE[k]}*", ("b", b.bid, "col", f))
+                    self.emit(f"WgAtomicFold<{opc}, {CTYPE[k]}>::f({col} + {idx.c}, {x.c});")
+            self.ind -= 1
+            self.emit("}")
+            return
+        raise DeviceUnsupported(f"merge into {kind}")
+
+    def _key_words(self, kinds, vals):
+        lay, nw = key_layout(kinds)
+        words = [self.tmp("kw") for _ in range(nw)]
+        for w in words:
+            self.emit(f"u64 {w} = 0;")
+        for (wi, sh, width), x, k in zip(lay, vals, kinds):
+            if k == I64:
+                bits = f"(u64)({x.c})"
+            elif k == I32:
+                bits = f"(u64)(u32)({x.c})"
+            elif k == F64:
+                bits = f"wg_key_f64({x.c})"
+            elif k == F32:
+                bits = f"wg_key_f32({x.c})"
+            else:
+                bits = f"(u64)({x.c} ? 1 : 0)"
+            self.emit(f"{words[wi]} |= ({bits}) << {sh};")
+        return words
+
+    def _dict_merge(self, b, v):
+        kind = b.kind
+        key, val = v.items
+        kks = leaves(kind.key)
+        vks = leaves(kind.value)
+        words = self._key_words(kks, _flat(key))
+        vals = _flat(val)
+        nw = len(words)
+        opc = OPCODE[kind.op]
+        sw = b.extra["slot_words"]
+        kbase = 1 if nw == 1 else 1 + nw
+        table = self.param(f"d{b.bid}_table", "u64*", ("b", b.bid, "table"))
+        mask = self.param(f"d{b.bid}_mask", "u64", ("b", b.bid, "mask"))
+        count = self.param(f"d{b.bid}_count", "unsigned long long*", ("b", b.bid, "count"))
+        limit = self.param(f"d{b.bid}_limit", "u64", ("b", b.bid, "limit"))
+        slot = self.tmp("sl")
+        self.emit("{")
+        self.ind += 1
+        if b.mode == "smem" and nw == 1:
+            # Privatised first level: per-CTA table in shared memory.
+            ssl = self.tmp("ss")
+            self.emit(f"const int {ssl} = wg_sht_find1(s_dk{b.bid}, {sw}, {b.extra['smem_slots'] - 1}, {words[0]});")
+            self.emit(f"if ({ssl} >= 0) {{")
+            self.ind += 1
+            for f, (x, k) in enumerate(zip(vals, vks)):
+                self.emit(f"wg_smem_fold<{opc}, {CTYPE[k]}>(({CTYPE[k]}*)(s_dk{b.bid} + (u64){ssl} * {sw} + {kbase + f}), {x.c});")
+            self.ind -= 1
+            self.emit("} else {")
+            self.ind += 1
+        if nw == 1:
+            self.emit(f"const i64 {slot} = wg_ht_find1({table}, {sw}, {mask}, {words[0]}, {count}, {limit});")
+        else:
+            arr = self.tmp("ka")
+            self.emit(f"const u64 {arr}[{nw}] = {{{', '.join(words)}}};")
+            self.emit(f"const i64 {slot} = wg_ht_findN({table}, {sw}, {mask}, {arr}, {nw}, {count}, {limit});")
+        self.emit(f"if ({slot} >= 0) {{")
+        self.ind += 1
+        for f, (x, k) in enumerate(zip(vals, vks)):
+            self.emit(f"WgAtomicFold<{opc}, {CTYPE[k]}>::f(({CTYPE[k]}*)({table} + (u64){slot} * {sw} + {kbase + f}), {x.c});")
+        self.ind -= 1
+        self.emit("} else {")
+        self.ind += 1
+        ocount = self.param(f"d{b.bid}_ocount", "unsigned long long*", ("b", b.bid, "ocount"))
+        ocap = self.param(f"d{b.bid}_ocap", "u64", ("b", b.bid, "ocap"))
+        self.emit(f"const u64 o_ = atomicAdd({ocount}, 1ULL);")
+        self.emit(f"if (o_ < {ocap}) {{")
+        self.ind += 1
+        for wi, w in enumerate(words):
+            col = self.param(f"d{b.bid}_ok{wi}", "u64*", ("b", b.bid, "okey", wi))
+            self.emit(f"{col}[o_] = {w};")
+        for f, (x, k) in enumerate(zip(vals, vks)):
+            col = self.param(f"d{b.bid}_ov{f}", "u64*", ("b", b.bid, "oval", f))
+            self.emit(f"{col}[o_] = wg_to_bits<{CTYPE[k]}>({x.c});")
+        self.ind -= 1
+        self.emit("} else { wg_raise(p.err, WG_ERR_INTERNAL, 1); }")
+        self.ind -= 1
+        self.emit("}")
+        if b.mode == "smem" and nw == 1:
+            self.ind -= 1
+            self.emit("}")
+        self.ind -= 1
+        self.emit("}")
+
+
+class _LocalMerger:
+    """A merger created inside the body: a sequential register fold."""
+
+    def __init__(self, g: Gen, kind: Merger):
+        self.g = g
+        self.kind = kind
+        self.ks = leaves(kind.elem)
+        self.names = [g.tmp("lm") for _ in self.ks]
+        self.has = g.tmp("lmh")
+        for n, k in zip(self.names, self.ks):
+            g.emit(f"{CTYPE[k]} {n} = {c_literal(k, internal_identity(kind.op, k))};")
+        g.emit(f"int {self.has} = 0;")
+
+    def merge(self, v):
+        if isinstance(v, Lanes):
+            for lane in v.lanes:
+                self.merge(lane)
+            return
+        for n, x, k in zip(self.names, _flat(v), self.ks):
+            self.g.emit(f"{n} = {OPSTRUCT[self.kind.op]}<{CTYPE[k]}>::f({n}, {x.c});")
+        self.g.emit(f"{self.has} = 1;")
+
+    def result(self):
+        vals = []
+        for n, k in zip(self.names, self.ks):
+            ident = c_literal(k, identity_value(self.kind.op, k))
+            vals.append(self.g.let(k, f"({self.has} ? {n} : {ident})"))
+        return _shape(self.kind.elem, vals)
+
+
+def _flat(v):
+    if isinstance(v, S):
+        return [v]
+    if isinstance(v, T):
+        out = []
+        for x in v.items:
+            out.extend(_flat(x))
+        return out
+    raise DeviceUnsupported("expected a scalar or struct value")
+
+
+def _shape(ty, vals):
+    it = iter(vals)
+
+    def go(t):
+        if isinstance(t, Scalar):
+            return next(it)
+        return T([go(f) for f in t.fields])
+
+    return go(ty)
+
+
+def _is_builder_struct(t):
+    return isinstance(t, Struct) and all(isinstance(f, Builder) or _is_builder_struct(f) for f in t.fields)
+
+
+def _benv_from(env):
+    return {k: v for k, v in env.items() if isinstance(v, (BRef, BTuple))}
+
+
+# ---------------------------------------------------------------------------
+# Static merge-count analysis: per outer builder, (min, max) scalar appends
+# per iteration over all control paths.
+
+
+INF = math.inf
+
+
+def _add(a, b):
+    out = dict(a)
+    for k, (mn, mx) in b.items():
+        x = out.get(k, (0, 0))
+        out[k] = (x[0] + mn, x[1] + mx)
+    return out
+
+
+def _branch(a, b):
+    out = {}
+    for k in set(a) | set(b):
+        x = a.get(k, (0, 0))
+        y = b.get(k, (0, 0))
+        out[k] = (min(x[0], y[0]), max(x[1], y[1]))
+    return out
+
+
+def _bref(e, benv):
+    """Resolve a builder-typed expression to BRef/BTuple plus its counts."""
+    if isinstance(e, Ident):
+        return benv.get(e.name), {}
+    if isinstance(e, FieldAccess):
+        base, c = _bref(e.base, benv)
+        if isinstance(base, BTuple):
+            return base.items[e.ordinal], c
+        return None, c
+    if isinstance(e, Merge):
+        r, c = _bref(e.builder, benv)
+        n = W if isinstance(e.value.ty, Simd) else 1
+        if isinstance(r, BRef):
+            c = _add(c, {r.b: (n, n)})
+        return r, c
+    if isinstance(e, If):
+        rt_, ct = _bref(e.on_true, benv)
+        _, cf = _bref(e.on_false, benv)
+        return rt_, _branch(ct, cf)
+    if isinstance(e, Let):
+        if isinstance(e.value.ty, Builder) or _is_builder_struct(e.value.ty):
+            r, c = _bref(e.value, benv)
+            r2, c2 = _bref(e.body, {**benv, e.name: r})
+            return r2, _add(c, c2)
+        return _bref(e.body, benv)
+    if isinstance(e, MakeStruct):
+        items, c = [], {}
+        for x in e.items:
+            r, cx = _bref(x, benv)
+            items.append(r)
+            c = _add(c, cx)
+        return BTuple(items), c
+    if isinstance(e, For):
+        r, c = _bref(e.builders, benv)
+        lam = e.func
+        pb = lam.params[0].name
+        _, cb = _bref(lam.body, {**benv, pb: r})
+        data = e.iters[0].data
+        if isinstance(data, MakeVector) and all(it.start is None for it in e.iters):
+            n = len(data.items)
+            cb = {k: (mn * n, mx * n) for k, (mn, mx) in cb.items()}
+        else:
+            cb = {k: (0, INF if mx > 0 else 0) for k, (mn, mx) in cb.items()}
+        return r, _add(c, cb)
+    if isinstance(e, NewBuilder):
+        return BRef(object()), {}
+    return None, {}
+
+
+def merge_counts(body, benv):
+    _, c = _bref(body, benv)
+    return c
+
+
+# ---------------------------------------------------------------------------
+# Kernel assembly
+
+
+def choose_items(iters):
+    row = 0
+    for it in iters:
+        row += sum(SIZE[k] for k in it.kinds) * (W if it.simd else 1)
+    row = max(row, 1)
+    items = 128 // row
+    p = 1
+    while p * 2 <= items:
+        p *= 2
+    return max(2, min(8, p))
+
+
+def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_loop", items=None) -> KernelPlan:
+    g = Gen(loop, iters, bstruct, captures, externs, strategy)
+    lam = loop.func
+    if not isinstance(lam, Lambda):
+        raise DeviceUnsupported("loop function must be a lambda literal")
+    pb, pi, px = (p.name for p in lam.params)
+
+    ITEMS = items or choose_items(iters)
+    g.items = ITEMS
+
+    # builders value seen by the body
+    def bref_of(bs):
+        if isinstance(bs, BSpec):
+            return BRef(bs)
+        return BTuple([bref_of(x) for x in bs])
+
+    bval = bref_of(bstruct)
+
+    # captured values
+    env = {}
+    for cname, (cty, cval) in captures.items():
+        env[cname] = _capture_val(g, cname, cty, cval)
+
+    # appender modes from the static merge counts
+    counts = merge_counts(lam.body, {pb: bval})
+    for b in g.bspecs:
+        mn, mx = counts.get(b, (0, 0))
+        b.extra["maxm"] = mx
+        if isinstance(b.kind, (VecBuilder, GroupBuilder)):
+            if isinstance(b.kind, VecBuilder):
+                b.extra["kinds"] = leaves(b.kind.elem)
+            else:
+                b.extra["kinds"] = leaves(b.kind.key) + leaves(b.kind.value)
+            if mx == 0:
+                b.mode, b.k = "none", 0
+            elif mn == mx:
+                b.mode, b.k = "direct", int(mn)
+                b.extra["buffered"] = ITEMS * b.k <= 32
+            elif mx < INF:
+                b.mode, b.k = "scan", int(mx)
+            else:
+                raise DeviceUnsupported("appends inside a data-dependent nested loop (two-pass sizing not lowered)")
+
+    scan_bs = [b for b in g.bspecs if b.mode == "scan"]
+    merger_bs = [b for b in g.bspecs if isinstance(b.kind, Merger)]
+    schedule = "scan" if scan_bs else "static"
+
+    # element loads ----------------------------------------------------------
+    g.param("n", "i64", ("n",))
+    g.param("idx0", "i64", ("idx0",))
+    g.param("err", "i64*", ("err",))
+    loads = []  # (array name, stype, kind, count_per_item, iter index, leaf)
+    for k, it in enumerate(iters):
+        per = W if it.simd else 1
+        for l, kk in enumerate(it.kinds):
+            col = g.param(f"it{k}_{l}", f"const {STYPE[kk]}*", ("itcol", k, l))
+            loads.append((f"x{k}_{l}", STYPE[kk], kk, per, k, l, col))
+        if it.strided:
+            g.param(f"it{k}_start", "i64", ("itstart", k))
+            g.param(f"it{k}_stride", "i64", ("itstride", k))
+
+    def elem_val(k, it):
+        """Element value of iter k at item j (C arrays indexed by j)."""
+        vals = []
+        for (arr, st, kk, per, kk_i, l, col) in loads:
+            if kk_i != k:
+                continue
+            if it.simd:
+                lanes = [S(f"({arr}[j * {W} + {q}] != 0)" if kk == BOOL else f"{arr}[j * {W} + {q}]", kk)
+                         for q in range(W)]
+                vals.append(Lanes(lanes, kk))
+            else:
+                vals.append(S(f"({arr}[j] != 0)" if kk == BOOL else f"{arr}[j]", kk))
+        if it.simd:
+            return vals[0]
+        return _shape(it.elem, vals)
+
+    # body, phase A -----------------------------------------------------------
+    def body_env():
+        e = dict(env)
+        elems = [elem_val(k, it) for k, it in enumerate(iters)]
+        e[px] = elems[0] if len(elems) == 1 else T(elems)
+        e[pi] = S("i", I64)
+        e[pb] = bval
+        return e
+
+    g.lines = []
+    g.ind = 3
+    g.phase = "A"
+    for b in g.bspecs:
+        if b.mode == "direct":
+            g.emit(f"int c{b.bid} = 0;")
+    g.ex(lam.body, body_env())
+    body_a = g.lines
+    body_b = []
+    if scan_bs:
+        g.lines = []
+        g.ind = 3
+        g.phase = "B"
+        g.ex(lam.body, body_env())
+        body_b = g.lines
+
+    # builder params / smem -------------------------------------------------
+    for b in merger_bs:
+        g.param(f"m{b.bid}_part", "u64*", ("b", b.bid, "part"))
+        g.param(f"m{b.bid}_slot", "u64*", ("b", b.bid, "slot"))
+    if merger_bs:
+        g.param("ticket", "unsigned int*", ("ticket",))
+    for b in g.bspecs:
+        if b.mode == "direct":
+            for f, kk in enumerate(b.extra["kinds"]):
+                g.param(f"a{b.bid}_{f}", f"{STYPE[kk]}*", ("b", b.bid, "col", f))
+        if b.mode == "scan":
+            g.param(f"a{b.bid}_status", "u64*", ("b", b.bid, "status"))
+            g.param(f"a{b.bid}_total", "i64*", ("b", b.bid, "total"))
+    if schedule == "scan":
+        g.param("tilectr", "unsigned long long*", ("tilectr",))
+
+    smem_decls = []
+    smem_init = []
+    smem_flush = []
+    dyn_smem = 0
+    for b in g.bspecs:
+        if isinstance(b.kind, VecMerger) and b.mode == "smem":
+            nb = b.extra["nbins"]
+            ks = leaves(b.kind.elem)
+            off = dyn_smem // 8
+            smem_decls.append(f"u64* s_vm{b.bid} = wg_dyn_smem + {off};")
+            dyn_smem += nb * len(ks) * 8
+            opc = OPCODE[b.kind.op]
+            for f, kk in enumerate(ks):
+                ident = c_literal(kk, internal_identity(b.kind.op, kk))
+                smem_init.append(f"for (int q = threadIdx.x; q < {nb}; q += {BLOCK}) (({CTYPE[kk]}*)(s_vm{b.bid} + {f * nb}))[q] = {ident};")
+                col = g.param(f"v{b.bid}_{f}", f"{CTYPE[kk]}*", ("b", b.bid, "col", f))
+                smem_flush.append(
+                    f"for (int q = threadIdx.x; q < {nb}; q += {BLOCK}) {{ const {CTYPE[kk]} v_ = (({CTYPE[kk]}*)(s_vm{b.bid} + {f * nb}))[q]; "
+                    f"if (wg_to_bits<{CTYPE[kk]}>(v_) != wg_to_bits<{CTYPE[kk]}>({ident})) WgAtomicFold<{opc}, {CTYPE[kk]}>::f({col} + q, v_); }}")
+        if isinstance(b.kind, DictMerger) and b.mode == "smem":
+            ns = b.extra["smem_slots"]
+            sw = b.extra["slot_words"]
+            off = dyn_smem // 8
+            smem_decls.append(f"u64* s_dk{b.bid} = wg_dyn_smem + {off};")
+            dyn_smem += ns * sw * 8
+            pat = b.extra["pattern"]
+            smem_init.append(f"for (int q = threadIdx.x; q < {ns * sw}; q += {BLOCK}) {{ const int w_ = q % {sw}; "
+                             f"s_dk{b.bid}[q] = {_pattern_switch(pat)}; }}")
+            table = g.param(f"d{b.bid}_table", "u64*", ("b", b.bid, "table"))
+            mask = g.param(f"d{b.bid}_mask", "u64", ("b", b.bid, "mask"))
+            count = g.param(f"d{b.bid}_count", "unsigned long long*", ("b", b.bid, "count"))
+            limit = g.param(f"d{b.bid}_limit", "u64", ("b", b.bid, "limit"))
+            ocount = g.param(f"d{b.bid}_ocount", "unsigned long long*", ("b", b.bid, "ocount"))
+            ocap = g.param(f"d{b.bid}_ocap", "u64", ("b", b.bid, "ocap"))
+            vks = leaves(b.kind.value)
+            opc = OPCODE[b.kind.op]
+            fl = [f"for (int q = threadIdx.x; q < {ns}; q += {BLOCK}) {{",
+                  f"  const u64 k_ = s_dk{b.bid}[(u64)q * {sw}];",
+                  "  if (k_ == WG_EMPTY_KEY) continue;",
+                  f"  const i64 sl_ = wg_ht_find1({table}, {sw}, {mask}, k_, {count}, {limit});",
+                  "  if (sl_ >= 0) {"]
+            for f, kk in enumerate(vks):
+                fl.append(f"    WgAtomicFold<{opc}, {CTYPE[kk]}>::f(({CTYPE[kk]}*)({table} + (u64)sl_ * {sw} + {1 + f}), "
+                          f"*({CTYPE[kk]}*)(s_dk{b.bid} + (u64)q * {sw} + {1 + f}));")
+            fl.append("  } else {")
+            fl.append(f"    const u64 o_ = atomicAdd({ocount}, 1ULL);")
+            fl.append(f"    if (o_ < {ocap}) {{")
+            okc = g.param(f"d{b.bid}_ok0", "u64*", ("b", b.bid, "okey", 0))
+            fl.append(f"      {okc}[o_] = k_;")
+            for f, kk in enumerate(vks):
+                col = g.param(f"d{b.bid}_ov{f}", "u64*", ("b", b.bid, "oval", f))
+                fl.append(f"      {col}[o_] = s_dk{b.bid}[(u64)q * {sw} + {1 + f}];")
+            fl.append("    } else { wg_raise(p.err, WG_ERR_INTERNAL, 1); }")
+            fl.append("  }")
+            fl.append("}")
+            smem_flush.append("\n    ".join(fl))
+
+    # ---- assemble ----------------------------------------------------------
+    src = []
+    src.append('#include "weld_device.cuh"')
+    src.append(f"#define BLOCK {BLOCK}")
+    src.append(f"#define ITEMS {ITEMS}")
+    src.append("#define TILE (BLOCK * ITEMS)")
+    src.append("struct Params {")
+    for p_ in g.params:
+        src.append(f"  {p_.ctype} {p_.name};")
+    src.append("};")
+    src.append(f'extern "C" __global__ void __launch_bounds__(BLOCK) {name}(const Params p) {{')
+    src.append("  extern __shared__ __align__(16) u64 wg_dyn_smem[];")
+    src.extend("  " + d for d in smem_decls)
+    src.extend("  " + d for d in smem_init)
+    if smem_init:
+        src.append("  __syncthreads();")
+    for b in merger_bs:
+        for f, kk in enumerate(leaves(b.kind.elem)):
+            src.append(f"  {CTYPE[kk]} m{b.bid}_{f} = {c_literal(kk, internal_identity(b.kind.op, kk))};")
+        src.append(f"  int m{b.bid}_h = 0;")
+    src.append("  const i64 n = p.n;")
+    src.append("  const i64 ntiles = (n + TILE - 1) / TILE;")
+    if scan_bs:
+        src.append("  __shared__ i64 s_scan[33];")
+        src.append(f"  __shared__ i64 s_toff[{len(scan_bs)}];")
+        src.append("  __shared__ i64 s_tile;")
+        src.append("  while (true) {")
+        src.append("    if (threadIdx.x == 0) s_tile = (i64)atomicAdd(p.tilectr, 1ULL);")
+        src.append("    __syncthreads();")
+        src.append("    const i64 tile = s_tile;")
+        src.append("    if (tile >= ntiles) break;")
+    else:
+        src.append("  for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {")
+    src.append("    const i64 t0 = tile * TILE + (i64)threadIdx.x * ITEMS;")
+    src.append("    const bool full = (t0 + ITEMS <= n);")
+    for (arr, st, kk, per, k, l, col) in loads:
+        cnt = f"ITEMS * {per}" if per > 1 else "ITEMS"
+        src.append(f"    alignas(16) {st} {arr}[{cnt}];")
+        if iters[k].strided:
+            src.append(f"    for (int q = 0; q < ITEMS; ++q) {{ const i64 li_ = t0 + q; "
+                       f"{arr}[q] = (li_ < n) ? {col}[p.it{k}_start + li_ * p.it{k}_stride] : ({st})0; }}")
+        else:
+            src.append(f"    if (full) wg_load_contig<{st}, {cnt}>({col} + t0 * {per}, {arr});")
+            src.append(f"    else {{ for (int q = 0; q < {cnt}; ++q) {{ const i64 e_ = t0 * {per} + q; "
+                       f"{arr}[q] = (e_ < n * {per}) ? {col}[e_] : ({st})0; }} }}")
+    for b in g.bspecs:
+        if b.mode == "direct" and b.extra.get("buffered"):
+            for f, kk in enumerate(b.extra["kinds"]):
+                src.append(f"    alignas(16) {STYPE[kk]} o{b.bid}_{f}[ITEMS * {b.k}];")
+        if b.mode == "scan":
+            src.append(f"    i64 cnt{b.bid} = 0;")
+    src.append("#pragma unroll")
+    src.append("    for (int j = 0; j < ITEMS; ++j) {")
+    src.append("      const i64 li = t0 + j;")
+    src.append("      if (li < n) {")
+    src.append("        const i64 i = p.idx0 + li;")
+    src.extend(body_a)
+    src.append("      }")
+    src.append("    }")
+    for b in g.bspecs:
+        if b.mode == "direct" and b.extra.get("buffered"):
+            for f, kk in enumerate(b.extra["kinds"]):
+                col = f"p.a{b.bid}_{f}"
+                src.append(f"    if (full) wg_store_contig<{STYPE[kk]}, ITEMS * {b.k}>({col} + t0 * {b.k}, o{b.bid}_{f});")
+                src.append(f"    else {{ for (int q = 0; q < ITEMS * {b.k}; ++q) if (t0 * {b.k} + q < n * {b.k}) "
+                           f"{col}[t0 * {b.k} + q] = o{b.bid}_{f}[q]; }}")
+    if scan_bs:
+        for si, b in enumerate(scan_bs):
+            src.append(f"    i64 agg{b.bid};")
+            src.append(f"    i64 wpos{b.bid} = wg_block_exclusive_scan(cnt{b.bid}, s_scan, &agg{b.bid});")
+            src.append("    if (threadIdx.x < 32) {")
+            src.append(f"      const i64 pre_ = wg_lookback(p.a{b.bid}_status, tile, agg{b.bid});")
+            src.append(f"      if (threadIdx.x == 0) {{ s_toff[{si}] = pre_; if (tile == ntiles - 1) *p.a{b.bid}_total = pre_ + agg{b.bid}; }}")
+            src.append("    }")
+        src.append("    __syncthreads();")
+        for si, b in enumerate(scan_bs):
+            src.append(f"    wpos{b.bid} += s_toff[{si}];")
+        src.append("#pragma unroll")
+        src.append("    for (int j = 0; j < ITEMS; ++j) {")
+        src.append("      const i64 li = t0 + j;")
+        src.append("      if (li < n) {")
+        src.append("        const i64 i = p.idx0 + li;")
+        src.extend(body_b)
+        src.append("      }")
+        src.append("    }")
+    src.append("  }")
+    # epilogue: shared-memory flushes
+    if smem_flush:
+        src.append("  __syncthreads();")
+        src.extend("  " + fl for fl in smem_flush)
+    # epilogue: mergers
+    if merger_bs:
+        src.append("  __shared__ u64 s_red[32];")
+        src.append("  __shared__ int s_redh[32];")
+        src.append("  __shared__ int s_last;")
+        for b in merger_bs:
+            ks = leaves(b.kind.elem)
+            F = len(ks)
+            for f, kk in enumerate(ks):
+                ct = CTYPE[kk]
+                ident = c_literal(kk, internal_identity(b.kind.op, kk))
+                src.append(f"  {{ int h_ = m{b.bid}_h; wg_block_fold<{ct}, {OPSTRUCT[b.kind.op]}<{ct}>>(m{b.bid}_{f}, h_, {ident}, ({ct}*)s_red, s_redh);")
+                src.append(f"    if (threadIdx.x == 0) {{ p.m{b.bid}_part[(u64)blockIdx.x * {F + 1} + {f}] = wg_to_bits<{ct}>(m{b.bid}_{f});"
+                           f" if ({f} == 0) p.m{b.bid}_part[(u64)blockIdx.x * {F + 1} + {F}] = (u64)h_; }} }}")
+        src.append("  __threadfence();")
+        src.append("  if (threadIdx.x == 0) s_last = (atomicAdd(p.ticket, 1u) == gridDim.x - 1);")
+        src.append("  __syncthreads();")
+        src.append("  if (s_last) {")
+        src.append("    __threadfence();")
+        for b in merger_bs:
+            ks = leaves(b.kind.elem)
+            F = len(ks)
+            for f, kk in enumerate(ks):
+                ct = CTYPE[kk]
+                op = f"{OPSTRUCT[b.kind.op]}<{ct}>"
+                ident = c_literal(kk, internal_identity(b.kind.op, kk))
+                src.append(f"    {{ {ct} a_ = {ident}; int h_ = 0;")
+                src.append(f"      for (unsigned q = threadIdx.x; q < gridDim.x; q += BLOCK) {{"
+                           f" a_ = {op}::f(a_, wg_from_bits<{ct}>(__ldcg(p.m{b.bid}_part + (u64)q * {F + 1} + {f})));"
+                           f" h_ |= (int)__ldcg(p.m{b.bid}_part + (u64)q * {F + 1} + {F}); }}")
+                src.append(f"      wg_block_fold<{ct}, {op}>(a_, h_, {ident}, ({ct}*)s_red, s_redh);")
+                src.append(f"      if (threadIdx.x == 0 && h_) {{ p.m{b.bid}_slot[{f}] = wg_to_bits<{ct}>({op}::f(wg_from_bits<{ct}>(p.m{b.bid}_slot[{f}]), a_));"
+                           f" p.m{b.bid}_slot[{F}] = 1; }} }}")
+        src.append("    if (threadIdx.x == 0) *p.ticket = 0;")
+        src.append("  }")
+    src.append("}")
+    source = "\n".join(src) + "\n"
+    return KernelPlan(source=source, name=name, params=g.params, schedule=schedule, items=ITEMS, block=BLOCK,
+                      smem=dyn_smem, builders=g.bspecs, scan_bids=[b.bid for b in scan_bs],
+                      merger_bids=[b.bid for b in merger_bs])
+
+
+def _pattern_switch(pat):
+    """C expression selecting the init word for slot word index w_."""
+    expr = f"0x{pat[-1] & 0xFFFFFFFFFFFFFFFF:016x}ULL"
+    for i in range(len(pat) - 2, -1, -1):
+        expr = f"(w_ == {i} ? 0x{pat[i] & 0xFFFFFFFFFFFFFFFF:016x}ULL : {expr})"
+    return expr
+
+
+def _capture_val(g: Gen, name, ty, val):
+    """Bind a loop-invariant value from the enclosing scope as kernel params."""
+    safe = "".join(ch if ch.isalnum() else "_" for ch in name)
+
+    def go(t, v, path):
+        tag = safe + "".join(f"_{q}" for q in path)
+        if isinstance(t, Scalar):
+            ct = {BOOL: "i64", I32: "i64", I64: "i64", F32: "double", F64: "double"}[t.kind]
+            pn = g.param(f"c_{tag}", ct, ("cap", name) + tuple(path))
+            if t.kind == BOOL:
+                return S(f"({pn} != 0)", BOOL)
+            if t.kind == I32:
+                return S(f"((i32){pn})", I32)
+            if t.kind == F32:
+                return S(f"((float){pn})", F32)
+            return S(pn, t.kind)
+        if isinstance(t, Struct):
+            return T([go(f, None, path + (i,)) for i, f in enumerate(t.fields)])
+        if isinstance(t, Vec):
+            ks = leaves(t.elem)
+            cols = [g.param(f"c_{tag}_c{l}", f"const {STYPE[k]}*", ("capcol", name) + tuple(path) + (l,))
+                    for l, k in enumerate(ks)]
+            nn = g.param(f"c_{tag}_n", "i64", ("caplen", name) + tuple(path))
+            return VRef(cols, nn, t.elem)
+        if isinstance(t, Builder):
+            return None
+        raise DeviceUnsupported(f"captured value of type {t}")
+
+    return go(ty, val, ())
+
+
+# ---------------------------------------------------------------------------
+# Static lowering (no device, no data): used by build() and the CPU test
+# suite to prove every loop of a program lowers and compiles for sm_100a.
+
+
+def static_plans(expr, env_types=None, externs=()):
+    """Yield a KernelPlan per ``for`` loop in a typed program, deriving the
+    iteration, builder and capture specs from types alone."""
+    from weldmill.expr import walk, free_variables as _fv
+
+    ext = {n: None for n in externs}
+    plans = []
+    nested = set()
+    for node in walk(expr):
+        if isinstance(node, For) and isinstance(node.func, Lambda):
+            for inner in walk(node.func.body):
+                if isinstance(inner, For):
+                    nested.add(id(inner))
+    for node in walk(expr):
+        if not isinstance(node, For) or id(node) in nested or not isinstance(node.func, Lambda):
+            continue
+        iters = []
+        for it in node.iters:
+            vt = it.data.ty
+            if not isinstance(vt, Vec):
+                raise DeviceUnsupported("loop over a non-vector")
+            iters.append(IterSpec(elem=vt.elem, simd=it.simd, strided=it.start is not None,
+                                  kinds=leaves(vt.elem)))
+        counter = [0]
+
+        def mk(t):
+            if isinstance(t, Builder):
+                bid = counter[0]
+                counter[0] += 1
+                bs = BSpec(bid=bid, kind=t.kind)
+                if isinstance(t.kind, DictMerger):
+                    nw = key_layout(leaves(t.kind.key))[1]
+                    bs.extra["slot_words"] = (1 if nw == 1 else 1 + nw) + len(leaves(t.kind.value))
+                    bs.mode = "global"
+                if isinstance(t.kind, VecMerger):
+                    bs.mode = "global"
+                return bs
+            if isinstance(t, Struct):
+                return tuple(mk(f) for f in t.fields)
+            raise DeviceUnsupported(f"builders of type {t}")
+
+        bstruct = mk(node.builders.ty)
+        pnames = {p.name for p in node.func.params}
+        caps = {}
+        for name in sorted(_fv(node.func) - pnames):
+            ty = None
+            for n2 in walk(node.func.body):
+                if isinstance(n2, Ident) and n2.name == name and n2.ty is not None:
+                    ty = n2.ty
+                    break
+            if isinstance(ty, Function):
+                continue
+            caps[name] = (ty, None)
+        plans.append(generate(node, iters, bstruct, caps, ext, "local"))
+    return plans

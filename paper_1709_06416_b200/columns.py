@@ -1,0 +1,264 @@
+"""Device-resident columnar values (the buffer manager's view of IR vectors).
+
+A ``vec[T]`` lives in HBM as structure-of-arrays: one contiguous column per
+scalar leaf of T (bool as one byte), so a zipped loop ``for({a, b, c}, ...)``
+and an AoS ``vec[{..}]`` read the same way.  Nested ``vec[vec[T]]`` (group
+results, vec-of-vec maps) carry an offsets column (n+1 i64) over a child
+layout.  The wire format of the reference (``boundary.py:1-12``: i64 count +
+packed little-endian elements, structs without padding) converts to and from
+this layout with numpy, without Python-object round trips.
+"""
+from __future__ import annotations
+
+import ctypes
+import struct as _struct
+
+import numpy as np
+
+from . import runtime as rt
+from .irtypes import (BOOL, F32, F64, I32, I64, NPTYPE, SIZE, DeviceUnsupported, Scalar, Struct, Vec, leaves)
+
+
+class Col:
+    """One device column: a pointer plus the buffer that owns it."""
+
+    __slots__ = ("ptr", "kind", "owner")
+
+    def __init__(self, ptr, kind, owner):
+        self.ptr = ptr
+        self.kind = kind
+        self.owner = owner
+
+    @classmethod
+    def alloc(cls, kind, n):
+        buf = rt.alloc(max(n, 1) * SIZE[kind])
+        return cls(buf.ptr, kind, buf)
+
+    def offset(self, k):
+        """A view starting k elements in."""
+        return Col(self.ptr + k * SIZE[self.kind], self.kind, self.owner)
+
+
+class ListLayout:
+    """Layout of a Vec-typed field: offsets (n+1, i64) over a child layout."""
+
+    __slots__ = ("offsets", "child", "total")
+
+    def __init__(self, offsets: Col, child, total: int):
+        self.offsets = offsets
+        self.child = child
+        self.total = total
+
+
+class DVec:
+    """A device vector: IR type vec[elem], length n, layout tree."""
+
+    __slots__ = ("elem", "n", "layout", "host_cache")
+
+    def __init__(self, elem, n, layout):
+        self.elem = elem
+        self.n = int(n)
+        self.layout = layout
+        self.host_cache = None
+
+    @property
+    def cols(self):
+        """Flat leaf columns (only for flat element types)."""
+        out = []
+
+        def go(t, lay):
+            if isinstance(t, Scalar):
+                out.append(lay)
+            elif isinstance(t, Struct):
+                for ft, fl in zip(t.fields, lay):
+                    go(ft, fl)
+            else:
+                raise DeviceUnsupported(f"element type {self.elem} is not flat")
+
+        go(self.elem, self.layout)
+        return out
+
+    def __len__(self):
+        return self.n
+
+    def __repr__(self):
+        return f"<DVec vec[{self.elem}] n={self.n}>"
+
+
+def layout_from_cols(elem, cols):
+    it = iter(cols)
+
+    def go(t):
+        if isinstance(t, Scalar):
+            return next(it)
+        if isinstance(t, Struct):
+            return tuple(go(f) for f in t.fields)
+        raise DeviceUnsupported(f"cannot build a flat layout for {t}")
+
+    return go(elem)
+
+
+def dvec_from_cols(elem, n, cols):
+    return DVec(elem, n, layout_from_cols(elem, cols))
+
+
+# ---------------------------------------------------------------------------
+# host -> device
+
+
+def _np_upload(arr: np.ndarray, kind) -> Col:
+    arr = np.ascontiguousarray(arr, dtype=np.dtype(NPTYPE[kind]))
+    col = Col.alloc(kind, arr.shape[0])
+    if arr.nbytes:
+        rt.h2d(col.ptr, arr.ctypes.data, arr.nbytes)
+    return col
+
+
+def _leaf_arrays_from_payload(elem, payload):
+    """Python payload (list of scalars / tuples) -> list of numpy leaf arrays."""
+    ks = leaves(elem)
+    n = len(payload)
+    if isinstance(elem, Scalar):
+        if n == 0:
+            return [np.zeros(0, dtype=NPTYPE[elem.kind])]
+        return [np.asarray(payload, dtype=NPTYPE[elem.kind])]
+    if n == 0:
+        return [np.zeros(0, dtype=NPTYPE[k]) for k in ks]
+    flat_rows = payload
+    if any(isinstance(f, Struct) for f in elem.fields):
+        from .irtypes import flatten_value
+        flat_rows = [flatten_value(elem, r) for r in payload]
+    cols = list(zip(*flat_rows))
+    return [np.asarray(c, dtype=NPTYPE[k]) for c, k in zip(cols, ks)]
+
+
+def to_device(ty, payload) -> DVec:
+    """Bind a host vector payload of IR type ``ty`` (a Vec) to the device.
+
+    Accepts the reference's payload (a list of scalars or tuples), a numpy
+    array (scalar elements, or a structured array), a tuple/list of numpy
+    arrays (SoA, one per leaf), boundary bytes, or an existing DVec.
+    """
+    if isinstance(payload, DVec):
+        return payload
+    if not isinstance(ty, Vec):
+        raise DeviceUnsupported(f"cannot bind {ty} as a device vector")
+    elem = ty.elem
+    if isinstance(elem, Vec) or (isinstance(elem, Struct) and any(isinstance(f, Vec) for f in elem.fields)):
+        return _nested_to_device(elem, payload)
+    ks = leaves(elem)
+    if isinstance(payload, (bytes, bytearray, memoryview)):
+        arrs = boundary_to_arrays(elem, bytes(payload))
+    elif isinstance(payload, np.ndarray):
+        if payload.dtype.names:
+            arrs = [payload[nm] for nm in payload.dtype.names]
+        else:
+            arrs = [payload]
+    elif isinstance(payload, tuple) and payload and all(isinstance(a, np.ndarray) for a in payload):
+        arrs = list(payload)
+    else:
+        arrs = _leaf_arrays_from_payload(elem, payload)
+    if len(arrs) != len(ks):
+        raise DeviceUnsupported(f"payload has {len(arrs)} columns, type {elem} needs {len(ks)}")
+    n = int(arrs[0].shape[0]) if arrs else 0
+    cols = [_np_upload(a, k) for a, k in zip(arrs, ks)]
+    return dvec_from_cols(elem, n, cols)
+
+
+def _nested_to_device(elem, payload):
+    if isinstance(payload, (bytes, bytearray, memoryview)):
+        from weldmill.boundary import decode_value
+        payload = decode_value(bytes(payload), Vec(elem))
+
+    def build(t, items):
+        if isinstance(t, Scalar):
+            return _np_upload(np.asarray(items if items else [], dtype=NPTYPE[t.kind]), t.kind)
+        if isinstance(t, Struct):
+            cols = list(zip(*items)) if items else [[] for _ in t.fields]
+            return tuple(build(ft, list(c)) for ft, c in zip(t.fields, cols))
+        if isinstance(t, Vec):
+            offs = np.zeros(len(items) + 1, dtype=np.int64)
+            flat = []
+            for j, it in enumerate(items):
+                offs[j + 1] = offs[j] + len(it)
+                flat.extend(it)
+            return ListLayout(_np_upload(offs, I64), build(t.elem, flat), int(offs[-1]))
+        raise DeviceUnsupported(f"cannot bind {t}")
+
+    items = list(payload)
+    return DVec(elem, len(items), build(elem, items))
+
+
+# ---------------------------------------------------------------------------
+# device -> host
+
+
+def col_to_numpy(col: Col, n: int) -> np.ndarray:
+    arr = np.empty(n, dtype=np.dtype(NPTYPE[col.kind]))
+    if n:
+        rt.d2h(arr.ctypes.data, col.ptr, arr.nbytes)
+    return arr
+
+
+def to_numpy(v: DVec):
+    """Flat vector -> numpy (scalar elem) or tuple of leaf arrays."""
+    arrs = [col_to_numpy(c, v.n) for c in v.cols]
+    if isinstance(v.elem, Scalar):
+        return arrs[0]
+    return tuple(arrs)
+
+
+def _layout_to_payload(t, lay, n):
+    if isinstance(t, Scalar):
+        a = col_to_numpy(lay, n)
+        if t.kind == BOOL:
+            return [bool(x) for x in a]
+        return a.tolist()
+    if isinstance(t, Struct):
+        parts = [_layout_to_payload(ft, fl, n) for ft, fl in zip(t.fields, lay)]
+        return list(zip(*parts)) if n else []
+    if isinstance(t, Vec):
+        offs = col_to_numpy(lay.offsets, n + 1)
+        flat = _layout_to_payload(t.elem, lay.child, int(offs[-1]) if n + 1 else 0)
+        return [flat[offs[j]:offs[j + 1]] for j in range(n)]
+    raise DeviceUnsupported(f"cannot read back {t}")
+
+
+def to_payload(v: DVec):
+    """The reference's payload form: a list of scalars / tuples / lists."""
+    if v.host_cache is None:
+        v.host_cache = _layout_to_payload(v.elem, v.layout, v.n)
+    return v.host_cache
+
+
+# ---------------------------------------------------------------------------
+# boundary bytes (boundary.py:59-141) for flat element types
+
+
+def _packed_dtype(elem):
+    ks = leaves(elem)
+    return np.dtype({"names": [f"f{i}" for i in range(len(ks))],
+                     "formats": [NPTYPE[k] for k in ks],
+                     "offsets": list(np.cumsum([0] + [SIZE[k] for k in ks])[:-1]),
+                     "itemsize": sum(SIZE[k] for k in ks)})
+
+
+def boundary_to_arrays(elem, data: bytes):
+    (count,) = _struct.unpack_from("<q", data, 0)
+    dt = _packed_dtype(elem)
+    rec = np.frombuffer(data, dtype=dt, count=count, offset=8)
+    return [np.ascontiguousarray(rec[nm]) for nm in dt.names]
+
+
+def to_boundary_bytes(v: DVec) -> bytes:
+    if not all(isinstance(c, Col) for c in v.cols):
+        raise DeviceUnsupported("nested vectors use the generic encoder")
+    dt = _packed_dtype(v.elem)
+    rec = np.empty(v.n, dtype=dt)
+    for nm, c in zip(dt.names, v.cols):
+        rec[nm] = col_to_numpy(c, v.n)
+    return _struct.pack("<q", v.n) + rec.tobytes()
+
+
+__all__ = ["Col", "DVec", "ListLayout", "to_device", "to_numpy", "to_payload", "to_boundary_bytes",
+           "dvec_from_cols", "col_to_numpy", "boundary_to_arrays", "ctypes"]

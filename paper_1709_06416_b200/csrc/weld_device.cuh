@@ -1,0 +1,540 @@
+// weld_device.cuh -- device-side building blocks for NVRTC-generated loop kernels.
+//
+// Every generated kernel (paper_1709_06416_b200/codegen.py) is this header plus
+// one fused loop body.  The header carries:
+//   * the reference's exact scalar semantics (wrapping ints, truncating
+//     division with a DivideByZero error word, NaN-aware min/max, wrapping
+//     float->int casts, per-op f32 rounding via -fmad=false);
+//   * merge folds and their *internal* identities (see wg_ident_*);
+//   * block reductions for merger partials, the single-pass decoupled
+//     look-back tile scan for order-preserving appenders, and the
+//     open-addressing hash table for dictmerger.
+//
+// Reference semantics cited against /root/reference/pkg/src/weldmill:
+//   ints wrap              engine/run.py:395-437
+//   float ops              engine/run.py:440-464
+//   casts                  engine/run.py:503-528
+//   merge folds            engine/builders.py:121-174
+//   identities             types.py:185-192
+// This file is compiled at run time by NVRTC for sm_100a (no host code here).
+#pragma once
+
+typedef long long i64;
+typedef unsigned long long u64;
+typedef int i32;
+typedef unsigned int u32;
+typedef unsigned char u8;
+
+#define WG_INF __longlong_as_double(0x7ff0000000000000LL)
+#define WG_NAN __longlong_as_double(0x7ff8000000000000LL)
+#define WG_INFF __int_as_float(0x7f800000)
+#define WG_NANF __int_as_float(0x7fc00000)
+
+// ---------------------------------------------------------------------------
+// Error word: first writer wins.  Layout {i64 code, i64 info}.
+enum {
+  WG_OK = 0,
+  WG_ERR_DIVZERO = 1,       // DivideByZero        run.py:411-425
+  WG_ERR_LOOKUP_OOB = 2,    // IndexOutOfBounds    run.py:693-700
+  WG_ERR_VECMERGER_OOB = 3, // IndexOutOfBounds    builders.py:413-417
+  WG_ERR_KEY_NOT_FOUND = 4, // KeyNotFound         run.py:704-710
+  WG_ERR_INTERNAL = 5,
+  WG_ERR_REMZERO = 6,       // DivideByZero (remainder)
+};
+
+__device__ __forceinline__ void wg_raise(i64* err, i64 code, i64 info) {
+  if (atomicCAS((u64*)err, 0ULL, (u64)code) == 0ULL) {
+    ((volatile i64*)err)[1] = info;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Integer arithmetic: wraps at the width (computed unsigned, no UB).
+__device__ __forceinline__ i64 wg_add_i64(i64 a, i64 b) { return (i64)((u64)a + (u64)b); }
+__device__ __forceinline__ i64 wg_sub_i64(i64 a, i64 b) { return (i64)((u64)a - (u64)b); }
+__device__ __forceinline__ i64 wg_mul_i64(i64 a, i64 b) { return (i64)((u64)a * (u64)b); }
+__device__ __forceinline__ i64 wg_neg_i64(i64 a) { return (i64)(0ULL - (u64)a); }
+__device__ __forceinline__ i32 wg_add_i32(i32 a, i32 b) { return (i32)((u32)a + (u32)b); }
+__device__ __forceinline__ i32 wg_sub_i32(i32 a, i32 b) { return (i32)((u32)a - (u32)b); }
+__device__ __forceinline__ i32 wg_mul_i32(i32 a, i32 b) { return (i32)((u32)a * (u32)b); }
+__device__ __forceinline__ i32 wg_neg_i32(i32 a) { return (i32)(0U - (u32)a); }
+
+// Truncating division / remainder; a zero divisor raises DivideByZero and
+// yields 0 (the host raises after the launch).  MIN / -1 wraps like the
+// reference's arbitrary-precision quotient followed by wrap().
+__device__ __forceinline__ i64 wg_div_i64(i64 a, i64 b, i64* err) {
+  if (b == 0) { wg_raise(err, WG_ERR_DIVZERO, 0); return 0; }
+  if (b == -1) return wg_neg_i64(a);
+  return a / b;
+}
+__device__ __forceinline__ i64 wg_rem_i64(i64 a, i64 b, i64* err) {
+  if (b == 0) { wg_raise(err, WG_ERR_REMZERO, 0); return 0; }
+  if (b == -1) return 0;
+  return a % b;
+}
+__device__ __forceinline__ i32 wg_div_i32(i32 a, i32 b, i64* err) {
+  if (b == 0) { wg_raise(err, WG_ERR_DIVZERO, 0); return 0; }
+  if (b == -1) return wg_neg_i32(a);
+  return a / b;
+}
+__device__ __forceinline__ i32 wg_rem_i32(i32 a, i32 b, i64* err) {
+  if (b == 0) { wg_raise(err, WG_ERR_REMZERO, 0); return 0; }
+  if (b == -1) return 0;
+  return a % b;
+}
+
+// ---------------------------------------------------------------------------
+// Float semantics.  min prefers a number over NaN; max propagates NaN
+// (builders.py:133-152).  -0.0 vs 0.0 follow the reference's `<=`/`>=`.
+__device__ __forceinline__ double wg_min_f64(double a, double b) {
+  if (a != a) return b;
+  if (b != b) return a;
+  return a <= b ? a : b;
+}
+__device__ __forceinline__ double wg_max_f64(double a, double b) {
+  if (a != a) return a;
+  if (b != b) return b;
+  return a >= b ? a : b;
+}
+__device__ __forceinline__ float wg_min_f32(float a, float b) {
+  if (a != a) return b;
+  if (b != b) return a;
+  return a <= b ? a : b;
+}
+__device__ __forceinline__ float wg_max_f32(float a, float b) {
+  if (a != a) return a;
+  if (b != b) return b;
+  return a >= b ? a : b;
+}
+// Binary-op min/max on ints: `b if b < a else a` (run.py:435-436).
+__device__ __forceinline__ i64 wg_min_i64(i64 a, i64 b) { return b < a ? b : a; }
+__device__ __forceinline__ i64 wg_max_i64(i64 a, i64 b) { return b > a ? b : a; }
+__device__ __forceinline__ i32 wg_min_i32(i32 a, i32 b) { return b < a ? b : a; }
+__device__ __forceinline__ i32 wg_max_i32(i32 a, i32 b) { return b > a ? b : a; }
+
+// Float remainder: NaN for a zero divisor, NaN operands, or infinite a;
+// otherwise C fmod (exact, so no f32 re-rounding is needed).
+__device__ __forceinline__ double wg_rem_f64(double a, double b) {
+  if (b == 0.0 || a != a || b != b || isinf(a)) return WG_NAN;
+  return fmod(a, b);
+}
+__device__ __forceinline__ float wg_rem_f32(float a, float b) {
+  if (b == 0.0f || a != a || b != b || isinf(a)) return WG_NANF;
+  return (float)fmod((double)a, (double)b);
+}
+
+// ---------------------------------------------------------------------------
+// Casts (run.py:503-528).  float->int: NaN -> 0, +-inf saturate, finite
+// values truncate then wrap modulo 2^width (CUDA's cvt saturates instead).
+__device__ __forceinline__ i64 wg_f64_to_i64(double v) {
+  if (v != v) return 0;
+  if (v == WG_INF) return 0x7fffffffffffffffLL;
+  if (v == -WG_INF) return (i64)0x8000000000000000ULL;
+  double t = trunc(v);
+  if (t >= -9223372036854775808.0 && t < 9223372036854775808.0) return (i64)t;
+  // |t| >= 2^63: t is a multiple of 2^11, so fmod and the shift are exact.
+  double r = fmod(t, 18446744073709551616.0);
+  if (r < 0) r += 18446744073709551616.0;
+  return (i64)(u64)r;
+}
+__device__ __forceinline__ i32 wg_f64_to_i32(double v) {
+  if (v != v) return 0;
+  if (v == WG_INF) return 0x7fffffff;
+  if (v == -WG_INF) return (i32)0x80000000U;
+  double t = trunc(v);
+  if (t >= -9223372036854775808.0 && t < 9223372036854775808.0) return (i32)(u32)(u64)(i64)t;
+  double r = fmod(t, 4294967296.0);
+  return (i32)(u32)(u64)(i64)r;
+}
+__device__ __forceinline__ i64 wg_f32_to_i64(float v) { return wg_f64_to_i64((double)v); }
+__device__ __forceinline__ i32 wg_f32_to_i32(float v) { return wg_f64_to_i32((double)v); }
+// int -> f32 goes through f64 first, like f32_round(float(v)) (types.py:177).
+__device__ __forceinline__ float wg_i64_to_f32(i64 v) { return (float)(double)v; }
+
+// ---------------------------------------------------------------------------
+// Merge folds.  A fold starts from an *internal* identity that is an exact
+// no-op for every input, so a slot can be pre-initialised:
+//   f +   : -0.0   (-0.0 + x == x for all x, including +-0.0)
+//   f *   : 1.0
+//   f min : NaN    (wg_min_f64 prefers the other side)
+//   f max : -inf
+//   int   : 0, 1, MAX, MIN
+// The reference starts from the first merged value (builders.py:304-306) and
+// yields identity_value (types.py:185-192) for an empty merger; a per-slot
+// "merged" flag restores that at finalisation.
+template <typename T> struct WgAdd { static __device__ __forceinline__ T f(T a, T b) { return a + b; } };
+template <> struct WgAdd<i64> { static __device__ __forceinline__ i64 f(i64 a, i64 b) { return wg_add_i64(a, b); } };
+template <> struct WgAdd<i32> { static __device__ __forceinline__ i32 f(i32 a, i32 b) { return wg_add_i32(a, b); } };
+template <typename T> struct WgMul { static __device__ __forceinline__ T f(T a, T b) { return a * b; } };
+template <> struct WgMul<i64> { static __device__ __forceinline__ i64 f(i64 a, i64 b) { return wg_mul_i64(a, b); } };
+template <> struct WgMul<i32> { static __device__ __forceinline__ i32 f(i32 a, i32 b) { return wg_mul_i32(a, b); } };
+template <typename T> struct WgMin { static __device__ __forceinline__ T f(T a, T b) { return a <= b ? a : b; } };
+template <> struct WgMin<double> { static __device__ __forceinline__ double f(double a, double b) { return wg_min_f64(a, b); } };
+template <> struct WgMin<float> { static __device__ __forceinline__ float f(float a, float b) { return wg_min_f32(a, b); } };
+template <typename T> struct WgMax { static __device__ __forceinline__ T f(T a, T b) { return a >= b ? a : b; } };
+template <> struct WgMax<double> { static __device__ __forceinline__ double f(double a, double b) { return wg_max_f64(a, b); } };
+template <> struct WgMax<float> { static __device__ __forceinline__ float f(float a, float b) { return wg_max_f32(a, b); } };
+
+// ---------------------------------------------------------------------------
+// 64-bit value punning for partial/slot storage (every slot field is 8 bytes).
+template <typename T> __device__ __forceinline__ u64 wg_to_bits(T v);
+template <> __device__ __forceinline__ u64 wg_to_bits<double>(double v) { return (u64)__double_as_longlong(v); }
+template <> __device__ __forceinline__ u64 wg_to_bits<float>(float v) { return (u64)(u32)__float_as_int(v); }
+template <> __device__ __forceinline__ u64 wg_to_bits<i64>(i64 v) { return (u64)v; }
+template <> __device__ __forceinline__ u64 wg_to_bits<i32>(i32 v) { return (u64)(u32)v; }
+template <> __device__ __forceinline__ u64 wg_to_bits<bool>(bool v) { return v ? 1ULL : 0ULL; }
+template <typename T> __device__ __forceinline__ T wg_from_bits(u64 b);
+template <> __device__ __forceinline__ double wg_from_bits<double>(u64 b) { return __longlong_as_double((i64)b); }
+template <> __device__ __forceinline__ float wg_from_bits<float>(u64 b) { return __int_as_float((int)(u32)b); }
+template <> __device__ __forceinline__ i64 wg_from_bits<i64>(u64 b) { return (i64)b; }
+template <> __device__ __forceinline__ i32 wg_from_bits<i32>(u64 b) { return (i32)(u32)b; }
+template <> __device__ __forceinline__ bool wg_from_bits<bool>(u64 b) { return b != 0; }
+
+// ---------------------------------------------------------------------------
+// Block-wide fold of one value (plus the merged flag) in a fixed tree
+// order; result valid in thread 0.  Lanes without data hold `ident`, the
+// fold's internal identity, so padding is an exact no-op.  smem >= 32.
+template <typename T, typename OP>
+__device__ __forceinline__ void wg_block_fold(T& v, int& has, T ident, T* smem_v, int* smem_h) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    T o = __shfl_down_sync(0xffffffffu, v, d);
+    int oh = __shfl_down_sync(0xffffffffu, has, d);
+    v = OP::f(v, o);
+    has |= oh;
+  }
+  __syncthreads();
+  if (lane == 0) { smem_v[warp] = v; smem_h[warp] = has; }
+  __syncthreads();
+  if (warp == 0) {
+    v = (lane < nw) ? smem_v[lane] : ident;
+    has = (lane < nw) ? smem_h[lane] : 0;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      T o = __shfl_down_sync(0xffffffffu, v, d);
+      int oh = __shfl_down_sync(0xffffffffu, has, d);
+      v = OP::f(v, o);
+      has |= oh;
+    }
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Block-wide exclusive scan of one i64 count per thread.  Returns the
+// exclusive prefix; *total receives the block aggregate (all threads).
+__device__ __forceinline__ i64 wg_block_exclusive_scan(i64 x, i64* smem /* >= 33 */, i64* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  i64 incl = x;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    i64 o = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += o;
+  }
+  __syncthreads();
+  if (lane == 31) smem[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    i64 w = (lane < nw) ? smem[lane] : 0;
+    i64 wi = w;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      i64 o = __shfl_up_sync(0xffffffffu, wi, d);
+      if (lane >= d) wi += o;
+    }
+    if (lane < nw) smem[lane] = wi - w;  // exclusive warp offsets
+    if (lane == nw - 1) smem[32] = wi;
+  }
+  __syncthreads();
+  *total = smem[32];
+  return smem[warp] + incl - x;
+}
+
+// ---------------------------------------------------------------------------
+// Single-pass decoupled look-back (Merrill & Garland).  status[t] packs a
+// 2-bit flag over a 62-bit count: 0 = not ready, 1 = aggregate, 2 = prefix.
+// Tiles are claimed in launch order through an atomic counter, so every
+// predecessor of a tile is held by a running block: spinning is safe.
+#define WG_ST_AGG (1ULL << 62)
+#define WG_ST_PRE (2ULL << 62)
+#define WG_ST_MASK ((1ULL << 62) - 1)
+
+__device__ __forceinline__ u64 wg_ld_volatile(const u64* p) {
+  u64 v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void wg_st_volatile(u64* p, u64 v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Called by warp 0 only.  Returns the exclusive prefix of `tile`.
+__device__ __forceinline__ i64 wg_lookback(u64* status, i64 tile, i64 aggregate) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) wg_st_volatile(status, WG_ST_PRE | (u64)aggregate);
+    return 0;
+  }
+  if (lane == 0) wg_st_volatile(status + tile, WG_ST_AGG | (u64)aggregate);
+  i64 excl = 0;
+  i64 t = tile - 1;
+  while (true) {
+    i64 idx = t - lane;
+    u64 s = (idx >= 0) ? wg_ld_volatile(status + idx) : WG_ST_PRE;
+    u64 flag = s >> 62;
+    unsigned mx = __ballot_sync(0xffffffffu, flag == 0);
+    unsigned mp = __ballot_sync(0xffffffffu, flag == 2);
+    unsigned upto;
+    if (mp) {
+      int first = __ffs(mp) - 1;
+      upto = (first == 31) ? 0xffffffffu : ((2u << first) - 1u);
+    } else {
+      upto = 0xffffffffu;
+    }
+    if (mx & upto) continue;  // a needed predecessor has not published yet
+    i64 val = ((1u << lane) & upto) ? (i64)(s & WG_ST_MASK) : 0;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) val += __shfl_xor_sync(0xffffffffu, val, d);
+    excl += val;
+    if (mp) break;
+    t -= 32;
+  }
+  if (lane == 0) wg_st_volatile(status + tile, WG_ST_PRE | (u64)(excl + aggregate));
+  return excl;
+}
+
+// ---------------------------------------------------------------------------
+// Atomic folds into 8-byte slots (dictmerger values, vecmerger bins).
+template <typename T> __device__ __forceinline__ void wg_atomic_add(T* p, T v);
+template <> __device__ __forceinline__ void wg_atomic_add<double>(double* p, double v) { atomicAdd(p, v); }
+template <> __device__ __forceinline__ void wg_atomic_add<float>(float* p, float v) { atomicAdd(p, v); }
+template <> __device__ __forceinline__ void wg_atomic_add<i64>(i64* p, i64 v) { atomicAdd((u64*)p, (u64)v); }
+template <> __device__ __forceinline__ void wg_atomic_add<i32>(i32* p, i32 v) { atomicAdd(p, v); }
+
+template <typename T, typename OP>
+__device__ __forceinline__ void wg_atomic_cas_fold(T* p, T v);
+template <typename OP>
+__device__ __forceinline__ void wg_atomic_cas_fold_f64(double* p, double v) {
+  u64* a = (u64*)p;
+  u64 old = *(volatile u64*)a, assumed;
+  do {
+    assumed = old;
+    double nv = OP::f(__longlong_as_double((i64)assumed), v);
+    u64 nb = (u64)__double_as_longlong(nv);
+    if (nb == assumed) return;
+    old = atomicCAS(a, assumed, nb);
+  } while (old != assumed);
+}
+template <typename OP>
+__device__ __forceinline__ void wg_atomic_cas_fold_f32(float* p, float v) {
+  u32* a = (u32*)p;
+  u32 old = *(volatile u32*)a, assumed;
+  do {
+    assumed = old;
+    float nv = OP::f(__int_as_float((int)assumed), v);
+    u32 nb = (u32)__float_as_int(nv);
+    if (nb == assumed) return;
+    old = atomicCAS(a, assumed, nb);
+  } while (old != assumed);
+}
+template <typename OP>
+__device__ __forceinline__ void wg_atomic_cas_fold_i64(i64* p, i64 v) {
+  u64* a = (u64*)p;
+  u64 old = *(volatile u64*)a, assumed;
+  do {
+    assumed = old;
+    u64 nb = (u64)OP::f((i64)assumed, v);
+    if (nb == assumed) return;
+    old = atomicCAS(a, assumed, nb);
+  } while (old != assumed);
+}
+template <typename OP>
+__device__ __forceinline__ void wg_atomic_cas_fold_i32(i32* p, i32 v) {
+  u32* a = (u32*)p;
+  u32 old = *(volatile u32*)a, assumed;
+  do {
+    assumed = old;
+    u32 nb = (u32)OP::f((i32)assumed, v);
+    if (nb == assumed) return;
+    old = atomicCAS(a, assumed, nb);
+  } while (old != assumed);
+}
+
+// op codes: 0 '+', 1 '*', 2 min, 3 max
+template <int OPC, typename T> struct WgAtomicFold;
+template <typename T> struct WgAtomicFold<0, T> { static __device__ __forceinline__ void f(T* p, T v) { wg_atomic_add<T>(p, v); } };
+template <> struct WgAtomicFold<1, double> { static __device__ __forceinline__ void f(double* p, double v) { wg_atomic_cas_fold_f64<WgMul<double>>(p, v); } };
+template <> struct WgAtomicFold<1, float> { static __device__ __forceinline__ void f(float* p, float v) { wg_atomic_cas_fold_f32<WgMul<float>>(p, v); } };
+template <> struct WgAtomicFold<1, i64> { static __device__ __forceinline__ void f(i64* p, i64 v) { wg_atomic_cas_fold_i64<WgMul<i64>>(p, v); } };
+template <> struct WgAtomicFold<1, i32> { static __device__ __forceinline__ void f(i32* p, i32 v) { wg_atomic_cas_fold_i32<WgMul<i32>>(p, v); } };
+template <> struct WgAtomicFold<2, double> { static __device__ __forceinline__ void f(double* p, double v) { wg_atomic_cas_fold_f64<WgMin<double>>(p, v); } };
+template <> struct WgAtomicFold<2, float> { static __device__ __forceinline__ void f(float* p, float v) { wg_atomic_cas_fold_f32<WgMin<float>>(p, v); } };
+template <> struct WgAtomicFold<2, i64> { static __device__ __forceinline__ void f(i64* p, i64 v) { atomicMin((long long*)p, (long long)v); } };
+template <> struct WgAtomicFold<2, i32> { static __device__ __forceinline__ void f(i32* p, i32 v) { atomicMin(p, v); } };
+template <> struct WgAtomicFold<3, double> { static __device__ __forceinline__ void f(double* p, double v) { wg_atomic_cas_fold_f64<WgMax<double>>(p, v); } };
+template <> struct WgAtomicFold<3, float> { static __device__ __forceinline__ void f(float* p, float v) { wg_atomic_cas_fold_f32<WgMax<float>>(p, v); } };
+template <> struct WgAtomicFold<3, i64> { static __device__ __forceinline__ void f(i64* p, i64 v) { atomicMax((long long*)p, (long long)v); } };
+template <> struct WgAtomicFold<3, i32> { static __device__ __forceinline__ void f(i32* p, i32 v) { atomicMax(p, v); } };
+
+// Shared-memory variants (same semantics, smem addresses).
+template <int OPC, typename T> __device__ __forceinline__ void wg_smem_fold(T* p, T v) { WgAtomicFold<OPC, T>::f(p, v); }
+
+// ---------------------------------------------------------------------------
+// Hash table for dictmerger / group ids.  Keys are packed into KW 64-bit
+// words.  KW == 1 uses the key word itself as the claim word with an EMPTY
+// sentinel; the (rare) key equal to the sentinel lives in slot `cap`.
+// Slot layout (AoS, 8-byte fields): [key words][value fields].
+#define WG_EMPTY_KEY 0xffffffffffffffffULL
+
+__device__ __forceinline__ u64 wg_mix64(u64 x) {
+  x ^= x >> 33; x *= 0xff51afd7ed558ccdULL;
+  x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ULL;
+  x ^= x >> 33;
+  return x;
+}
+
+// Insert-or-find a one-word key.  Returns the slot index, or -1 when the
+// table refuses new keys (distinct count reached `limit`): the caller
+// spills the merge to the overflow list and the host grows the table.
+__device__ __forceinline__ i64 wg_ht_find1(u64* table, int slot_words, u64 mask, u64 key,
+                                            unsigned long long* count, u64 limit) {
+  if (key == WG_EMPTY_KEY) {
+    // Dedicated overflow slot for the sentinel value.
+    u64* s = table + (mask + 1) * (u64)slot_words;
+    u64 prev = atomicCAS((unsigned long long*)s, WG_EMPTY_KEY, 0ULL);
+    if (prev == WG_EMPTY_KEY) atomicAdd(count, 1ULL);
+    return (i64)(mask + 1);
+  }
+  u64 h = wg_mix64(key) & mask;
+  while (true) {
+    u64* s = table + h * (u64)slot_words;
+    u64 cur = *(volatile u64*)s;
+    if (cur == key) return (i64)h;
+    if (cur == WG_EMPTY_KEY) {
+      // Reserve capacity before claiming so the load factor stays bounded.
+      unsigned long long c = atomicAdd(count, 1ULL);
+      if (c >= limit) { atomicAdd(count, 0xffffffffffffffffULL); return -1; }
+      u64 prev = atomicCAS((unsigned long long*)s, WG_EMPTY_KEY, key);
+      if (prev == WG_EMPTY_KEY) return (i64)h;
+      atomicAdd(count, 0xffffffffffffffffULL);
+      if (prev == key) return (i64)h;
+    }
+    h = (h + 1) & mask;
+  }
+}
+
+// Multi-word keys: word 0 of the slot is a state word (0 empty, 1 busy,
+// 2 full) followed by KW key words.
+__device__ __forceinline__ bool wg_keys_eq(const u64* a, const u64* b, int kw) {
+  for (int k = 0; k < kw; ++k) if (a[k] != b[k]) return false;
+  return true;
+}
+__device__ __forceinline__ i64 wg_ht_findN(u64* table, int slot_words, u64 mask, const u64* key, int kw,
+                                            unsigned long long* count, u64 limit) {
+  u64 hh = 0x9e3779b97f4a7c15ULL;
+  for (int k = 0; k < kw; ++k) hh = wg_mix64(hh ^ key[k]) + 0x9e3779b97f4a7c15ULL * (u64)(k + 1);
+  u64 h = hh & mask;
+  while (true) {
+    u64* s = table + h * (u64)slot_words;
+    u64 st = *(volatile u64*)s;
+    if (st == 0) {
+      unsigned long long c = atomicAdd(count, 1ULL);
+      if (c >= limit) { atomicAdd(count, 0xffffffffffffffffULL); return -1; }
+      u64 prev = atomicCAS((unsigned long long*)s, 0ULL, 1ULL);
+      if (prev == 0) {
+        for (int k = 0; k < kw; ++k) ((volatile u64*)s)[1 + k] = key[k];
+        __threadfence();
+        atomicExch((unsigned long long*)s, 2ULL);
+        return (i64)h;
+      }
+      atomicAdd(count, 0xffffffffffffffffULL);
+      st = prev;
+    }
+    while (st == 1) st = *(volatile u64*)s;  // another thread is writing the key
+    bool eq = true;
+    for (int k = 0; k < kw; ++k) if (((volatile u64*)s)[1 + k] != key[k]) { eq = false; break; }
+    if (eq) return (i64)h;
+    h = (h + 1) & mask;
+  }
+}
+
+// Canonical key words.  -0.0 and 0.0 are one dictionary key in the
+// reference (Python dict semantics); they map to the same word here.
+__device__ __forceinline__ u64 wg_key_f64(double v) { return v == 0.0 ? 0ULL : (u64)__double_as_longlong(v); }
+__device__ __forceinline__ u64 wg_key_f32(float v) { return v == 0.0f ? 0ULL : (u64)(u32)__float_as_int(v); }
+
+// ---------------------------------------------------------------------------
+// Contiguous per-thread column access (ITEMS consecutive elements): 16-byte
+// vector loads/stores when the address allows, streaming cache hints so the
+// single-use column traffic does not evict hash tables or bins from L2.
+template <typename T, int N>
+__device__ __forceinline__ void wg_load_contig(const T* __restrict__ src, T (&dst)[N]) {
+  constexpr int B = N * (int)sizeof(T);
+  const unsigned long long a = (unsigned long long)src;
+  if constexpr (B % 16 == 0) {
+    if ((a & 15) == 0) {
+#pragma unroll
+      for (int c = 0; c < B / 16; ++c) reinterpret_cast<uint4*>(&dst[0])[c] = __ldcs(reinterpret_cast<const uint4*>(src) + c);
+      return;
+    }
+  }
+  if constexpr (B % 8 == 0) {
+    if ((a & 7) == 0) {
+#pragma unroll
+      for (int c = 0; c < B / 8; ++c) reinterpret_cast<uint2*>(&dst[0])[c] = __ldcs(reinterpret_cast<const uint2*>(src) + c);
+      return;
+    }
+  }
+  if constexpr (B % 4 == 0) {
+    if ((a & 3) == 0) {
+#pragma unroll
+      for (int c = 0; c < B / 4; ++c) reinterpret_cast<unsigned*>(&dst[0])[c] = __ldcs(reinterpret_cast<const unsigned*>(src) + c);
+      return;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < N; ++q) dst[q] = src[q];
+}
+
+template <typename T, int N>
+__device__ __forceinline__ void wg_store_contig(T* __restrict__ dst, const T (&src)[N]) {
+  constexpr int B = N * (int)sizeof(T);
+  const unsigned long long a = (unsigned long long)dst;
+  if constexpr (B % 16 == 0) {
+    if ((a & 15) == 0) {
+#pragma unroll
+      for (int c = 0; c < B / 16; ++c) __stcs(reinterpret_cast<uint4*>(dst) + c, reinterpret_cast<const uint4*>(&src[0])[c]);
+      return;
+    }
+  }
+  if constexpr (B % 8 == 0) {
+    if ((a & 7) == 0) {
+#pragma unroll
+      for (int c = 0; c < B / 8; ++c) __stcs(reinterpret_cast<uint2*>(dst) + c, reinterpret_cast<const uint2*>(&src[0])[c]);
+      return;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < N; ++q) dst[q] = src[q];
+}
+
+// Per-CTA shared-memory table (privatised dictmerger level 1) for one-word
+// keys.  Bounded probing: a miss with no free slot returns -1 and the
+// caller merges straight into the global table instead.
+__device__ __forceinline__ int wg_sht_find1(u64* t, int sw, int mask, u64 key) {
+  if (key == WG_EMPTY_KEY) return -1;
+  int h = (int)(wg_mix64(key) & (u64)mask);
+#pragma unroll 1
+  for (int probe = 0; probe < 8; ++probe) {
+    u64* s = t + (u64)h * sw;
+    u64 cur = *(volatile u64*)s;
+    if (cur == key) return h;
+    if (cur == WG_EMPTY_KEY) {
+      u64 prev = atomicCAS((unsigned long long*)s, WG_EMPTY_KEY, key);
+      if (prev == WG_EMPTY_KEY || prev == key) return h;
+    }
+    h = (h + 1) & mask;
+  }
+  return -1;
+}

@@ -1,0 +1,723 @@
+// weldgpu.cu -- libweldgpu.so: the C-ABI under the Weld-IR GPU executor.
+//
+// Owns the device, one execution stream, a stream-ordered buffer pool, the
+// device error word, NVRTC compilation of generated loop kernels (sm_100a,
+// -fmad=false) and their launch, plus the fixed-function kernels every
+// builder's result() needs (table init/compaction, order-preserving key
+// transforms, stable radix sort, gathers, run heads) and the synthetic
+// column generators used by the benchmark.
+//
+// Every entry point is `extern "C"`, returns 0 on success and -1 on failure
+// with the message in wg_last_error() (thread-local).  Declarations and the
+// reference interface each one replaces are in include/weldgpu.h.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nvrtc.h>
+#include <cub/cub.cuh>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/weldgpu.h"
+
+namespace {
+
+thread_local std::string g_err;
+std::mutex g_mu;
+bool g_inited = false;
+int g_device = -1;
+cudaStream_t g_stream = nullptr;
+int g_sm_count = 0;
+int64_t* g_err_word = nullptr;      // device {code, info}
+int64_t* g_err_host = nullptr;      // pinned mirror
+uint64_t g_live = 0, g_peak = 0;    // device bytes handed out by wg_alloc
+std::mutex g_acct_mu;
+std::vector<std::pair<void*, uint64_t>> g_sizes;  // small registry for accounting
+
+int fail(const std::string& msg) {
+  g_err = msg;
+  return -1;
+}
+
+// Driver API entry points are resolved through cudart at wg_init() so the
+// library loads (for symbol checks and NVRTC compile checks) on hosts with
+// no GPU driver at all.
+typedef CUresult (*PFN_GetErrorString)(CUresult, const char**);
+typedef CUresult (*PFN_ModuleLoadData)(CUmodule*, const void*);
+typedef CUresult (*PFN_ModuleGetFunction)(CUfunction*, CUmodule, const char*);
+typedef CUresult (*PFN_LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                                     unsigned, CUstream, void**, void**);
+typedef CUresult (*PFN_Occupancy)(int*, CUfunction, int, size_t);
+typedef CUresult (*PFN_FuncSetAttribute)(CUfunction, CUfunction_attribute, int);
+PFN_GetErrorString p_cuGetErrorString = nullptr;
+PFN_ModuleLoadData p_cuModuleLoadData = nullptr;
+PFN_ModuleGetFunction p_cuModuleGetFunction = nullptr;
+PFN_LaunchKernel p_cuLaunchKernel = nullptr;
+PFN_Occupancy p_cuOccupancyMaxActiveBlocksPerMultiprocessor = nullptr;
+PFN_FuncSetAttribute p_cuFuncSetAttribute = nullptr;
+
+template <typename F>
+bool resolve(const char* name, F* out) {
+  void* fp = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &fp, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess || !fp)
+    return false;
+  *out = reinterpret_cast<F>(fp);
+  return true;
+}
+
+#define CK(x)                                                                          \
+  do {                                                                                 \
+    cudaError_t e_ = (x);                                                              \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(std::string(#x) + ": " + cudaGetErrorString(e_));                    \
+  } while (0)
+
+#define CKD(x)                                                                         \
+  do {                                                                                 \
+    CUresult r_ = (x);                                                                 \
+    if (r_ != CUDA_SUCCESS) {                                                          \
+      const char* s_ = nullptr;                                                        \
+      if (p_cuGetErrorString) p_cuGetErrorString(r_, &s_);                                                       \
+      return fail(std::string(#x) + ": " + (s_ ? s_ : "unknown driver error"));         \
+    }                                                                                  \
+  } while (0)
+
+#define CKN(x)                                                                         \
+  do {                                                                                 \
+    nvrtcResult r_ = (x);                                                              \
+    if (r_ != NVRTC_SUCCESS) return fail(std::string(#x) + ": " + nvrtcGetErrorString(r_)); \
+  } while (0)
+
+#define NEED_INIT() \
+  do { if (!g_inited) return fail("weldgpu: wg_init() has not been called"); } while (0)
+
+inline unsigned grid_for(uint64_t n, unsigned block) {
+  uint64_t g = (n + block - 1) / block;
+  uint64_t cap = (uint64_t)(g_sm_count > 0 ? g_sm_count : 148) * 16;
+  if (g > cap) g = cap;
+  if (g == 0) g = 1;
+  return (unsigned)g;
+}
+
+// ---------------------------------------------------------------------------
+// Fixed-function kernels.
+
+__global__ void k_table_init(uint64_t* table, uint64_t nslots, int slot_words, const uint64_t* pattern_dev) {
+  __shared__ uint64_t pat[64];
+  if (threadIdx.x < (unsigned)slot_words) pat[threadIdx.x] = pattern_dev[threadIdx.x];
+  __syncthreads();
+  uint64_t total = nslots * (uint64_t)slot_words;
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < total; w += (uint64_t)gridDim.x * blockDim.x)
+    table[w] = pat[w % slot_words];
+}
+
+// Compact occupied slots to SoA word arrays (order is irrelevant: results
+// are sorted by key afterwards).  mode 1: claim word is the key (EMPTY =
+// all ones); mode 2: claim word is a state word (2 = full).
+__global__ void k_table_compact(const uint64_t* table, uint64_t nslots, int slot_words, int mode,
+                                uint64_t** out_words, int nout, unsigned long long* counter) {
+  const int lane = threadIdx.x & 31;
+  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < nslots; base += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t s = base + threadIdx.x;
+    bool occ = false;
+    if (s < nslots) {
+      uint64_t w0 = table[s * slot_words];
+      occ = (mode == 1) ? (w0 != 0xffffffffffffffffULL) : (w0 == 2ULL);
+    }
+    unsigned m = __ballot_sync(0xffffffffu, occ);
+    unsigned long long wbase = 0;
+    if (lane == 0 && m) wbase = atomicAdd(counter, (unsigned long long)__popc(m));
+    wbase = __shfl_sync(0xffffffffu, wbase, 0);
+    if (occ) {
+      uint64_t dst = wbase + __popc(m & ((1u << lane) - 1u));
+      int first = (mode == 1) ? 0 : 1;
+      for (int k = 0; k < nout; ++k) out_words[k][dst] = table[s * slot_words + first + k];
+    }
+  }
+}
+
+// The sentinel-key slot (mode 1) sits at index nslots; occupied when its
+// claim word was CAS'ed from EMPTY to 0.
+__global__ void k_table_compact_sentinel(const uint64_t* table, uint64_t nslots, int slot_words,
+                                         uint64_t** out_words, int nout, unsigned long long* counter) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const uint64_t* s = table + nslots * slot_words;
+  if (s[0] == 0ULL) {
+    uint64_t dst = atomicAdd(counter, 1ULL);
+    out_words[0][dst] = 0xffffffffffffffffULL;
+    for (int k = 1; k < nout; ++k) out_words[k][dst] = s[k];
+  }
+}
+
+// Order-preserving u64 transform of a typed column (order_key,
+// builders.py:496-507): signed ints flip the sign bit; floats use the
+// IEEE total-order trick with every NaN mapped above +inf; -0.0 == 0.0.
+// kind: 0 bool(u8) 1 i32 2 i64 3 f32 4 f64 ; src elements are `kind`-typed.
+__global__ void k_order_key(const void* src, int kind, uint64_t n, const uint32_t* perm, uint64_t* dst) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t j = perm ? perm[i] : i;
+    uint64_t k;
+    switch (kind) {
+      case 0: k = ((const uint8_t*)src)[j]; break;
+      case 1: k = (uint64_t)(int64_t)((const int32_t*)src)[j] ^ 0x8000000000000000ULL; break;
+      case 2: k = (uint64_t)((const int64_t*)src)[j] ^ 0x8000000000000000ULL; break;
+      default: {
+        double v = (kind == 3) ? (double)((const float*)src)[j] : ((const double*)src)[j];
+        if (v != v) { k = 0xffffffffffffffffULL; break; }
+        if (v == 0.0) v = 0.0;
+        uint64_t b = (uint64_t)__double_as_longlong(v);
+        k = (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+        if (k == 0xffffffffffffffffULL) k = 0xfffffffffffffffeULL;  // keep NaN strictly last
+      }
+    }
+    dst[i] = k;
+  }
+}
+
+__global__ void k_iota_u32(uint32_t* dst, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = (uint32_t)i;
+}
+
+template <typename T>
+__global__ void k_gather(const T* src, const uint32_t* perm, T* dst, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = src[perm[i]];
+}
+
+// Narrow/widen an 8-byte word column into a typed column (table words to
+// i32/f32/u8 results and back).
+__global__ void k_narrow(const uint64_t* src, void* dst, int width, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t v = src[i];
+    if (width == 8) ((uint64_t*)dst)[i] = v;
+    else if (width == 4) ((uint32_t*)dst)[i] = (uint32_t)v;
+    else ((uint8_t*)dst)[i] = (uint8_t)v;
+  }
+}
+__global__ void k_widen(const void* src, uint64_t* dst, int width, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t v;
+    if (width == 8) v = ((const uint64_t*)src)[i];
+    else if (width == 4) v = ((const uint32_t*)src)[i];
+    else v = ((const uint8_t*)src)[i];
+    dst[i] = v;
+  }
+}
+
+// Segment heads over sorted multi-word keys: flag[i] = (i == 0) || key(i) != key(i-1).
+__global__ void k_heads(const uint64_t* const* words, int kw, uint64_t n, uint8_t* flags) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    bool h = (i == 0);
+    if (!h) for (int k = 0; k < kw; ++k) if (words[k][i] != words[k][i - 1]) { h = true; break; }
+    flags[i] = h ? 1 : 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Counter-based synthetic columns: h = splitmix64(seed ^
+// (col << 56) ^ row); u = (h >> 11) * 2^-53; ints = lo + h mod span.
+__device__ __forceinline__ uint64_t sm64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+// dist: 0 int uniform [lo, lo+span) ; 1 float lo + u*(hi-lo) ; 2 float (lo + h mod span) / div
+//       3 key scatter: sm64(lo + h mod span) as i64 (distinct keys spread over i64)
+//       4 categorical over up to 8 (value, cumulative-probability) pairs (for Q1 flags)
+struct GenSpec {
+  int dist; int width; uint64_t seed; uint64_t col; int64_t lo; uint64_t span; double flo, fhi, div;
+  double cum[8]; int64_t vals[8]; int ncat;
+};
+__global__ void k_gen(void* dst, uint64_t n, uint64_t row0, GenSpec g) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t h = sm64(g.seed ^ (g.col << 56) ^ (row0 + i));
+    double u = (double)(h >> 11) * (1.0 / 9007199254740992.0);
+    if (g.dist == 0 || g.dist == 3 || g.dist == 4) {
+      int64_t v;
+      if (g.dist == 0) v = g.lo + (int64_t)(h % g.span);
+      else if (g.dist == 3) v = (int64_t)sm64((uint64_t)(g.lo + (int64_t)(h % g.span)));
+      else {
+        v = g.vals[g.ncat - 1];
+        for (int c = 0; c < g.ncat; ++c) if (u < g.cum[c]) { v = g.vals[c]; break; }
+      }
+      if (g.width == 8) ((int64_t*)dst)[i] = v; else ((int32_t*)dst)[i] = (int32_t)v;
+    } else {
+      // explicit round-to-nearest ops: no FMA contraction, so numpy reproduces it bit for bit
+      double v = (g.dist == 1) ? __dadd_rn(g.flo, __dmul_rn(u, __dsub_rn(g.fhi, g.flo)))
+                               : __ddiv_rn((double)(g.lo + (int64_t)(h % g.span)), g.div);
+      if (g.width == 8) ((double*)dst)[i] = v; else ((float*)dst)[i] = (float)v;
+    }
+  }
+}
+
+// Multiply a float column elementwise by another in place (k = s * U(0.9, 1.1)).
+__global__ void k_mul_inplace(double* a, const double* b, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    a[i] = __dmul_rn(a[i], b[i]);
+}
+
+__global__ void k_flush(uint4* buf, uint64_t n16, uint32_t salt) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n16; i += (uint64_t)gridDim.x * blockDim.x)
+    buf[i] = make_uint4((uint32_t)i, salt, (uint32_t)(i >> 32), salt ^ 0x5a5a5a5a);
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* wg_last_error(void) { return g_err.c_str(); }
+
+int wg_version(void) { return 1; }
+
+int wg_device_count(int* n) {
+  CK(cudaGetDeviceCount(n));
+  return 0;
+}
+
+int wg_init(int device) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_inited) {
+    if (device == g_device) return 0;
+    return fail("weldgpu: already initialised on a different device");
+  }
+  CK(cudaSetDevice(device));
+  CK(cudaFree(0));
+  if (!resolve("cuGetErrorString", &p_cuGetErrorString) || !resolve("cuModuleLoadData", &p_cuModuleLoadData) ||
+      !resolve("cuModuleGetFunction", &p_cuModuleGetFunction) || !resolve("cuLaunchKernel", &p_cuLaunchKernel) ||
+      !resolve("cuOccupancyMaxActiveBlocksPerMultiprocessor", &p_cuOccupancyMaxActiveBlocksPerMultiprocessor) ||
+      !resolve("cuFuncSetAttribute", &p_cuFuncSetAttribute))
+    return fail("weldgpu: could not resolve CUDA driver entry points");
+  CK(cudaStreamCreateWithFlags(&g_stream, cudaStreamNonBlocking));
+  CK(cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, device));
+  cudaMemPool_t pool;
+  CK(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t thr = UINT64_MAX;
+  CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  CK(cudaMalloc((void**)&g_err_word, 64));
+  CK(cudaMemset(g_err_word, 0, 64));
+  CK(cudaMallocHost((void**)&g_err_host, 64));
+  g_device = device;
+  g_inited = true;
+  return 0;
+}
+
+int wg_sm_count(int* n) { NEED_INIT(); *n = g_sm_count; return 0; }
+
+int wg_stream(uint64_t* s) { NEED_INIT(); *s = (uint64_t)(uintptr_t)g_stream; return 0; }
+
+int wg_sync(void) { NEED_INIT(); CK(cudaStreamSynchronize(g_stream)); return 0; }
+
+// ---- buffer manager --------------------------------------------------------
+int wg_alloc(uint64_t bytes, uint64_t* dptr) {
+  NEED_INIT();
+  void* p = nullptr;
+  uint64_t b = bytes ? bytes : 1;
+  b = (b + 255) & ~255ULL;
+  CK(cudaMallocAsync(&p, b, g_stream));
+  *dptr = (uint64_t)(uintptr_t)p;
+  std::lock_guard<std::mutex> lk(g_acct_mu);
+  g_live += b;
+  if (g_live > g_peak) g_peak = g_live;
+  g_sizes.emplace_back(p, b);
+  return 0;
+}
+
+int wg_free(uint64_t dptr) {
+  NEED_INIT();
+  if (!dptr) return 0;
+  void* p = (void*)(uintptr_t)dptr;
+  CK(cudaFreeAsync(p, g_stream));
+  std::lock_guard<std::mutex> lk(g_acct_mu);
+  for (size_t i = g_sizes.size(); i-- > 0;) {
+    if (g_sizes[i].first == p) {
+      g_live -= g_sizes[i].second;
+      g_sizes[i] = g_sizes.back();
+      g_sizes.pop_back();
+      break;
+    }
+  }
+  return 0;
+}
+
+int wg_mem_stats(uint64_t* live, uint64_t* peak) {
+  std::lock_guard<std::mutex> lk(g_acct_mu);
+  *live = g_live;
+  *peak = g_peak;
+  return 0;
+}
+
+int wg_mem_reset_peak(void) {
+  std::lock_guard<std::mutex> lk(g_acct_mu);
+  g_peak = g_live;
+  return 0;
+}
+
+int wg_memset(uint64_t dptr, int value, uint64_t bytes) {
+  NEED_INIT();
+  if (!bytes) return 0;
+  CK(cudaMemsetAsync((void*)(uintptr_t)dptr, value, bytes, g_stream));
+  return 0;
+}
+
+int wg_h2d(uint64_t dst, const void* src, uint64_t bytes) {
+  NEED_INIT();
+  if (!bytes) return 0;
+  CK(cudaMemcpyAsync((void*)(uintptr_t)dst, src, bytes, cudaMemcpyHostToDevice, g_stream));
+  return 0;
+}
+
+int wg_d2h(void* dst, uint64_t src, uint64_t bytes) {
+  NEED_INIT();
+  if (!bytes) return 0;
+  CK(cudaMemcpyAsync(dst, (const void*)(uintptr_t)src, bytes, cudaMemcpyDeviceToHost, g_stream));
+  CK(cudaStreamSynchronize(g_stream));
+  return 0;
+}
+
+int wg_d2h_async(void* dst, uint64_t src, uint64_t bytes) {
+  NEED_INIT();
+  if (!bytes) return 0;
+  CK(cudaMemcpyAsync(dst, (const void*)(uintptr_t)src, bytes, cudaMemcpyDeviceToHost, g_stream));
+  return 0;
+}
+
+int wg_d2d(uint64_t dst, uint64_t src, uint64_t bytes) {
+  NEED_INIT();
+  if (!bytes) return 0;
+  CK(cudaMemcpyAsync((void*)(uintptr_t)dst, (const void*)(uintptr_t)src, bytes, cudaMemcpyDeviceToDevice, g_stream));
+  return 0;
+}
+
+int wg_host_alloc(uint64_t bytes, void** p) {
+  NEED_INIT();
+  CK(cudaMallocHost(p, bytes ? bytes : 1));
+  return 0;
+}
+
+int wg_host_free(void* p) {
+  NEED_INIT();
+  CK(cudaFreeHost(p));
+  return 0;
+}
+
+int wg_host_register(void* p, uint64_t bytes) {
+  NEED_INIT();
+  CK(cudaHostRegister(p, bytes, cudaHostRegisterDefault));
+  return 0;
+}
+
+int wg_host_unregister(void* p) {
+  NEED_INIT();
+  CK(cudaHostUnregister(p));
+  return 0;
+}
+
+// ---- device error word -----------------------------------------------------
+int wg_error_ptr(uint64_t* p) { NEED_INIT(); *p = (uint64_t)(uintptr_t)g_err_word; return 0; }
+
+int wg_read_error(int64_t* code, int64_t* info) {
+  NEED_INIT();
+  CK(cudaMemcpyAsync(g_err_host, g_err_word, 16, cudaMemcpyDeviceToHost, g_stream));
+  CK(cudaStreamSynchronize(g_stream));
+  *code = g_err_host[0];
+  *info = g_err_host[1];
+  if (g_err_host[0] != 0) CK(cudaMemsetAsync(g_err_word, 0, 16, g_stream));
+  return 0;
+}
+
+// ---- NVRTC compile + module cache -----------------------------------------
+int wg_compile(const char* src, const char* name, int nheaders, const char* const* header_srcs,
+               const char* const* header_names, int nopts, const char* const* opts,
+               uint64_t* module_out, char* log_buf, uint64_t log_cap) {
+  NEED_INIT();
+  nvrtcProgram prog;
+  CKN(nvrtcCreateProgram(&prog, src, name, nheaders, header_srcs, header_names));
+  nvrtcResult rc = nvrtcCompileProgram(prog, nopts, opts);
+  size_t log_size = 0;
+  nvrtcGetProgramLogSize(prog, &log_size);
+  std::string log(log_size, '\0');
+  if (log_size) nvrtcGetProgramLog(prog, &log[0]);
+  if (log_buf && log_cap) {
+    size_t n = log.size() < log_cap - 1 ? log.size() : log_cap - 1;
+    memcpy(log_buf, log.data(), n);
+    log_buf[n] = 0;
+  }
+  if (rc != NVRTC_SUCCESS) {
+    nvrtcDestroyProgram(&prog);
+    return fail(std::string("nvrtc compile failed: ") + nvrtcGetErrorString(rc) + "\n" + log);
+  }
+  size_t cubin_size = 0;
+  CKN(nvrtcGetCUBINSize(prog, &cubin_size));
+  std::vector<char> cubin(cubin_size);
+  CKN(nvrtcGetCUBIN(prog, cubin.data()));
+  nvrtcDestroyProgram(&prog);
+  CUmodule mod;
+  CKD(p_cuModuleLoadData(&mod, cubin.data()));
+  *module_out = (uint64_t)(uintptr_t)mod;
+  return 0;
+}
+
+// Compile only (no device needed): used by the CPU test-suite and build() to
+// prove every generated kernel compiles for sm_100a.  Returns the cubin size.
+int wg_compile_check(const char* src, const char* name, int nheaders, const char* const* header_srcs,
+                     const char* const* header_names, int nopts, const char* const* opts,
+                     uint64_t* cubin_bytes, char* log_buf, uint64_t log_cap) {
+  nvrtcProgram prog;
+  CKN(nvrtcCreateProgram(&prog, src, name, nheaders, header_srcs, header_names));
+  nvrtcResult rc = nvrtcCompileProgram(prog, nopts, opts);
+  size_t log_size = 0;
+  nvrtcGetProgramLogSize(prog, &log_size);
+  std::string log(log_size, '\0');
+  if (log_size) nvrtcGetProgramLog(prog, &log[0]);
+  if (log_buf && log_cap) {
+    size_t n = log.size() < log_cap - 1 ? log.size() : log_cap - 1;
+    memcpy(log_buf, log.data(), n);
+    log_buf[n] = 0;
+  }
+  if (rc != NVRTC_SUCCESS) {
+    nvrtcDestroyProgram(&prog);
+    return fail(std::string("nvrtc compile failed: ") + nvrtcGetErrorString(rc) + "\n" + log);
+  }
+  size_t cubin_size = 0;
+  CKN(nvrtcGetCUBINSize(prog, &cubin_size));
+  nvrtcDestroyProgram(&prog);
+  *cubin_bytes = cubin_size;
+  return 0;
+}
+
+int wg_module_function(uint64_t module, const char* name, uint64_t* fn) {
+  NEED_INIT();
+  CUfunction f;
+  CKD(p_cuModuleGetFunction(&f, (CUmodule)(uintptr_t)module, name));
+  *fn = (uint64_t)(uintptr_t)f;
+  return 0;
+}
+
+int wg_occupancy(uint64_t fn, int block, int dyn_smem, int* blocks_per_sm) {
+  NEED_INIT();
+  CKD(p_cuOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, (CUfunction)(uintptr_t)fn, block, (size_t)dyn_smem));
+  return 0;
+}
+
+int wg_launch(uint64_t fn, uint32_t grid, uint32_t block, uint32_t dyn_smem, const void* params, uint64_t params_size) {
+  NEED_INIT();
+  CUfunction f = (CUfunction)(uintptr_t)fn;
+  if (dyn_smem > 48 * 1024)
+    CKD(p_cuFuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)dyn_smem));
+  size_t sz = (size_t)params_size;
+  void* extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, const_cast<void*>(params), CU_LAUNCH_PARAM_BUFFER_SIZE, &sz,
+                   CU_LAUNCH_PARAM_END};
+  CKD(p_cuLaunchKernel(f, grid, 1, 1, block, 1, 1, dyn_smem, (CUstream)g_stream, nullptr, extra));
+  return 0;
+}
+
+// ---- builder finalisation helpers -------------------------------------------
+int wg_table_init(uint64_t table, uint64_t nslots, int slot_words, const uint64_t* pattern) {
+  NEED_INIT();
+  if (slot_words < 1 || slot_words > 64) return fail("wg_table_init: slot_words out of range");
+  uint64_t* pat = nullptr;
+  CK(cudaMallocAsync((void**)&pat, 64 * 8, g_stream));
+  CK(cudaMemcpyAsync(pat, pattern, slot_words * 8, cudaMemcpyHostToDevice, g_stream));
+  uint64_t total = nslots * (uint64_t)slot_words;
+  k_table_init<<<grid_for(total, 256), 256, 0, g_stream>>>((uint64_t*)(uintptr_t)table, nslots, slot_words, pat);
+  CK(cudaGetLastError());
+  CK(cudaFreeAsync(pat, g_stream));
+  return 0;
+}
+
+int wg_table_compact(uint64_t table, uint64_t nslots, int slot_words, int mode, const uint64_t* out_words,
+                     int nout, uint64_t* count_out) {
+  NEED_INIT();
+  uint64_t** d_out = nullptr;
+  unsigned long long* d_cnt = nullptr;
+  CK(cudaMallocAsync((void**)&d_out, sizeof(uint64_t*) * (nout + 1), g_stream));
+  CK(cudaMallocAsync((void**)&d_cnt, 8, g_stream));
+  CK(cudaMemcpyAsync(d_out, out_words, sizeof(uint64_t) * nout, cudaMemcpyHostToDevice, g_stream));
+  CK(cudaMemsetAsync(d_cnt, 0, 8, g_stream));
+  k_table_compact<<<grid_for(nslots, 256), 256, 0, g_stream>>>((const uint64_t*)(uintptr_t)table, nslots,
+                                                                slot_words, mode, d_out, nout, d_cnt);
+  CK(cudaGetLastError());
+  if (mode == 1) {
+    k_table_compact_sentinel<<<1, 32, 0, g_stream>>>((const uint64_t*)(uintptr_t)table, nslots, slot_words, d_out,
+                                                     nout, d_cnt);
+    CK(cudaGetLastError());
+  }
+  unsigned long long h = 0;
+  CK(cudaMemcpyAsync(&h, d_cnt, 8, cudaMemcpyDeviceToHost, g_stream));
+  CK(cudaStreamSynchronize(g_stream));
+  CK(cudaFreeAsync(d_out, g_stream));
+  CK(cudaFreeAsync(d_cnt, g_stream));
+  *count_out = h;
+  return 0;
+}
+
+int wg_order_key(uint64_t src, int kind, uint64_t n, uint64_t perm, uint64_t dst) {
+  NEED_INIT();
+  if (!n) return 0;
+  k_order_key<<<grid_for(n, 256), 256, 0, g_stream>>>((const void*)(uintptr_t)src, kind, n,
+                                                       (const uint32_t*)(uintptr_t)perm, (uint64_t*)(uintptr_t)dst);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int wg_iota_u32(uint64_t dst, uint64_t n) {
+  NEED_INIT();
+  if (!n) return 0;
+  k_iota_u32<<<grid_for(n, 256), 256, 0, g_stream>>>((uint32_t*)(uintptr_t)dst, n);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// Stable LSD radix sort of (u64 key, u32 value) pairs over key bits
+// [begin_bit, end_bit).  Stability is what makes multi-field lexicographic
+// sorts (last field first) and order-preserving grouping correct.
+int wg_sort_pairs(uint64_t keys_in, uint64_t vals_in, uint64_t keys_out, uint64_t vals_out, uint64_t n,
+                  int begin_bit, int end_bit) {
+  NEED_INIT();
+  if (!n) return 0;
+  if (n > 0xffffffffULL) return fail("wg_sort_pairs: more than 2^32 items");
+  size_t temp = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, temp, (const uint64_t*)(uintptr_t)keys_in,
+                                     (uint64_t*)(uintptr_t)keys_out, (const uint32_t*)(uintptr_t)vals_in,
+                                     (uint32_t*)(uintptr_t)vals_out, (int)n, begin_bit, end_bit, g_stream));
+  void* d_temp = nullptr;
+  CK(cudaMallocAsync(&d_temp, temp ? temp : 1, g_stream));
+  CK(cub::DeviceRadixSort::SortPairs(d_temp, temp, (const uint64_t*)(uintptr_t)keys_in,
+                                     (uint64_t*)(uintptr_t)keys_out, (const uint32_t*)(uintptr_t)vals_in,
+                                     (uint32_t*)(uintptr_t)vals_out, (int)n, begin_bit, end_bit, g_stream));
+  CK(cudaFreeAsync(d_temp, g_stream));
+  return 0;
+}
+
+int wg_gather(uint64_t src, uint64_t perm, uint64_t dst, uint64_t n, int width) {
+  NEED_INIT();
+  if (!n) return 0;
+  unsigned g = grid_for(n, 256);
+  const uint32_t* pm = (const uint32_t*)(uintptr_t)perm;
+  switch (width) {
+    case 8: k_gather<uint64_t><<<g, 256, 0, g_stream>>>((const uint64_t*)(uintptr_t)src, pm, (uint64_t*)(uintptr_t)dst, n); break;
+    case 4: k_gather<uint32_t><<<g, 256, 0, g_stream>>>((const uint32_t*)(uintptr_t)src, pm, (uint32_t*)(uintptr_t)dst, n); break;
+    case 1: k_gather<uint8_t><<<g, 256, 0, g_stream>>>((const uint8_t*)(uintptr_t)src, pm, (uint8_t*)(uintptr_t)dst, n); break;
+    default: return fail("wg_gather: width must be 1, 4 or 8");
+  }
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int wg_narrow(uint64_t src, uint64_t dst, int width, uint64_t n) {
+  NEED_INIT();
+  if (!n) return 0;
+  k_narrow<<<grid_for(n, 256), 256, 0, g_stream>>>((const uint64_t*)(uintptr_t)src, (void*)(uintptr_t)dst, width, n);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int wg_widen(uint64_t src, uint64_t dst, int width, uint64_t n) {
+  NEED_INIT();
+  if (!n) return 0;
+  k_widen<<<grid_for(n, 256), 256, 0, g_stream>>>((const void*)(uintptr_t)src, (uint64_t*)(uintptr_t)dst, width, n);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// Positions where a new key run starts in sorted multi-word keys; returns
+// the run starts (u32) and their count.
+int wg_run_starts(const uint64_t* key_words, int kw, uint64_t n, uint64_t starts_out, uint64_t* nruns) {
+  NEED_INIT();
+  if (!n) { *nruns = 0; return 0; }
+  if (n > 0xffffffffULL) return fail("wg_run_starts: more than 2^32 items");
+  uint64_t** d_words = nullptr;
+  uint8_t* flags = nullptr;
+  int* d_cnt = nullptr;
+  CK(cudaMallocAsync((void**)&d_words, sizeof(uint64_t*) * kw, g_stream));
+  CK(cudaMemcpyAsync(d_words, key_words, sizeof(uint64_t) * kw, cudaMemcpyHostToDevice, g_stream));
+  CK(cudaMallocAsync((void**)&flags, n, g_stream));
+  CK(cudaMallocAsync((void**)&d_cnt, 8, g_stream));
+  k_heads<<<grid_for(n, 256), 256, 0, g_stream>>>((const uint64_t* const*)d_words, kw, n, flags);
+  CK(cudaGetLastError());
+  cub::CountingInputIterator<uint32_t> it(0);
+  size_t temp = 0;
+  CK(cub::DeviceSelect::Flagged(nullptr, temp, it, flags, (uint32_t*)(uintptr_t)starts_out, d_cnt, (int)n, g_stream));
+  void* d_temp = nullptr;
+  CK(cudaMallocAsync(&d_temp, temp ? temp : 1, g_stream));
+  CK(cub::DeviceSelect::Flagged(d_temp, temp, it, flags, (uint32_t*)(uintptr_t)starts_out, d_cnt, (int)n, g_stream));
+  int h = 0;
+  CK(cudaMemcpyAsync(&h, d_cnt, 4, cudaMemcpyDeviceToHost, g_stream));
+  CK(cudaStreamSynchronize(g_stream));
+  CK(cudaFreeAsync(d_temp, g_stream));
+  CK(cudaFreeAsync(flags, g_stream));
+  CK(cudaFreeAsync(d_cnt, g_stream));
+  CK(cudaFreeAsync(d_words, g_stream));
+  *nruns = (uint64_t)h;
+  return 0;
+}
+
+// ---- synthetic data + measurement helpers ----------------------------------
+int wg_gen_column(uint64_t dst, uint64_t n, uint64_t row0, int dist, int width, uint64_t seed, uint64_t col,
+                  int64_t lo, uint64_t span, double flo, double fhi, double div, int ncat, const double* cum,
+                  const int64_t* vals) {
+  NEED_INIT();
+  if (!n) return 0;
+  GenSpec g;
+  memset(&g, 0, sizeof(g));
+  g.dist = dist; g.width = width; g.seed = seed; g.col = col; g.lo = lo; g.span = span ? span : 1;
+  g.flo = flo; g.fhi = fhi; g.div = div; g.ncat = ncat;
+  if (ncat > 8) return fail("wg_gen_column: at most 8 categories");
+  for (int c = 0; c < ncat; ++c) { g.cum[c] = cum[c]; g.vals[c] = vals[c]; }
+  k_gen<<<grid_for(n, 256), 256, 0, g_stream>>>((void*)(uintptr_t)dst, n, row0, g);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int wg_mul_inplace_f64(uint64_t a, uint64_t b, uint64_t n) {
+  NEED_INIT();
+  if (!n) return 0;
+  k_mul_inplace<<<grid_for(n, 256), 256, 0, g_stream>>>((double*)(uintptr_t)a, (const double*)(uintptr_t)b, n);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int wg_flush_l2(uint64_t buf, uint64_t bytes, uint32_t salt) {
+  NEED_INIT();
+  uint64_t n16 = bytes / 16;
+  k_flush<<<grid_for(n16, 512), 512, 0, g_stream>>>((uint4*)(uintptr_t)buf, n16, salt);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int wg_event_create(uint64_t* ev) {
+  NEED_INIT();
+  cudaEvent_t e;
+  CK(cudaEventCreate(&e));
+  *ev = (uint64_t)(uintptr_t)e;
+  return 0;
+}
+
+int wg_event_record(uint64_t ev) {
+  NEED_INIT();
+  CK(cudaEventRecord((cudaEvent_t)(uintptr_t)ev, g_stream));
+  return 0;
+}
+
+int wg_event_elapsed_ms(uint64_t start, uint64_t stop, float* ms) {
+  NEED_INIT();
+  CK(cudaEventSynchronize((cudaEvent_t)(uintptr_t)stop));
+  CK(cudaEventElapsedTime(ms, (cudaEvent_t)(uintptr_t)start, (cudaEvent_t)(uintptr_t)stop));
+  return 0;
+}
+
+int wg_event_destroy(uint64_t ev) {
+  NEED_INIT();
+  CK(cudaEventDestroy((cudaEvent_t)(uintptr_t)ev));
+  return 0;
+}
+
+}  // extern "C"

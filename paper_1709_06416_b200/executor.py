@@ -1,0 +1,911 @@
+"""``evaluate(e, env, config, externs) -> (Value, EvalStats)`` on the GPU.
+
+Drop-in for the reference executor seam
+``weldmill.engine.evaluate`` (/root/reference/pkg/src/weldmill/engine/run.py:1008-1074):
+same signature, same ``Value``/``EvalStats`` return types, same ``EvalError``
+subclasses.  The host walks the program's *control plane* (lets, struct
+assembly, loop bounds, scalar glue between loops) and every ``for`` loop
+runs as one NVRTC-compiled sm_100a kernel over device-resident columns
+(codegen.py); builders live in HBM (builders_dev.py) and are finalised on
+the device (sort / compaction / grouping).  There is no CPU fallback: IR
+the device path does not lower raises ``DeviceUnsupported`` (an EvalError).
+"""
+from __future__ import annotations
+
+import math
+import struct as _struct
+import threading
+
+import numpy as np
+
+from . import _ref  # noqa: F401
+from weldmill.engine import EngineConfig, EvalStats, Value
+from weldmill.engine.builders import STRATEGIES, payload_bytes
+from weldmill.engine.stats import note_evaluation
+from weldmill.errors import (DivideByZero, EvalError, ExternCallUnknown, IndexOutOfBounds, IterationLimit,
+                             KeyNotFound, MemoryLimitExceeded, UseAfterResult, ZipLengthMismatch)
+from weldmill.expr import (Apply, BinaryOp, BitSelect, Broadcast, CastScalar, ExternCall, FieldAccess, For, Ident,
+                           If, Iterate, IterSpec as XIterSpec, Lambda, Len, Let, Literal, Lookup, MakeStruct,
+                           MakeVector, Merge, NewBuilder, Param as XParam, Result, Sort, ToVec, UnaryOp,
+                           free_variables)
+
+from . import runtime as rt
+from . import semantics as sem
+from .builders_dev import (AppenderDev, DDict, DGroups, DictDev, GroupDev, MergerDev, VecMergerDev, dict_payload,
+                           finish_dict, finish_groups, gather_cols, sort_perm, tovec)
+from .codegen import BSpec, IterSpec, generate
+from .columns import Col, DVec, to_device, to_payload, dvec_from_cols
+from .irtypes import (BOOL, F32, F64, I64, SIZE, Builder, DeviceUnsupported as _DU, Dict, DictMerger, Function,
+                      GroupBuilder, Merger, Scalar, Simd, Struct, Vec, VecBuilder, VecMerger, is_flat, leaves)
+
+
+class DeviceUnsupported(EvalError, _DU):
+    """IR outside what the device executor lowers (no CPU fallback)."""
+
+
+ERR_CLASSES = {1: DivideByZero, 2: IndexOutOfBounds, 3: IndexOutOfBounds, 4: KeyNotFound, 5: EvalError,
+               6: DivideByZero}
+ERR_TEXT = {1: "integer division by zero", 2: "lookup index {info} outside vector",
+            3: "vecmerger index {info} out of range", 4: "key not in dictionary",
+            5: "internal device error ({info})", 6: "integer remainder by zero"}
+
+
+class HostVec:
+    """A host vector not yet bound to the device (uploaded on first use)."""
+
+    __slots__ = ("ty", "payload", "_dev", "n")
+
+    def __init__(self, ty, payload):
+        self.ty = ty
+        self.payload = payload
+        self._dev = None
+        if isinstance(payload, (bytes, bytearray, memoryview)):
+            self.n = _struct.unpack_from("<q", payload, 0)[0]
+        elif isinstance(payload, tuple) and payload and all(isinstance(a, np.ndarray) for a in payload):
+            self.n = int(payload[0].shape[0])
+        else:
+            self.n = len(payload)
+
+    def __len__(self):
+        return self.n
+
+    def dev(self):
+        if self._dev is None:
+            self._dev = to_device(self.ty, self.payload)
+        return self._dev
+
+    def host_item(self, i):
+        p = self.payload
+        if isinstance(p, list):
+            return p[i]
+        if isinstance(p, np.ndarray):
+            if p.dtype.names:
+                return tuple(_py(p[nm][i]) for nm in p.dtype.names)
+            return _py(p[i])
+        return None
+
+
+def _py(x):
+    if isinstance(x, np.generic):
+        return x.item()
+    return x
+
+
+class Closure:
+    __slots__ = ("lam", "env")
+
+    def __init__(self, lam, env):
+        self.lam = lam
+        self.env = env
+
+
+class _Plan:
+    __slots__ = ("plan", "kernel", "loop")
+
+
+_plan_cache = {}
+_plan_lock = threading.Lock()
+
+
+class Ctx:
+    def __init__(self, cfg: EngineConfig, externs, idx0=0):
+        self.cfg = cfg
+        self.externs = externs or {}
+        self.traversals = 0
+        self.allocs = 0
+        self.tasks = 0
+        self.live = 0
+        self.peak = 0
+        self.registry = []
+        self.idx0 = idx0
+        self.launches = 0
+        self._ticket = None
+
+    # -- memory accounting (run.py:208-228) --------------------------------
+    def alloc(self, n):
+        self.live += n
+        if self.live > self.peak:
+            self.peak = self.live
+        if self.live > self.cfg.memory_limit:
+            raise MemoryLimitExceeded(f"engine memory {self.live} bytes exceeds limit {self.cfg.memory_limit}")
+
+    def free(self, n):
+        self.live -= n
+
+    def materialized(self, obj, nbytes):
+        self.alloc(nbytes)
+        self.registry.append((obj, nbytes))
+        self.allocs += 1
+
+    def ticket(self):
+        if self._ticket is None:
+            self._ticket = rt.alloc(8)
+            rt.memset(self._ticket.ptr, 0, 8)
+        return self._ticket.ptr
+
+    # -- device error word ---------------------------------------------------
+    def check_device(self):
+        code, info = rt.read_error()
+        if code:
+            cls = ERR_CLASSES.get(code, EvalError)
+            raise cls(ERR_TEXT.get(code, "device error {info}").format(info=info))
+
+    # -- evaluation ------------------------------------------------------------
+    def ev(self, e, env):
+        m = getattr(self, "ev_" + type(e).__name__, None)
+        if m is None:
+            raise DeviceUnsupported(f"cannot evaluate node {type(e).__name__}")
+        return m(e, env)
+
+    def ev_Literal(self, e, env):
+        return sem.literal(e.ty.kind, e.value)
+
+    def ev_Ident(self, e, env):
+        try:
+            return env[e.name]
+        except KeyError:
+            raise EvalError(f"unbound name {e.name!r}") from None
+
+    def ev_Let(self, e, env):
+        v = self.ev(e.value, env)
+        env2 = dict(env)
+        env2[e.name] = v
+        return self.ev(e.body, env2)
+
+    def ev_Lambda(self, e, env):
+        return Closure(e, env)
+
+    def ev_Apply(self, e, env):
+        f = self.ev(e.func, env)
+        if not isinstance(f, Closure):
+            raise EvalError("attempted to call a non-function value")
+        args = [self.ev(a, env) for a in e.args]
+        if len(args) != len(f.lam.params):
+            raise EvalError(f"function takes {len(f.lam.params)} arguments, got {len(args)}")
+        env2 = dict(f.env)
+        for p, a in zip(f.lam.params, args):
+            env2[p.name] = a
+        return self.ev(f.lam.body, env2)
+
+    def ev_BinaryOp(self, e, env):
+        if e.op == "&&":
+            return bool(self.ev(e.rhs, env)) if self.ev(e.lhs, env) else False
+        if e.op == "||":
+            return True if self.ev(e.lhs, env) else bool(self.ev(e.rhs, env))
+        a = self.ev(e.lhs, env)
+        b = self.ev(e.rhs, env)
+        t = e.lhs.ty
+        if isinstance(t, Simd):
+            return tuple(sem.binop(e.op, t.kind, x, y) for x, y in zip(a, b))
+        return sem.binop(e.op, t.kind, a, b)
+
+    def ev_UnaryOp(self, e, env):
+        v = self.ev(e.operand, env)
+        t = e.operand.ty
+        if e.op == "!":
+            return tuple(not x for x in v) if isinstance(t, Simd) else (not v)
+        if isinstance(t, Simd):
+            return tuple(sem.neg(t.kind, x) for x in v)
+        return sem.neg(t.kind, v)
+
+    def ev_If(self, e, env):
+        return self.ev(e.on_true, env) if self.ev(e.cond, env) else self.ev(e.on_false, env)
+
+    def ev_BitSelect(self, e, env):
+        c = self.ev(e.cond, env)
+        a = self.ev(e.on_true, env)
+        b = self.ev(e.on_false, env)
+        if isinstance(e.cond.ty, Simd):
+            return tuple(x if ci else y for ci, x, y in zip(c, a, b))
+        return a if c else b
+
+    def ev_Broadcast(self, e, env):
+        return (self.ev(e.value, env),) * 4
+
+    def ev_CastScalar(self, e, env):
+        v = self.ev(e.value, env)
+        src = e.value.ty
+        if isinstance(src, Simd):
+            return tuple(sem.cast(src.kind, e.kind, x) for x in v)
+        return sem.cast(src.kind, e.kind, v)
+
+    def ev_MakeStruct(self, e, env):
+        return tuple(self.ev(x, env) for x in e.items)
+
+    def ev_FieldAccess(self, e, env):
+        return self.ev(e.base, env)[e.ordinal]
+
+    def ev_MakeVector(self, e, env):
+        items = [self.ev(x, env) for x in e.items]
+        hv = HostVec(e.ty, items)
+        self.materialized(hv, payload_bytes(e.ty, items) if is_flat(e.ty.elem) else 16)
+        return hv
+
+    def ev_Len(self, e, env):
+        v = self.ev(e.coll, env)
+        return len(v)
+
+    def ev_Lookup(self, e, env):
+        coll = self.ev(e.coll, env)
+        idx = self.ev(e.index, env)
+        if isinstance(coll, (HostVec, DVec)):
+            n = len(coll)
+            if not 0 <= idx < n:
+                raise IndexOutOfBounds(f"index {idx} outside vector of length {n}")
+            if isinstance(coll, HostVec):
+                item = coll.host_item(idx)
+                if item is not None:
+                    return item
+                coll = coll.dev()
+            return _dvec_item(coll, idx)
+        if isinstance(coll, (DDict, DGroups)):
+            d = dict_payload(coll)
+            try:
+                return d[idx]
+            except KeyError:
+                raise KeyNotFound(f"key {idx!r} not in dictionary") from None
+        raise EvalError("lookup into a non-collection")
+
+    def ev_Iterate(self, e, env):
+        state = self.ev(e.init, env)
+        upd = self.ev(e.update, env)
+        limit = self.cfg.max_iterations
+        steps = 0
+        while True:
+            env2 = dict(upd.env)
+            env2[upd.lam.params[0].name] = state
+            state, go = self.ev(upd.lam.body, env2)
+            steps += 1
+            if not go:
+                return state
+            if steps >= limit:
+                raise IterationLimit(f"iterate exceeded {limit} iterations")
+
+    def ev_ExternCall(self, e, env):
+        fn = self.externs.get(e.name)
+        if fn is None:
+            raise ExternCallUnknown(f"no extern function {e.name!r} registered")
+        args = [self.ev(a, env) for a in e.args]
+        try:
+            return fn(*args)
+        except Exception as exc:
+            raise EvalError(f"extern {e.name!r} failed: {exc}") from exc
+
+    # -- builders ----------------------------------------------------------------
+    def ev_NewBuilder(self, e, env):
+        kind = e.kind
+        if isinstance(kind, VecBuilder):
+            hint = self.ev(e.arg, env) if e.arg is not None else None
+            if hint is not None:
+                if hint < 0:
+                    raise EvalError(f"negative vector size hint {hint}")
+                self.alloc(hint * _slot_bytes(kind.elem))
+            b = AppenderDev(kind, leaves(kind.elem) if is_flat(kind.elem) else None, hint)
+            b.acct = hint * _slot_bytes(kind.elem) if hint is not None else 0
+            return b
+        if isinstance(kind, Merger):
+            return MergerDev(kind)
+        if isinstance(kind, DictMerger):
+            return DictDev(kind)
+        if isinstance(kind, GroupBuilder):
+            b = GroupDev(kind)
+            b.acct = 0
+            return b
+        if isinstance(kind, VecMerger):
+            init = self.ev(e.arg, env)
+            dv = init.dev() if isinstance(init, HostVec) else init
+            self.alloc(dv.n * _slot_bytes(kind.elem))
+            b = VecMergerDev(kind, dv)
+            b.acct = dv.n * _slot_bytes(kind.elem)
+            return b
+        raise EvalError(f"unknown builder kind {kind!r}")
+
+    def ev_Merge(self, e, env):
+        b = self.ev(e.builder, env)
+        v = self.ev(e.value, env)
+        if not hasattr(b, "pending"):
+            raise EvalError("merge into a non-builder value")
+        b.check()
+        if isinstance(e.value.ty, Simd):
+            b.pending.extend(v)
+        else:
+            b.pending.append(v)
+        b.pending_ty = e.value.ty.kind if isinstance(e.value.ty, Simd) else e.value.ty
+        if isinstance(b.pending_ty, str):
+            b.pending_ty = Scalar(b.pending_ty)
+        return b
+
+    def flush_pending(self, b):
+        """Merges issued outside loops run as a tiny device loop, in order."""
+        if not b.pending:
+            return
+        items = b.pending
+        b.pending = []
+        ty = Vec(b.pending_ty)
+        hv = HostVec(ty, items)
+        x = Ident("x", ty=b.pending_ty)
+        bid = Ident("b", ty=Builder(b.kind))
+        body = Merge(bid, x, ty=Builder(b.kind))
+        lam = Lambda((XParam("b"), XParam("i"), XParam("x")), body)
+        loop = For((XIterSpec(Ident("__pending", ty=ty)),), Ident("__b", ty=Builder(b.kind)), lam,
+                   ty=Builder(b.kind))
+        self.run_loop(loop, {"__pending": hv, "__b": b}, count_traversal=False)
+
+    def ev_Result(self, e, env):
+        b = self.ev(e.builder, env)
+        return self.finish(b, e.builder.ty)
+
+    def finish(self, b, ty):
+        if isinstance(b, tuple):
+            return tuple(self.finish(x, t) for x, t in zip(b, ty.fields))
+        if not hasattr(b, "pending"):
+            raise EvalError("result() applied to a non-builder value")
+        self.flush_pending(b)
+        b.consume()
+        kind = b.kind
+        if isinstance(kind, Merger):
+            self.check_device()
+            return b.read()
+        if isinstance(kind, VecBuilder):
+            if b.kinds is None:
+                raise DeviceUnsupported(f"vecbuilder[{kind.elem}] (nested element types) on the device")
+            if not b.segments:
+                cols = [Col.alloc(k, 0) for k in b.kinds]
+                n = 0
+            else:
+                cols, n = b.concat()
+            self.check_device()
+            self.free(getattr(b, "acct", 0))
+            out = dvec_from_cols(kind.elem, n, cols)
+            self.materialized(out, 16 + n * _slot_bytes(kind.elem))
+            return out
+        if isinstance(kind, VecMerger):
+            self.check_device()
+            self.free(getattr(b, "acct", 0))
+            out = dvec_from_cols(kind.elem, b.n, b.cols)
+            self.materialized(out, 16 + b.n * _slot_bytes(kind.elem))
+            return out
+        if isinstance(kind, DictMerger):
+            self.check_device()
+            if b.table is None:
+                b.ensure(1)
+            d = finish_dict(b, Dict(kind.key, kind.value))
+            self.materialized(d, 16 + d.n * (16 + _slot_bytes(kind.key) + _slot_bytes(kind.value)))
+            return d
+        if isinstance(kind, GroupBuilder):
+            self.check_device()
+            g = finish_groups(b, Dict(kind.key, Vec(kind.value)))
+            self.materialized(g, 16 + g.n * (16 + _slot_bytes(kind.key) + 16) + g.vals.n * _slot_bytes(kind.value))
+            return g
+        raise EvalError(f"unknown builder kind {kind!r}")
+
+    def ev_ToVec(self, e, env):
+        d = self.ev(e.mapping, env)
+        if not isinstance(d, (DDict, DGroups)):
+            raise EvalError("tovec of a non-dictionary")
+        out = tovec(d, e.ty.elem)
+        self.materialized(out, payload_bytes_dvec(e.ty, out))
+        return out
+
+    def ev_Sort(self, e, env):
+        v = self.ev(e.vec, env)
+        dv = v.dev() if isinstance(v, HostVec) else v
+        self.traversals += 1
+        n = dv.n
+        if n == 0:
+            out = dv
+        else:
+            keyf = e.key
+            if not isinstance(keyf, Lambda):
+                raise DeviceUnsupported("sort key must be a lambda literal")
+            kty = keyf.body.ty
+            # key column(s) by a device map loop: for(v, vecbuilder[K], (b,i,x) => merge(b, key(x)))
+            kb = AppenderDev(VecBuilder(kty), leaves(kty), n)
+            xname = keyf.params[0].name
+            body = Merge(Ident("__kb", ty=Builder(VecBuilder(kty))),
+                         Let(xname, Ident("__x", ty=e.vec.ty.elem), keyf.body, ty=kty),
+                         ty=Builder(VecBuilder(kty)))
+            lam = Lambda((XParam("__kb"), XParam("__i"), XParam("__x")), body)
+            loop = For((XIterSpec(Ident("__v", ty=e.vec.ty)),), Ident("__kbs", ty=Builder(VecBuilder(kty))),
+                       lam, ty=Builder(VecBuilder(kty)))
+            env2 = dict(env)
+            env2.update({"__v": dv, "__kbs": kb})
+            self.run_loop(loop, env2, count_traversal=False)
+            kcols, _ = kb.concat()
+            self.check_device()
+            perm = sort_perm(kcols, n)
+            out = dvec_from_cols(dv.elem, n, gather_cols(dv.cols, perm, n))
+        self.materialized(out, 16 + n * _slot_bytes(dv.elem))
+        return out
+
+    # -- loops ---------------------------------------------------------------------
+    def ev_For(self, e, env):
+        return self.run_loop(e, env)
+
+    def run_loop(self, e, env, count_traversal=True):
+        datas, specs, windows = [], [], []
+        count = None
+        for it in e.iters:
+            d = self.ev(it.data, env)
+            if not isinstance(d, (HostVec, DVec)):
+                raise EvalError("loop over a non-vector value")
+            length = len(d)
+            elem = d.ty.elem if isinstance(d, HostVec) else d.elem
+            if it.simd:
+                n = length // 4
+                win = (0, 1)
+            elif it.start is None:
+                n = length
+                win = (0, 1)
+            else:
+                s = self.ev(it.start, env)
+                end = self.ev(it.end, env)
+                st = self.ev(it.stride, env)
+                if st < 1:
+                    raise EvalError(f"iteration stride must be positive, got {st}")
+                if not (0 <= s <= end <= length):
+                    raise IndexOutOfBounds(f"iteration bounds [{s}, {end}) outside vector of length {length}")
+                n = (end - s + st - 1) // st
+                win = (s, st)
+            if count is None:
+                count = n
+            elif count != n:
+                raise ZipLengthMismatch(f"zipped iterations disagree: {count} vs {n}")
+            datas.append(d)
+            windows.append(win)
+            if not is_flat(elem):
+                raise DeviceUnsupported(f"iterating vec[{elem}] on the device")
+            specs.append(IterSpec(elem=elem, simd=it.simd, strided=(win[1] != 1), kinds=leaves(elem)))
+        builders = self.ev(e.builders, env)
+        if count == 0:
+            return builders
+        if count_traversal:
+            self.traversals += len(e.iters)
+
+        lam = e.func
+        lenv = env
+        if not isinstance(lam, Lambda):
+            f = self.ev(lam, env)
+            if not isinstance(f, Closure):
+                raise EvalError("loop body is not a function")
+            lam, lenv = f.lam, f.env
+        blist = []
+        _collect_builders(builders, blist)
+        for b in blist:
+            b.check()
+            self.flush_pending(b)
+        # loop-invariant captures
+        pnames = {p.name for p in lam.params}
+        captures = {}
+        for name in sorted(free_variables(lam) - pnames):
+            v = lenv.get(name)
+            if v is None and name not in lenv:
+                raise EvalError(f"unbound name {name!r}")
+            captures[name] = (_type_of(v, lam, name), v)
+
+        strategy = self.cfg.strategy
+        bstruct, bmap = _bspecs(builders, strategy, count)
+        key = (id(e), id(lam), tuple(repr(s) for s in specs), _bsig(bstruct),
+               tuple((k, repr(t)) for k, (t, _) in captures.items()), tuple(sorted(self.externs)),
+               tuple(bool(w[1] != 1 or w[0] != 0) for w in windows))
+        with _plan_lock:
+            cached = _plan_cache.get(key)
+        if cached is None:
+            plan = generate(e if lam is e.func else _with_func(e, lam), specs, bstruct, captures,
+                            self.externs, strategy)
+            kern = rt.get_kernel(plan.source, plan.name)
+            cached = (plan, kern, e, lam)
+            with _plan_lock:
+                if len(_plan_cache) > 4096:
+                    _plan_cache.clear()
+                _plan_cache[key] = cached
+        plan, kern = cached[0], cached[1]
+        self.launch(plan, kern, count, datas, windows, builders, bmap, captures)
+        return builders
+
+    def launch(self, plan, kern, count, datas, windows, builders, bmap, captures):
+        items = plan.items
+        tile = plan.block * items
+        ntiles = (count + tile - 1) // tile
+        occ = kern.blocks_per_sm(plan.block, plan.smem)
+        grid = max(1, min(ntiles, rt.sm_count() * occ))
+        self.tasks += grid
+        # per-launch builder resources
+        res = {}
+        for b in plan.builders:
+            st = bmap[b.bid]
+            if isinstance(b.kind, (VecBuilder, GroupBuilder)):
+                if b.mode == "direct":
+                    seg = st.new_segment(count * b.k, True)
+                    res[b.bid] = seg
+                    self._acct_append(st, count * b.k)
+                elif b.mode == "scan":
+                    seg = st.new_segment(count * b.k, False)
+                    status = rt.alloc(8 * max(ntiles, 1))
+                    rt.memset(status.ptr, 0, 8 * max(ntiles, 1))
+                    res[b.bid] = (seg, status)
+                    self._acct_append(st, count * b.k)
+            elif isinstance(b.kind, DictMerger):
+                st.ensure(count * max(1, b.extra.get("maxm", 1)))
+        tilectr = None
+        if plan.schedule == "scan":
+            tilectr = rt.alloc(8)
+            rt.memset(tilectr.ptr, 0, 8)
+
+        vals = {}
+        for p in plan.params:
+            vals[p.name] = self._param_value(p.key, count, datas, windows, bmap, res, captures, grid, tilectr)
+        blob = b"".join(_pack(p.ctype, vals[p.name]) for p in plan.params)
+        kern.launch(grid, plan.block, blob, plan.smem)
+        self.launches += 1
+        # dictmerger overflow: grow and replay spilled merges
+        for b in plan.builders:
+            if isinstance(b.kind, DictMerger):
+                st = bmap[b.bid]
+                spilled = st.overflow_rows()
+                if spilled:
+                    self._dict_regrow(st, spilled)
+        self._keep = (tilectr, res)
+
+    def _acct_append(self, st, rows):
+        if getattr(st, "hint", None) is None:
+            nbytes = rows * sum(SIZE[k] for k in st.kinds)
+            self.alloc(nbytes)
+            st.acct = getattr(st, "acct", 0) + nbytes
+
+    def _dict_regrow(self, st: DictDev, spilled):
+        """Grow the table 4x, re-insert existing entries and replay the
+        spilled merges (all folds are commutative)."""
+        import ctypes as _ct
+        kw, vw, n = st.compact()
+        old_over, old_cnt = st.over, spilled
+        st._alloc_table(st.cap * 4)
+        rt.memset(st.ocount.ptr, 0, 8)
+        # replay: entries from the old table then the spill list, as a device loop
+        kty = st.kind.key
+        vty = st.kind.value
+        for keys_w, vals_w, m in ((kw, vw, n), (old_over[0], old_over[1], old_cnt)):
+            if m == 0:
+                continue
+            from .builders_dev import _words_to_cols, _value_words_to_cols
+            kcols = _words_to_cols(keys_w, st.kks, st.lay, m)
+            vcols = _value_words_to_cols(vals_w, st.vks, m)
+            elem = Struct((kty, vty))
+            dv = DVec(elem, m, (_layout(kty, kcols), _layout(vty, vcols)))
+            saved_over = st.over
+            st.over, st.ocap = None, 0
+            x = Ident("x", ty=elem)
+            body = Merge(Ident("b", ty=Builder(st.kind)), x, ty=Builder(st.kind))
+            lam = Lambda((XParam("b"), XParam("i"), XParam("x")), body)
+            loop = For((XIterSpec(Ident("__rows", ty=Vec(elem))),), Ident("__b", ty=Builder(st.kind)), lam,
+                       ty=Builder(st.kind))
+            self.run_loop(loop, {"__rows": dv, "__b": st}, count_traversal=False)
+            del saved_over
+
+    def _param_value(self, key, count, datas, windows, bmap, res, captures, grid, tilectr):
+        k0 = key[0]
+        if k0 == "n":
+            return count
+        if k0 == "idx0":
+            return self.idx0
+        if k0 == "err":
+            return rt.error_ptr()
+        if k0 == "ticket":
+            return self.ticket()
+        if k0 == "tilectr":
+            return tilectr.ptr
+        if k0 == "itcol":
+            _, k, l = key
+            d = datas[k]
+            dv = d.dev() if isinstance(d, HostVec) else d
+            col = dv.cols[l]
+            s, st = windows[k]
+            if st == 1:
+                return col.ptr + s * SIZE[col.kind]
+            return col.ptr
+        if k0 == "itstart":
+            return windows[key[1]][0]
+        if k0 == "itstride":
+            return windows[key[1]][1]
+        if k0 in ("cap", "capcol", "caplen"):
+            name = key[1]
+            v = captures[name][1]
+            path = key[2:]
+            if k0 == "capcol":
+                path, leaf = path[:-1], path[-1]
+            for q in path:
+                v = v[q]
+            if k0 == "cap":
+                return v
+            dv = v.dev() if isinstance(v, HostVec) else v
+            if k0 == "caplen":
+                return dv.n
+            return dv.cols[leaf].ptr
+        if k0 == "b":
+            bid, what = key[1], key[2]
+            st = bmap[bid]
+            if isinstance(st, MergerDev):
+                if what == "part":
+                    return st.partials(grid)
+                if what == "slot":
+                    return st.slot.ptr
+            if isinstance(st, (AppenderDev, GroupDev)):
+                r = res[bid]
+                if what == "col":
+                    seg = r if not isinstance(r, tuple) else r[0]
+                    return seg.cols[key[3]].ptr
+                if what == "status":
+                    return r[1].ptr
+                if what == "total":
+                    return r[0].total_buf.ptr
+            if isinstance(st, VecMergerDev):
+                if what == "len":
+                    return st.n
+                if what == "col":
+                    return st.cols[key[3]].ptr
+            if isinstance(st, DictDev):
+                if what == "table":
+                    return st.table.ptr
+                if what == "mask":
+                    return st.cap - 1
+                if what == "count":
+                    return st.count.ptr
+                if what == "limit":
+                    return st.limit
+                if what == "ocount":
+                    return st.ocount.ptr
+                if what == "ocap":
+                    return st.ocap
+                if what == "okey":
+                    return st.over[0][key[3]].ptr
+                if what == "oval":
+                    return st.over[1][key[3]].ptr
+        raise EvalError(f"internal: no value for kernel parameter {key}")
+
+
+def _layout(t, cols):
+    from .columns import layout_from_cols
+    return layout_from_cols(t, cols)
+
+
+def _with_func(e, lam):
+    from dataclasses import replace
+    return replace(e, func=lam)
+
+
+def _pack(ctype, v):
+    if ctype == "double":
+        return _struct.pack("<d", float(v))
+    if isinstance(v, bool):
+        v = int(v)
+    if isinstance(v, float):
+        raise EvalError(f"internal: float for {ctype} parameter")
+    return _struct.pack("<Q", int(v) & 0xFFFFFFFFFFFFFFFF)
+
+
+def _dvec_item(dv: DVec, idx):
+    from .columns import col_to_numpy
+    vals = []
+    for c in dv.cols:
+        arr = np.empty(1, dtype=np.dtype({BOOL: "u1", "i32": "<i4", "i64": "<i8", "f32": "<f4", "f64": "<f8"}[c.kind]))
+        rt.d2h(arr.ctypes.data, c.ptr + idx * SIZE[c.kind], SIZE[c.kind])
+        x = arr[0].item()
+        vals.append(bool(x) if c.kind == BOOL else x)
+    from .irtypes import unflatten
+    return unflatten(dv.elem, vals)
+
+
+def _slot_bytes(t):
+    from weldmill.engine.builders import _slot_size
+    return _slot_size(t)
+
+
+def payload_bytes_dvec(ty, v):
+    fixed = _fixed(ty.elem)
+    if fixed is not None:
+        return 16 + v.n * fixed
+    return 16 + v.n * 16
+
+
+def _fixed(t):
+    if isinstance(t, Scalar):
+        return SIZE[t.kind]
+    if isinstance(t, Struct):
+        s = 0
+        for f in t.fields:
+            x = _fixed(f)
+            if x is None:
+                return None
+            s += x
+        return s
+    return None
+
+
+def _collect_builders(v, out):
+    if isinstance(v, tuple):
+        for x in v:
+            _collect_builders(x, out)
+    elif hasattr(v, "pending"):
+        out.append(v)
+    else:
+        raise EvalError("loop builders must be builders")
+
+
+def _bspecs(builders, strategy, count):
+    bmap = {}
+    counter = [0]
+
+    def go(v):
+        if isinstance(v, tuple):
+            return tuple(go(x) for x in v)
+        bid = counter[0]
+        counter[0] += 1
+        bmap[bid] = v
+        bs = BSpec(bid=bid, kind=v.kind)
+        if isinstance(v.kind, VecMerger):
+            F = len(leaves(v.kind.elem))
+            nb = v.n
+            if strategy != "global" and nb * F * 8 <= 96 * 1024 and nb <= count:
+                bs.mode = "smem"
+                bs.extra["nbins"] = nb
+            else:
+                bs.mode = "global"
+        if isinstance(v.kind, DictMerger):
+            bs.extra["slot_words"] = v.slot_words
+            if strategy != "global" and v.nw == 1:
+                ns = 512
+                if ns * v.slot_words * 8 <= 64 * 1024:
+                    bs.mode = "smem"
+                    bs.extra["smem_slots"] = ns
+                    bs.extra["pattern"] = v.pattern()
+                else:
+                    bs.mode = "global"
+            else:
+                bs.mode = "global"
+        if isinstance(v, (AppenderDev,)) and v.kinds is None:
+            raise DeviceUnsupported(f"vecbuilder[{v.kind.elem}] (nested element types) on the device")
+        return bs
+
+    return go(builders), bmap
+
+
+def _bsig(bs):
+    if isinstance(bs, tuple):
+        return tuple(_bsig(x) for x in bs)
+    return (repr(bs.kind), bs.mode, tuple(sorted((k, repr(v)) for k, v in bs.extra.items())))
+
+
+def _type_of(v, lam, name):
+    """IR type of a captured runtime value, recovered from the lambda body."""
+    from weldmill.expr import walk
+    for node in walk(lam.body):
+        if isinstance(node, Ident) and node.name == name and node.ty is not None:
+            return node.ty
+    raise EvalError(f"cannot type captured name {name!r}")
+
+
+# ---------------------------------------------------------------------------
+# result conversion
+
+
+def to_host_payload(v, ty):
+    if isinstance(ty, Scalar):
+        return v
+    if isinstance(ty, Struct):
+        return tuple(to_host_payload(x, t) for x, t in zip(v, ty.fields))
+    if isinstance(ty, Vec):
+        if isinstance(v, HostVec):
+            p = v.payload
+            if isinstance(p, list):
+                return p
+            v = v.dev()
+        return to_payload(v)
+    if isinstance(ty, Dict):
+        return dict_payload(v)
+    if isinstance(ty, Simd):
+        return tuple(v)
+    if isinstance(ty, Builder):
+        return v
+    raise DeviceUnsupported(f"cannot return a value of type {ty}")
+
+
+def _collect_ids(v, acc):
+    if isinstance(v, tuple):
+        for x in v:
+            _collect_ids(x, acc)
+    elif isinstance(v, (DVec, DDict, DGroups, HostVec)):
+        acc.add(id(v))
+
+
+def evaluate(e, env=None, config=None, externs=None, *, result="python", idx0=0, _ctx_out=None):
+    """Run a type-checked core expression on the GPU.  Returns (Value, EvalStats).
+
+    Same contract as weldmill.engine.evaluate (run.py:1008-1074).  Extra
+    keyword ``result``: "python" (the reference's payload: lists, tuples,
+    dicts), "device" (DVec / DDict handles left in HBM) or "numpy".
+    """
+    cfg = config or EngineConfig()
+    if cfg.threads < 1:
+        raise EvalError("threads must be at least 1")
+    if cfg.strategy not in STRATEGIES:
+        raise EvalError(f"unknown merge strategy {cfg.strategy!r}")
+    if cfg.grain_size < 1:
+        raise EvalError("grain_size must be at least 1")
+    if e.ty is None:
+        raise EvalError("expression must be type-checked before evaluation")
+    note_evaluation()
+    ctx = Ctx(cfg, externs, idx0=idx0)
+    if _ctx_out is not None:
+        _ctx_out.append(ctx)
+    frame = {}
+    for name, v in (env or {}).items():
+        payload = v.data if isinstance(v, Value) else v
+        ty = v.ty if isinstance(v, Value) else None
+        if isinstance(payload, DVec):
+            frame[name] = payload
+        elif ty is not None and isinstance(ty, Vec):
+            frame[name] = HostVec(ty, payload)
+        elif isinstance(payload, (list, np.ndarray)) and ty is None:
+            t = _infer_free_type(e, name)
+            frame[name] = HostVec(t, payload) if isinstance(t, Vec) else payload
+        else:
+            frame[name] = payload
+    try:
+        val = ctx.ev(e, frame)
+    except _DU as exc:
+        if isinstance(exc, EvalError):
+            raise
+        raise DeviceUnsupported(str(exc)) from None
+    ctx.check_device()
+    if result == "device":
+        payload = val
+    elif result == "numpy" and isinstance(val, DVec):
+        from .columns import to_numpy
+        payload = to_numpy(val)
+    else:
+        payload = to_host_payload(val, e.ty)
+
+    stats = EvalStats()
+    stats.vector_traversals = ctx.traversals
+    stats.vector_allocations = ctx.allocs
+    stats.tasks_created = ctx.tasks
+    reachable = set()
+    _collect_ids(val, reachable)
+    kept = 0
+    for obj, nbytes in ctx.registry:
+        if id(obj) in reachable:
+            kept += 1
+        else:
+            ctx.free(nbytes)
+    stats.peak_bytes = ctx.peak
+    stats.live_bytes = ctx.live
+    stats.intermediate_allocations = stats.vector_allocations - kept
+    return Value(e.ty, payload), stats
+
+
+def _infer_free_type(e, name):
+    from weldmill.expr import walk
+    for node in walk(e):
+        if isinstance(node, Ident) and node.name == name and node.ty is not None:
+            return node.ty
+    return None

@@ -1,0 +1,326 @@
+"""ctypes binding to libweldgpu.so (include/weldgpu.h).
+
+The library is built in-tree by ``__graft_entry__.build()``.  There is no
+fallback: if the library or a GPU is missing, device operations raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import hashlib
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libweldgpu.so")
+HEADER_PATH = os.path.join(_HERE, "csrc", "weld_device.cuh")
+
+NVRTC_OPTS = ("-arch=sm_100a", "-std=c++17", "-fmad=false", "-default-device", "-lineinfo")
+
+u64 = ctypes.c_uint64
+i64 = ctypes.c_int64
+c_int = ctypes.c_int
+c_char_p = ctypes.c_char_p
+c_void_p = ctypes.c_void_p
+
+_SIGS = {
+    "wg_last_error": (c_char_p, []),
+    "wg_version": (c_int, []),
+    "wg_device_count": (c_int, [ctypes.POINTER(c_int)]),
+    "wg_init": (c_int, [c_int]),
+    "wg_sm_count": (c_int, [ctypes.POINTER(c_int)]),
+    "wg_stream": (c_int, [ctypes.POINTER(u64)]),
+    "wg_sync": (c_int, []),
+    "wg_alloc": (c_int, [u64, ctypes.POINTER(u64)]),
+    "wg_free": (c_int, [u64]),
+    "wg_mem_stats": (c_int, [ctypes.POINTER(u64), ctypes.POINTER(u64)]),
+    "wg_mem_reset_peak": (c_int, []),
+    "wg_memset": (c_int, [u64, c_int, u64]),
+    "wg_h2d": (c_int, [u64, c_void_p, u64]),
+    "wg_d2h": (c_int, [c_void_p, u64, u64]),
+    "wg_d2h_async": (c_int, [c_void_p, u64, u64]),
+    "wg_d2d": (c_int, [u64, u64, u64]),
+    "wg_host_alloc": (c_int, [u64, ctypes.POINTER(c_void_p)]),
+    "wg_host_free": (c_int, [c_void_p]),
+    "wg_host_register": (c_int, [c_void_p, u64]),
+    "wg_host_unregister": (c_int, [c_void_p]),
+    "wg_error_ptr": (c_int, [ctypes.POINTER(u64)]),
+    "wg_read_error": (c_int, [ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+    "wg_compile": (c_int, [c_char_p, c_char_p, c_int, ctypes.POINTER(c_char_p), ctypes.POINTER(c_char_p), c_int,
+                           ctypes.POINTER(c_char_p), ctypes.POINTER(u64), c_char_p, u64]),
+    "wg_compile_check": (c_int, [c_char_p, c_char_p, c_int, ctypes.POINTER(c_char_p), ctypes.POINTER(c_char_p),
+                                 c_int, ctypes.POINTER(c_char_p), ctypes.POINTER(u64), c_char_p, u64]),
+    "wg_module_function": (c_int, [u64, c_char_p, ctypes.POINTER(u64)]),
+    "wg_occupancy": (c_int, [u64, c_int, c_int, ctypes.POINTER(c_int)]),
+    "wg_launch": (c_int, [u64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, c_void_p, u64]),
+    "wg_table_init": (c_int, [u64, u64, c_int, ctypes.POINTER(u64)]),
+    "wg_table_compact": (c_int, [u64, u64, c_int, c_int, ctypes.POINTER(u64), c_int, ctypes.POINTER(u64)]),
+    "wg_order_key": (c_int, [u64, c_int, u64, u64, u64]),
+    "wg_iota_u32": (c_int, [u64, u64]),
+    "wg_sort_pairs": (c_int, [u64, u64, u64, u64, u64, c_int, c_int]),
+    "wg_gather": (c_int, [u64, u64, u64, u64, c_int]),
+    "wg_narrow": (c_int, [u64, u64, c_int, u64]),
+    "wg_widen": (c_int, [u64, u64, c_int, u64]),
+    "wg_run_starts": (c_int, [ctypes.POINTER(u64), c_int, u64, u64, ctypes.POINTER(u64)]),
+    "wg_gen_column": (c_int, [u64, u64, u64, c_int, c_int, u64, u64, i64, u64, ctypes.c_double, ctypes.c_double,
+                              ctypes.c_double, c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]),
+    "wg_mul_inplace_f64": (c_int, [u64, u64, u64]),
+    "wg_flush_l2": (c_int, [u64, u64, ctypes.c_uint32]),
+    "wg_event_create": (c_int, [ctypes.POINTER(u64)]),
+    "wg_event_record": (c_int, [u64]),
+    "wg_event_elapsed_ms": (c_int, [u64, u64, ctypes.POINTER(ctypes.c_float)]),
+    "wg_event_destroy": (c_int, [u64]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+
+class WeldGpuError(RuntimeError):
+    pass
+
+
+_lib = None
+_lock = threading.RLock()
+_inited = False
+
+
+def load_library():
+    """Load libweldgpu.so (no device initialisation)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise WeldGpuError(
+                    f"{LIB_PATH} is missing: run __graft_entry__.build() (there is no CPU fallback)")
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, (res, args) in _SIGS.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+        return _lib
+
+
+def _check(rc):
+    if rc != 0:
+        raise WeldGpuError(load_library().wg_last_error().decode(errors="replace"))
+
+
+def call(name, *args):
+    _check(getattr(lib(), name)(*args))
+
+
+def lib():
+    """Library handle with the device initialised."""
+    global _inited
+    L = load_library()
+    if not _inited:
+        with _lock:
+            if not _inited:
+                dev = int(os.environ.get("LOCAL_RANK", os.environ.get("WELDGPU_DEVICE", "0")))
+                n = c_int(0)
+                rc = L.wg_device_count(ctypes.byref(n))
+                if rc != 0 or n.value == 0:
+                    raise WeldGpuError("no CUDA device visible: the weldgpu executor has no CPU fallback")
+                _check(L.wg_init(dev % n.value))
+                _inited = True
+    return L
+
+
+def sm_count():
+    n = c_int(0)
+    _check(lib().wg_sm_count(ctypes.byref(n)))
+    return n.value
+
+
+def stream_handle():
+    s = u64(0)
+    _check(lib().wg_stream(ctypes.byref(s)))
+    return s.value
+
+
+def sync():
+    _check(lib().wg_sync())
+
+
+# ---------------------------------------------------------------------------
+# Device buffers
+
+
+class DeviceBuffer:
+    """One stream-ordered device allocation; freed when garbage collected."""
+
+    __slots__ = ("ptr", "nbytes", "__weakref__")
+
+    def __init__(self, nbytes: int):
+        p = u64(0)
+        _check(lib().wg_alloc(max(int(nbytes), 1), ctypes.byref(p)))
+        self.ptr = p.value
+        self.nbytes = int(nbytes)
+
+    def free(self):
+        if self.ptr:
+            L = _lib
+            if L is not None:
+                L.wg_free(self.ptr)
+            self.ptr = 0
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    def __repr__(self):
+        return f"<DeviceBuffer 0x{self.ptr:x} {self.nbytes}B>"
+
+
+def alloc(nbytes):
+    return DeviceBuffer(nbytes)
+
+
+def memset(buf_ptr, value, nbytes):
+    _check(lib().wg_memset(buf_ptr, value, nbytes))
+
+
+def h2d(dst_ptr, host_ptr, nbytes):
+    _check(lib().wg_h2d(dst_ptr, host_ptr, nbytes))
+
+
+def d2h(host_ptr, src_ptr, nbytes):
+    _check(lib().wg_d2h(host_ptr, src_ptr, nbytes))
+
+
+def d2h_async(host_ptr, src_ptr, nbytes):
+    _check(lib().wg_d2h_async(host_ptr, src_ptr, nbytes))
+
+
+def d2d(dst_ptr, src_ptr, nbytes):
+    _check(lib().wg_d2d(dst_ptr, src_ptr, nbytes))
+
+
+def read_error():
+    c, i = i64(0), i64(0)
+    _check(lib().wg_read_error(ctypes.byref(c), ctypes.byref(i)))
+    return c.value, i.value
+
+
+def error_ptr():
+    p = u64(0)
+    _check(lib().wg_error_ptr(ctypes.byref(p)))
+    return p.value
+
+
+def mem_stats():
+    a, b = u64(0), u64(0)
+    _check(lib().wg_mem_stats(ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
+
+
+# ---------------------------------------------------------------------------
+# NVRTC kernels
+
+
+_header_text = None
+_modules = {}
+
+
+def header_text():
+    global _header_text
+    if _header_text is None:
+        with open(HEADER_PATH) as f:
+            _header_text = f.read()
+    return _header_text
+
+
+def _nvrtc_args(src):
+    hdr = header_text().encode()
+    hs = (c_char_p * 1)(hdr)
+    hn = (c_char_p * 1)(b"weld_device.cuh")
+    opts = [o.encode() for o in NVRTC_OPTS]
+    oa = (c_char_p * len(opts))(*opts)
+    return hs, hn, oa, len(opts)
+
+
+def compile_check(src: str, name="weld_loop.cu"):
+    """Compile for sm_100a without loading (works with no GPU).  Returns the
+    cubin size; raises WeldGpuError with the NVRTC log on failure."""
+    L = load_library()
+    hs, hn, oa, no = _nvrtc_args(src)
+    sz = u64(0)
+    log = ctypes.create_string_buffer(1 << 16)
+    rc = L.wg_compile_check(src.encode(), name.encode(), 1, hs, hn, no, oa, ctypes.byref(sz), log, 1 << 16)
+    if rc != 0:
+        raise WeldGpuError(L.wg_last_error().decode(errors="replace"))
+    return sz.value
+
+
+class Kernel:
+    __slots__ = ("fn", "name", "occ")
+
+    def __init__(self, fn, name):
+        self.fn = fn
+        self.name = name
+        self.occ = {}
+
+    def blocks_per_sm(self, block, smem=0):
+        key = (block, smem)
+        v = self.occ.get(key)
+        if v is None:
+            n = c_int(0)
+            _check(lib().wg_occupancy(self.fn, block, smem, ctypes.byref(n)))
+            v = self.occ[key] = max(1, n.value)
+        return v
+
+    def launch(self, grid, block, params: bytes, smem=0):
+        buf = ctypes.create_string_buffer(params, len(params))
+        _check(lib().wg_launch(self.fn, grid, block, smem, buf, len(params)))
+
+
+def get_kernel(src: str, name: str) -> Kernel:
+    """Compile (cached by source hash) and return the named kernel."""
+    key = hashlib.sha1(src.encode()).hexdigest()
+    with _lock:
+        mod = _modules.get(key)
+        if mod is None:
+            L = lib()
+            hs, hn, oa, no = _nvrtc_args(src)
+            m = u64(0)
+            log = ctypes.create_string_buffer(1 << 16)
+            rc = L.wg_compile(src.encode(), f"wg_{key[:12]}.cu".encode(), 1, hs, hn, no, oa, ctypes.byref(m),
+                              log, 1 << 16)
+            if rc != 0:
+                raise WeldGpuError(L.wg_last_error().decode(errors="replace"))
+            mod = _modules[key] = (m.value, {})
+        handle, fns = mod
+        k = fns.get(name)
+        if k is None:
+            f = u64(0)
+            _check(lib().wg_module_function(handle, name.encode(), ctypes.byref(f)))
+            k = fns[name] = Kernel(f.value, name)
+        return k
+
+
+# ---------------------------------------------------------------------------
+# Events (bench timing on the library's own stream)
+
+
+class Event:
+    def __init__(self):
+        e = u64(0)
+        _check(lib().wg_event_create(ctypes.byref(e)))
+        self.h = e.value
+
+    def record(self):
+        _check(lib().wg_event_record(self.h))
+
+    def elapsed_ms(self, later: "Event") -> float:
+        ms = ctypes.c_float(0)
+        _check(lib().wg_event_elapsed_ms(self.h, later.h, ctypes.byref(ms)))
+        return ms.value
+
+    def __del__(self):
+        try:
+            if _lib is not None:
+                _lib.wg_event_destroy(self.h)
+        except Exception:
+            pass

@@ -1,0 +1,137 @@
+"""GPU parity on the five benchmark programs (BASELINE.json configs).
+
+* n = 4096: against the reference engine's own outputs (golden fixture).
+* n = 2^20 (+ ragged tails): against the numpy oracle (pinned to the same
+  goldens by tests/test_oracle.py).
+* full / large n: size-independent properties (put-call parity, conserved
+  sums and counts, per-key order, sortedness).
+"""
+import math
+
+import numpy as np
+import pytest
+
+from helpers import F64_TOL, approx_equal, first_diff, load_golden, norm
+
+pytestmark = pytest.mark.gpu
+
+GOLD = load_golden("configs.json")
+
+
+def _run(name, n, row0=0, device_inputs=False, result="python"):
+    import paper_1709_06416_b200 as wg
+    from paper_1709_06416_b200 import workloads as W
+    from weldmill.engine import EngineConfig, Value
+    wl = W.WORKLOADS[name]
+    tree = W.compile_program(wl)
+    types = W.input_types(wl)
+    if device_inputs:
+        cols = W.device_columns(wl, n, row0)
+        env = {k: Value(types[k], v) for k, v in cols.items()}
+    else:
+        cols = W.host_columns(wl, n, row0)
+        env = {k: Value(types[k], v) for k, v in cols.items()}
+    val, stats = wg.evaluate(tree, env, EngineConfig(memory_limit=1 << 45), W.externs_for(wl), result=result)
+    return val.data, stats, cols
+
+
+@pytest.mark.parametrize("name", ["q6", "blackscholes", "q1", "dict", "group", "hist"])
+def test_matches_reference_goldens(name):
+    g = GOLD[name]
+    got, _, _ = _run(name, g["n"])
+    got = norm(got)
+    if name == "hist":
+        got = [[i, x] for i, x in enumerate(got) if x != 0.0]
+    want = g["expected"]
+    if name in ("dict", "group"):
+        assert got == want
+    else:
+        assert approx_equal(got, want, F64_TOL), first_diff(got, want, F64_TOL)
+
+
+@pytest.mark.parametrize("name", ["q6", "blackscholes", "q1", "dict", "group", "hist"])
+@pytest.mark.parametrize("n", [1, 1000, 1 << 20, (1 << 20) + 3])
+def test_matches_oracle(name, n):
+    from oracle import weld_oracle
+    got, _, cols = _run(name, n)
+    want = weld_oracle.as_reference_payload(name, weld_oracle.ORACLES[name](cols))
+    got = norm(got)
+    if name == "hist":
+        got = [[i, x] for i, x in enumerate(got) if x != 0.0]
+    want = norm(want)
+    if name in ("dict", "group"):
+        assert got == want
+    else:
+        assert approx_equal(got, want, F64_TOL), first_diff(got, want, F64_TOL)
+
+
+def test_empty_inputs_give_identities():
+    got, stats, _ = _run("q6", 0)
+    assert got == 0.0 and stats.vector_traversals == 0
+    assert _run("q1", 0)[0] == []
+    assert _run("dict", 0)[0] == []
+    assert _run("group", 0)[0] == []
+    assert _run("blackscholes", 0)[0] == ([], [])
+
+
+def test_device_generator_matches_host():
+    from paper_1709_06416_b200 import workloads as W
+    from paper_1709_06416_b200.columns import to_numpy
+    for name, wl in W.WORKLOADS.items():
+        h = W.host_columns(wl, 5000, row0=123)
+        d = W.device_columns(wl, 5000, row0=123)
+        for k in h:
+            np.testing.assert_array_equal(to_numpy(d[k]), h[k], err_msg=f"{name}.{k}")
+
+
+def test_blackscholes_large_put_call_parity():
+    """C - P = S - K e^{-rT} for every option (full-path property check)."""
+    from paper_1709_06416_b200.columns import to_numpy
+    n = 8 << 20
+    out, _, cols = _run("blackscholes", n, device_inputs=True, result="device")
+    call, put = (to_numpy(v) for v in out)
+    s, k, t, r = (to_numpy(cols[c]) for c in ("s", "k", "t", "r"))
+    resid = (call - put) - (s - k * np.exp(-r * t))
+    assert call.shape == (n,) and put.shape == (n,)
+    assert np.max(np.abs(resid)) < 1e-9 * 100
+
+
+def test_dict_large_conserves_sum_and_is_sorted():
+    from paper_1709_06416_b200.columns import to_numpy
+    n = 16 << 20
+    out, _, cols = _run("dict", n, device_inputs=True, result="device")
+    keys, sums = to_numpy(out)
+    v = to_numpy(cols["v"])
+    k = to_numpy(cols["k"])
+    assert int(sums.sum()) == int(v.sum())
+    assert np.all(keys[1:] > keys[:-1])
+    assert keys.size == np.unique(k).size
+
+
+def test_group_large_preserves_per_key_order():
+    from paper_1709_06416_b200.columns import to_numpy
+    from oracle import weld_oracle
+    n = 4 << 20
+    out, _, cols = _run("group", n, device_inputs=True, result="device")
+    k = to_numpy(cols["k"])
+    v = to_numpy(cols["v"])
+    ks, offs, vs = weld_oracle.group({"k": k, "v": v})
+    from paper_1709_06416_b200.columns import col_to_numpy
+    gk = col_to_numpy(out.layout[0], out.n)
+    lay = out.layout[1]
+    goffs = col_to_numpy(lay.offsets, out.n + 1)
+    gvals = col_to_numpy(lay.child, lay.total)
+    np.testing.assert_array_equal(gk, ks)
+    np.testing.assert_array_equal(goffs, offs)
+    np.testing.assert_array_equal(gvals, vs)
+
+
+def test_hist_large_conserves_weight():
+    from paper_1709_06416_b200.columns import to_numpy
+    n = 64 << 20
+    out, _, cols = _run("hist", n, device_inputs=True, result="device")
+    bins = to_numpy(out)
+    w = to_numpy(cols["w"])
+    idx = to_numpy(cols["idx"])
+    ref = np.bincount(idx, weights=w, minlength=bins.size)
+    assert np.allclose(bins, ref, rtol=1e-9, atol=1e-9)
