@@ -37,6 +37,7 @@ int wg_sync(void);
  *      run.py:184-228, builders.py:59-106) --------------------------------- */
 int wg_alloc(uint64_t bytes, uint64_t* dptr);
 int wg_free(uint64_t dptr);
+int wg_mem_trim(void);
 int wg_mem_stats(uint64_t* live, uint64_t* peak);
 int wg_mem_reset_peak(void);
 int wg_memset(uint64_t dptr, int value, uint64_t bytes);

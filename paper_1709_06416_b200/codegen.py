@@ -52,6 +52,13 @@ from .irtypes import (
 W = 4  # SIMD_WIDTH (types.py:15)
 BLOCK = 256
 
+import os as _os
+
+# Tuning knobs (defaults chosen from ncu measurements).
+PREFETCH = _os.environ.get("WELDGPU_PREFETCH", "1") == "1"
+MINBLOCKS = int(_os.environ.get("WELDGPU_MINBLOCKS", "0"))
+ITEMS_OVERRIDE = int(_os.environ.get("WELDGPU_ITEMS", "0"))
+
 # Extern names recognised as device intrinsics (the reference resolves
 # `call(name, ...)` through a host registry, run.py:832-846).
 EXTERN_F64 = {
@@ -937,7 +944,7 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
         raise DeviceUnsupported("loop function must be a lambda literal")
     pb, pi, px = (p.name for p in lam.params)
 
-    ITEMS = items or choose_items(iters)
+    ITEMS = items or ITEMS_OVERRIDE or choose_items(iters)
     g.items = ITEMS
 
     # builders value seen by the body
@@ -1115,7 +1122,8 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
     for p_ in g.params:
         src.append(f"  {p_.ctype} {p_.name};")
     src.append("};")
-    src.append(f'extern "C" __global__ void __launch_bounds__(BLOCK) {name}(const Params p) {{')
+    lb = f"BLOCK, {MINBLOCKS}" if MINBLOCKS else "BLOCK"
+    src.append(f'extern "C" __global__ void __launch_bounds__({lb}) {name}(const Params p) {{')
     src.append("  extern __shared__ __align__(16) u64 wg_dyn_smem[];")
     src.extend("  " + d for d in smem_decls)
     src.extend("  " + d for d in smem_init)
@@ -1136,20 +1144,45 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
         src.append("    __syncthreads();")
         src.append("    const i64 tile = s_tile;")
         src.append("    if (tile >= ntiles) break;")
-    else:
+    def load_lines(tvar, suffix, ind):
+        out = [f"{ind}{{ const i64 lt0_ = {tvar} * TILE + (i64)threadIdx.x * ITEMS; const bool lfull_ = (lt0_ + ITEMS <= n);"]
+        for (arr, st, kk, per, k, l, col) in loads:
+            cnt = f"ITEMS * {per}" if per > 1 else "ITEMS"
+            a = arr + suffix
+            if iters[k].strided:
+                out.append(f"{ind}  for (int q = 0; q < ITEMS; ++q) {{ const i64 li_ = lt0_ + q; "
+                           f"{a}[q] = (li_ < n) ? {col}[p.it{k}_start + li_ * p.it{k}_stride] : ({st})0; }}")
+            else:
+                out.append(f"{ind}  if (lfull_) wg_load_contig<{st}, {cnt}>({col} + lt0_ * {per}, {a});")
+                out.append(f"{ind}  else {{ for (int q = 0; q < {cnt}; ++q) {{ const i64 e_ = lt0_ * {per} + q; "
+                           f"{a}[q] = (e_ < n * {per}) ? {col}[e_] : ({st})0; }} }}")
+        out.append(f"{ind}}}")
+        return out
+
+    def decl_lines(suffix, ind):
+        return [f"{ind}alignas(16) {st} {arr}{suffix}[{'ITEMS * %d' % per if per > 1 else 'ITEMS'}];"
+                for (arr, st, kk, per, k, l, col) in loads]
+
+    prefetch = (not scan_bs) and PREFETCH
+    if not scan_bs and prefetch:
+        # register double buffering: the next tile's columns are in flight
+        # while the current tile computes
+        src.extend(decl_lines("", "  "))
+        src.append("  i64 tile = blockIdx.x;")
+        src.append("  if (tile < ntiles)")
+        src.extend(load_lines("tile", "", "  "))
+        src.append("  for (; tile < ntiles; tile += gridDim.x) {")
+        src.extend(decl_lines("_nx", "    "))
+        src.append("    const i64 ntile_ = tile + gridDim.x;")
+        src.append("    if (ntile_ < ntiles)")
+        src.extend(load_lines("ntile_", "_nx", "    "))
+    elif not scan_bs:
         src.append("  for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {")
+    if not prefetch:
+        src.extend(decl_lines("", "    "))
+        src.extend(load_lines("tile", "", "    "))
     src.append("    const i64 t0 = tile * TILE + (i64)threadIdx.x * ITEMS;")
     src.append("    const bool full = (t0 + ITEMS <= n);")
-    for (arr, st, kk, per, k, l, col) in loads:
-        cnt = f"ITEMS * {per}" if per > 1 else "ITEMS"
-        src.append(f"    alignas(16) {st} {arr}[{cnt}];")
-        if iters[k].strided:
-            src.append(f"    for (int q = 0; q < ITEMS; ++q) {{ const i64 li_ = t0 + q; "
-                       f"{arr}[q] = (li_ < n) ? {col}[p.it{k}_start + li_ * p.it{k}_stride] : ({st})0; }}")
-        else:
-            src.append(f"    if (full) wg_load_contig<{st}, {cnt}>({col} + t0 * {per}, {arr});")
-            src.append(f"    else {{ for (int q = 0; q < {cnt}; ++q) {{ const i64 e_ = t0 * {per} + q; "
-                       f"{arr}[q] = (e_ < n * {per}) ? {col}[e_] : ({st})0; }} }}")
     for b in g.bspecs:
         if b.mode == "direct" and b.extra.get("buffered"):
             for f, kk in enumerate(b.extra["kinds"]):
@@ -1190,6 +1223,10 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
         src.extend(body_b)
         src.append("      }")
         src.append("    }")
+    if prefetch:
+        for (arr, st, kk, per, k, l, col) in loads:
+            cnt = f"ITEMS * {per}" if per > 1 else "ITEMS"
+            src.append(f"#pragma unroll\n    for (int q = 0; q < {cnt}; ++q) {arr}[q] = {arr}_nx[q];")
     src.append("  }")
     # epilogue: shared-memory flushes
     if smem_flush:

@@ -18,7 +18,9 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -36,7 +38,9 @@ int64_t* g_err_word = nullptr;      // device {code, info}
 int64_t* g_err_host = nullptr;      // pinned mirror
 uint64_t g_live = 0, g_peak = 0;    // device bytes handed out by wg_alloc
 std::mutex g_acct_mu;
-std::vector<std::pair<void*, uint64_t>> g_sizes;  // small registry for accounting
+std::unordered_map<void*, uint64_t> g_sizes;       // live blocks -> rounded size
+std::multimap<uint64_t, void*> g_free;             // cached blocks by size
+uint64_t g_cached = 0;
 
 int fail(const std::string& msg) {
   g_err = msg;
@@ -299,7 +303,7 @@ int wg_init(int device) {
   CK(cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, device));
   cudaMemPool_t pool;
   CK(cudaDeviceGetDefaultMemPool(&pool, device));
-  uint64_t thr = UINT64_MAX;
+  uint64_t thr = UINT64_MAX;  // temporaries (CUB scratch) use the stream-ordered pool
   CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
   CK(cudaMalloc((void**)&g_err_word, 64));
   CK(cudaMemset(g_err_word, 0, 64));
@@ -316,17 +320,53 @@ int wg_stream(uint64_t* s) { NEED_INIT(); *s = (uint64_t)(uintptr_t)g_stream; re
 int wg_sync(void) { NEED_INIT(); CK(cudaStreamSynchronize(g_stream)); return 0; }
 
 // ---- buffer manager --------------------------------------------------------
+// Caching allocator.  Everything runs on one stream, so a freed block can
+// be handed to the next request immediately: stream order guarantees the
+// previous user's kernels finished before the new user's start.  Blocks
+// are rounded (pow2 below 2 MiB, 2 MiB multiples above) and a request
+// reuses any cached block up to 2x its size.  cudaMalloc runs only when
+// the cache cannot serve a request (and on OOM the cache is released and
+// the request retried).
 int wg_alloc(uint64_t bytes, uint64_t* dptr) {
   NEED_INIT();
-  void* p = nullptr;
   uint64_t b = bytes ? bytes : 1;
-  b = (b + 255) & ~255ULL;
-  CK(cudaMallocAsync(&p, b, g_stream));
+  if (b < (2ULL << 20)) {
+    uint64_t r = 256;
+    while (r < b) r <<= 1;
+    b = r;
+  } else {
+    b = (b + (2ULL << 20) - 1) & ~((2ULL << 20) - 1);
+  }
+  void* p = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_acct_mu);
+    auto it = g_free.lower_bound(b);
+    if (it != g_free.end() && it->first <= 2 * b) {
+      p = it->second;
+      b = it->first;
+      g_free.erase(it);
+      g_cached -= b;
+    }
+  }
+  if (!p) {
+    cudaError_t e = cudaMalloc(&p, b);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      CK(cudaStreamSynchronize(g_stream));
+      {
+        std::lock_guard<std::mutex> lk(g_acct_mu);
+        for (auto& kv : g_free) cudaFree(kv.second);
+        g_free.clear();
+        g_cached = 0;
+      }
+      CK(cudaMalloc(&p, b));
+    }
+  }
   *dptr = (uint64_t)(uintptr_t)p;
   std::lock_guard<std::mutex> lk(g_acct_mu);
   g_live += b;
   if (g_live > g_peak) g_peak = g_live;
-  g_sizes.emplace_back(p, b);
+  g_sizes[p] = b;
   return 0;
 }
 
@@ -334,16 +374,23 @@ int wg_free(uint64_t dptr) {
   NEED_INIT();
   if (!dptr) return 0;
   void* p = (void*)(uintptr_t)dptr;
-  CK(cudaFreeAsync(p, g_stream));
   std::lock_guard<std::mutex> lk(g_acct_mu);
-  for (size_t i = g_sizes.size(); i-- > 0;) {
-    if (g_sizes[i].first == p) {
-      g_live -= g_sizes[i].second;
-      g_sizes[i] = g_sizes.back();
-      g_sizes.pop_back();
-      break;
-    }
-  }
+  auto it = g_sizes.find(p);
+  if (it == g_sizes.end()) return fail("wg_free: unknown device pointer");
+  g_live -= it->second;
+  g_free.emplace(it->second, p);
+  g_cached += it->second;
+  g_sizes.erase(it);
+  return 0;
+}
+
+int wg_mem_trim(void) {
+  NEED_INIT();
+  CK(cudaStreamSynchronize(g_stream));
+  std::lock_guard<std::mutex> lk(g_acct_mu);
+  for (auto& kv : g_free) cudaFree(kv.second);
+  g_free.clear();
+  g_cached = 0;
   return 0;
 }
 

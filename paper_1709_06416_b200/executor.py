@@ -105,6 +105,7 @@ class _Plan:
 
 _plan_cache = {}
 _plan_lock = threading.Lock()
+_fv_cache = {}
 
 
 class Ctx:
@@ -374,26 +375,22 @@ class Ctx:
                 n = 0
             else:
                 cols, n = b.concat()
-            self.check_device()
             self.free(getattr(b, "acct", 0))
             out = dvec_from_cols(kind.elem, n, cols)
             self.materialized(out, 16 + n * _slot_bytes(kind.elem))
             return out
         if isinstance(kind, VecMerger):
-            self.check_device()
             self.free(getattr(b, "acct", 0))
             out = dvec_from_cols(kind.elem, b.n, b.cols)
             self.materialized(out, 16 + b.n * _slot_bytes(kind.elem))
             return out
         if isinstance(kind, DictMerger):
-            self.check_device()
             if b.table is None:
                 b.ensure(1)
             d = finish_dict(b, Dict(kind.key, kind.value))
             self.materialized(d, 16 + d.n * (16 + _slot_bytes(kind.key) + _slot_bytes(kind.value)))
             return d
         if isinstance(kind, GroupBuilder):
-            self.check_device()
             g = finish_groups(b, Dict(kind.key, Vec(kind.value)))
             self.materialized(g, 16 + g.n * (16 + _slot_bytes(kind.key) + 16) + g.vals.n * _slot_bytes(kind.value))
             return g
@@ -432,7 +429,6 @@ class Ctx:
             env2.update({"__v": dv, "__kbs": kb})
             self.run_loop(loop, env2, count_traversal=False)
             kcols, _ = kb.concat()
-            self.check_device()
             perm = sort_perm(kcols, n)
             out = dvec_from_cols(dv.elem, n, gather_cols(dv.cols, perm, n))
         self.materialized(out, 16 + n * _slot_bytes(dv.elem))
@@ -495,13 +491,16 @@ class Ctx:
             b.check()
             self.flush_pending(b)
         # loop-invariant captures
-        pnames = {p.name for p in lam.params}
+        fv = _fv_cache.get(id(lam))
+        if fv is None or fv[0] is not lam:
+            pn = {p.name for p in lam.params}
+            names = sorted(free_variables(lam) - pn)
+            fv = _fv_cache[id(lam)] = (lam, [(nm, _type_of(None, lam, nm)) for nm in names])
         captures = {}
-        for name in sorted(free_variables(lam) - pnames):
-            v = lenv.get(name)
-            if v is None and name not in lenv:
+        for name, cty in fv[1]:
+            if name not in lenv:
                 raise EvalError(f"unbound name {name!r}")
-            captures[name] = (_type_of(v, lam, name), v)
+            captures[name] = (cty, lenv[name])
 
         strategy = self.cfg.strategy
         bstruct, bmap = _bspecs(builders, strategy, count)
@@ -829,6 +828,17 @@ def to_host_payload(v, ty):
     raise DeviceUnsupported(f"cannot return a value of type {ty}")
 
 
+def _numpy_tree(v, ty):
+    from .columns import to_numpy
+    if isinstance(v, tuple) and isinstance(ty, Struct):
+        return tuple(_numpy_tree(x, t) for x, t in zip(v, ty.fields))
+    if isinstance(v, HostVec):
+        v = v.dev()
+    if isinstance(v, DVec) and is_flat(v.elem):
+        return to_numpy(v)
+    return to_host_payload(v, ty)
+
+
 def _collect_ids(v, acc):
     if isinstance(v, tuple):
         for x in v:
@@ -879,9 +889,8 @@ def evaluate(e, env=None, config=None, externs=None, *, result="python", idx0=0,
     ctx.check_device()
     if result == "device":
         payload = val
-    elif result == "numpy" and isinstance(val, DVec):
-        from .columns import to_numpy
-        payload = to_numpy(val)
+    elif result == "numpy":
+        payload = _numpy_tree(val, e.ty)
     else:
         payload = to_host_payload(val, e.ty)
 

@@ -32,6 +32,7 @@ _SIGS = {
     "wg_sync": (c_int, []),
     "wg_alloc": (c_int, [u64, ctypes.POINTER(u64)]),
     "wg_free": (c_int, [u64]),
+    "wg_mem_trim": (c_int, []),
     "wg_mem_stats": (c_int, [ctypes.POINTER(u64), ctypes.POINTER(u64)]),
     "wg_mem_reset_peak": (c_int, []),
     "wg_memset": (c_int, [u64, c_int, u64]),
@@ -107,6 +108,7 @@ def _check(rc):
 
 def call(name, *args):
     _check(getattr(lib(), name)(*args))
+    LAUNCHES[0] += _KERNEL_CALLS.get(name, 0)
 
 
 def lib():
@@ -176,6 +178,15 @@ class DeviceBuffer:
 
 def alloc(nbytes):
     return DeviceBuffer(nbytes)
+
+
+def host_register(arr):
+    """Pin a numpy array's pages (cudaHostRegister) for async copies."""
+    _check(lib().wg_host_register(arr.ctypes.data, arr.nbytes))
+
+
+def host_unregister(arr):
+    _check(lib().wg_host_unregister(arr.ctypes.data))
 
 
 def memset(buf_ptr, value, nbytes):
@@ -254,6 +265,15 @@ def compile_check(src: str, name="weld_loop.cu"):
     return sz.value
 
 
+# Instrumentation: number of this library's kernels launched, and an
+# optional hook called around each generated-kernel launch (bench timing).
+LAUNCHES = [0]
+LAUNCH_HOOK = [None]
+_KERNEL_CALLS = {"wg_table_init": 1, "wg_table_compact": 1, "wg_order_key": 1, "wg_iota_u32": 1,
+                 "wg_sort_pairs": 1, "wg_gather": 1, "wg_narrow": 1, "wg_widen": 1, "wg_run_starts": 2,
+                 "wg_gen_column": 1, "wg_mul_inplace_f64": 1, "wg_flush_l2": 1}
+
+
 class Kernel:
     __slots__ = ("fn", "name", "occ")
 
@@ -273,7 +293,13 @@ class Kernel:
 
     def launch(self, grid, block, params: bytes, smem=0):
         buf = ctypes.create_string_buffer(params, len(params))
+        hook = LAUNCH_HOOK[0]
+        if hook is not None:
+            hook("before", self)
         _check(lib().wg_launch(self.fn, grid, block, smem, buf, len(params)))
+        LAUNCHES[0] += 1
+        if hook is not None:
+            hook("after", self)
 
 
 def get_kernel(src: str, name: str) -> Kernel:
