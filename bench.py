@@ -260,17 +260,24 @@ def main():
         if dist is not None:
             dist.barrier()
 
+    # Warm-up mirrors the timed loop exactly (the previous step's result is
+    # still alive while the next one allocates), so the allocator cache is
+    # in steady state before timing starts.
+    out = None
     for _ in range(args.warmup):
-        wg.evaluate(tree, env, cfg, ext, result="device")
+        out = wg.evaluate(tree, env, cfg, ext, result="device")
     rt.sync()
 
     clocks = Clocks(int(os.environ.get("LOCAL_RANK", "0"))) if rank == 0 else None
+    if clocks:
+        clocks.start()
+        time.sleep(0.5)
+    import gc
+    gc.collect()
+    gc.disable()          # no collector pauses inside the timed region
     launches0 = rt.LAUNCHES[0]
     barrier()
     rt.sync()
-    if clocks:
-        clocks.start()
-        time.sleep(0.3)
     e0, e1 = rt.Event(), rt.Event()
     e0.record()
     for _ in range(args.steps):
@@ -288,6 +295,7 @@ def main():
         rt.sync()
         rt.LAUNCH_HOOK[0] = None
     clk = clocks.stop() if clocks else None
+    gc.enable()
 
     # dominant generated kernel
     dom_tot, dom_ms, dom_name = 0.0, 0.0, None

@@ -85,6 +85,8 @@ int wg_gather(uint64_t src, uint64_t perm, uint64_t dst, uint64_t n, int width);
 int wg_narrow(uint64_t src, uint64_t dst, int width, uint64_t n);
 int wg_widen(uint64_t src, uint64_t dst, int width, uint64_t n);
 int wg_run_starts(const uint64_t* key_words, int kw, uint64_t n, uint64_t starts_out, uint64_t* nruns);
+int wg_group_finish1(uint64_t keys, int key_kind, uint64_t vals, int val_width, uint64_t n, uint64_t ukeys_out,
+                     uint64_t offs_out, uint64_t vals_out, uint64_t* K_out);
 
 /* ---- synthetic inputs and measurement (bench.py; no reference analogue) -- */
 int wg_gen_column(uint64_t dst, uint64_t n, uint64_t row0, int dist, int width, uint64_t seed, uint64_t col,

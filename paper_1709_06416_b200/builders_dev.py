@@ -149,14 +149,21 @@ class VecMergerDev(BuilderBase):
             self.cols.append(nc)
 
 
+_SIZE_HINTS = {}   # loop identity -> distinct keys seen last time (table sizing)
+
+
 class DictDev(BuilderBase):
     """dictmerger state: an open-addressing table of 8-byte words.
 
     slot = [key word] + values          (one-word keys, EMPTY = all ones)
          = [state, key words] + values  (multi-word keys)
-    New keys are refused once the distinct count reaches `limit` (load
-    <= 0.5); refused merges spill to an overflow list and the host grows
-    the table and replays them (grow_and_replay)."""
+    Value fields are pre-initialised to the fold's internal identity, so a
+    claimed slot is merged into with plain atomics.  An insert that finds
+    WG_MAX_PROBE foreign keys in a row spills to the overflow list; the host
+    then grows the table (4x the distinct count), re-inserts the entries and
+    replays the spilled merges (all dict folds are commutative).  The table
+    is sized from the distinct count the same loop produced last time, else
+    from min(merges, 2^20)."""
 
     def __init__(self, kind: DictMerger):
         super().__init__(kind)
@@ -167,23 +174,33 @@ class DictDev(BuilderBase):
         self.slot_words = self.kbase + len(self.vks)
         self.table = None
         self.cap = 0
-        self.count = rt.alloc(8)
-        rt.memset(self.count.ptr, 0, 8)
-        self.ocount = rt.alloc(8)
-        rt.memset(self.ocount.ptr, 0, 8)
+        self.counters = rt.alloc(16)          # [distinct keys, spilled merges]
+        rt.memset(self.counters.ptr, 0, 16)
         self.over = None
         self.ocap = 0
+        self.hint_key = None
+        self.distinct = 0
+
+    @property
+    def count(self):
+        return _Ptr(self.counters.ptr)
+
+    @property
+    def ocount(self):
+        return _Ptr(self.counters.ptr + 8)
 
     def pattern(self):
         head = [ALL_ONES] if self.nw == 1 else [0] * (1 + self.nw)
         return head + [to_bits(k, internal_identity(self.kind.op, k)) for k in self.vks]
 
-    def ensure(self, rows):
-        """Size the table for up to `rows` new merges (capped; overflow
-        handles the rest) and the overflow list for one launch."""
+    def ensure(self, rows, hint_key=None):
+        """Size the table before a launch of `rows` merges, and the spill
+        list for that launch."""
         if self.table is None:
-            want = 1 << max(10, int(min(rows, 1 << 24) * 2 - 1).bit_length())
-            self._alloc_table(want)
+            self.hint_key = hint_key
+            seen = _SIZE_HINTS.get(hint_key)
+            want = seen if seen is not None else min(rows, 1 << 20)
+            self._alloc_table(1 << max(10, int(max(want, 1) * 2 - 1).bit_length()))
         if rows > self.ocap:
             self.over = ([rt.alloc(8 * rows) for _ in range(self.nw)],
                          [rt.alloc(8 * rows) for _ in self.vks])
@@ -194,26 +211,35 @@ class DictDev(BuilderBase):
         self.table = rt.alloc(8 * (cap + 1) * self.slot_words)
         pat = (ctypes.c_uint64 * self.slot_words)(*self.pattern())
         rt.call("wg_table_init", self.table.ptr, cap + 1, self.slot_words, pat)
-        rt.memset(self.count.ptr, 0, 8)
+        rt.memset(self.counters.ptr, 0, 16)
 
-    @property
-    def limit(self):
-        return self.cap // 2
-
-    def overflow_rows(self):
-        arr = np.zeros(1, dtype=np.uint64)
-        rt.d2h(arr.ctypes.data, self.ocount.ptr, 8)
-        return int(arr[0])
+    def read_counters(self):
+        arr = np.zeros(2, dtype=np.uint64)
+        rt.d2h(arr.ctypes.data, self.counters.ptr, 16)
+        self.distinct = int(arr[0])
+        if self.hint_key is not None:
+            _SIZE_HINTS[self.hint_key] = max(self.distinct, _SIZE_HINTS.get(self.hint_key, 0))
+        return self.distinct, int(arr[1])
 
     def compact(self):
         """Occupied entries as SoA word columns (keys words, value words)."""
+        distinct, _ = self.read_counters()
         nout = self.nw + len(self.vks)
-        outs = [rt.alloc(8 * (self.cap + 1)) for _ in range(nout)]
+        outs = [rt.alloc(8 * (distinct + 1)) for _ in range(nout)]
         ptrs = (ctypes.c_uint64 * nout)(*[o.ptr for o in outs])
         cnt = ctypes.c_uint64(0)
         mode = 1 if self.nw == 1 else 2
         rt.call("wg_table_compact", self.table.ptr, self.cap, self.slot_words, mode, ptrs, nout, ctypes.byref(cnt))
+        if cnt.value != distinct:
+            raise RuntimeError(f"dictmerger table holds {cnt.value} keys, counted {distinct}")
         return outs[:self.nw], outs[self.nw:], cnt.value
+
+
+class _Ptr:
+    __slots__ = ("ptr",)
+
+    def __init__(self, ptr):
+        self.ptr = ptr
 
 
 class GroupDev(AppenderDev):
@@ -349,6 +375,17 @@ def finish_groups(g: GroupDev, dict_ty):
     cols, n = g.concat()
     nk = len(g.kks)
     kcols, vcols = cols[:nk], cols[nk:]
+    if nk == 1 and len(vcols) == 1 and g.kks[0] in (BOOL, I32, I64) and n < (1 << 32):
+        # device fast path: adaptive-window radix sort + bucket sort + run starts
+        ukeys = Col.alloc(g.kks[0], max(n, 1))
+        offs = Col.alloc(I64, n + 1)
+        vout = Col.alloc(vcols[0].kind, max(n, 1))
+        K = ctypes.c_uint64(0)
+        rt.call("wg_group_finish1", kcols[0].ptr, KIND_CODE[g.kks[0]], vcols[0].ptr, SIZE[vcols[0].kind], n,
+                ukeys.ptr, offs.ptr, vout.ptr, ctypes.byref(K))
+        K = K.value
+        return DGroups(dict_ty, dvec_from_cols(dict_ty.key, K, [ukeys]), offs,
+                       dvec_from_cols(dict_ty.value.elem, n, [vout]))
     perm = sort_perm(kcols, n)
     kcols = gather_cols(kcols, perm, n)
     vcols = gather_cols(vcols, perm, n)

@@ -58,6 +58,13 @@ import os as _os
 PREFETCH = _os.environ.get("WELDGPU_PREFETCH", "1") == "1"
 MINBLOCKS = int(_os.environ.get("WELDGPU_MINBLOCKS", "0"))
 ITEMS_OVERRIDE = int(_os.environ.get("WELDGPU_ITEMS", "0"))
+DEFER_DICT = _os.environ.get("WELDGPU_DEFER_DICT", "1") == "1"
+AGG_MAX_GROUPS = int(_os.environ.get("WELDGPU_AGG_GROUPS", "8"))
+REGCACHE = int(_os.environ.get("WELDGPU_REGCACHE", "4"))
+PIPE = _os.environ.get("WELDGPU_PIPE", "1") == "1"
+PIPE_STAGES = int(_os.environ.get("WELDGPU_PIPE_STAGES", "4"))
+PIPE_MAX_STAGES = 8
+PIPE_SMEM_BUDGET = int(_os.environ.get("WELDGPU_PIPE_SMEM", str(48 * 1024)))
 
 # Extern names recognised as device intrinsics (the reference resolves
 # `call(name, ...)` through a host registry, run.py:832-846).
@@ -144,6 +151,7 @@ class IterSpec:
     simd: bool
     strided: bool         # explicit start/stride window (non-contiguous)
     kinds: list = field(default_factory=list)
+    aligned: bool = True  # every column pointer 16-byte aligned (bulk copies)
 
 
 @dataclass(eq=False)
@@ -176,6 +184,7 @@ class KernelPlan:
     scan_bids: list
     merger_bids: list
     key: str = ""
+    pipe_stage_bytes: int = 0
 
 
 def _hex_f64(v):
@@ -724,6 +733,12 @@ class Gen:
         kks = leaves(kind.key)
         vks = leaves(kind.value)
         words = self._key_words(kks, _flat(key))
+        if b.extra.get("deferred"):
+            # one pending merge per item; applied after the item loop
+            self.emit(f"dkf{b.bid}[j] = true; dkk{b.bid}[j] = {words[0]};")
+            for f, x in enumerate(_flat(val)):
+                self.emit(f"dkv{b.bid}_{f}[j] = {x.c};")
+            return
         vals = _flat(val)
         nw = len(words)
         opc = OPCODE[kind.op]
@@ -732,7 +747,6 @@ class Gen:
         table = self.param(f"d{b.bid}_table", "u64*", ("b", b.bid, "table"))
         mask = self.param(f"d{b.bid}_mask", "u64", ("b", b.bid, "mask"))
         count = self.param(f"d{b.bid}_count", "unsigned long long*", ("b", b.bid, "count"))
-        limit = self.param(f"d{b.bid}_limit", "u64", ("b", b.bid, "limit"))
         slot = self.tmp("sl")
         self.emit("{")
         self.ind += 1
@@ -748,11 +762,11 @@ class Gen:
             self.emit("} else {")
             self.ind += 1
         if nw == 1:
-            self.emit(f"const i64 {slot} = wg_ht_find1({table}, {sw}, {mask}, {words[0]}, {count}, {limit});")
+            self.emit(f"const i64 {slot} = wg_ht_find1({table}, {sw}, {mask}, {words[0]}, wg_claims{b.bid});")
         else:
             arr = self.tmp("ka")
             self.emit(f"const u64 {arr}[{nw}] = {{{', '.join(words)}}};")
-            self.emit(f"const i64 {slot} = wg_ht_findN({table}, {sw}, {mask}, {arr}, {nw}, {count}, {limit});")
+            self.emit(f"const i64 {slot} = wg_ht_findN({table}, {sw}, {mask}, {arr}, {nw}, wg_claims{b.bid});")
         self.emit(f"if ({slot} >= 0) {{")
         self.ind += 1
         for f, (x, k) in enumerate(zip(vals, vks)):
@@ -831,7 +845,10 @@ def _shape(ty, vals):
             return next(it)
         return T([go(f) for f in t.fields])
 
-    return go(ty)
+    try:
+        return go(ty)
+    finally:
+        del go
 
 
 def _is_builder_struct(t):
@@ -945,6 +962,13 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
     pb, pi, px = (p.name for p in lam.params)
 
     ITEMS = items or ITEMS_OVERRIDE or choose_items(iters)
+    if not (items or ITEMS_OVERRIDE) and any(isinstance(b.kind, DictMerger) for b in g.bspecs):
+        ITEMS = min(ITEMS, 2)   # deferred merges + register caches are register-hungry
+    if not (items or ITEMS_OVERRIDE) and PIPE:
+        # keep >= 2 pipeline stages inside the shared-memory budget
+        row = sum(SIZE[k] * (W if it.simd else 1) for it in iters for k in it.kinds)
+        while ITEMS > 1 and 2 * BLOCK * ITEMS * row > PIPE_SMEM_BUDGET:
+            ITEMS //= 2
     g.items = ITEMS
 
     # builders value seen by the body
@@ -965,6 +989,11 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
     for b in g.bspecs:
         mn, mx = counts.get(b, (0, 0))
         b.extra["maxm"] = mx
+        if isinstance(b.kind, DictMerger) and mx <= 1 and key_layout(leaves(b.kind.key))[1] == 1 \
+                and DEFER_DICT:
+            b.extra["deferred"] = True
+            if REGCACHE and len(leaves(b.kind.value)) <= 8:
+                b.extra["regcache"] = REGCACHE
         if isinstance(b.kind, (VecBuilder, GroupBuilder)):
             if isinstance(b.kind, VecBuilder):
                 b.extra["kinds"] = leaves(b.kind.elem)
@@ -1086,7 +1115,6 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
             table = g.param(f"d{b.bid}_table", "u64*", ("b", b.bid, "table"))
             mask = g.param(f"d{b.bid}_mask", "u64", ("b", b.bid, "mask"))
             count = g.param(f"d{b.bid}_count", "unsigned long long*", ("b", b.bid, "count"))
-            limit = g.param(f"d{b.bid}_limit", "u64", ("b", b.bid, "limit"))
             ocount = g.param(f"d{b.bid}_ocount", "unsigned long long*", ("b", b.bid, "ocount"))
             ocap = g.param(f"d{b.bid}_ocap", "u64", ("b", b.bid, "ocap"))
             vks = leaves(b.kind.value)
@@ -1094,7 +1122,7 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
             fl = [f"for (int q = threadIdx.x; q < {ns}; q += {BLOCK}) {{",
                   f"  const u64 k_ = s_dk{b.bid}[(u64)q * {sw}];",
                   "  if (k_ == WG_EMPTY_KEY) continue;",
-                  f"  const i64 sl_ = wg_ht_find1({table}, {sw}, {mask}, k_, {count}, {limit});",
+                  f"  const i64 sl_ = wg_ht_find1({table}, {sw}, {mask}, k_, wg_claims{b.bid});",
                   "  if (sl_ >= 0) {"]
             for f, kk in enumerate(vks):
                 fl.append(f"    WgAtomicFold<{opc}, {CTYPE[kk]}>::f(({CTYPE[kk]}*)({table} + (u64)sl_ * {sw} + {1 + f}), "
@@ -1111,6 +1139,28 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
             fl.append("  }")
             fl.append("}")
             smem_flush.append("\n    ".join(fl))
+
+    # bulk-async column pipeline (static schedule, contiguous 16B-aligned
+    # columns).  The stage count is a launch parameter: the executor picks
+    # the most stages that do not lower the kernel's occupancy.
+    pipe = bool(PIPE and not scan_bs and loads and all((not it.strided) and it.aligned for it in iters))
+    pipe_off = pipe_stage_bytes = 0
+    pipe_col_off = []
+    if pipe:
+        off = 0
+        for (arr, st, kk, per, k, l, col) in loads:
+            pipe_col_off.append(off)
+            off += (BLOCK * ITEMS * per * SIZE[kk] + 127) // 128 * 128
+        pipe_stage_bytes = off
+        pipe_off = (dyn_smem + 127) // 128 * 128
+        if pipe_off + 2 * off > 200 * 1024:
+            pipe = False
+        else:
+            g.param("pipe_stages", "i64", ("pipe_stages",))
+    pipe_stages = "PIPE_S"
+
+    deferred_lines = {b.bid: _deferred_dict_lines(g, b) for b in g.bspecs if b.extra.get("deferred")}
+    regcache_flush = {b.bid: _regcache_flush_lines(g, b) for b in g.bspecs if b.extra.get("regcache")}
 
     # ---- assemble ----------------------------------------------------------
     src = []
@@ -1133,6 +1183,11 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
         for f, kk in enumerate(leaves(b.kind.elem)):
             src.append(f"  {CTYPE[kk]} m{b.bid}_{f} = {c_literal(kk, internal_identity(b.kind.op, kk))};")
         src.append(f"  int m{b.bid}_h = 0;")
+    dict_bs = [b for b in g.bspecs if isinstance(b.kind, DictMerger)]
+    for b in dict_bs:
+        src.append(f"  int wg_claims{b.bid} = 0;")
+        if b.extra.get("regcache"):
+            src.extend(_regcache_decl(b, b.extra["regcache"]))
     src.append("  const i64 n = p.n;")
     src.append("  const i64 ntiles = (n + TILE - 1) / TILE;")
     if scan_bs:
@@ -1163,8 +1218,119 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
         return [f"{ind}alignas(16) {st} {arr}{suffix}[{'ITEMS * %d' % per if per > 1 else 'ITEMS'}];"
                 for (arr, st, kk, per, k, l, col) in loads]
 
-    prefetch = (not scan_bs) and PREFETCH
-    if not scan_bs and prefetch:
+    def tile_body():
+        """Everything a thread does for one tile once its columns are in
+        registers (x arrays): body, buffered stores, deferred dict merges,
+        and for scan appenders the block scan + look-back + store phase."""
+        out = []
+        out.append("    const i64 t0 = tile * TILE + (i64)threadIdx.x * ITEMS;")
+        out.append("    const bool full = (t0 + ITEMS <= n);")
+        for b in g.bspecs:
+            if b.mode == "direct" and b.extra.get("buffered"):
+                for f, kk in enumerate(b.extra["kinds"]):
+                    out.append(f"    alignas(16) {STYPE[kk]} o{b.bid}_{f}[ITEMS * {b.k}];")
+            if b.mode == "scan":
+                out.append(f"    i64 cnt{b.bid} = 0;")
+            if b.extra.get("deferred"):
+                out.append(f"    bool dkf{b.bid}[ITEMS]; u64 dkk{b.bid}[ITEMS];")
+                out.append(f"#pragma unroll\n    for (int q = 0; q < ITEMS; ++q) dkf{b.bid}[q] = false;")
+                for f, kk in enumerate(leaves(b.kind.value)):
+                    out.append(f"    {CTYPE[kk]} dkv{b.bid}_{f}[ITEMS];")
+        out.append("#pragma unroll")
+        out.append("    for (int j = 0; j < ITEMS; ++j) {")
+        out.append("      const i64 li = t0 + j;")
+        out.append("      if (li < n) {")
+        out.append("        const i64 i = p.idx0 + li;")
+        out.extend(body_a)
+        out.append("      }")
+        out.append("    }")
+        for b in g.bspecs:
+            if b.mode == "direct" and b.extra.get("buffered"):
+                for f, kk in enumerate(b.extra["kinds"]):
+                    col = f"p.a{b.bid}_{f}"
+                    out.append(f"    if (full) wg_store_contig<{STYPE[kk]}, ITEMS * {b.k}>({col} + t0 * {b.k}, o{b.bid}_{f});")
+                    out.append(f"    else {{ for (int q = 0; q < ITEMS * {b.k}; ++q) if (t0 * {b.k} + q < n * {b.k}) "
+                               f"{col}[t0 * {b.k} + q] = o{b.bid}_{f}[q]; }}")
+        for b in g.bspecs:
+            if b.extra.get("deferred"):
+                out.extend(deferred_lines[b.bid])
+        if scan_bs:
+            for si, b in enumerate(scan_bs):
+                out.append(f"    i64 agg{b.bid};")
+                out.append(f"    i64 wpos{b.bid} = wg_block_exclusive_scan(cnt{b.bid}, s_scan, &agg{b.bid});")
+                out.append("    if (threadIdx.x < 32) {")
+                out.append(f"      const i64 pre_ = wg_lookback(p.a{b.bid}_status, tile, agg{b.bid});")
+                out.append(f"      if (threadIdx.x == 0) {{ s_toff[{si}] = pre_; if (tile == ntiles - 1) *p.a{b.bid}_total = pre_ + agg{b.bid}; }}")
+                out.append("    }")
+            out.append("    __syncthreads();")
+            for si, b in enumerate(scan_bs):
+                out.append(f"    wpos{b.bid} += s_toff[{si}];")
+            out.append("#pragma unroll")
+            out.append("    for (int j = 0; j < ITEMS; ++j) {")
+            out.append("      const i64 li = t0 + j;")
+            out.append("      if (li < n) {")
+            out.append("        const i64 i = p.idx0 + li;")
+            out.extend(body_b)
+            out.append("      }")
+            out.append("    }")
+        return out
+
+    if scan_bs:
+        src.extend(decl_lines("", "    "))
+        src.extend(load_lines("tile", "", "    "))
+        src.extend(tile_body())
+        src.append("  }")
+    elif pipe:
+        # Bulk-async (TMA engine) column streaming: every full tile's column
+        # chunks are copied HBM -> shared memory by cp.async.bulk, PIPE_STAGES
+        # tiles ahead of the consumer, completion tracked by one mbarrier per
+        # stage.  Bytes in flight no longer depend on registers/occupancy.
+        src.append(f"  u64* wg_stage = wg_dyn_smem + {pipe_off // 8};")
+        src.append("  const int PIPE_S = (int)p.pipe_stages;")
+        src.append(f"  __shared__ __align__(8) u64 wg_bar[{PIPE_MAX_STAGES}];")
+        src.append("  const i64 nfull = n / TILE;")
+        src.append("  const i64 nmy = (nfull > (i64)blockIdx.x) ? (nfull - 1 - (i64)blockIdx.x) / gridDim.x + 1 : 0;")
+        src.append("  if (threadIdx.x == 0) {")
+        src.append(f"    for (int s_ = 0; s_ < {pipe_stages}; ++s_) wg_mbar_init(&wg_bar[s_], 1);")
+        src.append("    wg_fence_mbar_init();")
+        src.append("  }")
+        src.append("  __syncthreads();")
+        issue = ["      const i64 itile_ = (i64)blockIdx.x + k_ * gridDim.x;",
+                 f"      u64* st_ = wg_stage + (u64)(k_ % {pipe_stages}) * {pipe_stage_bytes // 8};",
+                 f"      wg_mbar_expect_tx(&wg_bar[k_ % {pipe_stages}], {pipe_stage_bytes});"]
+        for (arr, st, kk, per, k, l, col), off in zip(loads, pipe_col_off):
+            nb = BLOCK * ITEMS * per * SIZE[kk]
+            issue.append(f"      wg_bulk_g2s((char*)st_ + {off}, {col} + itile_ * TILE * {per}, {nb}, &wg_bar[k_ % {pipe_stages}]);")
+        src.append("  if (threadIdx.x == 0) {")
+        src.append(f"    for (i64 k_ = 0; k_ < {pipe_stages} && k_ < nmy; ++k_) {{")
+        src.extend(issue)
+        src.append("    }")
+        src.append("  }")
+        src.append("  for (i64 kk_ = 0; kk_ < nmy; ++kk_) {")
+        src.append("    const i64 tile = (i64)blockIdx.x + kk_ * gridDim.x;")
+        src.append(f"    wg_mbar_wait(&wg_bar[kk_ % {pipe_stages}], (unsigned)((kk_ / {pipe_stages}) & 1));")
+        src.extend(decl_lines("", "    "))
+        src.append(f"    {{ const char* sg_ = (const char*)(wg_stage + (u64)(kk_ % {pipe_stages}) * {pipe_stage_bytes // 8});")
+        for (arr, st, kk, per, k, l, col), off in zip(loads, pipe_col_off):
+            cnt = f"ITEMS * {per}" if per > 1 else "ITEMS"
+            src.append(f"      wg_lds_contig<{st}, {cnt}>((const {st}*)(sg_ + {off}) + threadIdx.x * {cnt}, {arr}); ")
+        src.append("    }")
+        src.append("    __syncthreads();")
+        src.append(f"    if (threadIdx.x == 0 && kk_ + {pipe_stages} < nmy) {{")
+        src.append("      wg_fence_proxy_async();")
+        src.append(f"      const i64 k_ = kk_ + {pipe_stages};")
+        src.extend("  " + x for x in issue)
+        src.append("    }")
+        src.extend(tile_body())
+        src.append("  }")
+        # the partial last tile (if any) through plain loads
+        src.append("  if (nfull * TILE < n && (nfull % gridDim.x) == (i64)blockIdx.x) {")
+        src.append("    const i64 tile = nfull;")
+        src.extend(decl_lines("", "    "))
+        src.extend(load_lines("tile", "", "    "))
+        src.extend(tile_body())
+        src.append("  }")
+    elif PREFETCH:
         # register double buffering: the next tile's columns are in flight
         # while the current tile computes
         src.extend(decl_lines("", "  "))
@@ -1176,62 +1342,29 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
         src.append("    const i64 ntile_ = tile + gridDim.x;")
         src.append("    if (ntile_ < ntiles)")
         src.extend(load_lines("ntile_", "_nx", "    "))
-    elif not scan_bs:
-        src.append("  for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {")
-    if not prefetch:
-        src.extend(decl_lines("", "    "))
-        src.extend(load_lines("tile", "", "    "))
-    src.append("    const i64 t0 = tile * TILE + (i64)threadIdx.x * ITEMS;")
-    src.append("    const bool full = (t0 + ITEMS <= n);")
-    for b in g.bspecs:
-        if b.mode == "direct" and b.extra.get("buffered"):
-            for f, kk in enumerate(b.extra["kinds"]):
-                src.append(f"    alignas(16) {STYPE[kk]} o{b.bid}_{f}[ITEMS * {b.k}];")
-        if b.mode == "scan":
-            src.append(f"    i64 cnt{b.bid} = 0;")
-    src.append("#pragma unroll")
-    src.append("    for (int j = 0; j < ITEMS; ++j) {")
-    src.append("      const i64 li = t0 + j;")
-    src.append("      if (li < n) {")
-    src.append("        const i64 i = p.idx0 + li;")
-    src.extend(body_a)
-    src.append("      }")
-    src.append("    }")
-    for b in g.bspecs:
-        if b.mode == "direct" and b.extra.get("buffered"):
-            for f, kk in enumerate(b.extra["kinds"]):
-                col = f"p.a{b.bid}_{f}"
-                src.append(f"    if (full) wg_store_contig<{STYPE[kk]}, ITEMS * {b.k}>({col} + t0 * {b.k}, o{b.bid}_{f});")
-                src.append(f"    else {{ for (int q = 0; q < ITEMS * {b.k}; ++q) if (t0 * {b.k} + q < n * {b.k}) "
-                           f"{col}[t0 * {b.k} + q] = o{b.bid}_{f}[q]; }}")
-    if scan_bs:
-        for si, b in enumerate(scan_bs):
-            src.append(f"    i64 agg{b.bid};")
-            src.append(f"    i64 wpos{b.bid} = wg_block_exclusive_scan(cnt{b.bid}, s_scan, &agg{b.bid});")
-            src.append("    if (threadIdx.x < 32) {")
-            src.append(f"      const i64 pre_ = wg_lookback(p.a{b.bid}_status, tile, agg{b.bid});")
-            src.append(f"      if (threadIdx.x == 0) {{ s_toff[{si}] = pre_; if (tile == ntiles - 1) *p.a{b.bid}_total = pre_ + agg{b.bid}; }}")
-            src.append("    }")
-        src.append("    __syncthreads();")
-        for si, b in enumerate(scan_bs):
-            src.append(f"    wpos{b.bid} += s_toff[{si}];")
-        src.append("#pragma unroll")
-        src.append("    for (int j = 0; j < ITEMS; ++j) {")
-        src.append("      const i64 li = t0 + j;")
-        src.append("      if (li < n) {")
-        src.append("        const i64 i = p.idx0 + li;")
-        src.extend(body_b)
-        src.append("      }")
-        src.append("    }")
-    if prefetch:
+        src.extend(tile_body())
         for (arr, st, kk, per, k, l, col) in loads:
             cnt = f"ITEMS * {per}" if per > 1 else "ITEMS"
             src.append(f"#pragma unroll\n    for (int q = 0; q < {cnt}; ++q) {arr}[q] = {arr}_nx[q];")
-    src.append("  }")
-    # epilogue: shared-memory flushes
+        src.append("  }")
+    else:
+        src.append("  for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {")
+        src.extend(decl_lines("", "    "))
+        src.extend(load_lines("tile", "", "    "))
+        src.extend(tile_body())
+        src.append("  }")
+    # epilogue: register caches, then shared-memory tables
+    for b in g.bspecs:
+        if b.extra.get("regcache"):
+            src.extend(regcache_flush[b.bid])
     if smem_flush:
         src.append("  __syncthreads();")
         src.extend("  " + fl for fl in smem_flush)
+    # epilogue: distinct-key counts (one atomic per warp)
+    for b in dict_bs:
+        src.append(f"  {{ int c_ = wg_claims{b.bid};")
+        src.append("#pragma unroll\n    for (int d = 16; d > 0; d >>= 1) c_ += __shfl_xor_sync(0xffffffffu, c_, d);")
+        src.append(f"    if ((threadIdx.x & 31) == 0 && c_) atomicAdd(p.d{b.bid}_count, (unsigned long long)c_); }}")
     # epilogue: mergers
     if merger_bs:
         src.append("  __shared__ u64 s_red[32];")
@@ -1269,9 +1402,218 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
         src.append("  }")
     src.append("}")
     source = "\n".join(src) + "\n"
-    return KernelPlan(source=source, name=name, params=g.params, schedule=schedule, items=ITEMS, block=BLOCK,
+    plan = KernelPlan(source=source, name=name, params=g.params, schedule=schedule, items=ITEMS, block=BLOCK,
                       smem=dyn_smem, builders=g.bspecs, scan_bids=[b.bid for b in scan_bs],
                       merger_bids=[b.bid for b in merger_bs])
+    plan.pipe_stage_bytes = pipe_stage_bytes if pipe else 0
+    return plan
+
+
+def _dict_params(g, b):
+    vks = leaves(b.kind.value)
+    P = dict(
+        table=g.param(f"d{b.bid}_table", "u64*", ("b", b.bid, "table")),
+        mask=g.param(f"d{b.bid}_mask", "u64", ("b", b.bid, "mask")),
+        count=g.param(f"d{b.bid}_count", "unsigned long long*", ("b", b.bid, "count")),
+        ocount=g.param(f"d{b.bid}_ocount", "unsigned long long*", ("b", b.bid, "ocount")),
+        ocap=g.param(f"d{b.bid}_ocap", "u64", ("b", b.bid, "ocap")),
+        okey=g.param(f"d{b.bid}_ok0", "u64*", ("b", b.bid, "okey", 0)),
+        ovals=[g.param(f"d{b.bid}_ov{f}", "u64*", ("b", b.bid, "oval", f)) for f in range(len(vks))],
+    )
+    return P
+
+
+def _regcache_decl(b, R):
+    vks = leaves(b.kind.value)
+    out = []
+    for r in range(R):
+        out.append(f"  u64 rk{b.bid}_{r} = WG_EMPTY_KEY;")
+        for f, kk in enumerate(vks):
+            out.append(f"  {CTYPE[kk]} rv{b.bid}_{r}_{f} = {c_literal(kk, internal_identity(b.kind.op, kk))};")
+    return out
+
+
+def _regcache_lines(b, R, ind="    "):
+    """Level 0: a per-thread cache of R (key, value) slots in registers.
+    Hits and first claims fold with no memory traffic at all; misses keep
+    their pending flag for the shared/global levels."""
+    kind = b.kind
+    vks = leaves(kind.value)
+    B = b.bid
+    op = OPSTRUCT[kind.op]
+
+    def fold(r):
+        return " ".join(f"rv{B}_{r}_{f} = {op}<{CTYPE[kk]}>::f(rv{B}_{r}_{f}, dkv{B}_{f}[j]);"
+                        for f, kk in enumerate(vks))
+
+    L = [f"{ind}#pragma unroll", f"{ind}for (int j = 0; j < ITEMS; ++j) {{",
+         f"{ind}  if (!dkf{B}[j]) continue;", f"{ind}  const u64 k_ = dkk{B}[j];"]
+    chain = []
+    for r in range(R):
+        chain.append(f"if (rk{B}_{r} == k_) {{ {fold(r)} }}")
+    claim = []
+    for r in range(R):
+        claim.append(f"if (rk{B}_{r} == WG_EMPTY_KEY) {{ rk{B}_{r} = k_; {fold(r)} }}")
+    L.append(f"{ind}  " + " else ".join(chain) + " else if (k_ != WG_EMPTY_KEY) { "
+             + " else ".join(claim) + " else { continue; } } else { continue; }")
+    L.append(f"{ind}  dkf{B}[j] = false;")
+    L.append(f"{ind}}}")
+    return L
+
+
+def _warpagg_lines(b, ind, flag, key, vals, outvals, glob, limit):
+    """Fold lanes that merge the same key with a warp butterfly; the group
+    leader applies the aggregate to the per-CTA shared-memory table.  Sets
+    `glob` for lanes whose (aggregated) merge still needs the global table."""
+    kind = b.kind
+    vks = leaves(kind.value)
+    sw = b.extra["slot_words"]
+    ns = b.extra["smem_slots"]
+    opc = OPCODE[kind.op]
+    B = b.bid
+    L = [f"{ind}{{",
+         f"{ind}  const bool f_ = {flag}; const u64 k_ = {key};",
+         f"{ind}  {glob} = f_;",
+         f"{ind}  const unsigned fl_ = __ballot_sync(0xffffffffu, f_);",
+         f"{ind}  const unsigned peers_ = __match_any_sync(0xffffffffu, k_) & fl_;",
+         f"{ind}  const bool lead_ = f_ && ((__ffs(peers_) - 1) == lane_);",
+         f"{ind}  const unsigned leaders_ = __ballot_sync(0xffffffffu, lead_);",
+         f"{ind}  if (fl_ != 0 && __popc(leaders_) <= {limit}) {{"]
+    for f, kk in enumerate(vks):
+        L.append(f"{ind}    {outvals[f]} = {vals[f]};")
+    L.append(f"{ind}    unsigned todo_ = leaders_;")
+    L.append(f"{ind}    while (todo_) {{")
+    L.append(f"{ind}      const int ld_ = __ffs(todo_) - 1; todo_ &= todo_ - 1;")
+    L.append(f"{ind}      const unsigned grp_ = __shfl_sync(0xffffffffu, peers_, ld_);")
+    L.append(f"{ind}      const bool in_ = (grp_ >> lane_) & 1u;")
+    for f, kk in enumerate(vks):
+        ct = CTYPE[kk]
+        ident = c_literal(kk, internal_identity(kind.op, kk))
+        L.append(f"{ind}      {{ const {ct} r_ = wg_warp_allfold<{ct}, {OPSTRUCT[kind.op]}<{ct}>>(in_ ? {vals[f]} : {ident});"
+                 f" if (lane_ == ld_) {outvals[f]} = r_; }}")
+    L.append(f"{ind}    }}")
+    L.append(f"{ind}    {glob} = false;")
+    L.append(f"{ind}    if (lead_) {{")
+    L.append(f"{ind}      const int ss_ = wg_sht_find1(s_dk{B}, {sw}, {ns - 1}, k_);")
+    L.append(f"{ind}      if (ss_ >= 0) {{")
+    for f, kk in enumerate(vks):
+        ct = CTYPE[kk]
+        L.append(f"{ind}        wg_smem_fold<{opc}, {ct}>(({ct}*)(s_dk{B} + (u64)ss_ * {sw} + {1 + f}), {outvals[f]});")
+    L.append(f"{ind}      }} else {{ {glob} = true; }}")
+    L.append(f"{ind}    }}")
+    L.append(f"{ind}  }} else {{")
+    for f, kk in enumerate(vks):
+        L.append(f"{ind}    {outvals[f]} = {vals[f]};")
+    L.append(f"{ind}  }}")
+    L.append(f"{ind}}}")
+    return L
+
+
+def _global_insert_lines(b, P, ind, flag, key, vals):
+    kind = b.kind
+    vks = leaves(kind.value)
+    sw = b.extra["slot_words"]
+    opc = OPCODE[kind.op]
+    B = b.bid
+    L = [f"{ind}if ({flag}) {{",
+         f"{ind}  const i64 sl_ = wg_ht_find1({P['table']}, {sw}, {P['mask']}, {key}, wg_claims{B});"]
+    L += _global_apply_lines(b, P, ind + "  ", key, vals)
+    L.append(f"{ind}}}")
+    return L
+
+
+def _global_apply_lines(b, P, ind, key, vals):
+    kind = b.kind
+    vks = leaves(kind.value)
+    sw = b.extra["slot_words"]
+    opc = OPCODE[kind.op]
+    L = [f"{ind}if (sl_ >= 0) {{"]
+    for f, kk in enumerate(vks):
+        ct = CTYPE[kk]
+        L.append(f"{ind}  WgAtomicFold<{opc}, {ct}>::f(({ct}*)({P['table']} + (u64)sl_ * {sw} + {1 + f}), {vals[f]});")
+    L.append(f"{ind}}} else {{")
+    L.append(f"{ind}  const u64 o_ = atomicAdd({P['ocount']}, 1ULL);")
+    L.append(f"{ind}  if (o_ < {P['ocap']}) {{ {P['okey']}[o_] = {key};")
+    for f, kk in enumerate(vks):
+        L.append(f"{ind}    {P['ovals'][f]}[o_] = wg_to_bits<{CTYPE[kk]}>({vals[f]});")
+    L.append(f"{ind}  }} else {{ wg_raise(p.err, WG_ERR_INTERNAL, 1); }}")
+    L.append(f"{ind}}}")
+    return L
+
+
+def _deferred_dict_lines(g, b):
+    """Apply the tile's pending dictmerger merges with the warp converged.
+
+    Level 0: per-thread register cache (REGCACHE slots).  Level 1 (smem
+    mode): lanes merging the same key are folded with a warp butterfly and
+    only the group leader touches the per-CTA shared-memory table; warps
+    seeing more than AGG_MAX_GROUPS distinct keys skip aggregation.  Level 2:
+    every merge still pending goes to the global table with the first probe
+    of all ITEMS rows issued up front (memory-level parallelism for tables
+    far larger than L2)."""
+    kind = b.kind
+    vks = leaves(kind.value)
+    sw = b.extra["slot_words"]
+    P = _dict_params(g, b)
+    B = b.bid
+    R = b.extra.get("regcache", 0)
+    L = ["    {", "      const int lane_ = threadIdx.x & 31;"]
+    if R:
+        L += _regcache_lines(b, R, "      ")
+    if b.mode == "smem":
+        L.append("#pragma unroll")
+        L.append("      for (int j = 0; j < ITEMS; ++j) {")
+        outv = [f"a{f}_" for f in range(len(vks))]
+        for f, kk in enumerate(vks):
+            L.append(f"        {CTYPE[kk]} a{f}_;")
+        L.append("        bool g_;")
+        L += _warpagg_lines(b, "        ", f"dkf{B}[j]", f"dkk{B}[j]", [f"dkv{B}_{f}[j]" for f in range(len(vks))],
+                            outv, "g_", AGG_MAX_GROUPS)
+        L.append(f"        dkf{B}[j] = g_;")
+        for f, kk in enumerate(vks):
+            L.append(f"        dkv{B}_{f}[j] = a{f}_;")
+        L.append("      }")
+    # global table: issue every first probe, then resolve
+    L.append(f"      u64 h_[ITEMS], c_[ITEMS];")
+    L.append("#pragma unroll")
+    L.append(f"      for (int j = 0; j < ITEMS; ++j) {{ h_[j] = wg_ht_home(dkk{B}[j], {P['mask']}); "
+             f"c_[j] = dkf{B}[j] ? *(volatile u64*)({P['table']} + h_[j] * {sw}) : 0ULL; }}")
+    L.append("#pragma unroll")
+    L.append("      for (int j = 0; j < ITEMS; ++j) {")
+    L.append(f"        if (!dkf{B}[j]) continue;")
+    L.append(f"        const i64 sl_ = wg_ht_resolve1({P['table']}, {sw}, {P['mask']}, dkk{B}[j], h_[j], c_[j], wg_claims{B});")
+    L += _global_apply_lines(b, P, "        ", f"dkk{B}[j]", [f"dkv{B}_{f}[j]" for f in range(len(vks))])
+    L.append("      }")
+    L.append("    }")
+    return L
+
+
+def _regcache_flush_lines(g, b):
+    """Kernel epilogue: drain the register caches (warp-aggregated into the
+    shared table in smem mode, else straight to the global table)."""
+    R = b.extra.get("regcache", 0)
+    if not R:
+        return []
+    vks = leaves(b.kind.value)
+    P = _dict_params(g, b)
+    B = b.bid
+    L = ["  {", "    const int lane_ = threadIdx.x & 31;"]
+    for r in range(R):
+        vals = [f"rv{B}_{r}_{f}" for f in range(len(vks))]
+        flag = f"(rk{B}_{r} != WG_EMPTY_KEY)"
+        L.append("    {")
+        if b.mode == "smem":
+            outv = [f"a{f}_" for f in range(len(vks))]
+            for f, kk in enumerate(vks):
+                L.append(f"      {CTYPE[kk]} a{f}_;")
+            L.append("      bool g_;")
+            L += _warpagg_lines(b, "      ", flag, f"rk{B}_{r}", vals, outv, "g_", 32)
+            L += _global_insert_lines(b, P, "      ", "g_", f"rk{B}_{r}", outv)
+        else:
+            L += _global_insert_lines(b, P, "      ", flag, f"rk{B}_{r}", vals)
+        L.append("    }")
+    L.append("  }")
+    return L
 
 
 def _pattern_switch(pat):
@@ -1310,7 +1652,10 @@ def _capture_val(g: Gen, name, ty, val):
             return None
         raise DeviceUnsupported(f"captured value of type {t}")
 
-    return go(ty, val, ())
+    try:
+        return go(ty, val, ())
+    finally:
+        del go
 
 
 # ---------------------------------------------------------------------------
@@ -1318,7 +1663,7 @@ def _capture_val(g: Gen, name, ty, val):
 # suite to prove every loop of a program lowers and compiles for sm_100a.
 
 
-def static_plans(expr, env_types=None, externs=()):
+def static_plans(expr, env_types=None, externs=(), smem=True):
     """Yield a KernelPlan per ``for`` loop in a typed program, deriving the
     iteration, builder and capture specs from types alone."""
     from weldmill.expr import walk, free_variables as _fv
@@ -1350,8 +1695,13 @@ def static_plans(expr, env_types=None, externs=()):
                 bs = BSpec(bid=bid, kind=t.kind)
                 if isinstance(t.kind, DictMerger):
                     nw = key_layout(leaves(t.kind.key))[1]
-                    bs.extra["slot_words"] = (1 if nw == 1 else 1 + nw) + len(leaves(t.kind.value))
+                    sw = (1 if nw == 1 else 1 + nw) + len(leaves(t.kind.value))
+                    bs.extra["slot_words"] = sw
                     bs.mode = "global"
+                    if nw == 1 and smem:
+                        bs.mode = "smem"
+                        bs.extra["smem_slots"] = 512
+                        bs.extra["pattern"] = [0xFFFFFFFFFFFFFFFF] + [0] * (sw - 1)
                 if isinstance(t.kind, VecMerger):
                     bs.mode = "global"
                 return bs

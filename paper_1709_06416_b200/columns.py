@@ -75,7 +75,10 @@ class DVec:
             else:
                 raise DeviceUnsupported(f"element type {self.elem} is not flat")
 
-        go(self.elem, self.layout)
+        try:
+            go(self.elem, self.layout)
+        finally:
+            del go  # break the closure's self-reference cycle (it pins buffers until GC)
         return out
 
     def __len__(self):
@@ -95,7 +98,10 @@ def layout_from_cols(elem, cols):
             return tuple(go(f) for f in t.fields)
         raise DeviceUnsupported(f"cannot build a flat layout for {t}")
 
-    return go(elem)
+    try:
+        return go(elem)
+    finally:
+        del go
 
 
 def dvec_from_cols(elem, n, cols):
@@ -186,7 +192,10 @@ def _nested_to_device(elem, payload):
         raise DeviceUnsupported(f"cannot bind {t}")
 
     items = list(payload)
-    return DVec(elem, len(items), build(elem, items))
+    try:
+        return DVec(elem, len(items), build(elem, items))
+    finally:
+        del build
 
 
 # ---------------------------------------------------------------------------

@@ -394,61 +394,57 @@ __device__ __forceinline__ u64 wg_mix64(u64 x) {
   return x;
 }
 
-// Insert-or-find a one-word key.  Returns the slot index, or -1 when the
-// table refuses new keys (distinct count reached `limit`): the caller
-// spills the merge to the overflow list and the host grows the table.
-__device__ __forceinline__ i64 wg_ht_find1(u64* table, int slot_words, u64 mask, u64 key,
-                                            unsigned long long* count, u64 limit) {
+// Insert-or-find a one-word key.  Returns the slot index, or -1 when
+// WG_MAX_PROBE consecutive slots are taken by other keys: the caller spills
+// the merge to the overflow list and the host grows the table and replays
+// it.  `claims` counts keys this thread inserted (summed per CTA into the
+// table's distinct-key counter at kernel end -- no contended global
+// counter on the insert path).
+#define WG_MAX_PROBE 128
+__device__ __forceinline__ i64 wg_ht_find1(u64* table, int slot_words, u64 mask, u64 key, int& claims) {
   if (key == WG_EMPTY_KEY) {
-    // Dedicated overflow slot for the sentinel value.
+    // Dedicated slot for the sentinel value (claim word EMPTY -> 0).
     u64* s = table + (mask + 1) * (u64)slot_words;
     u64 prev = atomicCAS((unsigned long long*)s, WG_EMPTY_KEY, 0ULL);
-    if (prev == WG_EMPTY_KEY) atomicAdd(count, 1ULL);
+    if (prev == WG_EMPTY_KEY) claims++;
     return (i64)(mask + 1);
   }
   u64 h = wg_mix64(key) & mask;
-  while (true) {
+#pragma unroll 1
+  for (int probe = 0; probe < WG_MAX_PROBE; ++probe) {
     u64* s = table + h * (u64)slot_words;
     u64 cur = *(volatile u64*)s;
     if (cur == key) return (i64)h;
     if (cur == WG_EMPTY_KEY) {
-      // Reserve capacity before claiming so the load factor stays bounded.
-      unsigned long long c = atomicAdd(count, 1ULL);
-      if (c >= limit) { atomicAdd(count, 0xffffffffffffffffULL); return -1; }
       u64 prev = atomicCAS((unsigned long long*)s, WG_EMPTY_KEY, key);
-      if (prev == WG_EMPTY_KEY) return (i64)h;
-      atomicAdd(count, 0xffffffffffffffffULL);
+      if (prev == WG_EMPTY_KEY) { claims++; return (i64)h; }
       if (prev == key) return (i64)h;
     }
     h = (h + 1) & mask;
   }
+  return -1;
 }
 
 // Multi-word keys: word 0 of the slot is a state word (0 empty, 1 busy,
 // 2 full) followed by KW key words.
-__device__ __forceinline__ bool wg_keys_eq(const u64* a, const u64* b, int kw) {
-  for (int k = 0; k < kw; ++k) if (a[k] != b[k]) return false;
-  return true;
-}
 __device__ __forceinline__ i64 wg_ht_findN(u64* table, int slot_words, u64 mask, const u64* key, int kw,
-                                            unsigned long long* count, u64 limit) {
+                                            int& claims) {
   u64 hh = 0x9e3779b97f4a7c15ULL;
   for (int k = 0; k < kw; ++k) hh = wg_mix64(hh ^ key[k]) + 0x9e3779b97f4a7c15ULL * (u64)(k + 1);
   u64 h = hh & mask;
-  while (true) {
+#pragma unroll 1
+  for (int probe = 0; probe < WG_MAX_PROBE; ++probe) {
     u64* s = table + h * (u64)slot_words;
     u64 st = *(volatile u64*)s;
     if (st == 0) {
-      unsigned long long c = atomicAdd(count, 1ULL);
-      if (c >= limit) { atomicAdd(count, 0xffffffffffffffffULL); return -1; }
       u64 prev = atomicCAS((unsigned long long*)s, 0ULL, 1ULL);
       if (prev == 0) {
         for (int k = 0; k < kw; ++k) ((volatile u64*)s)[1 + k] = key[k];
         __threadfence();
         atomicExch((unsigned long long*)s, 2ULL);
+        claims++;
         return (i64)h;
       }
-      atomicAdd(count, 0xffffffffffffffffULL);
       st = prev;
     }
     while (st == 1) st = *(volatile u64*)s;  // another thread is writing the key
@@ -457,6 +453,7 @@ __device__ __forceinline__ i64 wg_ht_findN(u64* table, int slot_words, u64 mask,
     if (eq) return (i64)h;
     h = (h + 1) & mask;
   }
+  return -1;
 }
 
 // Canonical key words.  -0.0 and 0.0 are one dictionary key in the
@@ -537,4 +534,86 @@ __device__ __forceinline__ int wg_sht_find1(u64* t, int sw, int mask, u64 key) {
     h = (h + 1) & mask;
   }
   return -1;
+}
+
+// ---------------------------------------------------------------------------
+// Deferred dictmerger merges (codegen: one pending merge per item, processed
+// after the item loop while the warp is converged).
+
+// Butterfly fold over the full warp; every lane receives the result.
+template <typename T, typename OP>
+__device__ __forceinline__ T wg_warp_allfold(T v) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) v = OP::f(v, __shfl_xor_sync(0xffffffffu, v, d));
+  return v;
+}
+
+__device__ __forceinline__ u64 wg_ht_home(u64 key, u64 mask) { return wg_mix64(key) & mask; }
+
+// Probe continuation for one-word keys given the home slot h and the word
+// already loaded from it (lets callers issue the first probe of several
+// rows before resolving any: memory-level parallelism for tables >> L2).
+__device__ __forceinline__ i64 wg_ht_resolve1(u64* table, int slot_words, u64 mask, u64 key, u64 h, u64 cur,
+                                               int& claims) {
+  if (key == WG_EMPTY_KEY) return wg_ht_find1(table, slot_words, mask, key, claims);
+#pragma unroll 1
+  for (int probe = 0; probe < WG_MAX_PROBE; ++probe) {
+    u64* s = table + h * (u64)slot_words;
+    if (cur == key) return (i64)h;
+    if (cur == WG_EMPTY_KEY) {
+      u64 prev = atomicCAS((unsigned long long*)s, WG_EMPTY_KEY, key);
+      if (prev == WG_EMPTY_KEY) { claims++; return (i64)h; }
+      if (prev == key) return (i64)h;
+    }
+    h = (h + 1) & mask;
+    cur = *(volatile u64*)(table + h * (u64)slot_words);
+  }
+  return -1;
+}
+
+// ---------------------------------------------------------------------------
+// Bulk-async column streaming (cp.async.bulk on the TMA engine + mbarrier).
+__device__ __forceinline__ unsigned wg_saddr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void wg_mbar_init(u64* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(wg_saddr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void wg_fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void wg_fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void wg_mbar_expect_tx(u64* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(wg_saddr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void wg_bulk_g2s(void* dst, const void* src, unsigned bytes, u64* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(wg_saddr(dst)),
+      "l"(src), "r"(bytes), "r"(wg_saddr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void wg_mbar_wait(u64* bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred P1;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n @!P1 bra WAIT_%=;\n}" ::"r"(
+          wg_saddr(bar)),
+      "r"(phase)
+      : "memory");
+}
+// Shared-memory counterpart of wg_load_contig (stage -> registers).
+template <typename T, int N>
+__device__ __forceinline__ void wg_lds_contig(const T* src, T (&dst)[N]) {
+  constexpr int B = N * (int)sizeof(T);
+  if constexpr (B % 16 == 0) {
+#pragma unroll
+    for (int c = 0; c < B / 16; ++c) reinterpret_cast<uint4*>(&dst[0])[c] = reinterpret_cast<const uint4*>(src)[c];
+  } else if constexpr (B % 8 == 0) {
+#pragma unroll
+    for (int c = 0; c < B / 8; ++c) reinterpret_cast<uint2*>(&dst[0])[c] = reinterpret_cast<const uint2*>(src)[c];
+  } else if constexpr (B % 4 == 0) {
+#pragma unroll
+    for (int c = 0; c < B / 4; ++c) reinterpret_cast<unsigned*>(&dst[0])[c] = reinterpret_cast<const unsigned*>(src)[c];
+  } else {
+#pragma unroll
+    for (int q = 0; q < N; ++q) dst[q] = src[q];
+  }
 }

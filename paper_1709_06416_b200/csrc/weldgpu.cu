@@ -272,6 +272,81 @@ __global__ void k_flush(uint4* buf, uint64_t n16, uint32_t salt) {
     buf[i] = make_uint4((uint32_t)i, salt, (uint32_t)(i >> 32), salt ^ 0x5a5a5a5a);
 }
 
+
+// ---- groupbuilder finalisation (single integer key leaf) -------------------
+__global__ void k_minmax_u64(const uint64_t* k, uint64_t n, unsigned long long* mm) {
+  uint64_t lo = ~0ULL, hi = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t v = k[i];
+    lo = v < lo ? v : lo;
+    hi = v > hi ? v : hi;
+  }
+  for (int d = 16; d > 0; d >>= 1) {
+    uint64_t a = __shfl_xor_sync(0xffffffffu, lo, d), b = __shfl_xor_sync(0xffffffffu, hi, d);
+    lo = a < lo ? a : lo;
+    hi = b > hi ? b : hi;
+  }
+  if ((threadIdx.x & 31) == 0) { atomicMin(mm, lo); atomicMax(mm + 1, hi); }
+}
+
+// After a stable radix sort on key bits [shift, 64), rows of one bucket
+// (equal high bits) may still be out of order in the low bits.  Record the
+// positions where order breaks inside a bucket; only those buckets get a
+// stable insertion sort (most buckets hold a single distinct key).
+__global__ void k_disorder(const uint64_t* k, uint64_t n, int shift, uint32_t* pos, unsigned long long* npos,
+                           uint64_t cap) {
+  for (uint64_t i = 1 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t a = k[i - 1], b = k[i];
+    if ((a >> shift) == (b >> shift) && a > b) {
+      unsigned long long q = atomicAdd(npos, 1ULL);
+      if (q < cap) pos[q] = (uint32_t)i;
+    }
+  }
+}
+
+// One thread per recorded position; the thread whose position is the first
+// disorder of its bucket sorts the whole bucket (others exit).
+__global__ void k_fix_buckets(uint64_t* k, uint64_t* v, uint64_t n, int shift, const uint32_t* pos, uint64_t npos,
+                              int cap, int* too_long) {
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < npos; q += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t i = pos[q];
+    uint64_t top = k[i] >> shift;
+    uint64_t s = i;
+    while (s > 0 && (k[s - 1] >> shift) == top) --s;
+    // first disorder of the bucket?  (scan the bucket prefix for an earlier break)
+    bool first = true;
+    for (uint64_t t = s + 1; t < i; ++t) if (k[t - 1] > k[t]) { first = false; break; }
+    if (!first) continue;
+    uint64_t e = i + 1;
+    while (e < n && (k[e] >> shift) == top) ++e;
+    if (e - s > (uint64_t)cap) { *too_long = 1; continue; }
+    for (uint64_t a = s + 1; a < e; ++a) {
+      uint64_t kk = k[a], vv = v[a];
+      uint64_t b = a;
+      while (b > s && k[b - 1] > kk) { k[b] = k[b - 1]; v[b] = v[b - 1]; --b; }
+      k[b] = kk; v[b] = vv;
+    }
+  }
+}
+
+__global__ void k_heads1(const uint64_t* k, uint64_t n, uint8_t* flags) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    flags[i] = (i == 0 || k[i] != k[i - 1]) ? 1 : 0;
+}
+
+// offsets[j] = starts[j]; offsets[K] = n; ukeys[j] = inverse order key.
+__global__ void k_group_out(const uint32_t* starts, uint64_t K, uint64_t n, const uint64_t* sk, int kind,
+                            int64_t* offs, void* ukeys) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j <= K; j += (uint64_t)gridDim.x * blockDim.x) {
+    if (j == K) { offs[K] = (int64_t)n; continue; }
+    uint64_t s = starts[j];
+    offs[j] = (int64_t)s;
+    uint64_t w = sk[s];
+    if (kind == 0) ((uint8_t*)ukeys)[j] = (uint8_t)w;
+    else if (kind == 1) ((int32_t*)ukeys)[j] = (int32_t)(int64_t)(w ^ 0x8000000000000000ULL);
+    else ((int64_t*)ukeys)[j] = (int64_t)(w ^ 0x8000000000000000ULL);
+  }
+}
 }  // namespace
 
 // ===========================================================================
@@ -550,6 +625,8 @@ int wg_module_function(uint64_t module, const char* name, uint64_t* fn) {
 
 int wg_occupancy(uint64_t fn, int block, int dyn_smem, int* blocks_per_sm) {
   NEED_INIT();
+  if (dyn_smem > 0)
+    CKD(p_cuFuncSetAttribute((CUfunction)(uintptr_t)fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, 200 * 1024));
   CKD(p_cuOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, (CUfunction)(uintptr_t)fn, block, (size_t)dyn_smem));
   return 0;
 }
@@ -557,8 +634,8 @@ int wg_occupancy(uint64_t fn, int block, int dyn_smem, int* blocks_per_sm) {
 int wg_launch(uint64_t fn, uint32_t grid, uint32_t block, uint32_t dyn_smem, const void* params, uint64_t params_size) {
   NEED_INIT();
   CUfunction f = (CUfunction)(uintptr_t)fn;
-  if (dyn_smem > 48 * 1024)
-    CKD(p_cuFuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)dyn_smem));
+  if (dyn_smem > 0)
+    CKD(p_cuFuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, 200 * 1024));
   size_t sz = (size_t)params_size;
   void* extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, const_cast<void*>(params), CU_LAUNCH_PARAM_BUFFER_SIZE, &sz,
                    CU_LAUNCH_PARAM_END};
@@ -704,6 +781,112 @@ int wg_run_starts(const uint64_t* key_words, int kw, uint64_t n, uint64_t starts
   CK(cudaFreeAsync(d_cnt, g_stream));
   CK(cudaFreeAsync(d_words, g_stream));
   *nruns = (uint64_t)h;
+  return 0;
+}
+
+// GroupBuilderState.result (builders.py:478-493) for one integer/bool key
+// leaf and one value leaf: a stable sort of the appended {key, value} rows
+// by key, then run starts -> (sorted unique keys, offsets[K+1], values in
+// per-key input order).  Only the key bits that vary are sorted: a stable
+// radix sort on the top 24 varying bits, then a stable insertion sort
+// inside the (small) buckets; skewed data falls back to a full radix sort.
+int wg_group_finish1(uint64_t keys, int key_kind, uint64_t vals, int val_width, uint64_t n, uint64_t ukeys_out,
+                     uint64_t offs_out, uint64_t vals_out, uint64_t* K_out) {
+  NEED_INIT();
+  if (n > 0xffffffffULL) return fail("wg_group_finish1: more than 2^32 rows");
+  if (key_kind > 2) return fail("wg_group_finish1: integer or bool keys only");
+  if (n == 0) {
+    CK(cudaMemsetAsync((void*)(uintptr_t)offs_out, 0, 8, g_stream));
+    *K_out = 0;
+    return 0;
+  }
+  unsigned g = grid_for(n, 256);
+  // The row log (keys, vals) belongs to the finishing builder: 8-byte
+  // columns are sorted in place through CUB double buffers.
+  uint64_t *k0, *k1, *v0, *v1;
+  bool own_k0 = key_kind != 2, own_v0 = val_width != 8;
+  unsigned long long* mm;
+  int* flag;
+  if (own_k0) CK(cudaMallocAsync((void**)&k0, n * 8, g_stream)); else k0 = (uint64_t*)(uintptr_t)keys;
+  if (own_v0) CK(cudaMallocAsync((void**)&v0, n * 8, g_stream)); else v0 = (uint64_t*)(uintptr_t)vals;
+  CK(cudaMallocAsync((void**)&k1, n * 8, g_stream));
+  CK(cudaMallocAsync((void**)&v1, n * 8, g_stream));
+  CK(cudaMallocAsync((void**)&mm, 32, g_stream));
+  flag = (int*)(mm + 2);
+  k_order_key<<<g, 256, 0, g_stream>>>((const void*)(uintptr_t)keys, key_kind, n, nullptr, k0);
+  if (own_v0) k_widen<<<g, 256, 0, g_stream>>>((const void*)(uintptr_t)vals, v0, val_width, n);
+  uint64_t init[4] = {~0ULL, 0ULL, 0ULL, 0ULL};
+  CK(cudaMemcpyAsync(mm, init, 32, cudaMemcpyHostToDevice, g_stream));
+  k_minmax_u64<<<g, 256, 0, g_stream>>>(k0, n, mm);
+  unsigned long long hmm[2];
+  CK(cudaMemcpyAsync(hmm, mm, 16, cudaMemcpyDeviceToHost, g_stream));
+  CK(cudaStreamSynchronize(g_stream));
+  uint64_t diff = hmm[0] ^ hmm[1];
+  int end_bit = diff ? 64 - __builtin_clzll(diff) : 1;  // only bits that vary
+  int begin_bit = end_bit > 32 ? end_bit - 32 : 0;
+  cub::DoubleBuffer<uint64_t> dk(k0, k1), dv(v0, v1);
+  size_t temp = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, temp, dk, dv, (int)n, begin_bit, end_bit, g_stream));
+  void* d_temp = nullptr;
+  CK(cudaMallocAsync(&d_temp, temp ? temp : 1, g_stream));
+  CK(cub::DeviceRadixSort::SortPairs(d_temp, temp, dk, dv, (int)n, begin_bit, end_bit, g_stream));
+  if (begin_bit > 0) {
+    uint64_t cap = n / 8 + 1024;
+    uint32_t* pos;
+    unsigned long long* npos = mm + 3;
+    CK(cudaMallocAsync((void**)&pos, cap * 4, g_stream));
+    CK(cudaMemsetAsync(npos, 0, 8, g_stream));
+    CK(cudaMemsetAsync(flag, 0, 4, g_stream));
+    k_disorder<<<g, 256, 0, g_stream>>>(dk.Current(), n, begin_bit, pos, npos, cap);
+    unsigned long long hn = 0;
+    CK(cudaMemcpyAsync(&hn, npos, 8, cudaMemcpyDeviceToHost, g_stream));
+    CK(cudaStreamSynchronize(g_stream));
+    int hflag = hn > cap;
+    if (!hflag && hn) {
+      k_fix_buckets<<<grid_for(hn, 128), 128, 0, g_stream>>>(dk.Current(), dv.Current(), n, begin_bit, pos, hn, 512,
+                                                             flag);
+      CK(cudaMemcpyAsync(&hflag, flag, 4, cudaMemcpyDeviceToHost, g_stream));
+      CK(cudaStreamSynchronize(g_stream));
+    }
+    if (hflag)  // skewed buckets: finish with a full stable sort of the low bits
+      CK(cub::DeviceRadixSort::SortPairs(d_temp, temp, dk, dv, (int)n, 0, begin_bit, g_stream));
+    CK(cudaFreeAsync(pos, g_stream));
+  }
+  uint8_t* heads;
+  uint32_t* starts;
+  int* d_cnt;
+  CK(cudaMallocAsync((void**)&heads, n, g_stream));
+  CK(cudaMallocAsync((void**)&starts, n * 4, g_stream));
+  CK(cudaMallocAsync((void**)&d_cnt, 8, g_stream));
+  k_heads1<<<g, 256, 0, g_stream>>>(dk.Current(), n, heads);
+  cub::CountingInputIterator<uint32_t> it(0);
+  size_t temp2 = 0;
+  CK(cub::DeviceSelect::Flagged(nullptr, temp2, it, heads, starts, d_cnt, (int)n, g_stream));
+  void* d_temp2 = nullptr;
+  CK(cudaMallocAsync(&d_temp2, temp2 ? temp2 : 1, g_stream));
+  CK(cub::DeviceSelect::Flagged(d_temp2, temp2, it, heads, starts, d_cnt, (int)n, g_stream));
+  int hK = 0;
+  CK(cudaMemcpyAsync(&hK, d_cnt, 4, cudaMemcpyDeviceToHost, g_stream));
+  CK(cudaStreamSynchronize(g_stream));
+  k_group_out<<<grid_for((uint64_t)hK + 1, 256), 256, 0, g_stream>>>(starts, (uint64_t)hK, n, dk.Current(), key_kind,
+                                                                     (int64_t*)(uintptr_t)offs_out,
+                                                                     (void*)(uintptr_t)ukeys_out);
+  if (val_width == 8)
+    CK(cudaMemcpyAsync((void*)(uintptr_t)vals_out, dv.Current(), n * 8, cudaMemcpyDeviceToDevice, g_stream));
+  else
+    k_narrow<<<g, 256, 0, g_stream>>>(dv.Current(), (void*)(uintptr_t)vals_out, val_width, n);
+  CK(cudaGetLastError());
+  CK(cudaFreeAsync(d_temp, g_stream));
+  CK(cudaFreeAsync(d_temp2, g_stream));
+  CK(cudaFreeAsync(heads, g_stream));
+  CK(cudaFreeAsync(starts, g_stream));
+  CK(cudaFreeAsync(d_cnt, g_stream));
+  CK(cudaFreeAsync(mm, g_stream));
+  if (own_k0) CK(cudaFreeAsync(k0, g_stream));
+  if (own_v0) CK(cudaFreeAsync(v0, g_stream));
+  CK(cudaFreeAsync(k1, g_stream));
+  CK(cudaFreeAsync(v1, g_stream));
+  *K_out = (uint64_t)hK;
   return 0;
 }
 

@@ -33,7 +33,7 @@ from . import runtime as rt
 from . import semantics as sem
 from .builders_dev import (AppenderDev, DDict, DGroups, DictDev, GroupDev, MergerDev, VecMergerDev, dict_payload,
                            finish_dict, finish_groups, gather_cols, sort_perm, tovec)
-from .codegen import BSpec, IterSpec, generate
+from .codegen import PIPE_STAGES, BSpec, IterSpec, generate
 from .columns import Col, DVec, to_device, to_payload, dvec_from_cols
 from .irtypes import (BOOL, F32, F64, I64, SIZE, Builder, DeviceUnsupported as _DU, Dict, DictMerger, Function,
                       GroupBuilder, Merger, Scalar, Simd, Struct, Vec, VecBuilder, VecMerger, is_flat, leaves)
@@ -471,7 +471,12 @@ class Ctx:
             windows.append(win)
             if not is_flat(elem):
                 raise DeviceUnsupported(f"iterating vec[{elem}] on the device")
-            specs.append(IterSpec(elem=elem, simd=it.simd, strided=(win[1] != 1), kinds=leaves(elem)))
+            aligned = False
+            if win[1] == 1 and count:
+                dv = d.dev() if isinstance(d, HostVec) else d
+                aligned = all((c.ptr + win[0] * SIZE[c.kind]) % 16 == 0 for c in dv.cols)
+            specs.append(IterSpec(elem=elem, simd=it.simd, strided=(win[1] != 1), kinds=leaves(elem),
+                                  aligned=aligned))
         builders = self.ev(e.builders, env)
         if count == 0:
             return builders
@@ -512,6 +517,7 @@ class Ctx:
         if cached is None:
             plan = generate(e if lam is e.func else _with_func(e, lam), specs, bstruct, captures,
                             self.externs, strategy)
+            plan.key_id = id(e)
             kern = rt.get_kernel(plan.source, plan.name)
             cached = (plan, kern, e, lam)
             with _plan_lock:
@@ -526,7 +532,19 @@ class Ctx:
         items = plan.items
         tile = plan.block * items
         ntiles = (count + tile - 1) // tile
-        occ = kern.blocks_per_sm(plan.block, plan.smem)
+        smem = plan.smem
+        stages = 0
+        if plan.pipe_stage_bytes:
+            # most pipeline stages that keep the occupancy of a 2-stage pipe
+            base = kern.blocks_per_sm(plan.block, plan.smem + 2 * plan.pipe_stage_bytes)
+            stages = 2
+            for s_ in range(PIPE_STAGES, 2, -1):
+                sm_ = plan.smem + s_ * plan.pipe_stage_bytes
+                if sm_ <= 200 * 1024 and kern.blocks_per_sm(plan.block, sm_) >= base:
+                    stages = s_
+                    break
+            smem = plan.smem + stages * plan.pipe_stage_bytes
+        occ = kern.blocks_per_sm(plan.block, smem)
         grid = max(1, min(ntiles, rt.sm_count() * occ))
         self.tasks += grid
         # per-launch builder resources
@@ -545,7 +563,7 @@ class Ctx:
                     res[b.bid] = (seg, status)
                     self._acct_append(st, count * b.k)
             elif isinstance(b.kind, DictMerger):
-                st.ensure(count * max(1, b.extra.get("maxm", 1)))
+                st.ensure(count * max(1, b.extra.get("maxm", 1)), hint_key=(plan.key_id, b.bid))
         tilectr = None
         if plan.schedule == "scan":
             tilectr = rt.alloc(8)
@@ -554,14 +572,15 @@ class Ctx:
         vals = {}
         for p in plan.params:
             vals[p.name] = self._param_value(p.key, count, datas, windows, bmap, res, captures, grid, tilectr)
+        vals["pipe_stages"] = stages
         blob = b"".join(_pack(p.ctype, vals[p.name]) for p in plan.params)
-        kern.launch(grid, plan.block, blob, plan.smem)
+        kern.launch(grid, plan.block, blob, smem)
         self.launches += 1
         # dictmerger overflow: grow and replay spilled merges
         for b in plan.builders:
             if isinstance(b.kind, DictMerger):
                 st = bmap[b.bid]
-                spilled = st.overflow_rows()
+                _, spilled = st.read_counters()
                 if spilled:
                     self._dict_regrow(st, spilled)
         self._keep = (tilectr, res)
@@ -578,7 +597,8 @@ class Ctx:
         import ctypes as _ct
         kw, vw, n = st.compact()
         old_over, old_cnt = st.over, spilled
-        st._alloc_table(st.cap * 4)
+        newcap = max(4 * st.cap, 1 << int(max(2 * n, 1) - 1).bit_length())
+        st._alloc_table(newcap)
         rt.memset(st.ocount.ptr, 0, 8)
         # replay: entries from the old table then the spill list, as a device loop
         kty = st.kind.key
@@ -613,6 +633,8 @@ class Ctx:
             return self.ticket()
         if k0 == "tilectr":
             return tilectr.ptr
+        if k0 == "pipe_stages":
+            return 0
         if k0 == "itcol":
             _, k, l = key
             d = datas[k]
@@ -669,8 +691,6 @@ class Ctx:
                     return st.cap - 1
                 if what == "count":
                     return st.count.ptr
-                if what == "limit":
-                    return st.limit
                 if what == "ocount":
                     return st.ocount.ptr
                 if what == "ocap":
@@ -785,7 +805,10 @@ def _bspecs(builders, strategy, count):
             raise DeviceUnsupported(f"vecbuilder[{v.kind.elem}] (nested element types) on the device")
         return bs
 
-    return go(builders), bmap
+    try:
+        return go(builders), bmap
+    finally:
+        del go  # the recursive closure would otherwise pin every builder (and its HBM) until GC
 
 
 def _bsig(bs):

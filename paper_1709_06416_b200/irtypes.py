@@ -63,7 +63,10 @@ def unflatten(t, values):
             return next(it)
         return tuple(go(f) for f in tt.fields)
 
-    return go(t)
+    try:
+        return go(t)
+    finally:
+        del go
 
 
 def flatten_value(t, v):

@@ -62,6 +62,7 @@ _SIGS = {
     "wg_narrow": (c_int, [u64, u64, c_int, u64]),
     "wg_widen": (c_int, [u64, u64, c_int, u64]),
     "wg_run_starts": (c_int, [ctypes.POINTER(u64), c_int, u64, u64, ctypes.POINTER(u64)]),
+    "wg_group_finish1": (c_int, [u64, c_int, u64, c_int, u64, u64, u64, u64, ctypes.POINTER(u64)]),
     "wg_gen_column": (c_int, [u64, u64, u64, c_int, c_int, u64, u64, i64, u64, ctypes.c_double, ctypes.c_double,
                               ctypes.c_double, c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]),
     "wg_mul_inplace_f64": (c_int, [u64, u64, u64]),
@@ -106,8 +107,25 @@ def _check(rc):
         raise WeldGpuError(load_library().wg_last_error().decode(errors="replace"))
 
 
+TRACE = os.environ.get("WELDGPU_TRACE", "") == "1"
+TRACE_TIMES = {}
+
+
+def _traced(name, fn):
+    import time
+    _check(lib().wg_sync())
+    t0 = time.perf_counter()
+    r = fn()
+    _check(lib().wg_sync())
+    TRACE_TIMES[name] = TRACE_TIMES.get(name, 0.0) + time.perf_counter() - t0
+    return r
+
+
 def call(name, *args):
-    _check(getattr(lib(), name)(*args))
+    if TRACE:
+        _traced(name, lambda: _check(getattr(lib(), name)(*args)))
+    else:
+        _check(getattr(lib(), name)(*args))
     LAUNCHES[0] += _KERNEL_CALLS.get(name, 0)
 
 
@@ -155,7 +173,10 @@ class DeviceBuffer:
 
     def __init__(self, nbytes: int):
         p = u64(0)
-        _check(lib().wg_alloc(max(int(nbytes), 1), ctypes.byref(p)))
+        if TRACE:
+            _traced("alloc", lambda: _check(lib().wg_alloc(max(int(nbytes), 1), ctypes.byref(p))))
+        else:
+            _check(lib().wg_alloc(max(int(nbytes), 1), ctypes.byref(p)))
         self.ptr = p.value
         self.nbytes = int(nbytes)
 
@@ -194,11 +215,17 @@ def memset(buf_ptr, value, nbytes):
 
 
 def h2d(dst_ptr, host_ptr, nbytes):
-    _check(lib().wg_h2d(dst_ptr, host_ptr, nbytes))
+    if TRACE:
+        _traced("h2d", lambda: _check(lib().wg_h2d(dst_ptr, host_ptr, nbytes)))
+    else:
+        _check(lib().wg_h2d(dst_ptr, host_ptr, nbytes))
 
 
 def d2h(host_ptr, src_ptr, nbytes):
-    _check(lib().wg_d2h(host_ptr, src_ptr, nbytes))
+    if TRACE:
+        _traced("d2h", lambda: _check(lib().wg_d2h(host_ptr, src_ptr, nbytes)))
+    else:
+        _check(lib().wg_d2h(host_ptr, src_ptr, nbytes))
 
 
 def d2h_async(host_ptr, src_ptr, nbytes):
@@ -270,7 +297,7 @@ def compile_check(src: str, name="weld_loop.cu"):
 LAUNCHES = [0]
 LAUNCH_HOOK = [None]
 _KERNEL_CALLS = {"wg_table_init": 1, "wg_table_compact": 1, "wg_order_key": 1, "wg_iota_u32": 1,
-                 "wg_sort_pairs": 1, "wg_gather": 1, "wg_narrow": 1, "wg_widen": 1, "wg_run_starts": 2,
+                 "wg_sort_pairs": 1, "wg_gather": 1, "wg_narrow": 1, "wg_widen": 1, "wg_run_starts": 2, "wg_group_finish1": 12,
                  "wg_gen_column": 1, "wg_mul_inplace_f64": 1, "wg_flush_l2": 1}
 
 
@@ -296,7 +323,10 @@ class Kernel:
         hook = LAUNCH_HOOK[0]
         if hook is not None:
             hook("before", self)
-        _check(lib().wg_launch(self.fn, grid, block, smem, buf, len(params)))
+        if TRACE:
+            _traced("kernel:" + self.name, lambda: _check(lib().wg_launch(self.fn, grid, block, smem, buf, len(params))))
+        else:
+            _check(lib().wg_launch(self.fn, grid, block, smem, buf, len(params)))
         LAUNCHES[0] += 1
         if hook is not None:
             hook("after", self)
