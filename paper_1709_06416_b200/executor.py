@@ -941,3 +941,66 @@ def _infer_free_type(e, name):
         if isinstance(node, Ident) and node.name == name and node.ty is not None:
             return node.ty
     return None
+
+
+def evaluate_partials(loop, env, config=None, externs=None, idx0=0, rank=0):
+    """Run one ``for`` loop over this rank's row shard and return each
+    builder's *partial* state as host arrays (for distributed.combine_*).
+    Vecmerger bins on ranks > 0 start from the fold identity so ``init`` is
+    counted once."""
+    from dataclasses import replace
+    from .builders_dev import _value_words_to_cols, _words_to_cols
+    from .columns import col_to_numpy
+    from .irtypes import internal_identity as _iid
+    cfg = config or EngineConfig(memory_limit=1 << 46)
+    ctx = Ctx(cfg, externs, idx0=idx0)
+    frame = {}
+    for name, v in (env or {}).items():
+        payload = v.data if isinstance(v, Value) else v
+        ty = v.ty if isinstance(v, Value) else None
+        frame[name] = payload if isinstance(payload, DVec) or not isinstance(ty, Vec) else HostVec(ty, payload)
+    bval = ctx.ev(loop.builders, frame)
+    blist = []
+    _collect_builders(bval, blist)
+    for b in blist:
+        if isinstance(b, VecMergerDev) and rank > 0:
+            for c, k in zip(b.cols, b.ks):
+                arr = np.full(b.n, _iid(b.kind.op, k), dtype=np.dtype(
+                    {"i32": "<i4", "i64": "<i8", "f32": "<f4", "f64": "<f8"}[k]))
+                rt.h2d(c.ptr, arr.ctypes.data, arr.nbytes)
+    frame["__wg_b"] = bval
+    ctx.run_loop(replace(loop, builders=Ident("__wg_b", ty=loop.builders.ty)), frame)
+    ctx.check_device()
+    out = []
+    for b in blist:
+        b.consume()
+        kind = b.kind
+        if isinstance(kind, Merger):
+            F = len(b.ks)
+            w = np.empty(F + 1, dtype=np.uint64)
+            rt.d2h(w.ctypes.data, b.slot.ptr, w.nbytes)
+            from .irtypes import from_bits
+            out.append({"kind": "merger", "op": kind.op, "kinds": b.ks, "has": bool(w[F]),
+                        "values": [from_bits(k, int(x)) for k, x in zip(b.ks, w[:F])]})
+        elif isinstance(kind, VecBuilder):
+            cols, n = b.concat() if b.segments else ([], 0)
+            out.append({"kind": "appender", "cols": [col_to_numpy(c, n) for c in cols] if cols else
+                        [np.zeros(0, dtype={"bool": "u1", "i32": "<i4", "i64": "<i8", "f32": "<f4",
+                                            "f64": "<f8"}[k]) for k in b.kinds]})
+        elif isinstance(kind, VecMerger):
+            out.append({"kind": "vecmerger", "op": kind.op, "kinds": b.ks,
+                        "cols": [col_to_numpy(c, b.n) for c in b.cols]})
+        elif isinstance(kind, DictMerger):
+            if b.table is None:
+                b.ensure(1)
+            kw, vw, n = b.compact()
+            kc = _words_to_cols(kw, b.kks, b.lay, n)
+            vc = _value_words_to_cols(vw, b.vks, n)
+            out.append({"kind": "dict", "op": kind.op, "vkinds": b.vks,
+                        "keys": [col_to_numpy(c, n) for c in kc], "vals": [col_to_numpy(c, n) for c in vc]})
+        elif isinstance(kind, GroupBuilder):
+            cols, n = b.concat() if b.segments else ([Col.alloc(k, 0) for k in b.kinds], 0)
+            nk = len(b.kks)
+            arrs = [col_to_numpy(c, n) for c in cols]
+            out.append({"kind": "group", "keys": arrs[:nk], "vals": arrs[nk:]})
+    return out

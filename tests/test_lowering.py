@@ -1,0 +1,78 @@
+"""Every loop of the reference's differential corpus, at several optimizer
+levels, lowers to CUDA and (a sample of) compiles with NVRTC for sm_100a --
+no GPU needed.  The five benchmark kernels always compile."""
+import os
+
+import pytest
+
+from helpers import load_golden
+
+CORPUS = load_golden("corpus.json")["programs"]
+UNSUPPORTED = {"vec-of-vec-0", "vec-of-vec-1", "vec-of-vec-2"}
+
+
+def _tree(src, inputs, level):
+    import paper_1709_06416_b200  # noqa: F401
+    from weldmill.optim import OptLevel, optimize
+    from weldmill.parser import parse, parse_type_text
+    from weldmill.sugar import expand
+    from weldmill.typecheck import check_linearity, infer
+    env = {k: parse_type_text(t) for k, t in inputs.items()}
+    typed = infer(expand(parse(src)), env)
+    check_linearity(typed)
+    lv = OptLevel.all() if level == "O3" else (OptLevel.none() if level == "none" else
+                                               OptLevel.all().disable(level))
+    return optimize(typed, lv)[0]
+
+
+@pytest.mark.parametrize("level", ["O3", "none", "vectorize", "fuse"])
+def test_corpus_lowers(level):
+    from paper_1709_06416_b200 import codegen
+    n = 0
+    for p in CORPUS:
+        if p["name"] in UNSUPPORTED:
+            continue
+        plans = codegen.static_plans(_tree(p["source"], p["inputs"], level))
+        for pl in plans:
+            assert "extern \"C\" __global__" in pl.source
+        n += len(plans)
+    assert n > 250
+
+
+def test_unsupported_shapes_raise():
+    from paper_1709_06416_b200 import codegen
+    from paper_1709_06416_b200.irtypes import DeviceUnsupported
+    p = next(p for p in CORPUS if p["name"] == "vec-of-vec-0")
+    with pytest.raises(DeviceUnsupported):
+        codegen.static_plans(_tree(p["source"], p["inputs"], "O3"))
+
+
+def test_benchmark_kernels_compile_for_sm100a():
+    from paper_1709_06416_b200 import codegen, runtime, workloads as W
+    for wl in W.WORKLOADS.values():
+        for smem in (True, False):
+            for plan in codegen.static_plans(W.compile_program(wl), externs=wl.externs, smem=smem):
+                assert runtime.compile_check(plan.source) > 0
+
+
+def test_corpus_sample_compiles():
+    from paper_1709_06416_b200 import codegen, runtime
+    seen = set()
+    step = int(os.environ.get("WELDGPU_TEST_COMPILE_STRIDE", "7"))
+    for p in CORPUS[::step]:
+        if p["name"] in UNSUPPORTED:
+            continue
+        for pl in codegen.static_plans(_tree(p["source"], p["inputs"], "O3")):
+            if pl.source in seen:
+                continue
+            seen.add(pl.source)
+            assert runtime.compile_check(pl.source) > 0, p["name"]
+    assert len(seen) > 20
+
+
+def test_generated_literals_are_exact():
+    from paper_1709_06416_b200.codegen import c_literal
+    assert c_literal("f64", 0.1) == "__longlong_as_double(0x3fb999999999999aLL)"
+    assert c_literal("i64", -(2**63)) == "((i64)0x8000000000000000ULL)"
+    assert c_literal("i32", -1) == "((i32)0xffffffffU)"
+    assert c_literal("f64", float("inf")).endswith("0x7ff0000000000000LL)")
