@@ -52,14 +52,15 @@ class BuilderBase:
 
 
 class MergerDev(BuilderBase):
+    """Slot = F value words + merged flag.  The first kernel launch into the
+    merger writes the slot (no host-side initialisation copy); a merger
+    that never ran a loop reads as the reference identity."""
+
     def __init__(self, kind: Merger):
         super().__init__(kind)
         self.ks = leaves(kind.elem)
-        words = [to_bits(k, internal_identity(kind.op, k)) for k in self.ks] + [0]
-        self.slot = rt.alloc(8 * len(words))
-        arr = np.array(words, dtype=np.uint64)
-        rt.h2d(self.slot.ptr, arr.ctypes.data, arr.nbytes)
-        self._keep = arr
+        self.slot = rt.alloc(8 * (len(self.ks) + 1))
+        self.launched = False
         self.part = None
         self.part_cap = 0
 
@@ -71,11 +72,24 @@ class MergerDev(BuilderBase):
             self.part_cap = need
         return self.part.ptr
 
-    def read(self):
+    def take_init_flag(self):
+        first = not self.launched
+        self.launched = True
+        return 1 if first else 0
+
+    def read_words(self):
+        """Slot words (values..., flag) or None if no loop ever ran."""
+        if not self.launched:
+            return None
         F = len(self.ks)
         arr = np.empty(F + 1, dtype=np.uint64)
         rt.d2h(arr.ctypes.data, self.slot.ptr, arr.nbytes)
-        if not arr[F]:
+        return arr
+
+    def read(self):
+        arr = self.read_words()
+        F = len(self.ks)
+        if arr is None or not arr[F]:
             vals = [identity_value(self.kind.op, k) for k in self.ks]
         else:
             vals = [from_bits(k, int(w)) for k, w in zip(self.ks, arr[:F])]
@@ -163,7 +177,7 @@ class DictDev(BuilderBase):
     then grows the table (4x the distinct count), re-inserts the entries and
     replays the spilled merges (all dict folds are commutative).  The table
     is sized from the distinct count the same loop produced last time, else
-    from min(merges, 2^20)."""
+    from min(merges, 2^24)."""
 
     def __init__(self, kind: DictMerger):
         super().__init__(kind)
@@ -199,7 +213,7 @@ class DictDev(BuilderBase):
         if self.table is None:
             self.hint_key = hint_key
             seen = _SIZE_HINTS.get(hint_key)
-            want = seen if seen is not None else min(rows, 1 << 20)
+            want = seen if seen is not None else min(rows, 1 << 24)
             self._alloc_table(1 << max(10, int(max(want, 1) * 2 - 1).bit_length()))
         if rows > self.ocap:
             self.over = ([rt.alloc(8 * rows) for _ in range(self.nw)],

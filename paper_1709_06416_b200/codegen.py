@@ -62,6 +62,11 @@ DEFER_DICT = _os.environ.get("WELDGPU_DEFER_DICT", "1") == "1"
 AGG_MAX_GROUPS = int(_os.environ.get("WELDGPU_AGG_GROUPS", "8"))
 REGCACHE = int(_os.environ.get("WELDGPU_REGCACHE", "4"))
 PIPE = _os.environ.get("WELDGPU_PIPE", "1") == "1"
+STAGE_SCAN = _os.environ.get("WELDGPU_STAGE_SCAN", "1") == "1"
+SCAN_PREFETCH = _os.environ.get("WELDGPU_SCAN_PREFETCH", "0") == "1"
+LB_PER = int(_os.environ.get("WELDGPU_LB_PER", "1"))
+LB_SLEEP = int(_os.environ.get("WELDGPU_LB_SLEEP", "64"))
+SCAN_PIPE = _os.environ.get("WELDGPU_SCAN_PIPE", "0") == "1"
 PIPE_STAGES = int(_os.environ.get("WELDGPU_PIPE_STAGES", "4"))
 PIPE_MAX_STAGES = 8
 PIPE_SMEM_BUDGET = int(_os.environ.get("WELDGPU_PIPE_SMEM", str(48 * 1024)))
@@ -678,7 +683,10 @@ class Gen:
                     for f, (x, k) in enumerate(zip(vals, ks)):
                         val = f"(u8)({x.c})" if k == BOOL else x.c
                         col = self.param(f"a{b.bid}_{f}", f"{STYPE[k]}*", ("b", b.bid, "col", f))
-                        self.emit(f"{col}[wpos{b.bid}] = {val};")
+                        if b.extra.get("staged"):
+                            self.emit(f"s_ap{b.bid}_{f}[wpos{b.bid}] = {val};")
+                        else:
+                            self.emit(f"{col}[wpos{b.bid}] = {val};")
                     self.emit(f"wpos{b.bid} += 1;")
                 return
             raise DeviceUnsupported(f"appender mode {b.mode}")
@@ -750,6 +758,24 @@ class Gen:
         slot = self.tmp("sl")
         self.emit("{")
         self.ind += 1
+        R = b.extra.get("regcache", 0)
+        if R and nw == 1:
+            # level 0: per-thread register cache (hits fold with no memory traffic)
+            op = OPSTRUCT[kind.op]
+            kc = words[0]
+
+            def fold(r):
+                return " ".join(f"rv{b.bid}_{r}_{f} = {op}<{CTYPE[k]}>::f(rv{b.bid}_{r}_{f}, {x.c});"
+                                for f, (x, k) in enumerate(zip(vals, vks)))
+            hit = self.tmp("hit")
+            self.emit(f"bool {hit} = true;")
+            chain = " else ".join(f"if (rk{b.bid}_{r} == {kc}) {{ {fold(r)} }}" for r in range(R))
+            claim = " else ".join(f"if (rk{b.bid}_{r} == WG_EMPTY_KEY) {{ rk{b.bid}_{r} = {kc}; {fold(r)} }}"
+                                  for r in range(R))
+            self.emit(f"{chain} else if ({kc} != WG_EMPTY_KEY) {{ {claim} else {{ {hit} = false; }} }} "
+                      f"else {{ {hit} = false; }}")
+            self.emit(f"if (!{hit}) {{")
+            self.ind += 1
         if b.mode == "smem" and nw == 1:
             # Privatised first level: per-CTA table in shared memory.
             ssl = self.tmp("ss")
@@ -790,6 +816,9 @@ class Gen:
         self.ind -= 1
         self.emit("}")
         if b.mode == "smem" and nw == 1:
+            self.ind -= 1
+            self.emit("}")
+        if R and nw == 1:
             self.ind -= 1
             self.emit("}")
         self.ind -= 1
@@ -989,11 +1018,14 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
     for b in g.bspecs:
         mn, mx = counts.get(b, (0, 0))
         b.extra["maxm"] = mx
-        if isinstance(b.kind, DictMerger) and mx <= 1 and key_layout(leaves(b.kind.key))[1] == 1 \
-                and DEFER_DICT:
-            b.extra["deferred"] = True
-            if REGCACHE and len(leaves(b.kind.value)) <= 8:
-                b.extra["regcache"] = REGCACHE
+        if isinstance(b.kind, DictMerger) and mx <= 1 and key_layout(leaves(b.kind.key))[1] == 1:
+            if b.extra.get("lowcard"):
+                # low cardinality: inline register cache in front of the shared table
+                if REGCACHE and len(leaves(b.kind.value)) <= 8:
+                    b.extra["regcache"] = REGCACHE
+            elif DEFER_DICT:
+                # high / unknown cardinality: deferred merges, batched HBM probes
+                b.extra["deferred"] = True
         if isinstance(b.kind, (VecBuilder, GroupBuilder)):
             if isinstance(b.kind, VecBuilder):
                 b.extra["kinds"] = leaves(b.kind.elem)
@@ -1010,6 +1042,25 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
                 raise DeviceUnsupported("appends inside a data-dependent nested loop (two-pass sizing not lowered)")
 
     scan_bs = [b for b in g.bspecs if b.mode == "scan"]
+    if scan_bs and not (items or ITEMS_OVERRIDE):
+        # larger tiles for look-back kernels: half as many tiles to resolve
+        ITEMS = min(16, ITEMS * 2)
+        g.items = ITEMS
+        for b in g.bspecs:
+            if b.mode == "direct":
+                b.extra["buffered"] = ITEMS * b.k <= 32
+    # order-preserving appenders stage their tile output in shared memory so
+    # the global stores are contiguous per tile (coalesced)
+    staged_bytes = 0
+    for b in scan_bs:
+        b.extra["staged"] = False
+    if scan_bs and STAGE_SCAN:
+        need = sum(BLOCK * ITEMS * b.k * SIZE[k] for b in scan_bs for k in b.extra["kinds"])
+        if need <= 40 * 1024:
+            for b in scan_bs:
+                b.extra["staged"] = True
+            staged_bytes = need
+
     merger_bs = [b for b in g.bspecs if isinstance(b.kind, Merger)]
     schedule = "scan" if scan_bs else "static"
 
@@ -1072,6 +1123,7 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
     for b in merger_bs:
         g.param(f"m{b.bid}_part", "u64*", ("b", b.bid, "part"))
         g.param(f"m{b.bid}_slot", "u64*", ("b", b.bid, "slot"))
+        g.param(f"m{b.bid}_init", "i64", ("b", b.bid, "init"))
     if merger_bs:
         g.param("ticket", "unsigned int*", ("ticket",))
     for b in g.bspecs:
@@ -1143,7 +1195,10 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
     # bulk-async column pipeline (static schedule, contiguous 16B-aligned
     # columns).  The stage count is a launch parameter: the executor picks
     # the most stages that do not lower the kernel's occupancy.
-    pipe = bool(PIPE and not scan_bs and loads and all((not it.strided) and it.aligned for it in iters))
+    # Scan kernels use it too: with a persistent, fully resident grid the
+    # static round-robin tile order is a valid look-back order.
+    pipe = bool(PIPE and (SCAN_PIPE or not scan_bs) and loads
+                and all((not it.strided) and it.aligned for it in iters))
     pipe_off = pipe_stage_bytes = 0
     pipe_col_off = []
     if pipe:
@@ -1164,6 +1219,8 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
 
     # ---- assemble ----------------------------------------------------------
     src = []
+    src.append(f"#define WG_LB_PER {LB_PER}")
+    src.append(f"#define WG_LB_SLEEP {LB_SLEEP}")
     src.append('#include "weld_device.cuh"')
     src.append(f"#define BLOCK {BLOCK}")
     src.append(f"#define ITEMS {ITEMS}")
@@ -1193,12 +1250,11 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
     if scan_bs:
         src.append("  __shared__ i64 s_scan[33];")
         src.append(f"  __shared__ i64 s_toff[{len(scan_bs)}];")
-        src.append("  __shared__ i64 s_tile;")
-        src.append("  while (true) {")
-        src.append("    if (threadIdx.x == 0) s_tile = (i64)atomicAdd(p.tilectr, 1ULL);")
-        src.append("    __syncthreads();")
-        src.append("    const i64 tile = s_tile;")
-        src.append("    if (tile >= ntiles) break;")
+        src.append("  __shared__ i64 s_tile[2];")
+        for b in scan_bs:
+            if b.extra["staged"]:
+                for f, kk in enumerate(b.extra["kinds"]):
+                    src.append(f"  __shared__ __align__(16) {STYPE[kk]} s_ap{b.bid}_{f}[TILE * {b.k}];")
     def load_lines(tvar, suffix, ind):
         out = [f"{ind}{{ const i64 lt0_ = {tvar} * TILE + (i64)threadIdx.x * ITEMS; const bool lfull_ = (lt0_ + ITEMS <= n);"]
         for (arr, st, kk, per, k, l, col) in loads:
@@ -1218,7 +1274,7 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
         return [f"{ind}alignas(16) {st} {arr}{suffix}[{'ITEMS * %d' % per if per > 1 else 'ITEMS'}];"
                 for (arr, st, kk, per, k, l, col) in loads]
 
-    def tile_body():
+    def tile_body(mid=None):
         """Everything a thread does for one tile once its columns are in
         registers (x arrays): body, buffered stores, deferred dict merges,
         and for scan appenders the block scan + look-back + store phase."""
@@ -1263,8 +1319,10 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
                 out.append(f"      if (threadIdx.x == 0) {{ s_toff[{si}] = pre_; if (tile == ntiles - 1) *p.a{b.bid}_total = pre_ + agg{b.bid}; }}")
                 out.append("    }")
             out.append("    __syncthreads();")
+            out.extend(mid or [])
             for si, b in enumerate(scan_bs):
-                out.append(f"    wpos{b.bid} += s_toff[{si}];")
+                if not b.extra["staged"]:
+                    out.append(f"    wpos{b.bid} += s_toff[{si}];")
             out.append("#pragma unroll")
             out.append("    for (int j = 0; j < ITEMS; ++j) {")
             out.append("      const i64 li = t0 + j;")
@@ -1273,12 +1331,51 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
             out.extend(body_b)
             out.append("      }")
             out.append("    }")
+            if any(b.extra["staged"] for b in scan_bs):
+                out.append("    __syncthreads();")
+                for si, b in enumerate(scan_bs):
+                    if not b.extra["staged"]:
+                        continue
+                    for f, kk in enumerate(b.extra["kinds"]):
+                        out.append(f"    for (int q = threadIdx.x; q < (int)agg{b.bid}; q += BLOCK) "
+                                   f"__stcs(p.a{b.bid}_{f} + s_toff[{si}] + q, s_ap{b.bid}_{f}[q]);")
+                out.append("    __syncthreads();")
         return out
 
-    if scan_bs:
+    if scan_bs and not pipe and not SCAN_PREFETCH:
+        # Dynamic tiles, claimed in order through an atomic counter (so every
+        # predecessor a tile's look-back waits on is held by a running CTA).
+        src.append("  while (true) {")
+        src.append("    if (threadIdx.x == 0) s_tile[0] = (i64)atomicAdd(p.tilectr, 1ULL);")
+        src.append("    __syncthreads();")
+        src.append("    const i64 tile = s_tile[0];")
+        src.append("    if (tile >= ntiles) break;")
         src.extend(decl_lines("", "    "))
         src.extend(load_lines("tile", "", "    "))
         src.extend(tile_body())
+        src.append("  }")
+    elif scan_bs and not pipe:
+        # (experimental) the next tile is claimed at the top of the current
+        # one and its columns loaded before the store phase.  Measured slower:
+        # a claimed-but-unstarted tile lengthens every successor's look-back.
+        src.append("  if (threadIdx.x == 0) s_tile[0] = (i64)atomicAdd(p.tilectr, 1ULL);")
+        src.append("  __syncthreads();")
+        src.append("  i64 tile = s_tile[0];")
+        src.append("  int par_ = 0;")
+        src.extend(decl_lines("", "  "))
+        src.append("  if (tile < ntiles)")
+        src.extend(load_lines("tile", "", "  "))
+        src.append("  while (tile < ntiles) {")
+        src.append("    if (threadIdx.x == 0) s_tile[par_ ^ 1] = (i64)atomicAdd(p.tilectr, 1ULL);")
+        mid = ["    const i64 ntile_ = s_tile[par_ ^ 1];"]
+        mid += decl_lines("_nx", "    ")
+        mid.append("    if (ntile_ < ntiles)")
+        mid += load_lines("ntile_", "_nx", "    ")
+        src.extend(tile_body(mid))
+        for (arr, st, kk, per, k, l, col) in loads:
+            cnt = f"ITEMS * {per}" if per > 1 else "ITEMS"
+            src.append(f"#pragma unroll\n    for (int q = 0; q < {cnt}; ++q) {arr}[q] = {arr}_nx[q];")
+        src.append("    tile = ntile_; par_ ^= 1;")
         src.append("  }")
     elif pipe:
         # Bulk-async (TMA engine) column streaming: every full tile's column
@@ -1396,8 +1493,11 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
                            f" a_ = {op}::f(a_, wg_from_bits<{ct}>(__ldcg(p.m{b.bid}_part + (u64)q * {F + 1} + {f})));"
                            f" h_ |= (int)__ldcg(p.m{b.bid}_part + (u64)q * {F + 1} + {F}); }}")
                 src.append(f"      wg_block_fold<{ct}, {op}>(a_, h_, {ident}, ({ct}*)s_red, s_redh);")
-                src.append(f"      if (threadIdx.x == 0 && h_) {{ p.m{b.bid}_slot[{f}] = wg_to_bits<{ct}>({op}::f(wg_from_bits<{ct}>(p.m{b.bid}_slot[{f}]), a_));"
-                           f" p.m{b.bid}_slot[{F}] = 1; }} }}")
+                # first launch into this merger writes the slot (no host-side init copy)
+                src.append(f"      if (threadIdx.x == 0) {{ if (p.m{b.bid}_init) {{ p.m{b.bid}_slot[{f}] = wg_to_bits<{ct}>(a_);"
+                           f" if ({f} == 0) p.m{b.bid}_slot[{F}] = (u64)h_; }}"
+                           f" else if (h_) {{ p.m{b.bid}_slot[{f}] = wg_to_bits<{ct}>({op}::f(wg_from_bits<{ct}>(p.m{b.bid}_slot[{f}]), a_));"
+                           f" p.m{b.bid}_slot[{F}] = 1; }} }} }}")
         src.append("    if (threadIdx.x == 0) *p.ticket = 0;")
         src.append("  }")
     src.append("}")
@@ -1663,7 +1763,7 @@ def _capture_val(g: Gen, name, ty, val):
 # suite to prove every loop of a program lowers and compiles for sm_100a.
 
 
-def static_plans(expr, env_types=None, externs=(), smem=True):
+def static_plans(expr, env_types=None, externs=(), smem=True, lowcard=False):
     """Yield a KernelPlan per ``for`` loop in a typed program, deriving the
     iteration, builder and capture specs from types alone."""
     from weldmill.expr import walk, free_variables as _fv
@@ -1702,6 +1802,7 @@ def static_plans(expr, env_types=None, externs=(), smem=True):
                         bs.mode = "smem"
                         bs.extra["smem_slots"] = 512
                         bs.extra["pattern"] = [0xFFFFFFFFFFFFFFFF] + [0] * (sw - 1)
+                        bs.extra["lowcard"] = lowcard
                 if isinstance(t.kind, VecMerger):
                     bs.mode = "global"
                 return bs

@@ -53,17 +53,20 @@ class ListLayout:
 class DVec:
     """A device vector: IR type vec[elem], length n, layout tree."""
 
-    __slots__ = ("elem", "n", "layout", "host_cache")
+    __slots__ = ("elem", "n", "layout", "host_cache", "_cols")
 
     def __init__(self, elem, n, layout):
         self.elem = elem
         self.n = int(n)
         self.layout = layout
         self.host_cache = None
+        self._cols = None
 
     @property
     def cols(self):
         """Flat leaf columns (only for flat element types)."""
+        if self._cols is not None:
+            return self._cols
         out = []
 
         def go(t, lay):
@@ -79,6 +82,7 @@ class DVec:
             go(self.elem, self.layout)
         finally:
             del go  # break the closure's self-reference cycle (it pins buffers until GC)
+        self._cols = out
         return out
 
     def __len__(self):
@@ -209,9 +213,59 @@ def col_to_numpy(col: Col, n: int) -> np.ndarray:
     return arr
 
 
+class _PinnedBlock:
+    """Page-locked host memory from cudaHostAlloc, recycled through a
+    size-keyed pool when the numpy array viewing it dies."""
+
+    __slots__ = ("ptr", "nbytes", "__weakref__")
+    _pool = {}
+
+    def __init__(self, nbytes):
+        free = _PinnedBlock._pool.get(nbytes)
+        if free:
+            self.ptr = free.pop()
+        else:
+            p = ctypes.c_void_p(0)
+            rt.call("wg_host_alloc", nbytes, ctypes.byref(p))
+            self.ptr = p.value
+        self.nbytes = nbytes
+
+    def __del__(self):
+        try:
+            _PinnedBlock._pool.setdefault(self.nbytes, []).append(self.ptr)
+        except Exception:
+            pass
+
+
+PINNED_MIN_BYTES = 1 << 20
+
+
+def pinned_empty(n, dtype):
+    """A numpy array in pinned host memory (full-bandwidth async D2H)."""
+    dt = np.dtype(dtype)
+    nbytes = max(n * dt.itemsize, 1)
+    blk = _PinnedBlock(nbytes)
+    raw = (ctypes.c_char * nbytes).from_address(blk.ptr)
+    raw._wg_owner = blk          # the array keeps the block alive
+    return np.frombuffer(raw, dtype=dt, count=n)
+
+
 def to_numpy(v: DVec):
-    """Flat vector -> numpy (scalar elem) or tuple of leaf arrays."""
-    arrs = [col_to_numpy(c, v.n) for c in v.cols]
+    """Flat vector -> numpy (scalar elem) or tuple of leaf arrays.  Large
+    columns land in pinned host memory: one async copy per column, one sync."""
+    cols = v.cols
+    arrs = []
+    for c in cols:
+        nb = v.n * SIZE[c.kind]
+        if nb >= PINNED_MIN_BYTES:
+            a = pinned_empty(v.n, NPTYPE[c.kind])
+            rt.d2h_async(a.ctypes.data, c.ptr, nb)
+        else:
+            a = np.empty(v.n, dtype=np.dtype(NPTYPE[c.kind]))
+            if nb:
+                rt.d2h_async(a.ctypes.data, c.ptr, nb)
+        arrs.append(a)
+    rt.sync()
     if isinstance(v.elem, Scalar):
         return arrs[0]
     return tuple(arrs)

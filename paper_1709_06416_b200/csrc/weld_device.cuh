@@ -269,7 +269,17 @@ __device__ __forceinline__ void wg_st_volatile(u64* p, u64 v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// Called by warp 0 only.  Returns the exclusive prefix of `tile`.
+// Called by warp 0 only.  Returns the exclusive prefix of `tile`.  Each
+// look-back step inspects a window of 32 x WG_LB_PER predecessors (lane L
+// covers distances 4L..4L+3), so the inclusive-prefix front moves 4x faster
+// than a one-status-per-lane window -- with ~600 tiles in flight that front
+// is what bounds a scan's throughput.
+#ifndef WG_LB_PER
+#define WG_LB_PER 1
+#endif
+#ifndef WG_LB_SLEEP
+#define WG_LB_SLEEP 0
+#endif
 __device__ __forceinline__ i64 wg_lookback(u64* status, i64 tile, i64 aggregate) {
   const int lane = threadIdx.x & 31;
   if (tile == 0) {
@@ -280,25 +290,39 @@ __device__ __forceinline__ i64 wg_lookback(u64* status, i64 tile, i64 aggregate)
   i64 excl = 0;
   i64 t = tile - 1;
   while (true) {
-    i64 idx = t - lane;
-    u64 s = (idx >= 0) ? wg_ld_volatile(status + idx) : WG_ST_PRE;
-    u64 flag = s >> 62;
-    unsigned mx = __ballot_sync(0xffffffffu, flag == 0);
-    unsigned mp = __ballot_sync(0xffffffffu, flag == 2);
-    unsigned upto;
-    if (mp) {
-      int first = __ffs(mp) - 1;
-      upto = (first == 31) ? 0xffffffffu : ((2u << first) - 1u);
-    } else {
-      upto = 0xffffffffu;
+    u64 s[WG_LB_PER];
+    int qp = WG_LB_PER;   // first prefix entry among this lane's span
+#pragma unroll
+    for (int q = 0; q < WG_LB_PER; ++q) {
+      const i64 idx = t - (i64)(lane * WG_LB_PER + q);
+      s[q] = (idx >= 0) ? wg_ld_volatile(status + idx) : WG_ST_PRE;
     }
-    if (mx & upto) continue;  // a needed predecessor has not published yet
-    i64 val = ((1u << lane) & upto) ? (i64)(s & WG_ST_MASK) : 0;
+#pragma unroll
+    for (int q = WG_LB_PER - 1; q >= 0; --q) if ((s[q] >> 62) == 2) qp = q;
+    bool xb = false;      // a not-ready entry before this lane's first prefix
+#pragma unroll
+    for (int q = 0; q < WG_LB_PER; ++q) if (q < qp && (s[q] >> 62) == 0) xb = true;
+    const unsigned mp = __ballot_sync(0xffffffffu, qp < WG_LB_PER);
+    const int first = mp ? __ffs(mp) - 1 : 32;        // lane holding the nearest prefix
+    const unsigned mx = __ballot_sync(0xffffffffu, xb);
+    const unsigned upto = (first >= 31) ? 0xffffffffu : ((2u << first) - 1u);
+    if (mx & upto) {  // a needed predecessor has not published yet: back off, retry
+#if WG_LB_SLEEP > 0
+      __nanosleep(WG_LB_SLEEP);
+#endif
+      continue;
+    }
+    i64 val = 0;
+    if (lane <= first) {
+      const int lim = (lane == first) ? qp : WG_LB_PER - 1;
+#pragma unroll
+      for (int q = 0; q < WG_LB_PER; ++q) if (q <= lim) val += (i64)(s[q] & WG_ST_MASK);
+    }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) val += __shfl_xor_sync(0xffffffffu, val, d);
     excl += val;
     if (mp) break;
-    t -= 32;
+    t -= 32 * WG_LB_PER;
   }
   if (lane == 0) wg_st_volatile(status + tile, WG_ST_PRE | (u64)(excl + aggregate));
   return excl;

@@ -625,8 +625,8 @@ int wg_module_function(uint64_t module, const char* name, uint64_t* fn) {
 
 int wg_occupancy(uint64_t fn, int block, int dyn_smem, int* blocks_per_sm) {
   NEED_INIT();
-  if (dyn_smem > 0)
-    CKD(p_cuFuncSetAttribute((CUfunction)(uintptr_t)fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, 200 * 1024));
+  if (dyn_smem > 0)  // opt in to exactly the requested dynamic shared memory (static + dynamic <= 227 KB)
+    CKD(p_cuFuncSetAttribute((CUfunction)(uintptr_t)fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, dyn_smem));
   CKD(p_cuOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, (CUfunction)(uintptr_t)fn, block, (size_t)dyn_smem));
   return 0;
 }
@@ -635,7 +635,7 @@ int wg_launch(uint64_t fn, uint32_t grid, uint32_t block, uint32_t dyn_smem, con
   NEED_INIT();
   CUfunction f = (CUfunction)(uintptr_t)fn;
   if (dyn_smem > 0)
-    CKD(p_cuFuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, 200 * 1024));
+    CKD(p_cuFuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)dyn_smem));
   size_t sz = (size_t)params_size;
   void* extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, const_cast<void*>(params), CU_LAUNCH_PARAM_BUFFER_SIZE, &sz,
                    CU_LAUNCH_PARAM_END};

@@ -33,9 +33,9 @@ from . import runtime as rt
 from . import semantics as sem
 from .builders_dev import (AppenderDev, DDict, DGroups, DictDev, GroupDev, MergerDev, VecMergerDev, dict_payload,
                            finish_dict, finish_groups, gather_cols, sort_perm, tovec)
-from .codegen import PIPE_STAGES, BSpec, IterSpec, generate
+from .codegen import DEFER_DICT, PIPE_STAGES, BSpec, IterSpec, generate
 from .columns import Col, DVec, to_device, to_payload, dvec_from_cols
-from .irtypes import (BOOL, F32, F64, I64, SIZE, Builder, DeviceUnsupported as _DU, Dict, DictMerger, Function,
+from .irtypes import (BOOL, F32, F64, I64, SIZE, identity_value, Builder, DeviceUnsupported as _DU, Dict, DictMerger, Function,
                       GroupBuilder, Merger, Scalar, Simd, Struct, Vec, VecBuilder, VecMerger, is_flat, leaves)
 
 
@@ -121,6 +121,7 @@ class Ctx:
         self.idx0 = idx0
         self.launches = 0
         self._ticket = None
+        self.dirty = False
 
     # -- memory accounting (run.py:208-228) --------------------------------
     def alloc(self, n):
@@ -146,6 +147,9 @@ class Ctx:
 
     # -- device error word ---------------------------------------------------
     def check_device(self):
+        if not self.dirty:
+            return
+        self.dirty = False
         code, info = rt.read_error()
         if code:
             cls = ERR_CLASSES.get(code, EvalError)
@@ -508,10 +512,11 @@ class Ctx:
             captures[name] = (cty, lenv[name])
 
         strategy = self.cfg.strategy
-        bstruct, bmap = _bspecs(builders, strategy, count)
-        key = (id(e), id(lam), tuple(repr(s) for s in specs), _bsig(bstruct),
-               tuple((k, repr(t)) for k, (t, _) in captures.items()), tuple(sorted(self.externs)),
-               tuple(bool(w[1] != 1 or w[0] != 0) for w in windows))
+        bstruct, bmap = _bspecs(builders, strategy, count, loop_id=id(e))
+        # The expression identities fix every type in the loop; only the
+        # runtime choices (strides, alignment, builder modes, externs) vary.
+        key = (id(e), id(lam), tuple((s.strided, s.aligned) for s in specs), _bsig(bstruct),
+               tuple(sorted(self.externs)))
         with _plan_lock:
             cached = _plan_cache.get(key)
         if cached is None:
@@ -576,6 +581,7 @@ class Ctx:
         blob = b"".join(_pack(p.ctype, vals[p.name]) for p in plan.params)
         kern.launch(grid, plan.block, blob, smem)
         self.launches += 1
+        self.dirty = True
         # dictmerger overflow: grow and replay spilled merges
         for b in plan.builders:
             if isinstance(b.kind, DictMerger):
@@ -670,6 +676,8 @@ class Ctx:
                     return st.partials(grid)
                 if what == "slot":
                     return st.slot.ptr
+                if what == "init":
+                    return st.take_init_flag()
             if isinstance(st, (AppenderDev, GroupDev)):
                 r = res[bid]
                 if what == "col":
@@ -770,7 +778,10 @@ def _collect_builders(v, out):
         raise EvalError("loop builders must be builders")
 
 
-def _bspecs(builders, strategy, count):
+LOWCARD_MAX = 4096
+
+
+def _bspecs(builders, strategy, count, loop_id=None):
     bmap = {}
     counter = [0]
 
@@ -791,12 +802,19 @@ def _bspecs(builders, strategy, count):
                 bs.mode = "global"
         if isinstance(v.kind, DictMerger):
             bs.extra["slot_words"] = v.slot_words
-            if strategy != "global" and v.nw == 1:
+            # Cardinality seen the last time this loop ran decides the
+            # variant: low -> register cache + shared table, otherwise (or
+            # unknown) -> deferred merges with batched HBM probes.
+            from .builders_dev import _SIZE_HINTS
+            seen = _SIZE_HINTS.get((loop_id, bid))
+            lowcard = seen is not None and seen <= LOWCARD_MAX
+            if strategy != "global" and v.nw == 1 and (lowcard or not DEFER_DICT):
                 ns = 512
                 if ns * v.slot_words * 8 <= 64 * 1024:
                     bs.mode = "smem"
                     bs.extra["smem_slots"] = ns
                     bs.extra["pattern"] = v.pattern()
+                    bs.extra["lowcard"] = lowcard
                 else:
                     bs.mode = "global"
             else:
@@ -814,7 +832,7 @@ def _bspecs(builders, strategy, count):
 def _bsig(bs):
     if isinstance(bs, tuple):
         return tuple(_bsig(x) for x in bs)
-    return (repr(bs.kind), bs.mode, tuple(sorted((k, repr(v)) for k, v in bs.extra.items())))
+    return (bs.mode, bs.extra.get("nbins"), bs.extra.get("smem_slots"))
 
 
 def _type_of(v, lam, name):
@@ -977,11 +995,14 @@ def evaluate_partials(loop, env, config=None, externs=None, idx0=0, rank=0):
         kind = b.kind
         if isinstance(kind, Merger):
             F = len(b.ks)
-            w = np.empty(F + 1, dtype=np.uint64)
-            rt.d2h(w.ctypes.data, b.slot.ptr, w.nbytes)
+            w = b.read_words()
             from .irtypes import from_bits
-            out.append({"kind": "merger", "op": kind.op, "kinds": b.ks, "has": bool(w[F]),
-                        "values": [from_bits(k, int(x)) for k, x in zip(b.ks, w[:F])]})
+            if w is None:
+                out.append({"kind": "merger", "op": kind.op, "kinds": b.ks, "has": False,
+                            "values": [identity_value(kind.op, k) for k in b.ks]})
+            else:
+                out.append({"kind": "merger", "op": kind.op, "kinds": b.ks, "has": bool(w[F]),
+                            "values": [from_bits(k, int(x)) for k, x in zip(b.ks, w[:F])]})
         elif isinstance(kind, VecBuilder):
             cols, n = b.concat() if b.segments else ([], 0)
             out.append({"kind": "appender", "cols": [col_to_numpy(c, n) for c in cols] if cols else

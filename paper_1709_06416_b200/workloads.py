@@ -77,6 +77,10 @@ Q1_PROGRAM = ("tovec(result(for({returnflag, linestatus, quantity, price, discou
 DICT_PROGRAM = "tovec(result(for({k, v}, dictmerger[i64, i64, +], (b, i, x) => merge(b, {x.0, x.1}))))"
 GROUP_PROGRAM = "tovec(result(for({k, v}, groupbuilder[i64, i64], (b, i, x) => merge(b, {x.0, x.1}))))"
 HIST_PROGRAM = "result(for({idx, w}, vecmerger[f64, +](bins), (b, i, x) => merge(b, {x.0, x.1})))"
+# Appender scans measured on their own: an order-preserving
+# filter (scan schedule: decoupled look-back) and a size-hinted map (DIRECT).
+FILTER_PROGRAM = "filter(v, (x) => x > 0)"
+MAP_PROGRAM = "map(v, (x) => x * 3 + 1)"
 
 _Q1_CUM = (0.25, 0.26, 0.75, 1.0)
 
@@ -123,6 +127,14 @@ WORKLOADS = {
          ColSpec("w", "f64", 1, 1, flo=0.0, fhi=1.0)],
         n=1_000_000_000, bytes_per_row=16, out_bytes=lambda n: 16_000_000,
         extra_inputs={"bins": ("vec[f64]", 1_000_000)}),
+    "filter": Workload(
+        "filter", "appender scan: order-preserving filter over i64 (~50% selectivity)", FILTER_PROGRAM,
+        [ColSpec("v", "i64", 0, 0, lo=-1000, span=2001)],
+        n=500_000_000, bytes_per_row=8, out_bytes=lambda n: n * 4, dtype="i64"),
+    "map": Workload(
+        "map", "appender scan: size-hinted map over i64", MAP_PROGRAM,
+        [ColSpec("v", "i64", 0, 0, lo=-1000, span=2001)],
+        n=500_000_000, bytes_per_row=16, out_bytes=lambda n: 0, dtype="i64"),
 }
 
 
@@ -231,8 +243,10 @@ def algorithmic_bytes(wl: Workload, n: int) -> int:
     if wl.name == "hist":
         extra = 2 * 8 * 1_000_000  # init read + bins written
         return n * wl.bytes_per_row + extra
-    if wl.name == "blackscholes":
+    if wl.name in ("blackscholes", "map"):
         return n * wl.bytes_per_row
+    if wl.name == "filter":
+        return n * 8 + n * 4          # read every row, write the ~50% kept (8 B each)
     if wl.name in ("dict", "group"):
         distinct = min(n, 10_000_000)
         out = distinct * 16 + (n * 8 if wl.name == "group" else 0)

@@ -50,8 +50,8 @@ def test_unsupported_shapes_raise():
 def test_benchmark_kernels_compile_for_sm100a():
     from paper_1709_06416_b200 import codegen, runtime, workloads as W
     for wl in W.WORKLOADS.values():
-        for smem in (True, False):
-            for plan in codegen.static_plans(W.compile_program(wl), externs=wl.externs, smem=smem):
+        for smem, low in ((True, False), (True, True), (False, False)):
+            for plan in codegen.static_plans(W.compile_program(wl), externs=wl.externs, smem=smem, lowcard=low):
                 assert runtime.compile_check(plan.source) > 0
 
 
