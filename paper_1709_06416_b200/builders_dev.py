@@ -220,6 +220,18 @@ class DictDev(BuilderBase):
                          [rt.alloc(8 * rows) for _ in self.vks])
             self.ocap = rows
 
+    def ensure_part(self, rows, nparts):
+        """Buckets for the partitioned mode: nparts x pcap records of
+        (key word, value words); counters zeroed for this launch."""
+        pcap = (rows * 5) // (4 * nparts) + 64
+        if getattr(self, "pcap", 0) < pcap or getattr(self, "nparts", 0) != nparts:
+            self.pcap = pcap
+            self.nparts = nparts
+            self.pcount = rt.alloc(8 * nparts)
+            self.pk = rt.alloc(8 * nparts * pcap)
+            self.pv = [rt.alloc(8 * nparts * pcap) for _ in self.vks]
+        rt.memset(self.pcount.ptr, 0, 8 * nparts)
+
     def _alloc_table(self, cap):
         self.cap = cap
         self.table = rt.alloc(8 * (cap + 1) * self.slot_words)

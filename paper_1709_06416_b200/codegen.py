@@ -993,6 +993,8 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
     ITEMS = items or ITEMS_OVERRIDE or choose_items(iters)
     if not (items or ITEMS_OVERRIDE) and any(isinstance(b.kind, DictMerger) for b in g.bspecs):
         ITEMS = min(ITEMS, 2)   # deferred merges + register caches are register-hungry
+    if any(b.extra.get("part") for b in g.bspecs):
+        ITEMS = min(ITEMS, 4)   # the tile's records are staged in static shared memory
     if not (items or ITEMS_OVERRIDE) and PIPE:
         # keep >= 2 pipeline stages inside the shared-memory budget
         row = sum(SIZE[k] * (W if it.simd else 1) for it in iters for k in it.kinds)
@@ -1641,6 +1643,58 @@ def _global_apply_lines(b, P, ind, key, vals):
     return L
 
 
+def dict_agg_source(kind, slot_words, S, pbits, name="wg_dagg"):
+    """Second kernel of the partitioned dictmerger: insert the bucketed
+    records into the HBM table in partition order (grid-stride over the
+    partition-major bucket array), so the CTAs' working set is a few
+    L2-resident table regions instead of the whole table."""
+    vks = leaves(kind.value)
+    V = len(vks)
+    opc = OPCODE[kind.op]
+    L = ['#include "weld_device.cuh"', "#define BLOCK 256", "struct Params {",
+         "  u64* pk;"] + [f"  u64* pv{f};" for f in range(V)] + [
+        "  unsigned long long* pcount; u64 pcap; u64 nparts;",
+        "  u64* table; u64 mask; unsigned long long* count; unsigned long long* ocount; u64 ocap;",
+        "  u64* ok0;"] + [f"  u64* ov{f};" for f in range(V)] + ["  i64* err;", "};",
+        f'extern "C" __global__ void __launch_bounds__(BLOCK) {name}(const Params p) {{',
+        "  int wg_claims = 0;",
+        "  const u64 total = p.nparts * p.pcap;",
+        "  for (u64 idx = blockIdx.x * (u64)BLOCK + threadIdx.x; idx < total; idx += (u64)gridDim.x * BLOCK) {",
+        "    const u64 part = idx / p.pcap, r = idx - part * p.pcap;",
+        "    if (r >= p.pcount[part]) continue;",
+        "    const u64 k_ = p.pk[idx];"]
+    for f, kk in enumerate(vks):
+        L.append(f"    const {CTYPE[kk]} v{f}_ = wg_from_bits<{CTYPE[kk]}>(p.pv{f}[idx]);")
+    L.append(f"    const i64 sl_ = wg_ht_find1(p.table, {slot_words}, p.mask, k_, wg_claims);")
+    L += _agg_apply(vks, opc, slot_words, "    ", "k_", [f"v{f}_" for f in range(V)])
+    L.append("  }")
+    L.append("  { int c_ = wg_claims;")
+    L.append("    for (int d = 16; d > 0; d >>= 1) c_ += __shfl_xor_sync(0xffffffffu, c_, d);")
+    L.append("    if ((threadIdx.x & 31) == 0 && c_) atomicAdd(p.count, (unsigned long long)c_); }")
+    L.append("}")
+    return "\n".join(L) + "\n", 0
+
+
+def _agg_apply(vks, opc, slot_words, ind, key, vals):
+    L = [f"{ind}if (sl_ >= 0) {{"]
+    for f, kk in enumerate(vks):
+        ct = CTYPE[kk]
+        L.append(f"{ind}  WgAtomicFold<{opc}, {ct}>::f(({ct}*)(p.table + (u64)sl_ * {slot_words} + {1 + f}), {vals[f]});")
+    L.append(f"{ind}}} else {{")
+    L.append(f"{ind}  const u64 o_ = atomicAdd(p.ocount, 1ULL);")
+    L.append(f"{ind}  if (o_ < p.ocap) {{ p.ok0[o_] = {key};")
+    for f, kk in enumerate(vks):
+        L.append(f"{ind}    p.ov{f}[o_] = wg_to_bits<{CTYPE[kk]}>({vals[f]});")
+    L.append(f"{ind}  }} else {{ wg_raise(p.err, WG_ERR_INTERNAL, 1); }}")
+    L.append(f"{ind}}}")
+    return L
+
+
+def to_bits_c(kind, v):
+    from .irtypes import to_bits
+    return to_bits(kind, v)
+
+
 def _deferred_dict_lines(g, b):
     """Apply the tile's pending dictmerger merges with the warp converged.
 
@@ -1673,6 +1727,76 @@ def _deferred_dict_lines(g, b):
         for f, kk in enumerate(vks):
             L.append(f"        dkv{B}_{f}[j] = a{f}_;")
         L.append("      }")
+    if b.extra.get("part"):
+        # Partitioned mode (cardinality >> L2).  Partition = the region of the
+        # HBM table a key's home slot falls in (pbits top bits of the slot
+        # index), so a second kernel that inserts the buckets in partition
+        # order touches one L2-resident region at a time.  Records are
+        # ranked per partition in shared memory so each tile issues one
+        # global atomic per non-empty partition (not one per record).
+        NP = 1 << b.extra["pbits"]
+        pcount = g.param(f"d{B}_pcount", "unsigned long long*", ("b", B, "pcount"))
+        pcap = g.param(f"d{B}_pcap", "u64", ("b", B, "pcap"))
+        pshift = g.param(f"d{B}_pshift", "u64", ("b", B, "pshift"))
+        pk = g.param(f"d{B}_pk", "u64*", ("b", B, "pk"))
+        pvs = [g.param(f"d{B}_pv{f}", "u64*", ("b", B, "pv", f)) for f in range(len(vks))]
+        V = len(vks)
+        L.append(f"      __shared__ unsigned s_ph{B}[{NP}], s_po{B}[{NP}];")
+        L.append(f"      __shared__ u64 s_pb{B}[{NP}];")
+        L.append(f"      __shared__ u64 s_rk{B}[TILE];")
+        for f in range(V):
+            L.append(f"      __shared__ u64 s_rv{B}_{f}[TILE];")
+        L.append(f"      __shared__ unsigned short s_rp{B}[TILE];")
+        L.append(f"      __shared__ i64 s_sc{B}[33];")
+        L.append(f"      unsigned pp_[ITEMS], pr_[ITEMS];")
+        L.append(f"      for (int q = threadIdx.x; q < {NP}; q += BLOCK) s_ph{B}[q] = 0u;")
+        L.append("      __syncthreads();")
+        L.append("#pragma unroll")
+        L.append("      for (int j = 0; j < ITEMS; ++j) {")
+        L.append(f"        if (!dkf{B}[j]) continue;")
+        L.append(f"        pp_[j] = (unsigned)((wg_mix64(dkk{B}[j]) & {P['mask']}) >> {pshift});")
+        L.append(f"        pr_[j] = atomicAdd(&s_ph{B}[pp_[j]], 1u);")
+        L.append("      }")
+        L.append("      __syncthreads();")
+        # tile-local counting sort by partition: exclusive offsets + one global
+        # reservation per non-empty partition
+        L.append(f"      {{ i64 tot_; for (int q0 = 0; q0 < {NP}; q0 += BLOCK) {{ const int q = q0 + threadIdx.x;")
+        L.append(f"          const unsigned c_ = (q < {NP}) ? s_ph{B}[q] : 0u;")
+        L.append(f"          const i64 ex_ = wg_block_exclusive_scan((i64)c_, s_sc{B}, &tot_);")
+        L.append(f"          if (q < {NP}) {{ s_po{B}[q] = (unsigned)ex_ + (q0 ? s_po{B}[q0 - 1] + s_ph{B}[q0 - 1] : 0u);"
+                 f" if (c_) s_pb{B}[q] = atomicAdd({pcount} + q, (unsigned long long)c_); }}")
+        L.append("          __syncthreads(); } }")
+        L.append("#pragma unroll")
+        L.append("      for (int j = 0; j < ITEMS; ++j) {")
+        L.append(f"        if (!dkf{B}[j]) continue;")
+        L.append(f"        const unsigned lp_ = s_po{B}[pp_[j]] + pr_[j];")
+        L.append(f"        s_rk{B}[lp_] = dkk{B}[j]; s_rp{B}[lp_] = (unsigned short)pp_[j];")
+        for f, kk in enumerate(vks):
+            L.append(f"        s_rv{B}_{f}[lp_] = wg_to_bits<{CTYPE[kk]}>(dkv{B}_{f}[j]);")
+        L.append(f"        dkf{B}[j] = false;")
+        L.append("      }")
+        L.append("      __syncthreads();")
+        # coalesced bucket writes: consecutive threads -> consecutive slots of
+        # one partition's run
+        L.append(f"      {{ const unsigned m_ = s_po{B}[{NP - 1}] + s_ph{B}[{NP - 1}];")
+        L.append("        for (unsigned t_ = threadIdx.x; t_ < m_; t_ += BLOCK) {")
+        L.append(f"          const unsigned pq_ = s_rp{B}[t_];")
+        L.append(f"          const u64 pos_ = s_pb{B}[pq_] + (t_ - s_po{B}[pq_]);")
+        L.append(f"          if (pos_ < {pcap}) {{")
+        L.append(f"            const u64 at_ = (u64)pq_ * {pcap} + pos_;")
+        L.append(f"            __stcs({pk} + at_, s_rk{B}[t_]);")
+        for f in range(V):
+            L.append(f"            __stcs({pvs[f]} + at_, s_rv{B}_{f}[t_]);")
+        L.append("          } else {")
+        L.append(f"            const u64 k_ = s_rk{B}[t_];")
+        for f, kk in enumerate(vks):
+            L.append(f"            const {CTYPE[kk]} v{f}_ = wg_from_bits<{CTYPE[kk]}>(s_rv{B}_{f}[t_]);")
+        L.append(f"            const i64 sl_ = wg_ht_find1({P['table']}, {sw}, {P['mask']}, k_, wg_claims{B});")
+        L += _global_apply_lines(b, P, "            ", "k_", [f"v{f}_" for f in range(V)])
+        L.append("          }")
+        L.append("        }")
+        L.append("      }")
+        L.append("      __syncthreads();")
     # global table: issue every first probe, then resolve
     L.append(f"      u64 h_[ITEMS], c_[ITEMS];")
     L.append("#pragma unroll")
@@ -1763,7 +1887,7 @@ def _capture_val(g: Gen, name, ty, val):
 # suite to prove every loop of a program lowers and compiles for sm_100a.
 
 
-def static_plans(expr, env_types=None, externs=(), smem=True, lowcard=False):
+def static_plans(expr, env_types=None, externs=(), smem=True, lowcard=False, part=False):
     """Yield a KernelPlan per ``for`` loop in a typed program, deriving the
     iteration, builder and capture specs from types alone."""
     from weldmill.expr import walk, free_variables as _fv
@@ -1798,7 +1922,9 @@ def static_plans(expr, env_types=None, externs=(), smem=True, lowcard=False):
                     sw = (1 if nw == 1 else 1 + nw) + len(leaves(t.kind.value))
                     bs.extra["slot_words"] = sw
                     bs.mode = "global"
-                    if nw == 1 and smem:
+                    if nw == 1 and part:
+                        bs.extra.update(part=True, pbits=8, agg_S=0)
+                    elif nw == 1 and smem:
                         bs.mode = "smem"
                         bs.extra["smem_slots"] = 512
                         bs.extra["pattern"] = [0xFFFFFFFFFFFFFFFF] + [0] * (sw - 1)

@@ -540,6 +540,24 @@ __device__ __forceinline__ void wg_store_contig(T* __restrict__ dst, const T (&s
   for (int q = 0; q < N; ++q) dst[q] = src[q];
 }
 
+// Shared-memory table probe with a caller-chosen probe limit.
+__device__ __forceinline__ int wg_sht_findp(u64* t, int sw, int mask, u64 key, int max_probe) {
+  if (key == WG_EMPTY_KEY) return -1;
+  int h = (int)(wg_mix64(key) & (u64)mask);
+#pragma unroll 1
+  for (int probe = 0; probe < max_probe; ++probe) {
+    u64* s = t + (u64)h * sw;
+    u64 cur = *(volatile u64*)s;
+    if (cur == key) return h;
+    if (cur == WG_EMPTY_KEY) {
+      u64 prev = atomicCAS((unsigned long long*)s, WG_EMPTY_KEY, key);
+      if (prev == WG_EMPTY_KEY || prev == key) return h;
+    }
+    h = (h + 1) & mask;
+  }
+  return -1;
+}
+
 // Per-CTA shared-memory table (privatised dictmerger level 1) for one-word
 // keys.  Bounded probing: a miss with no free slot returns -1 and the
 // caller merges straight into the global table instead.

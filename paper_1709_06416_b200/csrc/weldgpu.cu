@@ -125,7 +125,10 @@ __global__ void k_table_init(uint64_t* table, uint64_t nslots, int slot_words, c
 // all ones); mode 2: claim word is a state word (2 = full).
 __global__ void k_table_compact(const uint64_t* table, uint64_t nslots, int slot_words, int mode,
                                 uint64_t** out_words, int nout, unsigned long long* counter) {
-  const int lane = threadIdx.x & 31;
+  // one output reservation per CTA iteration (block scan of occupancy)
+  __shared__ unsigned s_w[32];
+  __shared__ unsigned long long s_base;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < nslots; base += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t s = base + threadIdx.x;
     bool occ = false;
@@ -134,14 +137,20 @@ __global__ void k_table_compact(const uint64_t* table, uint64_t nslots, int slot
       occ = (mode == 1) ? (w0 != 0xffffffffffffffffULL) : (w0 == 2ULL);
     }
     unsigned m = __ballot_sync(0xffffffffu, occ);
-    unsigned long long wbase = 0;
-    if (lane == 0 && m) wbase = atomicAdd(counter, (unsigned long long)__popc(m));
-    wbase = __shfl_sync(0xffffffffu, wbase, 0);
+    if (lane == 0) s_w[warp] = __popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned tot = 0;
+      for (int w = 0; w < nw; ++w) { unsigned c = s_w[w]; s_w[w] = tot; tot += c; }
+      s_base = tot ? atomicAdd(counter, (unsigned long long)tot) : 0ULL;
+    }
+    __syncthreads();
     if (occ) {
-      uint64_t dst = wbase + __popc(m & ((1u << lane) - 1u));
+      uint64_t dst = s_base + s_w[warp] + __popc(m & ((1u << lane) - 1u));
       int first = (mode == 1) ? 0 : 1;
       for (int k = 0; k < nout; ++k) out_words[k][dst] = table[s * slot_words + first + k];
     }
+    __syncthreads();
   }
 }
 

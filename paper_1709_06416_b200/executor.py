@@ -569,6 +569,9 @@ class Ctx:
                     self._acct_append(st, count * b.k)
             elif isinstance(b.kind, DictMerger):
                 st.ensure(count * max(1, b.extra.get("maxm", 1)), hint_key=(plan.key_id, b.bid))
+                if b.extra.get("part") and b.extra.get("deferred"):
+                    st.ensure_part(count, 1 << b.extra["pbits"])
+                    st.pbits = b.extra["pbits"]
         tilectr = None
         if plan.schedule == "scan":
             tilectr = rt.alloc(8)
@@ -582,6 +585,10 @@ class Ctx:
         kern.launch(grid, plan.block, blob, smem)
         self.launches += 1
         self.dirty = True
+        # partitioned dictmergers: fold every bucket, merge into the HBM table
+        for b in plan.builders:
+            if isinstance(b.kind, DictMerger) and b.extra.get("part") and b.extra.get("deferred"):
+                self._dict_aggregate(bmap[b.bid], b)
         # dictmerger overflow: grow and replay spilled merges
         for b in plan.builders:
             if isinstance(b.kind, DictMerger):
@@ -590,6 +597,20 @@ class Ctx:
                 if spilled:
                     self._dict_regrow(st, spilled)
         self._keep = (tilectr, res)
+
+    def _dict_aggregate(self, st, b):
+        from .codegen import dict_agg_source
+        src, smem = dict_agg_source(st.kind, st.slot_words, b.extra["agg_S"], b.extra["pbits"])
+        kern = rt.get_kernel(src, "wg_dagg")
+        P = 1 << b.extra["pbits"]
+        grid = rt.sm_count() * kern.blocks_per_sm(256, smem)
+        words = [st.pk.ptr] + [v.ptr for v in st.pv] + [st.pcount.ptr, st.pcap, P, st.table.ptr, st.cap - 1,
+                                                           st.count.ptr, st.ocount.ptr, st.ocap, st.over[0][0].ptr]
+        words += [o.ptr for o in st.over[1]] + [rt.error_ptr()]
+        blob = b"".join(_pack("u64", w) for w in words)
+        kern.launch(grid, 256, blob, smem)
+        self.launches += 1
+        self.dirty = True
 
     def _acct_append(self, st, rows):
         if getattr(st, "hint", None) is None:
@@ -705,6 +726,16 @@ class Ctx:
                     return st.ocap
                 if what == "okey":
                     return st.over[0][key[3]].ptr
+                if what == "pcount":
+                    return st.pcount.ptr
+                if what == "pcap":
+                    return st.pcap
+                if what == "pshift":
+                    return max(0, st.cap.bit_length() - 1 - st.pbits)
+                if what == "pk":
+                    return st.pk.ptr
+                if what == "pv":
+                    return st.pv[key[3]].ptr
                 if what == "oval":
                     return st.over[1][key[3]].ptr
         raise EvalError(f"internal: no value for kernel parameter {key}")
@@ -779,6 +810,7 @@ def _collect_builders(v, out):
 
 
 LOWCARD_MAX = 4096
+PART_MIN_KEYS = 1 << 20
 
 
 def _bspecs(builders, strategy, count, loop_id=None):
@@ -808,6 +840,11 @@ def _bspecs(builders, strategy, count, loop_id=None):
             from .builders_dev import _SIZE_HINTS
             seen = _SIZE_HINTS.get((loop_id, bid))
             lowcard = seen is not None and seen <= LOWCARD_MAX
+            if seen is not None and seen > PART_MIN_KEYS and strategy != "global" and v.nw == 1 and DEFER_DICT:
+                # cardinality far beyond L2: partitioned two-kernel aggregation
+                bs.extra["part"] = True
+                bs.extra["agg_S"] = 0
+                bs.extra["pbits"] = 8
             if strategy != "global" and v.nw == 1 and (lowcard or not DEFER_DICT):
                 ns = 512
                 if ns * v.slot_words * 8 <= 64 * 1024:
@@ -832,7 +869,8 @@ def _bspecs(builders, strategy, count, loop_id=None):
 def _bsig(bs):
     if isinstance(bs, tuple):
         return tuple(_bsig(x) for x in bs)
-    return (bs.mode, bs.extra.get("nbins"), bs.extra.get("smem_slots"))
+    return (bs.mode, bs.extra.get("nbins"), bs.extra.get("smem_slots"), bs.extra.get("lowcard"),
+            bs.extra.get("part"), bs.extra.get("pbits"))
 
 
 def _type_of(v, lam, name):

@@ -50,9 +50,22 @@ def test_unsupported_shapes_raise():
 def test_benchmark_kernels_compile_for_sm100a():
     from paper_1709_06416_b200 import codegen, runtime, workloads as W
     for wl in W.WORKLOADS.values():
-        for smem, low in ((True, False), (True, True), (False, False)):
-            for plan in codegen.static_plans(W.compile_program(wl), externs=wl.externs, smem=smem, lowcard=low):
+        for smem, low, part in ((True, False, False), (True, True, False), (False, False, False),
+                                (False, False, True)):
+            for plan in codegen.static_plans(W.compile_program(wl), externs=wl.externs, smem=smem, lowcard=low,
+                                             part=part):
                 assert runtime.compile_check(plan.source) > 0
+
+
+def test_partitioned_dict_aggregation_kernel_compiles():
+    from paper_1709_06416_b200 import codegen, runtime
+    from weldmill.types import DictMerger, Scalar, Struct
+    for key, val, op in (("i64", Scalar("i64"), "+"), ("i32", Struct((Scalar("f64"), Scalar("i64"))), "+"),
+                         ("i64", Scalar("f64"), "min")):
+        kind = DictMerger(Scalar(key), val, op)
+        sw = 1 + (len(val.fields) if isinstance(val, Struct) else 1)
+        src, smem = codegen.dict_agg_source(kind, sw, 0, 8)
+        assert runtime.compile_check(src) > 0
 
 
 def test_corpus_sample_compiles():
