@@ -220,8 +220,13 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as tdist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
-        tdist.init_process_group("nccl")
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        ngpu = torch.cuda.device_count()
+        torch.cuda.set_device(local % max(ngpu, 1))
+        # one process per GPU over NCCL; more ranks than GPUs (a single-GPU
+        # smoke of the multi-rank path) falls back to gloo for the barrier /
+        # timing reductions -- the timed data path has no collective either way
+        tdist.init_process_group("nccl" if ngpu >= world else "gloo")
         dist = tdist
 
     import numpy as np
@@ -326,7 +331,7 @@ def main():
 
     if dist is not None:
         import torch
-        t = torch.tensor([ms, dom_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([ms, dom_ms], dtype=torch.float64, device=_coll_dev(dist))
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, dom_ms = float(t[0]), float(t[1])
 
@@ -359,7 +364,7 @@ def main():
         d2h = _nbytes(res)
         if dist is not None:
             import torch
-            t = torch.tensor([el], dtype=torch.float64, device="cuda")
+            t = torch.tensor([el], dtype=torch.float64, device=_coll_dev(dist))
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t[0])
         e2e = {"value": rows / el, "unit": "rows/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
@@ -396,6 +401,10 @@ def main():
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _coll_dev(dist):
+    return "cuda" if dist.get_backend() == "nccl" else "cpu"
 
 
 def _nbytes(v):
