@@ -98,6 +98,10 @@ int wg_event_create(uint64_t* ev);
 int wg_event_record(uint64_t ev);
 int wg_event_elapsed_ms(uint64_t start, uint64_t stop, float* ms);
 int wg_event_destroy(uint64_t ev);
+/* Copy/compute overlap for host-resident inputs (executor streaming path). */
+int wg_stream_select(int which);
+int wg_stream_wait_event(uint64_t ev);
+int wg_sync_all(void);
 
 #ifdef __cplusplus
 }

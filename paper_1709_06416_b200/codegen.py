@@ -993,8 +993,13 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
     ITEMS = items or ITEMS_OVERRIDE or choose_items(iters)
     if not (items or ITEMS_OVERRIDE) and any(isinstance(b.kind, DictMerger) for b in g.bspecs):
         ITEMS = min(ITEMS, 2)   # deferred merges + register caches are register-hungry
-    if any(b.extra.get("part") for b in g.bspecs):
-        ITEMS = min(ITEMS, 4)   # the tile's records are staged in static shared memory
+    for b in g.bspecs:
+        if b.extra.get("part"):
+            # the tile's records are staged in static shared memory (<= 40 KB)
+            rec = 8 + 8 * len(leaves(b.kind.value)) + 2
+            while ITEMS > 1 and BLOCK * ITEMS * rec > 40 * 1024:
+                ITEMS //= 2
+            ITEMS = min(ITEMS, 4)
     if not (items or ITEMS_OVERRIDE) and PIPE:
         # keep >= 2 pipeline stages inside the shared-memory budget
         row = sum(SIZE[k] * (W if it.simd else 1) for it in iters for k in it.kinds)

@@ -32,7 +32,8 @@ thread_local std::string g_err;
 std::mutex g_mu;
 bool g_inited = false;
 int g_device = -1;
-cudaStream_t g_stream = nullptr;
+cudaStream_t g_stream = nullptr;      // current stream (every call below enqueues here)
+cudaStream_t g_streams[3] = {nullptr, nullptr, nullptr};  // 0 compute, 1 host->device, 2 device->host
 int g_sm_count = 0;
 int64_t* g_err_word = nullptr;      // device {code, info}
 int64_t* g_err_host = nullptr;      // pinned mirror
@@ -383,7 +384,8 @@ int wg_init(int device) {
       !resolve("cuOccupancyMaxActiveBlocksPerMultiprocessor", &p_cuOccupancyMaxActiveBlocksPerMultiprocessor) ||
       !resolve("cuFuncSetAttribute", &p_cuFuncSetAttribute))
     return fail("weldgpu: could not resolve CUDA driver entry points");
-  CK(cudaStreamCreateWithFlags(&g_stream, cudaStreamNonBlocking));
+  for (int i = 0; i < 3; ++i) CK(cudaStreamCreateWithFlags(&g_streams[i], cudaStreamNonBlocking));
+  g_stream = g_streams[0];
   CK(cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, device));
   cudaMemPool_t pool;
   CK(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -950,6 +952,29 @@ int wg_event_elapsed_ms(uint64_t start, uint64_t stop, float* ms) {
   NEED_INIT();
   CK(cudaEventSynchronize((cudaEvent_t)(uintptr_t)stop));
   CK(cudaEventElapsedTime(ms, (cudaEvent_t)(uintptr_t)start, (cudaEvent_t)(uintptr_t)stop));
+  return 0;
+}
+
+// Copy/compute overlap for host-resident inputs: select which of the three
+// streams subsequent calls enqueue on, and order streams with events.
+// (Buffers handed between streams must stay alive until the consumer's
+// event; the caching allocator is only stream-ordered on stream 0.)
+int wg_stream_select(int which) {
+  NEED_INIT();
+  if (which < 0 || which > 2) return fail("wg_stream_select: stream 0, 1 or 2");
+  g_stream = g_streams[which];
+  return 0;
+}
+
+int wg_stream_wait_event(uint64_t ev) {
+  NEED_INIT();
+  CK(cudaStreamWaitEvent(g_stream, (cudaEvent_t)(uintptr_t)ev, 0));
+  return 0;
+}
+
+int wg_sync_all(void) {
+  NEED_INIT();
+  for (int i = 0; i < 3; ++i) CK(cudaStreamSynchronize(g_streams[i]));
   return 0;
 }
 

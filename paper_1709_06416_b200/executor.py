@@ -810,6 +810,8 @@ def _collect_builders(v, out):
 
 
 LOWCARD_MAX = 4096
+import os as _os
+STREAMING = _os.environ.get("WELDGPU_STREAM", "1") == "1"
 PART_MIN_KEYS = 1 << 20
 
 
@@ -959,6 +961,14 @@ def evaluate(e, env=None, config=None, externs=None, *, result="python", idx0=0,
             frame[name] = HostVec(t, payload) if isinstance(t, Vec) else payload
         else:
             frame[name] = payload
+    if result == "numpy" and STREAMING:
+        cand = _stream_candidate(e, frame)
+        if cand is not None:
+            payload = _stream_evaluate(ctx, e, frame, cand)
+            stats = EvalStats()
+            stats.vector_traversals = ctx.traversals
+            stats.tasks_created = ctx.tasks
+            return Value(e.ty, payload), stats
     try:
         val = ctx.ev(e, frame)
     except _DU as exc:
@@ -1063,3 +1073,154 @@ def evaluate_partials(loop, env, config=None, externs=None, idx0=0, rank=0):
             arrs = [col_to_numpy(c, n) for c in cols]
             out.append({"kind": "group", "keys": arrs[:nk], "vals": arrs[nk:]})
     return out
+
+
+# ---------------------------------------------------------------------------
+# Streaming path for host-resident inputs: copy/compute overlap.
+
+STREAM_MIN_ROWS = 1 << 22
+STREAM_CHUNK_ROWS = 1 << 23
+
+
+def _stream_candidate(e, frame):
+    """Host numpy inputs feeding one `result(for(...))` whose builders are
+    vecbuilders / mergers: returns (loop, iter HostVecs, builder kinds) or None."""
+    from weldmill.expr import walk
+    if not isinstance(e, Result) or not isinstance(e.builder, For):
+        return None
+    loop = e.builder
+    if not isinstance(loop.func, Lambda):
+        return None
+    hvs = []
+    for it in loop.iters:
+        if it.simd or it.start is not None or not isinstance(it.data, Ident):
+            return None
+        hv = frame.get(it.data.name)
+        if not isinstance(hv, HostVec) or hv._dev is not None:
+            return None
+        p = hv.payload
+        arrs = list(p) if isinstance(p, tuple) else [p]
+        if not all(isinstance(a, np.ndarray) and a.ndim == 1 and a.flags.c_contiguous and not a.dtype.names
+                   for a in arrs):
+            return None
+        hvs.append(hv)
+    n = len(hvs[0])
+    if n < STREAM_MIN_ROWS or any(len(h) != n for h in hvs):
+        return None
+
+    def ok_builders(x):
+        if isinstance(x, MakeStruct):
+            return all(ok_builders(i) for i in x.items)
+        return isinstance(x, NewBuilder) and isinstance(x.kind, (VecBuilder, Merger)) and (
+            not isinstance(x.kind, VecBuilder) or is_flat(x.kind.elem))
+
+    if not ok_builders(loop.builders):
+        return None
+    # loop-invariant captures must be scalars (vectors would be re-uploaded per chunk)
+    names = free_variables(loop.func) - {p.name for p in loop.func.params}
+    for nm in names:
+        v = frame.get(nm)
+        if isinstance(v, (HostVec, DVec)) or hasattr(v, "pending"):
+            return None
+    return loop, hvs
+
+
+def _stream_evaluate(ctx, e, frame, cand):
+    """Chunked, double-buffered execution: the next chunk's columns copy in on
+    stream 1 while the current chunk computes on stream 0 and the previous
+    chunk's appends copy out on stream 2 (straight into pinned numpy
+    results).  The loop index stays global (idx0 = chunk start)."""
+    from dataclasses import replace
+    from .columns import Col, dvec_from_cols, pinned_empty
+    loop, hvs = cand
+    n = len(hvs[0])
+    C = min(STREAM_CHUNK_ROWS, n)
+    nch = (n + C - 1) // C
+    leaves_np = []
+    for hv in hvs:
+        p = hv.payload
+        leaves_np.append(list(p) if isinstance(p, tuple) else [p])
+    kinds = [leaves(hv.ty.elem) for hv in hvs]
+    sets = [[[Col.alloc(k, C) for k in ks] for ks in kinds] for _ in range(2)]
+    bval = ctx.ev(loop.builders, frame)
+    blist = []
+    _collect_builders(bval, blist)
+    loop2 = _STREAM_LOOPS.get(id(loop))
+    if loop2 is None or loop2[0] is not loop:
+        loop2 = (loop, replace(loop, builders=Ident("__wg_sb", ty=loop.builders.ty)))
+        _STREAM_LOOPS[id(loop)] = loop2
+    loop2 = loop2[1]
+    outs = {}
+    ev_in = [rt.Event() for _ in range(nch)]
+    ev_k = [rt.Event() for _ in range(nch)]
+    try:
+        for c in range(nch):
+            lo = c * C
+            m = min(C, n - lo)
+            b = c % 2
+            # copy in (stream 1), after the kernel that last read this buffer set
+            rt.stream_select(1)
+            if c >= 2:
+                rt.stream_wait(ev_k[c - 2])
+            for k, arrs in enumerate(leaves_np):
+                for l, a in enumerate(arrs):
+                    col = sets[b][k][l]
+                    rt.h2d(col.ptr, a.ctypes.data + lo * a.itemsize, m * a.itemsize)
+            ev_in[c].record()
+            # compute (stream 0)
+            rt.stream_select(0)
+            rt.stream_wait(ev_in[c])
+            f2 = dict(frame)
+            for it, hv, cols, ks in zip(loop.iters, hvs, sets[b], kinds):
+                f2[it.data.name] = dvec_from_cols(hv.ty.elem, m, [Col(cc.ptr, kk, cc.owner) for cc, kk in zip(cols, ks)])
+            f2["__wg_sb"] = bval
+            ctx.idx0 = lo
+            ctx.run_loop(loop2, f2, count_traversal=(c == 0))
+            ev_k[c].record()
+            # copy out (stream 2): this chunk's appended rows
+            rt.stream_select(2)
+            rt.stream_wait(ev_k[c])
+            for st in blist:
+                if isinstance(st, AppenderDev) and st.segments:
+                    seg = st.segments[-1]
+                    if seg.n is None:
+                        continue
+                    if id(st) not in outs:
+                        outs[id(st)] = [pinned_empty(n * (seg.n // m if m else 1), {"bool": "u1", "i32": "<i4", "i64": "<i8", "f32": "<f4", "f64": "<f8"}[k])
+                                        for k in st.kinds]
+                    per = seg.n // m if m else 1
+                    for arr, col in zip(outs[id(st)], seg.cols):
+                        rt.d2h_async(arr.ctypes.data + lo * per * arr.itemsize, col.ptr, seg.n * arr.itemsize)
+    finally:
+        rt.stream_select(0)
+        ctx.idx0 = 0
+    rt.sync_all()
+    ctx.dirty = True
+    ctx.check_device()
+
+    def build(x, st_iter):
+        st = next(st_iter)
+        st.consume()
+        if isinstance(st, MergerDev):
+            return st.read()
+        if id(st) in outs and all(s.n is not None for s in st.segments):
+            o = outs[id(st)]
+            return o[0] if isinstance(st.kind.elem, Scalar) else tuple(o)
+        cols, tot = st.concat() if st.segments else ([Col.alloc(k, 0) for k in st.kinds], 0)
+        from .columns import to_numpy
+        return to_numpy(dvec_from_cols(st.kind.elem, tot, cols))
+
+    it_ = iter(blist)
+    try:
+        return _shape_like(bval, lambda: build(None, it_))
+    finally:
+        del build   # no closure cycle may keep the pinned results' pool blocks alive
+
+
+def _shape_like(v, leaf):
+    if isinstance(v, tuple):
+        return tuple(_shape_like(x, leaf) for x in v)
+    return leaf()
+
+
+_STREAM_LOOPS = {}

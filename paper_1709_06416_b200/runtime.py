@@ -71,6 +71,9 @@ _SIGS = {
     "wg_event_record": (c_int, [u64]),
     "wg_event_elapsed_ms": (c_int, [u64, u64, ctypes.POINTER(ctypes.c_float)]),
     "wg_event_destroy": (c_int, [u64]),
+    "wg_stream_select": (c_int, [c_int]),
+    "wg_stream_wait_event": (c_int, [u64]),
+    "wg_sync_all": (c_int, []),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -358,6 +361,18 @@ def get_kernel(src: str, name: str) -> Kernel:
 
 # ---------------------------------------------------------------------------
 # Events (bench timing on the library's own stream)
+
+
+def stream_select(which):
+    _check(lib().wg_stream_select(which))
+
+
+def stream_wait(ev):
+    _check(lib().wg_stream_wait_event(ev.h))
+
+
+def sync_all():
+    _check(lib().wg_sync_all())
 
 
 class Event:
