@@ -105,7 +105,20 @@ def hist(c):
     return bins + np.bincount(idx, weights=w, minlength=bins.size)
 
 
-ORACLES = {"q6": q6, "blackscholes": blackscholes, "q1": q1, "dict": dict_sum, "group": group, "hist": hist}
+def filt(c):
+    """filter(v, x > 0): vecbuilder appends in row order (builders.py:274-283)."""
+    v = c["v"]
+    return v[v > 0]
+
+
+def map3(c):
+    """map(v, x * 3 + 1) with i64 wraparound (run.py:395-405)."""
+    with np.errstate(over="ignore"):
+        return c["v"] * np.int64(3) + np.int64(1)
+
+
+ORACLES = {"q6": q6, "blackscholes": blackscholes, "q1": q1, "dict": dict_sum, "group": group, "hist": hist,
+           "filter": filt, "map": map3}
 
 
 def as_reference_payload(name, out):
@@ -123,4 +136,6 @@ def as_reference_payload(name, out):
         return [[int(kk), vs[offs[j]:offs[j + 1]].tolist()] for j, kk in enumerate(ks)]
     if name == "hist":
         return [[i, x] for i, x in enumerate(out.tolist()) if x != 0.0]
+    if name in ("filter", "map"):
+        return out.tolist()
     raise KeyError(name)

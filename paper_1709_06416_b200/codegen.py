@@ -1250,6 +1250,7 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
     dict_bs = [b for b in g.bspecs if isinstance(b.kind, DictMerger)]
     for b in dict_bs:
         src.append(f"  int wg_claims{b.bid} = 0;")
+        src.extend(b.extra.get("smem_decl", []))
         if b.extra.get("regcache"):
             src.extend(_regcache_decl(b, b.extra["regcache"]))
     src.append("  const i64 n = p.n;")
@@ -1746,13 +1747,12 @@ def _deferred_dict_lines(g, b):
         pk = g.param(f"d{B}_pk", "u64*", ("b", B, "pk"))
         pvs = [g.param(f"d{B}_pv{f}", "u64*", ("b", B, "pv", f)) for f in range(len(vks))]
         V = len(vks)
-        L.append(f"      __shared__ unsigned s_ph{B}[{NP}], s_po{B}[{NP}];")
-        L.append(f"      __shared__ u64 s_pb{B}[{NP}];")
-        L.append(f"      __shared__ u64 s_rk{B}[TILE];")
-        for f in range(V):
-            L.append(f"      __shared__ u64 s_rv{B}_{f}[TILE];")
-        L.append(f"      __shared__ unsigned short s_rp{B}[TILE];")
-        L.append(f"      __shared__ i64 s_sc{B}[33];")
+        # (shared arrays are declared once at kernel scope: this block can be
+        # emitted twice -- main tile loop and tail tile)
+        decl = [f"  __shared__ unsigned s_ph{B}[{NP}], s_po{B}[{NP}];", f"  __shared__ u64 s_pb{B}[{NP}];",
+                f"  __shared__ u64 s_rk{B}[TILE];"] + [f"  __shared__ u64 s_rv{B}_{f}[TILE];" for f in range(V)] + [
+                f"  __shared__ unsigned short s_rp{B}[TILE];", f"  __shared__ i64 s_sc{B}[33];"]
+        b.extra["smem_decl"] = decl
         L.append(f"      unsigned pp_[ITEMS], pr_[ITEMS];")
         L.append(f"      for (int q = threadIdx.x; q < {NP}; q += BLOCK) s_ph{B}[q] = 0u;")
         L.append("      __syncthreads();")

@@ -35,7 +35,7 @@ def _run(name, n, row0=0, device_inputs=False, result="python"):
     return val.data, stats, cols
 
 
-@pytest.mark.parametrize("name", ["q6", "blackscholes", "q1", "dict", "group", "hist"])
+@pytest.mark.parametrize("name", ["q6", "blackscholes", "q1", "dict", "group", "hist", "filter", "map"])
 def test_matches_reference_goldens(name):
     g = GOLD[name]
     got, _, _ = _run(name, g["n"])
@@ -43,13 +43,13 @@ def test_matches_reference_goldens(name):
     if name == "hist":
         got = [[i, x] for i, x in enumerate(got) if x != 0.0]
     want = g["expected"]
-    if name in ("dict", "group"):
+    if name in ("dict", "group", "filter", "map"):
         assert got == want
     else:
         assert approx_equal(got, want, F64_TOL), first_diff(got, want, F64_TOL)
 
 
-@pytest.mark.parametrize("name", ["q6", "blackscholes", "q1", "dict", "group", "hist"])
+@pytest.mark.parametrize("name", ["q6", "blackscholes", "q1", "dict", "group", "hist", "filter", "map"])
 @pytest.mark.parametrize("n", [1, 1000, 1 << 20, (1 << 20) + 3])
 def test_matches_oracle(name, n):
     from oracle import weld_oracle
@@ -59,7 +59,7 @@ def test_matches_oracle(name, n):
     if name == "hist":
         got = [[i, x] for i, x in enumerate(got) if x != 0.0]
     want = norm(want)
-    if name in ("dict", "group"):
+    if name in ("dict", "group", "filter", "map"):
         assert got == want
     else:
         assert approx_equal(got, want, F64_TOL), first_diff(got, want, F64_TOL)
