@@ -409,7 +409,7 @@ def _coll_dev(dist):
 
 def _nbytes(v):
     import numpy as np
-    if isinstance(v, np.ndarray):
+    if isinstance(v, np.ndarray) or hasattr(v, "offsets"):
         return v.nbytes
     if isinstance(v, (tuple, list)):
         return sum(_nbytes(x) for x in v)

@@ -51,6 +51,7 @@ from .irtypes import (
 
 W = 4  # SIMD_WIDTH (types.py:15)
 BLOCK = 256
+BLOCK_DEFAULT = BLOCK
 
 import os as _os
 
@@ -990,10 +991,15 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
         raise DeviceUnsupported("loop function must be a lambda literal")
     pb, pi, px = (p.name for p in lam.params)
 
+    # range-partitioned dictmergers hold per-partition chunk buffers in shared
+    # memory (one CTA per SM): twice the threads per CTA to hide latency
+    BLOCK = 512 if any(b.extra.get("rpart") for b in g.bspecs) else BLOCK_DEFAULT
     ITEMS = items or ITEMS_OVERRIDE or choose_items(iters)
     if not (items or ITEMS_OVERRIDE) and any(isinstance(b.kind, DictMerger) for b in g.bspecs):
         ITEMS = min(ITEMS, 2)   # deferred merges + register caches are register-hungry
     for b in g.bspecs:
+        if b.extra.get("rpart") and not (items or ITEMS_OVERRIDE):
+            ITEMS = 2
         if b.extra.get("part"):
             # the tile's records are staged in static shared memory (<= 40 KB)
             rec = 8 + 8 * len(leaves(b.kind.value)) + 2
@@ -1162,6 +1168,19 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
                 smem_flush.append(
                     f"for (int q = threadIdx.x; q < {nb}; q += {BLOCK}) {{ const {CTYPE[kk]} v_ = (({CTYPE[kk]}*)(s_vm{b.bid} + {f * nb}))[q]; "
                     f"if (wg_to_bits<{CTYPE[kk]}>(v_) != wg_to_bits<{CTYPE[kk]}>({ident})) WgAtomicFold<{opc}, {CTYPE[kk]}>::f({col} + q, v_); }}")
+        if isinstance(b.kind, DictMerger) and b.extra.get("rpart"):
+            # per-partition tile counts, window cursors, tile bases (u32 x 4)
+            NP = 1 << b.extra["pbits"]
+            off = dyn_smem // 8
+            B = b.bid
+            V_ = len(leaves(b.kind.value))
+            smem_decls.append(f"unsigned* s_ph{B} = (unsigned*)(wg_dyn_smem + {off}); unsigned* s_wc{B} = s_ph{B} + {NP}; "
+                              f"unsigned* s_pb{B} = s_wc{B} + {NP}; unsigned* s_nb{B} = s_pb{B} + {NP};")
+            smem_decls.append(f"u64* s_bk{B} = wg_dyn_smem + {off + NP * 2};"
+                              + "".join(f" u64* s_bv{B}_{f} = wg_dyn_smem + {off + NP * 2 + NP * 4 * (1 + f)};"
+                                        for f in range(V_)))
+            smem_init.append(f"for (int q = threadIdx.x; q < {NP}; q += {BLOCK}) {{ s_ph{B}[q] = 0u; s_wc{B}[q] = 0u; }}")
+            dyn_smem += NP * 16 + NP * 4 * 8 * (1 + V_)
         if isinstance(b.kind, DictMerger) and b.mode == "smem":
             ns = b.extra["smem_slots"]
             sw = b.extra["slot_words"]
@@ -1462,6 +1481,7 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
     for b in g.bspecs:
         if b.extra.get("regcache"):
             src.extend(regcache_flush[b.bid])
+        src.extend(b.extra.get("epilogue", []))
     if smem_flush:
         src.append("  __syncthreads();")
         src.extend("  " + fl for fl in smem_flush)
@@ -1681,6 +1701,343 @@ def dict_agg_source(kind, slot_words, S, pbits, name="wg_dagg"):
     return "\n".join(L) + "\n", 0
 
 
+# ---------------------------------------------------------------------------
+# Range-partitioned dictmerger (cardinality far beyond L2).
+#
+# DictMergerState.result (builders.py:380-392) folds the per-chunk tables and
+# sorts the entries by order_key (builders.py:496-507); tovec keeps that
+# order (run.py:737-747).  Here the sort is folded into the aggregation: the
+# loop kernel scatters every merge into one of NP partitions by the top bits
+# of the key's *order key* (so partition p holds a contiguous key range),
+# and a second kernel aggregates each partition in a shared-memory table,
+# sorts its few thousand distinct keys locally and writes them at the
+# partition's output offset (decoupled look-back over partitions).  No global
+# hash table, no global sort.
+
+RPART_W = int(_os.environ.get("WELDGPU_RPART_W", "64"))   # rows per reserved window (per CTA, per partition)
+
+
+def rpart_ok(kinds):
+    """Key layouts the range partitioner handles: integer/bool leaves packed
+    into one word (the order key is computed from the word)."""
+    lay, nw = key_layout(kinds)
+    return nw == 1 and all(k in (I64, I32, BOOL) for k in kinds)
+
+
+def okey_expr(kinds, w):
+    """C expression: order_key of a packed one-word key as an unsigned 64-bit
+    integer (builders.py:496-507: signed ints ordered, tuples lexicographic;
+    the first leaf is the most significant)."""
+    lay, _ = key_layout(kinds)
+    parts = []
+    pos = 64
+    for (word, sh, width), k in zip(lay, kinds):
+        leaf = f"(({w} >> {sh}) & 0x{(1 << width) - 1 if width < 64 else 0xFFFFFFFFFFFFFFFF:x}ULL)"
+        if k in (I64, I32):
+            leaf = f"({leaf} ^ 0x{1 << (width - 1):x}ULL)"
+        pos -= width
+        parts.append(f"({leaf} << {pos})" if pos else leaf)
+    return "(" + " | ".join(parts) + ")"
+
+
+def okey_py(kinds, word):
+    lay, _ = key_layout(kinds)
+    out, pos = 0, 64
+    for (wi, sh, width), k in zip(lay, kinds):
+        leaf = (word >> sh) & ((1 << width) - 1)
+        if k in (I64, I32):
+            leaf ^= 1 << (width - 1)
+        pos -= width
+        out |= leaf << pos
+    return out
+
+
+def _rpart_loop_lines(g, b):
+    """Loop side.  Partition q's bucket is split into one private slice per
+    CTA (slice capacity scap rows), so no global atomics are needed.  Per
+    tile: rank the pending merges per partition in shared memory, advance the
+    CTA's cursor of each touched partition once, and write records in whole
+    32-byte chunks (4 rows): a chunk that completes inside the tile is
+    stored straight from registers, the partial last chunk waits in a
+    per-partition shared-memory buffer until a later tile completes it -- the
+    L2 only sees full-sector writes however many partitions are open.  The
+    epilogue writes the partial chunks and the slice fill counts."""
+    B = b.bid
+    NP = 1 << b.extra["pbits"]
+    vks = leaves(b.kind.value)
+    kks = leaves(b.kind.key)
+    V = len(vks)
+    scap = g.param(f"d{B}_pcap", "u64", ("b", B, "pcap"))
+    rlo = g.param(f"d{B}_rlo", "u64", ("b", B, "rlo"))
+    rsh = g.param(f"d{B}_rshift", "u64", ("b", B, "rshift"))
+    pk = g.param(f"d{B}_pk", "u64*", ("b", B, "pk"))
+    pvs = [g.param(f"d{B}_pv{f}", "u64*", ("b", B, "pv", f)) for f in range(V)]
+    fill = g.param(f"d{B}_pcount", "unsigned*", ("b", B, "pcount"))
+    oflow = g.param(f"d{B}_oflow", "unsigned long long*", ("b", B, "oflow"))
+    ok = okey_expr(kks, f"dkk{B}[j]")
+    vbits = [f"wg_to_bits<{CTYPE[kk]}>(dkv{B}_{f}[j])" for f, kk in enumerate(vks)]
+    sbase = f"(((u64)q_ * gridDim.x + blockIdx.x) * {scap})"
+    L = [f"      unsigned pp_[ITEMS], pr_[ITEMS];",
+         "#pragma unroll",
+         "      for (int j = 0; j < ITEMS; ++j) {",
+         f"        if (!dkf{B}[j]) continue;",
+         f"        const u64 ok_ = {ok};",
+         f"        const u64 d_ = ok_ < {rlo} ? 0ULL : ((ok_ - {rlo}) >> {rsh});",
+         f"        pp_[j] = (unsigned)(d_ < {NP - 1}ULL ? d_ : {NP - 1}ULL);",
+         f"        pr_[j] = atomicAdd(&s_ph{B}[pp_[j]], 1u);",
+         "      }",
+         "      __syncthreads();",
+         # the first-ranked record of a partition advances the cursor (and
+         # clears the tile count) and, if this tile completes the buffered
+         # chunk, stores the chunk's head from shared memory
+         "#pragma unroll",
+         "      for (int j = 0; j < ITEMS; ++j) {",
+         f"        if (!dkf{B}[j] || pr_[j] != 0u) continue;",
+         f"        const unsigned q_ = pp_[j], c_ = s_ph{B}[q_], cur_ = s_wc{B}[q_], f_ = cur_ & 3u;",
+         f"        s_ph{B}[q_] = 0u; s_pb{B}[q_] = cur_; s_wc{B}[q_] = cur_ + c_;",
+         "        if (f_ && c_ >= 4u - f_ && (u64)cur_ <= " + scap + ") {",
+         f"          const u64 h_ = {sbase} + (cur_ - f_);",
+         "          for (unsigned s_ = 0; s_ < f_; ++s_) {",
+         f"            __stcs({pk} + h_ + s_, s_bk{B}[q_ * 4u + s_]);"] + [
+         f"            __stcs({pvs[f]} + h_ + s_, s_bv{B}_{f}[q_ * 4u + s_]);" for f in range(V)] + [
+         "          }",
+         "        }",
+         "      }",
+         "      __syncthreads();",
+         "#pragma unroll",
+         "      for (int j = 0; j < ITEMS; ++j) {",
+         f"        if (!dkf{B}[j]) continue;",
+         f"        const unsigned q_ = pp_[j], g_ = s_pb{B}[q_] + pr_[j];",
+         f"        if ((g_ | 3u) < s_wc{B}[q_]) {{",
+         f"          if ((u64)g_ < {scap}) {{ const u64 at_ = {sbase} + g_; __stcs({pk} + at_, dkk{B}[j]);"]
+    L[-1] += "".join(f" __stcs({pvs[f]} + at_, {vbits[f]});" for f in range(V))
+    L[-1] += f" }} else atomicAdd({oflow}, 1ULL);"
+    L += [f"          dkf{B}[j] = false;",
+          "        }",
+          "      }",
+          "      __syncthreads();",
+          # rows of the still-incomplete last chunk wait in shared memory
+          "#pragma unroll",
+          "      for (int j = 0; j < ITEMS; ++j) {",
+          f"        if (!dkf{B}[j]) continue;",
+          f"        const unsigned sl_ = pp_[j] * 4u + ((s_pb{B}[pp_[j]] + pr_[j]) & 3u); s_bk{B}[sl_] = dkk{B}[j];"]
+    L[-1] += "".join(f" s_bv{B}_{f}[sl_] = {vbits[f]};" for f in range(V))
+    L += [f"        dkf{B}[j] = false;",
+          "      }"]
+    # epilogue: each partition's partial chunk, then the slice fill counts
+    ep = ["  __syncthreads();",
+          f"  for (int q_ = threadIdx.x; q_ < {NP}; q_ += BLOCK) {{",
+          f"    const unsigned cur_ = s_wc{B}[q_], f_ = cur_ & 3u;",
+          f"    if (f_ && (u64)cur_ <= {scap}) for (unsigned s_ = 0; s_ < f_; ++s_) {{",
+          f"      {pk}[{sbase} + cur_ - f_ + s_] = s_bk{B}[q_ * 4 + s_];"]
+    for f in range(V):
+        ep.append(f"      {pvs[f]}[{sbase} + cur_ - f_ + s_] = s_bv{B}_{f}[q_ * 4 + s_];")
+    ep += ["    }",
+           f"    {fill}[(u64)q_ * gridDim.x + blockIdx.x] = (u64)cur_ <= {scap} ? cur_ : (unsigned){scap};",
+           "  }"]
+    b.extra["epilogue"] = ep
+    return L
+
+
+def rpart_table_slots(nvals):
+    """Shared-memory table size of the aggregation kernel (power of two):
+    keys + value words + u32 sub-bucket counters + u16 permutation."""
+    ts = 8192
+    while ts > 1024 and ts * (8 * (1 + nvals) + 6) + 4096 > 200 * 1024:
+        ts //= 2
+    return ts
+
+
+def dict_rpart_source(kind, TS, name="wg_drp"):
+    """Aggregation kernel of the range-partitioned dictmerger.  One CTA per
+    partition (claimed in order through a ticket): fold the partition's
+    records into a shared-memory open-addressing table, order the distinct
+    keys (counting sort on the partition's actual key range, insertion sort
+    inside sub-buckets), find the partition's output offset by decoupled
+    look-back and write the sorted (key word, value words) rows.  Overflow
+    (a partition with more than TS distinct keys) is flagged; the executor
+    then re-runs the loop through the hash-table path."""
+    vks = leaves(kind.value)
+    kks = leaves(kind.key)
+    V = len(vks)
+    opc = OPCODE[kind.op]
+    LOG = TS.bit_length() - 1
+    BLK = 1024
+    assert TS % BLK == 0
+    ident = [f"0x{to_bits_c(kk, internal_identity(kind.op, kk)):016x}ULL" for kk in vks]
+    ok = lambda w: okey_expr(kks, w)  # noqa: E731
+    L = ['#define WG_LB_PER 1', '#define WG_LB_SLEEP 32', '#include "weld_device.cuh"',
+         f"#define BLOCK {BLK}", f"#define TS {TS}", f"#define LOGTS {LOG}", "#define RITEMS 4",
+         "struct Params {", "  const u64* pk;"] + [f"  const u64* pv{f};" for f in range(V)] + [
+        "  const unsigned* fill; u64 scap; u64 nslices; u64 nparts;",
+        "  u64* outk;"] + [f"  u64* outv{f};" for f in range(V)] + [
+        "  u64* status; unsigned long long* ticket; unsigned long long* oflow; unsigned long long* nout;",
+        "};",
+        f'extern "C" __global__ void __launch_bounds__(BLOCK) {name}(const Params p) {{',
+        "  extern __shared__ __align__(16) u64 sm_[];",
+        "  u64* s_k = sm_;"]
+    for f in range(V):
+        L.append(f"  u64* s_v{f} = sm_ + {(1 + f)} * TS;")
+    L += [f"  unsigned* s_cnt = (unsigned*)(sm_ + {1 + V} * TS);",
+          "  unsigned short* s_perm = (unsigned short*)(s_cnt + TS);",
+          "  __shared__ u64 s_sk[1 + " + str(V) + "];   // the key equal to the EMPTY sentinel",
+          "  __shared__ int s_has, s_part, s_fail;",
+          "  __shared__ unsigned long long s_min, s_max;",
+          "  __shared__ i64 s_off, s_sc[33];",
+          "  __shared__ unsigned s_c;",
+          "  for (int q = threadIdx.x; q < TS; q += BLOCK) { s_k[q] = WG_EMPTY_KEY;"]
+    for f in range(V):
+        L[-1] += f" s_v{f}[q] = {ident[f]};"
+    L[-1] += " }"
+    L += ["  for (;;) {",
+          "    if (threadIdx.x == 0) {",
+          "      s_part = (int)atomicAdd(p.ticket, 1ULL); s_has = 0; s_fail = 0;",
+          "      s_min = ~0ULL; s_max = 0ULL;"]
+    for f in range(V):
+        L.append(f"      s_sk[{f}] = {ident[f]};")
+    L += ["    }",
+          "    __syncthreads();",
+          "    const i64 part = s_part;",
+          "    if (part >= (i64)p.nparts) break;",
+          # ---- fold the partition's records (one private slice per loop CTA;
+          # warp w streams slices w, w + 32, ...) into the shared table
+          "    const int lane = threadIdx.x & 31;",
+          "    for (u64 sl = threadIdx.x >> 5; sl < p.nslices; sl += BLOCK / 32) {",
+          "      const u64 base = ((u64)part * p.nslices + sl) * p.scap;",
+          "      const unsigned rows = p.fill[(u64)part * p.nslices + sl];",
+          "      for (unsigned r0 = 0; r0 < rows; r0 += 32 * RITEMS) {",
+          "        u64 k_[RITEMS];"] + [f"        u64 v{f}_[RITEMS];" for f in range(V)] + [
+          "#pragma unroll",
+          "        for (int j = 0; j < RITEMS; ++j) {",
+          "          const unsigned r = r0 + j * 32 + lane;",
+          "          k_[j] = r < rows ? __ldcs(p.pk + base + r) : WG_EMPTY_KEY;"]
+    for f in range(V):
+        L.append(f"          v{f}_[j] = r < rows ? __ldcs(p.pv{f} + base + r) : 0ULL;")
+    L += ["        }",
+          "#pragma unroll",
+          "        for (int j = 0; j < RITEMS; ++j) {",
+          "          if (r0 + j * 32 + lane >= rows) continue;",
+          "          const u64 key = k_[j];",
+          "          if (*(volatile int*)&s_fail) continue;     // overflowed: the host re-runs the loop",
+          "          if (key == WG_EMPTY_KEY) {",
+          "            s_has = 1;"]
+    for f, kk in enumerate(vks):
+        ct = CTYPE[kk]
+        L.append(f"            WgSmemFold<{opc}, {ct}>::f(({ct}*)(s_sk + {f}), wg_from_bits<{ct}>(v{f}_[j]));")
+    L += ["            continue;",
+          "          }",
+          # Fibonacci hashing: the keys of one partition share their high bits
+          "          unsigned h = (unsigned)((key * 0x9E3779B97F4A7C15ULL) >> (64 - LOGTS));",
+          "          int probe = 0;",
+          "          for (; probe < TS; ++probe) {",
+          "            const u64 cur = *(volatile u64*)(s_k + h);",
+          "            if (cur == key) break;",
+          "            if (cur == WG_EMPTY_KEY) {",
+          "              const u64 prev = atomicCAS((unsigned long long*)(s_k + h), WG_EMPTY_KEY, key);",
+          "              if (prev == WG_EMPTY_KEY || prev == key) break;",
+          "            }",
+          "            h = (h + 1) & (TS - 1);",
+          "          }",
+          "          if (probe == TS) { s_fail = 1; continue; }"]
+    for f, kk in enumerate(vks):
+        ct = CTYPE[kk]
+        L.append(f"          WgSmemFold<{opc}, {ct}>::f(({ct}*)(s_v{f} + h), wg_from_bits<{ct}>(v{f}_[j]));")
+    L += ["        }",
+          "      }",
+          "    }",
+          "    __syncthreads();",
+          "    if (threadIdx.x == 0 && s_fail) atomicAdd(p.oflow, 1ULL);",
+          # ---- order the distinct keys: counting sort on the actual key range
+          "    {",
+          "      u64 mn = ~0ULL, mx = 0ULL;",
+          "      for (int q = threadIdx.x; q < TS; q += BLOCK) {",
+          "        s_cnt[q] = 0u;",
+          "        const u64 w = s_k[q];",
+          "        if (w != WG_EMPTY_KEY) { const u64 o = " + ok("w") + "; mn = o < mn ? o : mn; mx = o > mx ? o : mx; }",
+          "      }",
+          "#pragma unroll",
+          "      for (int d = 16; d > 0; d >>= 1) {",
+          "        const u64 a = __shfl_xor_sync(0xffffffffu, mn, d), b = __shfl_xor_sync(0xffffffffu, mx, d);",
+          "        mn = a < mn ? a : mn; mx = b > mx ? b : mx;",
+          "      }",
+          "      if ((threadIdx.x & 31) == 0 && mx >= mn) { atomicMin(&s_min, mn); atomicMax(&s_max, mx); }",
+          "    }",
+          "    __syncthreads();",
+          "    const u64 omin = s_min, span = s_max >= s_min ? s_max - s_min : 0ULL;",
+          "    const int ssh = span ? max(0, 64 - __clzll(span) - LOGTS) : 0;",
+          "    for (int q = threadIdx.x; q < TS; q += BLOCK) {",
+          "      const u64 w = s_k[q];",
+          "      if (w != WG_EMPTY_KEY) atomicAdd(&s_cnt[(unsigned)((" + ok("w") + " - omin) >> ssh)], 1u);",
+          "    }",
+          "    __syncthreads();",
+          "    {  // exclusive scan of the TS counters (TS / BLOCK consecutive per thread)",
+          "      constexpr int PER = TS / BLOCK;",
+          "      unsigned loc[PER]; unsigned s = 0;",
+          "#pragma unroll",
+          "      for (int t = 0; t < PER; ++t) { loc[t] = s_cnt[threadIdx.x * PER + t]; s += loc[t]; }",
+          "      i64 tot; const i64 ex = wg_block_exclusive_scan((i64)s, s_sc, &tot);",
+          "      unsigned run = (unsigned)ex;",
+          "#pragma unroll",
+          "      for (int t = 0; t < PER; ++t) { s_cnt[threadIdx.x * PER + t] = run; run += loc[t]; }",
+          "      if (threadIdx.x == 0) s_c = (unsigned)tot;",
+          "    }",
+          "    __syncthreads();",
+          "    for (int q = threadIdx.x; q < TS; q += BLOCK) {",
+          "      const u64 w = s_k[q];",
+          "      if (w != WG_EMPTY_KEY) s_perm[atomicAdd(&s_cnt[(unsigned)((" + ok("w") + " - omin) >> ssh)], 1u)] = (unsigned short)q;",
+          "    }",
+          "    __syncthreads();",
+          "    const unsigned c = s_c;",
+          # s_cnt[b] is now the end of sub-bucket b; insertion-sort the rare multi-key buckets
+          "    for (int q = threadIdx.x; q < TS; q += BLOCK) {",
+          "      const unsigned s0 = q ? s_cnt[q - 1] : 0u, e0 = s_cnt[q];",
+          "      for (unsigned a = s0 + 1; a < e0; ++a) {",
+          "        const unsigned short x = s_perm[a];",
+          "        const u64 kx = " + ok("s_k[x]") + ";",
+          "        unsigned bb = a;",
+          "        while (bb > s0 && " + ok("s_k[s_perm[bb - 1]]") + " > kx) { s_perm[bb] = s_perm[bb - 1]; --bb; }",
+          "        s_perm[bb] = x;",
+          "      }",
+          "    }",
+          # ---- output offset: decoupled look-back over partitions (claim order)
+          "    const unsigned ctot = c + (unsigned)s_has;",
+          "    if (threadIdx.x < 32) {",
+          "      const i64 ex = wg_lookback(p.status, part, (i64)ctot);",
+          "      if (threadIdx.x == 0) { s_off = ex; if (part == (i64)p.nparts - 1) *p.nout = (unsigned long long)(ex + ctot); }",
+          "    }",
+          "    __syncthreads();",
+          "    const u64 off = (u64)s_off;",
+          # position of the sentinel-valued key among the sorted keys
+          "    unsigned lb = c;",
+          "    if (s_has) {",
+          "      const u64 ke = " + ok("WG_EMPTY_KEY") + ";",
+          "      unsigned lo_ = 0, hi_ = c;",
+          "      while (lo_ < hi_) { const unsigned m = (lo_ + hi_) >> 1; if (" + ok("s_k[s_perm[m]]") + " < ke) lo_ = m + 1; else hi_ = m; }",
+          "      lb = lo_;",
+          "      if (threadIdx.x == 0) { p.outk[off + lb] = WG_EMPTY_KEY;"]
+    for f in range(V):
+        L[-1] += f" p.outv{f}[off + lb] = s_sk[{f}];"
+    L[-1] += " }"
+    L += ["    }",
+          "    for (unsigned i = threadIdx.x; i < c; i += BLOCK) {",
+          "      const unsigned x = s_perm[i];",
+          "      const u64 dst = off + i + (i >= lb ? (u64)s_has : 0ULL);",
+          "      __stcs(p.outk + dst, s_k[x]);"]
+    for f in range(V):
+        L.append(f"      __stcs(p.outv{f} + dst, s_v{f}[x]);")
+    L += ["    }",
+          "    __syncthreads();",
+          "    for (int q = threadIdx.x; q < TS; q += BLOCK) { s_k[q] = WG_EMPTY_KEY;"]
+    for f in range(V):
+        L[-1] += f" s_v{f}[q] = {ident[f]};"
+    L[-1] += " }"
+    L += ["    __syncthreads();",
+          "  }",
+          "}"]
+    smem = TS * 8 * (1 + V) + TS * 4 + TS * 2
+    return "\n".join(L) + "\n", smem
+
+
 def _agg_apply(vks, opc, slot_words, ind, key, vals):
     L = [f"{ind}if (sl_ >= 0) {{"]
     for f, kk in enumerate(vks):
@@ -1733,6 +2090,10 @@ def _deferred_dict_lines(g, b):
         for f, kk in enumerate(vks):
             L.append(f"        dkv{B}_{f}[j] = a{f}_;")
         L.append("      }")
+    if b.extra.get("rpart"):
+        L += _rpart_loop_lines(g, b)
+        L.append("    }")
+        return L
     if b.extra.get("part"):
         # Partitioned mode (cardinality >> L2).  Partition = the region of the
         # HBM table a key's home slot falls in (pbits top bits of the slot
@@ -1892,7 +2253,7 @@ def _capture_val(g: Gen, name, ty, val):
 # suite to prove every loop of a program lowers and compiles for sm_100a.
 
 
-def static_plans(expr, env_types=None, externs=(), smem=True, lowcard=False, part=False):
+def static_plans(expr, env_types=None, externs=(), smem=True, lowcard=False, part=False, rpart=False):
     """Yield a KernelPlan per ``for`` loop in a typed program, deriving the
     iteration, builder and capture specs from types alone."""
     from weldmill.expr import walk, free_variables as _fv
@@ -1927,7 +2288,9 @@ def static_plans(expr, env_types=None, externs=(), smem=True, lowcard=False, par
                     sw = (1 if nw == 1 else 1 + nw) + len(leaves(t.kind.value))
                     bs.extra["slot_words"] = sw
                     bs.mode = "global"
-                    if nw == 1 and part:
+                    if nw == 1 and rpart and rpart_ok(leaves(t.kind.key)):
+                        bs.extra.update(rpart=True, pbits=11)
+                    elif nw == 1 and part:
                         bs.extra.update(part=True, pbits=8, agg_S=0)
                     elif nw == 1 and smem:
                         bs.mode = "smem"

@@ -271,6 +271,80 @@ def to_numpy(v: DVec):
     return tuple(arrs)
 
 
+class Ragged:
+    """numpy form of a nested ``vec[T]`` column: ``offsets`` (n+1 i64) over
+    ``values`` (the child's numpy form).  Row j is values[offsets[j]:
+    offsets[j+1]] -- the reference's list-of-lists (builders.py:478-493)
+    without one Python object per element."""
+
+    __slots__ = ("offsets", "values")
+
+    def __init__(self, offsets, values):
+        self.offsets = offsets
+        self.values = values
+
+    def __len__(self):
+        return len(self.offsets) - 1
+
+    def __getitem__(self, j):
+        a, b = int(self.offsets[j]), int(self.offsets[j + 1])
+        v = self.values
+        if isinstance(v, tuple):
+            return tuple(x[a:b] for x in v)
+        return v[a:b]
+
+    def tolist(self):
+        return [_np_tolist(self[j]) for j in range(len(self))]
+
+    @property
+    def nbytes(self):
+        return self.offsets.nbytes + _np_nbytes(self.values)
+
+
+def _np_tolist(v):
+    if isinstance(v, tuple):
+        return list(zip(*(_np_tolist(x) for x in v)))
+    if isinstance(v, Ragged):
+        return v.tolist()
+    return v.tolist()
+
+
+def _np_nbytes(v):
+    if isinstance(v, tuple):
+        return sum(_np_nbytes(x) for x in v)
+    return v.nbytes
+
+
+def to_numpy_nested(v: DVec):
+    """Any vector -> numpy: flat leaves as arrays, structs as tuples, nested
+    vectors as :class:`Ragged`.  One async copy per column into pinned
+    memory, one sync."""
+
+    def pull(kind, col, n):
+        nb = n * SIZE[kind]
+        a = pinned_empty(n, NPTYPE[kind]) if nb >= PINNED_MIN_BYTES else np.empty(n, dtype=np.dtype(NPTYPE[kind]))
+        if nb:
+            rt.d2h_async(a.ctypes.data, col.ptr, nb)
+        return a
+
+    def go(t, lay, n):
+        if isinstance(t, Scalar):
+            return pull(t.kind, lay, n)
+        if isinstance(t, Struct):
+            return tuple(go(ft, fl, n) for ft, fl in zip(t.fields, lay))
+        if isinstance(t, Vec):
+            offs = pull(I64, lay.offsets, n + 1)
+            return Ragged(offs, go(t.elem, lay.child, int(lay.total)))
+        raise DeviceUnsupported(f"cannot read back {t}")
+
+    try:
+        out = go(v.elem, v.layout, v.n)
+    finally:
+        del go
+    rt.sync()
+    return out
+
+
 def _layout_to_payload(t, lay, n):
     if isinstance(t, Scalar):
         a = col_to_numpy(lay, n)

@@ -404,6 +404,21 @@ template <> struct WgAtomicFold<3, i32> { static __device__ __forceinline__ void
 // Shared-memory variants (same semantics, smem addresses).
 template <int OPC, typename T> __device__ __forceinline__ void wg_smem_fold(T* p, T v) { WgAtomicFold<OPC, T>::f(p, v); }
 
+// sm_100 has no native 64-bit shared-memory atomic add (it is a CAS spin
+// loop).  Integer + splits into two native 32-bit adds: the low word's old
+// value tells each adder whether its low half carried, and the carries sum
+// to the number of low-word wraps, so the 64-bit total is exact.
+__device__ __forceinline__ void wg_smem_add_i64(i64* p, i64 v) {
+  unsigned* w = reinterpret_cast<unsigned*>(p);
+  const u64 uv = (u64)v;
+  const unsigned lo = (unsigned)uv, hi = (unsigned)(uv >> 32);
+  const unsigned old = atomicAdd(w, lo);
+  const unsigned up = hi + ((unsigned)(old + lo) < old ? 1u : 0u);
+  if (up) atomicAdd(w + 1, up);
+}
+template <int OPC, typename T> struct WgSmemFold { static __device__ __forceinline__ void f(T* p, T v) { WgAtomicFold<OPC, T>::f(p, v); } };
+template <> struct WgSmemFold<0, i64> { static __device__ __forceinline__ void f(i64* p, i64 v) { wg_smem_add_i64(p, v); } };
+
 // ---------------------------------------------------------------------------
 // Hash table for dictmerger / group ids.  Keys are packed into KW 64-bit
 // words.  KW == 1 uses the key word itself as the claim word with an EMPTY

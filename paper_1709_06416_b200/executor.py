@@ -31,9 +31,9 @@ from weldmill.expr import (Apply, BinaryOp, BitSelect, Broadcast, CastScalar, Ex
 
 from . import runtime as rt
 from . import semantics as sem
-from .builders_dev import (AppenderDev, DDict, DGroups, DictDev, GroupDev, MergerDev, VecMergerDev, dict_payload,
-                           finish_dict, finish_groups, gather_cols, sort_perm, tovec)
-from .codegen import DEFER_DICT, PIPE_STAGES, BSpec, IterSpec, generate
+from .builders_dev import (_RANGE_HINTS, AppenderDev, DDict, DGroups, DictDev, GroupDev, MergerDev, VecMergerDev,
+                           dict_payload, finish_dict, finish_groups, gather_cols, sort_perm, tovec)
+from .codegen import DEFER_DICT, PIPE_STAGES, BSpec, IterSpec, generate, rpart_ok, rpart_table_slots
 from .columns import Col, DVec, to_device, to_payload, dvec_from_cols
 from .irtypes import (BOOL, F32, F64, I64, SIZE, identity_value, Builder, DeviceUnsupported as _DU, Dict, DictMerger, Function,
                       GroupBuilder, Merger, Scalar, Simd, Struct, Vec, VecBuilder, VecMerger, is_flat, leaves)
@@ -498,6 +498,8 @@ class Ctx:
         _collect_builders(builders, blist)
         for b in blist:
             b.check()
+            if getattr(b, "rpart_out", None) is not None:
+                self._rpart_to_table(b)
             self.flush_pending(b)
         # loop-invariant captures
         fv = _fv_cache.get(id(lam))
@@ -530,7 +532,16 @@ class Ctx:
                     _plan_cache.clear()
                 _plan_cache[key] = cached
         plan, kern = cached[0], cached[1]
-        self.launch(plan, kern, count, datas, windows, builders, bmap, captures)
+        try:
+            self.launch(plan, kern, count, datas, windows, builders, bmap, captures)
+        except _RpartFallback:
+            # skewed keys overflowed a partition: forget the merges and run
+            # the loop again through the hash-table dictmerger
+            for bid, st in bmap.items():
+                if isinstance(st, DictDev):
+                    _RPART_BAD.add((id(e), bid))
+                    st.reset()
+            return self.run_loop(e, env, count_traversal=False)
         return builders
 
     def launch(self, plan, kern, count, datas, windows, builders, bmap, captures):
@@ -567,6 +578,10 @@ class Ctx:
                     rt.memset(status.ptr, 0, 8 * max(ntiles, 1))
                     res[b.bid] = (seg, status)
                     self._acct_append(st, count * b.k)
+            elif isinstance(b.kind, DictMerger) and b.extra.get("rpart"):
+                st.ensure(1)            # (unused) table keeps the kernel's table parameters valid
+                st.hint_key = (plan.key_id, b.bid)
+                st.ensure_rpart(count, 1 << b.extra["pbits"], grid, _RANGE_HINTS[st.hint_key])
             elif isinstance(b.kind, DictMerger):
                 st.ensure(count * max(1, b.extra.get("maxm", 1)), hint_key=(plan.key_id, b.bid))
                 if b.extra.get("part") and b.extra.get("deferred"):
@@ -589,6 +604,8 @@ class Ctx:
         for b in plan.builders:
             if isinstance(b.kind, DictMerger) and b.extra.get("part") and b.extra.get("deferred"):
                 self._dict_aggregate(bmap[b.bid], b)
+            if isinstance(b.kind, DictMerger) and b.extra.get("rpart"):
+                self._dict_rpart_aggregate(bmap[b.bid], b)
         # dictmerger overflow: grow and replay spilled merges
         for b in plan.builders:
             if isinstance(b.kind, DictMerger):
@@ -611,6 +628,58 @@ class Ctx:
         kern.launch(grid, 256, blob, smem)
         self.launches += 1
         self.dirty = True
+
+    def _dict_rpart_aggregate(self, st, b):
+        """Second kernel of the range-partitioned dictmerger: per-partition
+        shared-memory aggregation + local sort, written at look-back
+        offsets.  Leaves the sorted entries in st.rpart_out."""
+        from .codegen import dict_rpart_source
+        V = len(st.vks)
+        ts = rpart_table_slots(V)
+        src, smem = dict_rpart_source(st.kind, ts)
+        kern = rt.get_kernel(src, "wg_drp")
+        P = st.nparts
+        cap = min(st.rows_in, P * ts) + 1
+        outk = rt.alloc(8 * cap)
+        outv = [rt.alloc(8 * cap) for _ in range(V)]
+        status = rt.alloc(8 * P)
+        rt.memset(status.ptr, 0, 8 * P)
+        grid = max(1, min(P, rt.sm_count() * max(1, kern.blocks_per_sm(1024, smem))))
+        rc = st.rcounters.ptr
+        words = [st.pk.ptr] + [v.ptr for v in st.pv] + [st.pcount.ptr, st.pcap, st.nslices, P, outk.ptr]
+        words += [o.ptr for o in outv]
+        words += [status.ptr, rc + 16, rc, rc + 8]
+        blob = b"".join(_pack("u64", w) for w in words)
+        kern.launch(grid, 1024, blob, smem)
+        self.launches += 1
+        global RPART_RUNS
+        RPART_RUNS += 1
+        cnt = np.empty(2, dtype=np.uint64)
+        rt.d2h(cnt.ctypes.data, rc, 16)
+        if int(cnt[0]):
+            raise _RpartFallback()
+        st.rpart_out = ([outk], outv, int(cnt[1]))
+
+    def _rpart_to_table(self, st):
+        """A range-partitioned result that receives further merges: replay
+        its entries into a hash table first (all folds are commutative)."""
+        kw, vw, n = st.rpart_out
+        st.rpart_out = None
+        st.ensure(max(n, 1))
+        if n == 0:
+            return
+        from .builders_dev import _words_to_cols, _value_words_to_cols
+        kcols = _words_to_cols(kw, st.kks, st.lay, n)
+        vcols = _value_words_to_cols(vw, st.vks, n)
+        kty, vty = st.kind.key, st.kind.value
+        elem = Struct((kty, vty))
+        dv = DVec(elem, n, (_layout(kty, kcols), _layout(vty, vcols)))
+        x = Ident("x", ty=elem)
+        body = Merge(Ident("b", ty=Builder(st.kind)), x, ty=Builder(st.kind))
+        lam = Lambda((XParam("b"), XParam("i"), XParam("x")), body)
+        loop = For((XIterSpec(Ident("__rows", ty=Vec(elem))),), Ident("__b", ty=Builder(st.kind)), lam,
+                   ty=Builder(st.kind))
+        self.run_loop(loop, {"__rows": dv, "__b": st}, count_traversal=False)
 
     def _acct_append(self, st, rows):
         if getattr(st, "hint", None) is None:
@@ -726,6 +795,12 @@ class Ctx:
                     return st.ocap
                 if what == "okey":
                     return st.over[0][key[3]].ptr
+                if what == "rlo":
+                    return st.rlo
+                if what == "rshift":
+                    return st.rshift
+                if what == "oflow":
+                    return st.rcounters.ptr
                 if what == "pcount":
                     return st.pcount.ptr
                 if what == "pcap":
@@ -815,9 +890,26 @@ STREAMING = _os.environ.get("WELDGPU_STREAM", "1") == "1"
 PART_MIN_KEYS = 1 << 20
 
 
+# Range-partitioned dictmerger (codegen.dict_rpart_source): correct for every
+# key distribution (overflow re-runs the loop), but on B200 its per-CTA
+# partition slices turn the bucket writes into isolated 32-byte DRAM writes;
+# at 2048 partitions the hash-partitioned path is faster, so it
+# is opt-in.
+RPART = _os.environ.get("WELDGPU_RPART", "0") == "1"
+RPART_MAX_PARTS = 4096
+_RPART_BAD = set()      # loops whose range-partitioned run overflowed once
+RPART_RUNS = 0
+
+
+class _RpartFallback(Exception):
+    """A range-partitioned dictmerger overflowed (skewed keys): re-run the
+    loop through the hash-table path."""
+
+
 def _bspecs(builders, strategy, count, loop_id=None):
     bmap = {}
     counter = [0]
+    single = not isinstance(builders, tuple)
 
     def go(v):
         if isinstance(v, tuple):
@@ -839,10 +931,24 @@ def _bspecs(builders, strategy, count, loop_id=None):
             # Cardinality seen the last time this loop ran decides the
             # variant: low -> register cache + shared table, otherwise (or
             # unknown) -> deferred merges with batched HBM probes.
-            from .builders_dev import _SIZE_HINTS
+            from .builders_dev import _SIZE_HINTS, _RANGE_HINTS
             seen = _SIZE_HINTS.get((loop_id, bid))
             lowcard = seen is not None and seen <= LOWCARD_MAX
-            if seen is not None and seen > PART_MIN_KEYS and strategy != "global" and v.nw == 1 and DEFER_DICT:
+            rng = _RANGE_HINTS.get((loop_id, bid))
+            if (seen is not None and seen > PART_MIN_KEYS and strategy != "global" and v.nw == 1 and DEFER_DICT
+                    and RPART and single and rng is not None and rpart_ok(v.kks) and v.table is None
+                    and v.rpart_out is None and not v.pending and (loop_id, bid) not in _RPART_BAD):
+                # cardinality far beyond L2: range-partitioned aggregation, the
+                # key order falls out of the partitioning (no global sort)
+                ts = rpart_table_slots(len(v.vks))
+                nparts = 1 << max(6, int(-(-seen * 5 // (3 * ts)) - 1).bit_length())
+                loop_smem = nparts * (16 + 32 * (1 + len(v.vks)))      # chunk buffers + cursors
+                if (ts * (8 * (1 + len(v.vks)) + 6) + 4096 <= 200 * 1024 and nparts <= RPART_MAX_PARTS
+                        and loop_smem <= 168 * 1024):
+                    bs.extra["rpart"] = True
+                    bs.extra["pbits"] = int(_os.environ.get("WELDGPU_RPART_PBITS", nparts.bit_length() - 1))
+            if (not bs.extra.get("rpart") and seen is not None and seen > PART_MIN_KEYS and strategy != "global"
+                    and v.nw == 1 and DEFER_DICT):
                 # cardinality far beyond L2: partitioned two-kernel aggregation
                 bs.extra["part"] = True
                 bs.extra["agg_S"] = 0
@@ -872,7 +978,7 @@ def _bsig(bs):
     if isinstance(bs, tuple):
         return tuple(_bsig(x) for x in bs)
     return (bs.mode, bs.extra.get("nbins"), bs.extra.get("smem_slots"), bs.extra.get("lowcard"),
-            bs.extra.get("part"), bs.extra.get("pbits"))
+            bs.extra.get("part"), bs.extra.get("pbits"), bs.extra.get("rpart"))
 
 
 def _type_of(v, lam, name):
@@ -910,13 +1016,15 @@ def to_host_payload(v, ty):
 
 
 def _numpy_tree(v, ty):
-    from .columns import to_numpy
+    from .columns import to_numpy, to_numpy_nested
     if isinstance(v, tuple) and isinstance(ty, Struct):
         return tuple(_numpy_tree(x, t) for x, t in zip(v, ty.fields))
     if isinstance(v, HostVec):
         v = v.dev()
     if isinstance(v, DVec) and is_flat(v.elem):
         return to_numpy(v)
+    if isinstance(v, DVec):
+        return to_numpy_nested(v)     # nested vectors: Ragged (offsets + values)
     return to_host_payload(v, ty)
 
 

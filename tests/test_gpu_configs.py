@@ -126,6 +126,26 @@ def test_group_large_preserves_per_key_order():
     np.testing.assert_array_equal(gvals, vs)
 
 
+def test_group_numpy_result_is_ragged():
+    """result="numpy" reads a nested vec back as columns (keys, Ragged(offsets,
+    values)) -- no per-element Python objects -- equal to the oracle."""
+    from oracle import weld_oracle
+    n = (1 << 20) + 5
+    got, _, cols = _run("group", n, result="numpy")
+    ks, offs, vs = weld_oracle.group(cols)
+    gk, rag = got
+    np.testing.assert_array_equal(gk, ks)
+    np.testing.assert_array_equal(rag.offsets, offs)
+    np.testing.assert_array_equal(rag.values, vs)
+    assert len(rag) == len(ks)
+    j = len(ks) // 2
+    np.testing.assert_array_equal(rag[j], vs[offs[j]:offs[j + 1]])
+    small, _, scols = _run("group", 3000, result="numpy")
+    pyres, _, _ = _run("group", 3000)
+    assert [(int(k), list(map(int, v))) for k, v in zip(small[0], small[1].tolist())] == \
+        [(k, list(v)) for k, v in pyres]
+
+
 def test_hist_large_conserves_weight():
     from paper_1709_06416_b200.columns import to_numpy
     n = 64 << 20

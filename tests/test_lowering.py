@@ -89,3 +89,35 @@ def test_generated_literals_are_exact():
     assert c_literal("i64", -(2**63)) == "((i64)0x8000000000000000ULL)"
     assert c_literal("i32", -1) == "((i32)0xffffffffU)"
     assert c_literal("f64", float("inf")).endswith("0x7ff0000000000000LL)")
+
+
+def test_range_partitioned_dict_kernels_compile():
+    """Loop side (range digit + windowed bucket writes) and the shared-memory
+    aggregation/sort kernel, for each fold op and a two-field value."""
+    from paper_1709_06416_b200 import codegen, runtime, workloads as W
+    from paper_1709_06416_b200.irtypes import DictMerger, leaves
+    plans = codegen.static_plans(W.compile_program(W.WORKLOADS["dict"]), rpart=True)
+    assert any("d0_rlo" in p.source for p in plans)
+    for plan in plans:
+        assert runtime.compile_check(plan.source) > 0
+    kind = plans[0].builders[0].kind
+    for op in ("+", "*", "min", "max"):
+        k = DictMerger(kind.key, kind.value, op)
+        src, smem = codegen.dict_rpart_source(k, codegen.rpart_table_slots(len(leaves(k.value))))
+        assert smem <= 200 * 1024
+        assert runtime.compile_check(src, "drp.cu") > 0
+
+
+def test_order_key_expression_matches_python():
+    """okey_expr (device) and okey_py (host) agree with the reference's
+    order_key on packed integer keys: signed order, first leaf major."""
+    from paper_1709_06416_b200 import codegen
+    from paper_1709_06416_b200.irtypes import I32, I64, BOOL
+    vals = [-(1 << 63), -5, -1, 0, 1, 7, (1 << 63) - 1]
+    oks = [codegen.okey_py([I64], v & 0xFFFFFFFFFFFFFFFF) for v in vals]
+    assert oks == sorted(oks) and len(set(oks)) == len(oks)
+    pairs = [(a, b) for a in (-3, 0, 2) for b in (-(1 << 31), -1, 0, (1 << 31) - 1)]
+    words = [(a & 0xFFFFFFFF) | ((b & 0xFFFFFFFF) << 32) for a, b in pairs]
+    oks = [codegen.okey_py([I32, I32], w) for w in words]
+    assert [p for _, p in sorted(zip(oks, pairs))] == sorted(pairs)
+    assert codegen.rpart_ok([I64]) and codegen.rpart_ok([I32, I32]) and codegen.rpart_ok([BOOL])
