@@ -64,6 +64,10 @@ int wg_compile(const char* src, const char* name, int nheaders, const char* cons
 int wg_compile_check(const char* src, const char* name, int nheaders, const char* const* header_srcs,
                      const char* const* header_names, int nopts, const char* const* opts, uint64_t* cubin_bytes,
                      char* log_buf, uint64_t log_cap);
+int wg_compile_ptx(const char* src, const char* name, int nheaders, const char* const* header_srcs,
+                   const char* const* header_names, int nopts, const char* const* opts, char* ptx_out,
+                   uint64_t ptx_cap, uint64_t* ptx_size, char* log_buf, uint64_t log_cap);
+int wg_module_load(const char* image, uint64_t* module_out);
 int wg_module_function(uint64_t module, const char* name, uint64_t* fn);
 int wg_occupancy(uint64_t fn, int block, int dyn_smem, int* blocks_per_sm);
 int wg_launch(uint64_t fn, uint32_t grid, uint32_t block, uint32_t dyn_smem, const void* params,
@@ -77,6 +81,13 @@ int wg_launch(uint64_t fn, uint32_t grid, uint32_t block, uint32_t dyn_smem, con
 int wg_table_init(uint64_t table, uint64_t nslots, int slot_words, const uint64_t* pattern);
 int wg_table_compact(uint64_t table, uint64_t nslots, int slot_words, int mode, const uint64_t* out_words, int nout,
                      uint64_t* count_out);
+/* Small dictmerger result in one launch: occupied slots -> entries sorted by
+ * the order_key tuple -> typed key/value columns (DictMergerState.result,
+ * builders.py:380-392 + order_key :496-507).  key_desc = 4 ints per key leaf
+ * (word, shift, width, kind); *count_out > 4096 means nothing was written. */
+int wg_dict_finish_small(uint64_t table, uint64_t nslots, int slot_words, int mode, int nw, int nkl,
+                         const int* key_desc, int nvl, const int* val_kinds, const uint64_t* outs,
+                         uint64_t* count_out);
 int wg_order_key(uint64_t src, int kind, uint64_t n, uint64_t perm, uint64_t dst);
 int wg_iota_u32(uint64_t dst, uint64_t n);
 int wg_sort_pairs(uint64_t keys_in, uint64_t vals_in, uint64_t keys_out, uint64_t vals_out, uint64_t n, int begin_bit,

@@ -441,6 +441,34 @@ def _pack_word(d: DictDev, cols, j):
     return w
 
 
+SMALL_DICT = 4096
+
+
+def _finish_small(d: DictDev, dict_ty):
+    """Results of <= SMALL_DICT entries: one launch (wg_dict_finish_small)
+    instead of compaction + per-leaf radix sorts + gathers."""
+    distinct, spilled = d.read_counters()
+    nkl, nvl = len(d.kks), len(d.vks)
+    if distinct > SMALL_DICT or spilled or nkl > 6 or nvl > 16:
+        return None
+    n = distinct
+    kcols = [Col.alloc(k, max(n, 1)) for k in d.kks]
+    vcols = [Col.alloc(k, max(n, 1)) for k in d.vks]
+    desc = []
+    for (wi, sh, width), k in zip(d.lay, d.kks):
+        desc += [wi, sh, width, KIND_CODE[k]]
+    kd = (ctypes.c_int * len(desc))(*desc)
+    vk = (ctypes.c_int * max(nvl, 1))(*[KIND_CODE[k] for k in d.vks])
+    outs = (ctypes.c_uint64 * (nkl + nvl))(*[c.ptr for c in kcols + vcols])
+    cnt = ctypes.c_uint64(0)
+    mode = 1 if d.nw == 1 else 2
+    rt.call("wg_dict_finish_small", d.table.ptr, d.cap, d.slot_words, mode, d.nw, nkl, kd, nvl, vk, outs,
+            ctypes.byref(cnt))
+    if cnt.value != n:
+        raise RuntimeError(f"dictmerger table holds {cnt.value} keys, counted {n}")
+    return DDict(dict_ty, dvec_from_cols(dict_ty.key, n, kcols), dvec_from_cols(dict_ty.value, n, vcols))
+
+
 def finish_dict(d: DictDev, dict_ty):
     if d.rpart_out is not None:
         # range-partitioned: the aggregation kernel wrote the entries sorted
@@ -456,6 +484,9 @@ def finish_dict(d: DictDev, dict_ty):
             rt.d2h(ends[1:].ctypes.data, kw[0].ptr + 8 * (n - 1), 8)
             _record_range(d, int(ends[0]), int(ends[1]))
         return DDict(dict_ty, dvec_from_cols(dict_ty.key, n, kcols), dvec_from_cols(dict_ty.value, n, vcols))
+    small = _finish_small(d, dict_ty)
+    if small is not None:
+        return small
     kw, vw, n = d.compact()
     kcols = _words_to_cols(kw, d.kks, d.lay, n)
     vcols = _value_words_to_cols(vw, d.vks, n)

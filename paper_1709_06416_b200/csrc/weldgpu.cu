@@ -357,6 +357,119 @@ __global__ void k_group_out(const uint32_t* starts, uint64_t K, uint64_t n, cons
     else ((int64_t*)ukeys)[j] = (int64_t)(w ^ 0x8000000000000000ULL);
   }
 }
+
+// ---- small dictmerger result (DictMergerState.result, builders.py:380-392,
+// entries sorted by order_key builders.py:496-507) in ONE launch: collect the
+// occupied slots, order them by the key's order-key tuple (bitonic sort in
+// shared memory), and write typed key / value columns.  For results of up to
+// WG_SMALL_DICT entries (TPC-H style group counts) this replaces
+// compaction + per-leaf radix sorts + gathers (and their host round trips).
+#define WG_SMALL_DICT 4096
+struct SmallDictDesc {
+  int nkl, nvl, mode, nw, sw, kbase;
+  int kword[8], kshift[8], kwidth[8], kkind[8];
+  int vkind[16];
+  void* out[24];
+};
+
+__device__ __forceinline__ uint64_t wg_leaf_okey(uint64_t bits, int kind) {
+  switch (kind) {
+    case 0: return bits & 0xffULL;
+    case 1: return (uint64_t)(int64_t)(int32_t)(uint32_t)bits ^ 0x8000000000000000ULL;
+    case 2: return bits ^ 0x8000000000000000ULL;
+    default: {
+      double v = (kind == 3) ? (double)__int_as_float((int)(uint32_t)bits) : __longlong_as_double((long long)bits);
+      if (v != v) return 0xffffffffffffffffULL;
+      if (v == 0.0) v = 0.0;
+      uint64_t b = (uint64_t)__double_as_longlong(v);
+      uint64_t k = (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+      return k == 0xffffffffffffffffULL ? 0xfffffffffffffffeULL : k;
+    }
+  }
+}
+
+__device__ __forceinline__ void wg_store_leaf(void* col, uint64_t i, uint64_t bits, int kind) {
+  switch (kind) {
+    case 0: ((uint8_t*)col)[i] = (uint8_t)bits; break;
+    case 1: case 3: ((uint32_t*)col)[i] = (uint32_t)bits; break;
+    default: ((uint64_t*)col)[i] = bits;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_dict_finish_small(const uint64_t* table, uint64_t nslots, SmallDictDesc d,
+                                                            unsigned long long* count_out) {
+  __shared__ uint32_t s_idx[WG_SMALL_DICT];
+  __shared__ unsigned s_n;
+  extern __shared__ uint64_t s_ok[];      // [WG_SMALL_DICT * nkl] order keys
+  if (threadIdx.x == 0) s_n = 0;
+  __syncthreads();
+  const uint64_t total = nslots + (d.mode == 1 ? 1 : 0);
+  for (uint64_t s = threadIdx.x; s < total; s += blockDim.x) {
+    const uint64_t w0 = table[s * d.sw];
+    const bool occ = (s == nslots) ? (w0 == 0ULL) : (d.mode == 1 ? w0 != 0xffffffffffffffffULL : w0 == 2ULL);
+    if (occ) {
+      const unsigned e = atomicAdd(&s_n, 1u);
+      if (e < WG_SMALL_DICT) s_idx[e] = (uint32_t)s;
+    }
+  }
+  __syncthreads();
+  const unsigned n = s_n;
+  if (threadIdx.x == 0) *count_out = n;
+  if (n > WG_SMALL_DICT) return;             // the host takes the general path
+  unsigned np = 1;
+  while (np < n) np <<= 1;
+  for (unsigned e = threadIdx.x; e < np; e += blockDim.x) {
+    if (e >= n) { s_idx[e] = 0xffffffffu; continue; }
+    const uint64_t s = s_idx[e];
+    for (int l = 0; l < d.nkl; ++l) {
+      uint64_t w;
+      if (d.mode == 1) w = (s == nslots) ? 0xffffffffffffffffULL : table[s * d.sw];
+      else w = table[s * d.sw + 1 + d.kword[l]];
+      const uint64_t bits = d.kwidth[l] == 64 ? (w >> d.kshift[l]) : ((w >> d.kshift[l]) & ((1ULL << d.kwidth[l]) - 1));
+      s_ok[(uint64_t)e * d.nkl + l] = wg_leaf_okey(bits, d.kkind[l]);
+    }
+  }
+  __syncthreads();
+  // bitonic sort of entry positions; the key tuple travels with its entry
+  for (unsigned k = 2; k <= np; k <<= 1) {
+    for (unsigned j = k >> 1; j > 0; j >>= 1) {
+      for (unsigned i = threadIdx.x; i < np; i += blockDim.x) {
+        const unsigned l = i ^ j;
+        if (l <= i) continue;
+        const bool up = (i & k) == 0;
+        // compare entries i and l (padding sorts last)
+        int c = 0;
+        const bool pi = s_idx[i] == 0xffffffffu, pl = s_idx[l] == 0xffffffffu;
+        if (pi || pl) c = (pi == pl) ? 0 : (pi ? 1 : -1);
+        else
+          for (int q = 0; q < d.nkl && !c; ++q) {
+            const uint64_t a = s_ok[(uint64_t)i * d.nkl + q], b = s_ok[(uint64_t)l * d.nkl + q];
+            c = a < b ? -1 : (a > b ? 1 : 0);
+          }
+        if ((c > 0) == up && c != 0) {
+          const uint32_t t = s_idx[i]; s_idx[i] = s_idx[l]; s_idx[l] = t;
+          for (int q = 0; q < d.nkl; ++q) {
+            const uint64_t u = s_ok[(uint64_t)i * d.nkl + q];
+            s_ok[(uint64_t)i * d.nkl + q] = s_ok[(uint64_t)l * d.nkl + q];
+            s_ok[(uint64_t)l * d.nkl + q] = u;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (unsigned i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint64_t s = s_idx[i];
+    for (int l = 0; l < d.nkl; ++l) {
+      uint64_t w;
+      if (d.mode == 1) w = (s == nslots) ? 0xffffffffffffffffULL : table[s * d.sw];
+      else w = table[s * d.sw + 1 + d.kword[l]];
+      const uint64_t bits = d.kwidth[l] == 64 ? (w >> d.kshift[l]) : ((w >> d.kshift[l]) & ((1ULL << d.kwidth[l]) - 1));
+      wg_store_leaf(d.out[l], i, bits, d.kkind[l]);
+    }
+    for (int f = 0; f < d.nvl; ++f) wg_store_leaf(d.out[d.nkl + f], i, table[s * d.sw + d.kbase + f], d.vkind[f]);
+  }
+}
 }  // namespace
 
 // ===========================================================================
@@ -626,6 +739,45 @@ int wg_compile_check(const char* src, const char* name, int nheaders, const char
   return 0;
 }
 
+// PTX of a program (the executor's constant-pool pass rewrites it before the
+// driver JIT compiles it for the device): *ptx_size is the PTX length + 1; a
+// NULL / too-small buffer just reports the size.
+int wg_compile_ptx(const char* src, const char* name, int nheaders, const char* const* header_srcs,
+                   const char* const* header_names, int nopts, const char* const* opts, char* ptx_out,
+                   uint64_t ptx_cap, uint64_t* ptx_size, char* log_buf, uint64_t log_cap) {
+  nvrtcProgram prog;
+  CKN(nvrtcCreateProgram(&prog, src, name, nheaders, header_srcs, header_names));
+  nvrtcResult rc = nvrtcCompileProgram(prog, nopts, opts);
+  size_t log_size = 0;
+  nvrtcGetProgramLogSize(prog, &log_size);
+  std::string log(log_size, '\0');
+  if (log_size) nvrtcGetProgramLog(prog, &log[0]);
+  if (log_buf && log_cap) {
+    size_t n = log.size() < log_cap - 1 ? log.size() : log_cap - 1;
+    memcpy(log_buf, log.data(), n);
+    log_buf[n] = 0;
+  }
+  if (rc != NVRTC_SUCCESS) {
+    nvrtcDestroyProgram(&prog);
+    return fail(std::string("nvrtc compile failed: ") + nvrtcGetErrorString(rc) + "\n" + log);
+  }
+  size_t n = 0;
+  CKN(nvrtcGetPTXSize(prog, &n));
+  *ptx_size = n;
+  if (ptx_out && ptx_cap >= n) CKN(nvrtcGetPTX(prog, ptx_out));
+  nvrtcDestroyProgram(&prog);
+  return 0;
+}
+
+// Load a module image (cubin, or PTX text that the driver JIT-compiles).
+int wg_module_load(const char* image, uint64_t* module_out) {
+  NEED_INIT();
+  CUmodule mod;
+  CKD(p_cuModuleLoadData(&mod, image));
+  *module_out = (uint64_t)(uintptr_t)mod;
+  return 0;
+}
+
 int wg_module_function(uint64_t module, const char* name, uint64_t* fn) {
   NEED_INIT();
   CUfunction f;
@@ -690,6 +842,42 @@ int wg_table_compact(uint64_t table, uint64_t nslots, int slot_words, int mode, 
   CK(cudaStreamSynchronize(g_stream));
   CK(cudaFreeAsync(d_out, g_stream));
   CK(cudaFreeAsync(d_cnt, g_stream));
+  *count_out = h;
+  return 0;
+}
+
+// Small dictmerger result in one launch (see k_dict_finish_small).  key_desc:
+// 4 ints per key leaf (word, shift, width, kind); val_kinds: one per value
+// field; outs: nkl + nvl typed device columns of capacity >= the entry
+// count.  *count_out receives the number of entries; when it exceeds
+// WG_SMALL_DICT nothing is written and the caller uses the general path.
+int wg_dict_finish_small(uint64_t table, uint64_t nslots, int slot_words, int mode, int nw, int nkl,
+                         const int* key_desc, int nvl, const int* val_kinds, const uint64_t* outs,
+                         uint64_t* count_out) {
+  NEED_INIT();
+  if (nkl > 6 || nvl > 16) return fail("wg_dict_finish_small: too many key/value leaves");
+  SmallDictDesc d;
+  memset(&d, 0, sizeof(d));
+  d.nkl = nkl; d.nvl = nvl; d.mode = mode; d.nw = nw; d.sw = slot_words;
+  d.kbase = mode == 1 ? 1 : 1 + nw;
+  for (int l = 0; l < nkl; ++l) {
+    d.kword[l] = key_desc[4 * l]; d.kshift[l] = key_desc[4 * l + 1];
+    d.kwidth[l] = key_desc[4 * l + 2]; d.kkind[l] = key_desc[4 * l + 3];
+  }
+  for (int f = 0; f < nvl; ++f) d.vkind[f] = val_kinds[f];
+  for (int i = 0; i < nkl + nvl; ++i) d.out[i] = (void*)(uintptr_t)outs[i];
+  unsigned long long* d_cnt = (unsigned long long*)g_err_word + 2;   // scratch word next to the error word
+  const int smem = WG_SMALL_DICT * nkl * 8;
+  static bool attr_set = false;
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(k_dict_finish_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 * WG_SMALL_DICT * 8));
+    attr_set = true;
+  }
+  k_dict_finish_small<<<1, 1024, smem, g_stream>>>((const uint64_t*)(uintptr_t)table, nslots, d, d_cnt);
+  CK(cudaGetLastError());
+  unsigned long long h = 0;
+  CK(cudaMemcpyAsync(&h, d_cnt, 8, cudaMemcpyDeviceToHost, g_stream));
+  CK(cudaStreamSynchronize(g_stream));
   *count_out = h;
   return 0;
 }

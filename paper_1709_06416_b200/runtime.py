@@ -7,6 +7,7 @@ from __future__ import annotations
 
 import ctypes
 import hashlib
+import re
 import os
 import threading
 
@@ -50,11 +51,16 @@ _SIGS = {
                            ctypes.POINTER(c_char_p), ctypes.POINTER(u64), c_char_p, u64]),
     "wg_compile_check": (c_int, [c_char_p, c_char_p, c_int, ctypes.POINTER(c_char_p), ctypes.POINTER(c_char_p),
                                  c_int, ctypes.POINTER(c_char_p), ctypes.POINTER(u64), c_char_p, u64]),
+    "wg_compile_ptx": (c_int, [c_char_p, c_char_p, c_int, ctypes.POINTER(c_char_p), ctypes.POINTER(c_char_p), c_int,
+                               ctypes.POINTER(c_char_p), c_char_p, u64, ctypes.POINTER(u64), c_char_p, u64]),
+    "wg_module_load": (c_int, [c_char_p, ctypes.POINTER(u64)]),
     "wg_module_function": (c_int, [u64, c_char_p, ctypes.POINTER(u64)]),
     "wg_occupancy": (c_int, [u64, c_int, c_int, ctypes.POINTER(c_int)]),
     "wg_launch": (c_int, [u64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, c_void_p, u64]),
     "wg_table_init": (c_int, [u64, u64, c_int, ctypes.POINTER(u64)]),
     "wg_table_compact": (c_int, [u64, u64, c_int, c_int, ctypes.POINTER(u64), c_int, ctypes.POINTER(u64)]),
+    "wg_dict_finish_small": (c_int, [u64, u64, c_int, c_int, c_int, c_int, ctypes.POINTER(c_int), c_int,
+                                     ctypes.POINTER(c_int), ctypes.POINTER(u64), ctypes.POINTER(u64)]),
     "wg_order_key": (c_int, [u64, c_int, u64, u64, u64]),
     "wg_iota_u32": (c_int, [u64, u64]),
     "wg_sort_pairs": (c_int, [u64, u64, u64, u64, u64, c_int, c_int]),
@@ -299,7 +305,7 @@ def compile_check(src: str, name="weld_loop.cu"):
 # optional hook called around each generated-kernel launch (bench timing).
 LAUNCHES = [0]
 LAUNCH_HOOK = [None]
-_KERNEL_CALLS = {"wg_table_init": 1, "wg_table_compact": 1, "wg_order_key": 1, "wg_iota_u32": 1,
+_KERNEL_CALLS = {"wg_dict_finish_small": 1, "wg_table_init": 1, "wg_table_compact": 1, "wg_order_key": 1, "wg_iota_u32": 1,
                  "wg_sort_pairs": 1, "wg_gather": 1, "wg_narrow": 1, "wg_widen": 1, "wg_run_starts": 2, "wg_group_finish1": 12,
                  "wg_gen_column": 1, "wg_mul_inplace_f64": 1, "wg_flush_l2": 1}
 
@@ -335,6 +341,61 @@ class Kernel:
             hook("after", self)
 
 
+KPOOL = os.environ.get("WELDGPU_KPOOL", "0") == "1"
+
+
+def compile_ptx(src: str, name="weld_loop.cu") -> str:
+    L = load_library()
+    hs, hn, oa, no = _nvrtc_args(src)
+    size = u64(0)
+    log = ctypes.create_string_buffer(1 << 16)
+    if L.wg_compile_ptx(src.encode(), name.encode(), 1, hs, hn, no, oa, None, 0, ctypes.byref(size), log, 1 << 16):
+        raise WeldGpuError(L.wg_last_error().decode(errors="replace"))
+    buf = ctypes.create_string_buffer(size.value)
+    _check(L.wg_compile_ptx(src.encode(), name.encode(), 1, hs, hn, no, oa, buf, size.value, ctypes.byref(size),
+                            log, 1 << 16))
+    return buf.value.decode()
+
+
+_IMM = re.compile(r"0d([0-9A-Fa-f]{16})")
+_ARITH = re.compile(r"^\s*(fma|mul|add|sub|min|max)\.[a-z.]*f64\b")
+
+
+def const_pool_ptx(ptx: str) -> str:
+    """Move the 64-bit FP immediates of f64 arithmetic (polynomial
+    coefficients of libdevice exp/log/erf) into a .const pool.  ptxas
+    materialises each such immediate with two UMOVs per use inside the
+    loop; from the constant bank it is one load (or an operand)."""
+    pool = {}
+    out = []
+    nreg = 0
+    for line in ptx.split("\n"):
+        if _ARITH.match(line):
+            loads = []
+
+            def rep(m):
+                nonlocal nreg
+                h = m.group(1).upper()
+                if int(h, 16) & 0xFFFFFFFF == 0:
+                    return m.group(0)          # encodable as a 32-bit immediate
+                idx = pool.setdefault(h, len(pool))
+                r = f"%wgk{nreg}"
+                nreg += 1
+                loads.append(f"\tld.const.f64 \t{r}, [wg_kpool+{8 * idx}];")
+                return r
+            line = _IMM.sub(rep, line)
+            out.extend(loads)
+        out.append(line)
+    if not pool:
+        return ptx
+    txt = "\n".join(out)
+    decl = ".const .align 8 .b64 wg_kpool[%d] = {%s};\n" % (
+        len(pool), ", ".join("0x" + h for h in sorted(pool, key=pool.get)))
+    txt = re.sub(r"(\.address_size \d+\n)", lambda m: m.group(1) + decl, txt, count=1)
+    txt = re.sub(r"(\.entry [^{]*\{\n)", lambda m: m.group(1) + f"\t.reg .f64 \t%wgk<{nreg}>;\n", txt)
+    return txt
+
+
 def get_kernel(src: str, name: str) -> Kernel:
     """Compile (cached by source hash) and return the named kernel."""
     key = hashlib.sha1(src.encode()).hexdigest()
@@ -345,8 +406,14 @@ def get_kernel(src: str, name: str) -> Kernel:
             hs, hn, oa, no = _nvrtc_args(src)
             m = u64(0)
             log = ctypes.create_string_buffer(1 << 16)
-            rc = L.wg_compile(src.encode(), f"wg_{key[:12]}.cu".encode(), 1, hs, hn, no, oa, ctypes.byref(m),
-                              log, 1 << 16)
+            if KPOOL and "double" in src:
+                # NVRTC -> PTX -> constant-pool pass -> driver JIT
+                ptx = compile_ptx(src, f"wg_{key[:12]}.cu")
+                _check(L.wg_module_load(const_pool_ptx(ptx).encode() + b"\0", ctypes.byref(m)))
+                rc = 0
+            else:
+                rc = L.wg_compile(src.encode(), f"wg_{key[:12]}.cu".encode(), 1, hs, hn, no, oa, ctypes.byref(m),
+                                  log, 1 << 16)
             if rc != 0:
                 raise WeldGpuError(L.wg_last_error().decode(errors="replace"))
             mod = _modules[key] = (m.value, {})

@@ -1,4 +1,6 @@
 mkdir -p gpurun_out/t2
-for pb in 0 4 8; do
-WELDGPU_RPART_PBITS=$pb timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/t2/launches_pb$pb.csv python bench.py --workload dict --n 20000000 --steps 1 --warmup 2 --no-cpu --no-e2e --no-kernel-timing > /dev/null 2>&1
+for kp in 0 1; do
+WELDGPU_KPOOL=$kp timeout 600 python bench.py --workload blackscholes --steps 10 --warmup 3 --no-cpu --no-e2e 2>&1 | tail -1 > gpurun_out/t2/bs_kp$kp.log
 done
+WELDGPU_KPOOL=1 WELDGPU_MINBLOCKS=3 timeout 600 python bench.py --workload blackscholes --steps 10 --warmup 3 --no-cpu --no-e2e 2>&1 | tail -1 > gpurun_out/t2/bs_kp1_mb3.log
+WELDGPU_KPOOL=1 WELDGPU_MINBLOCKS=4 timeout 600 python bench.py --workload blackscholes --steps 10 --warmup 3 --no-cpu --no-e2e 2>&1 | tail -1 > gpurun_out/t2/bs_kp1_mb4.log
