@@ -284,21 +284,6 @@ __global__ void k_flush(uint4* buf, uint64_t n16, uint32_t salt) {
 
 
 // ---- groupbuilder finalisation (single integer key leaf) -------------------
-__global__ void k_minmax_u64(const uint64_t* k, uint64_t n, unsigned long long* mm) {
-  uint64_t lo = ~0ULL, hi = 0;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t v = k[i];
-    lo = v < lo ? v : lo;
-    hi = v > hi ? v : hi;
-  }
-  for (int d = 16; d > 0; d >>= 1) {
-    uint64_t a = __shfl_xor_sync(0xffffffffu, lo, d), b = __shfl_xor_sync(0xffffffffu, hi, d);
-    lo = a < lo ? a : lo;
-    hi = b > hi ? b : hi;
-  }
-  if ((threadIdx.x & 31) == 0) { atomicMin(mm, lo); atomicMax(mm + 1, hi); }
-}
-
 // After a stable radix sort on key bits [shift, 64), rows of one bucket
 // (equal high bits) may still be out of order in the low bits.  Record the
 // positions where order breaks inside a bucket; only those buckets get a
@@ -314,19 +299,18 @@ __global__ void k_disorder(const uint64_t* k, uint64_t n, int shift, uint32_t* p
   }
 }
 
-// One thread per recorded position; the thread whose position is the first
-// disorder of its bucket sorts the whole bucket (others exit).
+// One thread per recorded disorder position: find the bucket's start (bucket
+// membership -- equal bits [shift, 64) -- is unaffected by reordering inside
+// the bucket, so the walk is race-free) and claim the bucket through a bit
+// in `claimed`; the single owner stable-insertion-sorts it.
 __global__ void k_fix_buckets(uint64_t* k, uint64_t* v, uint64_t n, int shift, const uint32_t* pos, uint64_t npos,
-                              int cap, int* too_long) {
+                              int cap, int* too_long, unsigned* claimed) {
   for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < npos; q += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t i = pos[q];
     uint64_t top = k[i] >> shift;
     uint64_t s = i;
     while (s > 0 && (k[s - 1] >> shift) == top) --s;
-    // first disorder of the bucket?  (scan the bucket prefix for an earlier break)
-    bool first = true;
-    for (uint64_t t = s + 1; t < i; ++t) if (k[t - 1] > k[t]) { first = false; break; }
-    if (!first) continue;
+    if (atomicOr(&claimed[s >> 5], 1u << (s & 31)) & (1u << (s & 31))) continue;
     uint64_t e = i + 1;
     while (e < n && (k[e] >> shift) == top) ++e;
     if (e - s > (uint64_t)cap) { *too_long = 1; continue; }
@@ -345,13 +329,13 @@ __global__ void k_heads1(const uint64_t* k, uint64_t n, uint8_t* flags) {
 }
 
 // offsets[j] = starts[j]; offsets[K] = n; ukeys[j] = inverse order key.
-__global__ void k_group_out(const uint32_t* starts, uint64_t K, uint64_t n, const uint64_t* sk, int kind,
-                            int64_t* offs, void* ukeys) {
+__global__ void k_group_out(const uint32_t* starts, uint64_t K, uint64_t n, const uint64_t* sk, uint64_t kmin,
+                            int kind, int64_t* offs, void* ukeys) {
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j <= K; j += (uint64_t)gridDim.x * blockDim.x) {
     if (j == K) { offs[K] = (int64_t)n; continue; }
     uint64_t s = starts[j];
     offs[j] = (int64_t)s;
-    uint64_t w = sk[s];
+    uint64_t w = sk[s] + kmin;
     if (kind == 0) ((uint8_t*)ukeys)[j] = (uint8_t)w;
     else if (kind == 1) ((int32_t*)ukeys)[j] = (int32_t)(int64_t)(w ^ 0x8000000000000000ULL);
     else ((int64_t*)ukeys)[j] = (int64_t)(w ^ 0x8000000000000000ULL);
@@ -470,6 +454,32 @@ __global__ void __launch_bounds__(1024) k_dict_finish_small(const uint64_t* tabl
     for (int f = 0; f < d.nvl; ++f) wg_store_leaf(d.out[d.nkl + f], i, table[s * d.sw + d.kbase + f], d.vkind[f]);
   }
 }
+
+// order key of element j of a typed integer/bool column (kind 0/1/2)
+__device__ __forceinline__ uint64_t wg_okey_col(const void* src, int kind, uint64_t j) {
+  switch (kind) {
+    case 0: return ((const uint8_t*)src)[j];
+    case 1: return (uint64_t)(int64_t)((const int32_t*)src)[j] ^ 0x8000000000000000ULL;
+    default: return (uint64_t)((const int64_t*)src)[j] ^ 0x8000000000000000ULL;
+  }
+}
+
+__global__ void k_okey_minmax(const void* keys, int kind, uint64_t n, unsigned long long* mm, uint64_t* ok) {
+  uint64_t lo = ~0ULL, hi = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t v = wg_okey_col(keys, kind, i);
+    ok[i] = v;
+    lo = v < lo ? v : lo;
+    hi = v > hi ? v : hi;
+  }
+  for (int d = 16; d > 0; d >>= 1) {
+    uint64_t a = __shfl_xor_sync(0xffffffffu, lo, d), b = __shfl_xor_sync(0xffffffffu, hi, d);
+    lo = a < lo ? a : lo;
+    hi = b > hi ? b : hi;
+  }
+  if ((threadIdx.x & 31) == 0) { atomicMin(mm, lo); atomicMax(mm + 1, hi); }
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -1000,35 +1010,39 @@ int wg_group_finish1(uint64_t keys, int key_kind, uint64_t vals, int val_width, 
     return 0;
   }
   unsigned g = grid_for(n, 256);
-  // The row log (keys, vals) belongs to the finishing builder: 8-byte
-  // columns are sorted in place through CUB double buffers.
+  // Order keys (one fused pass with the min/max reduction) and 64-bit
+  // values, stably radix-sorted on the top 32 varying bits; rows whose keys
+  // share those bits are ordered by the bucket fix-up.
+  // (Sorting (32-bit window, row index) pairs halves the bytes per radix pass
+  // but the value/key gather afterwards is a random permutation -- 11 ms at
+  // 200M rows on B200 vs 4.5 ms saved; carrying the payload through the
+  // passes is cheaper.)
   uint64_t *k0, *k1, *v0, *v1;
-  bool own_k0 = key_kind != 2, own_v0 = val_width != 8;
   unsigned long long* mm;
   int* flag;
-  if (own_k0) CK(cudaMallocAsync((void**)&k0, n * 8, g_stream)); else k0 = (uint64_t*)(uintptr_t)keys;
+  const bool own_v0 = val_width != 8;
+  CK(cudaMallocAsync((void**)&k0, n * 8, g_stream));
   if (own_v0) CK(cudaMallocAsync((void**)&v0, n * 8, g_stream)); else v0 = (uint64_t*)(uintptr_t)vals;
   CK(cudaMallocAsync((void**)&k1, n * 8, g_stream));
   CK(cudaMallocAsync((void**)&v1, n * 8, g_stream));
   CK(cudaMallocAsync((void**)&mm, 32, g_stream));
   flag = (int*)(mm + 2);
-  k_order_key<<<g, 256, 0, g_stream>>>((const void*)(uintptr_t)keys, key_kind, n, nullptr, k0);
-  if (own_v0) k_widen<<<g, 256, 0, g_stream>>>((const void*)(uintptr_t)vals, v0, val_width, n);
   uint64_t init[4] = {~0ULL, 0ULL, 0ULL, 0ULL};
   CK(cudaMemcpyAsync(mm, init, 32, cudaMemcpyHostToDevice, g_stream));
-  k_minmax_u64<<<g, 256, 0, g_stream>>>(k0, n, mm);
+  k_okey_minmax<<<g, 256, 0, g_stream>>>((const void*)(uintptr_t)keys, key_kind, n, mm, k0);
+  if (own_v0) k_widen<<<g, 256, 0, g_stream>>>((const void*)(uintptr_t)vals, v0, val_width, n);
   unsigned long long hmm[2];
   CK(cudaMemcpyAsync(hmm, mm, 16, cudaMemcpyDeviceToHost, g_stream));
   CK(cudaStreamSynchronize(g_stream));
-  uint64_t diff = hmm[0] ^ hmm[1];
-  int end_bit = diff ? 64 - __builtin_clzll(diff) : 1;  // only bits that vary
-  int begin_bit = end_bit > 32 ? end_bit - 32 : 0;
+  const uint64_t diff = hmm[0] ^ hmm[1];
+  const int vbits = diff ? 64 - __builtin_clzll(diff) : 1;   // bits above vbits are equal in every key
+  const int begin_bit = vbits > 32 ? vbits - 32 : 0;
   cub::DoubleBuffer<uint64_t> dk(k0, k1), dv(v0, v1);
   size_t temp = 0;
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, temp, dk, dv, (int)n, begin_bit, end_bit, g_stream));
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, temp, dk, dv, (int)n, begin_bit, vbits, g_stream));
   void* d_temp = nullptr;
   CK(cudaMallocAsync(&d_temp, temp ? temp : 1, g_stream));
-  CK(cub::DeviceRadixSort::SortPairs(d_temp, temp, dk, dv, (int)n, begin_bit, end_bit, g_stream));
+  CK(cub::DeviceRadixSort::SortPairs(d_temp, temp, dk, dv, (int)n, begin_bit, vbits, g_stream));
   if (begin_bit > 0) {
     uint64_t cap = n / 8 + 1024;
     uint32_t* pos;
@@ -1042,8 +1056,12 @@ int wg_group_finish1(uint64_t keys, int key_kind, uint64_t vals, int val_width, 
     CK(cudaStreamSynchronize(g_stream));
     int hflag = hn > cap;
     if (!hflag && hn) {
+      unsigned* claimed;
+      CK(cudaMallocAsync((void**)&claimed, (n / 32 + 1) * 4, g_stream));
+      CK(cudaMemsetAsync(claimed, 0, (n / 32 + 1) * 4, g_stream));
       k_fix_buckets<<<grid_for(hn, 128), 128, 0, g_stream>>>(dk.Current(), dv.Current(), n, begin_bit, pos, hn, 512,
-                                                             flag);
+                                                             flag, claimed);
+      CK(cudaFreeAsync(claimed, g_stream));
       CK(cudaMemcpyAsync(&hflag, flag, 4, cudaMemcpyDeviceToHost, g_stream));
       CK(cudaStreamSynchronize(g_stream));
     }
@@ -1067,7 +1085,8 @@ int wg_group_finish1(uint64_t keys, int key_kind, uint64_t vals, int val_width, 
   int hK = 0;
   CK(cudaMemcpyAsync(&hK, d_cnt, 4, cudaMemcpyDeviceToHost, g_stream));
   CK(cudaStreamSynchronize(g_stream));
-  k_group_out<<<grid_for((uint64_t)hK + 1, 256), 256, 0, g_stream>>>(starts, (uint64_t)hK, n, dk.Current(), key_kind,
+  k_group_out<<<grid_for((uint64_t)hK + 1, 256), 256, 0, g_stream>>>(starts, (uint64_t)hK, n, dk.Current(), 0ULL,
+                                                                     key_kind,
                                                                      (int64_t*)(uintptr_t)offs_out,
                                                                      (void*)(uintptr_t)ukeys_out);
   if (val_width == 8)
@@ -1081,7 +1100,7 @@ int wg_group_finish1(uint64_t keys, int key_kind, uint64_t vals, int val_width, 
   CK(cudaFreeAsync(starts, g_stream));
   CK(cudaFreeAsync(d_cnt, g_stream));
   CK(cudaFreeAsync(mm, g_stream));
-  if (own_k0) CK(cudaFreeAsync(k0, g_stream));
+  CK(cudaFreeAsync(k0, g_stream));
   if (own_v0) CK(cudaFreeAsync(v0, g_stream));
   CK(cudaFreeAsync(k1, g_stream));
   CK(cudaFreeAsync(v1, g_stream));
