@@ -45,7 +45,7 @@ from weldmill.expr import (
 
 from .irtypes import (
     BOOL, CTYPE, F32, F64, FLOAT_KINDS, I32, I64, INT_KINDS, OPCODE, OPSTRUCT, SIZE, STYPE, Builder, DeviceUnsupported,
-    DictMerger, GroupBuilder, Merger, Scalar, Simd, Struct, Vec, VecBuilder, VecMerger, identity_value,
+    Dict, DictMerger, Function, GroupBuilder, Merger, Scalar, Simd, Struct, Vec, VecBuilder, VecMerger, identity_value,
     internal_identity, leaves,
 )
 
@@ -121,6 +121,16 @@ class VRef:
         self.cols = cols  # C pointer expressions, one per leaf
         self.n = n        # C expression for the length
         self.elem = elem
+
+
+class DRef:
+    """A loop-invariant finalised dictionary visible inside the body: key
+    leaf columns sorted by order_key (builders.py:496-507), value leaf
+    columns (dictmerger) or offsets + value columns (groupbuilder)."""
+    __slots__ = ("kcols", "vcols", "offs", "n", "kty", "vty")
+
+    def __init__(self, kcols, vcols, offs, n, kty, vty):
+        self.kcols, self.vcols, self.offs, self.n, self.kty, self.vty = kcols, vcols, offs, n, kty, vty
 
 
 class SVec:
@@ -513,6 +523,8 @@ class Gen:
             return S(v.n, I64)
         if isinstance(v, SVec):
             return S(c_literal(I64, len(v.items)), I64)
+        if isinstance(v, DRef):
+            return S(v.n, I64)
         raise DeviceUnsupported("len() of this value inside a loop body")
 
     def _load_elem(self, vref, idx_c):
@@ -548,7 +560,54 @@ class Gen:
             self.emit(f"default: wg_raise(p.err, WG_ERR_LOOKUP_OOB, {idx.c});")
             self.emit("}")
             return out
-        raise DeviceUnsupported("lookup into this collection inside a loop body (dict probes are not lowered yet)")
+        if isinstance(coll, DRef):
+            return self._dict_probe(coll, idx)
+        raise DeviceUnsupported("lookup into this collection inside a loop body")
+
+    def _dict_probe(self, d, key):
+        """Hash-join probe (run.py:702-712): lower_bound over the entries'
+        order-key tuples (they are sorted by it), KeyNotFound on a miss.
+        Float keys compare through the canonical order key (-0.0 == 0.0,
+        NaN after +inf), matching Python dict equality for the reference's
+        key domain."""
+        kks = leaves(d.kty)
+        kv = _flat(key)
+        oks = [self.let(I64, f"(i64)wg_okey<{CTYPE[k]}>({v.c})") for v, k in zip(kv, kks)]
+        lo, hi, pos = self.tmp("lo"), self.tmp("hi"), self.tmp("pos")
+        self.emit(f"i64 {lo} = 0, {hi} = {d.n};")
+        self.emit(f"while ({lo} < {hi}) {{")
+        self.ind += 1
+        mid = self.tmp("m")
+        self.emit(f"const i64 {mid} = ({lo} + {hi}) >> 1;")
+        # entry < key  (lexicographic over the leaves' order keys)
+        conds = []
+        for l, (col, k) in enumerate(zip(d.kcols, kks)):
+            e_ok = f"(u64)wg_okey<{CTYPE[k]}>(({CTYPE[k]}){col}[{mid}])"
+            conds.append((e_ok, f"(u64){oks[l].c}"))
+        less = self.tmp("lt")
+        self.emit(f"bool {less} = false;")
+        expr = ""
+        for l in reversed(range(len(conds))):
+            a, b = conds[l]
+            expr = f"({a} < {b})" if not expr else f"(({a} < {b}) || (({a} == {b}) && {expr}))"
+        self.emit(f"{less} = {expr};")
+        self.emit(f"if ({less}) {lo} = {mid} + 1; else {hi} = {mid};")
+        self.ind -= 1
+        self.emit("}")
+        found = " && ".join(f"((u64)wg_okey<{CTYPE[k]}>(({CTYPE[k]}){col}[{lo}]) == (u64){ok.c})"
+                            for col, k, ok in zip(d.kcols, kks, oks))
+        self.emit(f"const bool {pos} = ({lo} < {d.n}) && {found};")
+        self.emit(f"if (!{pos}) wg_raise(p.err, WG_ERR_KEY_NOT_FOUND, 0);")
+        j = self.let(I64, f"({pos} ? {lo} : (i64)0)")
+        if d.offs is not None:
+            # groupbuilder result: the key's value vector is a slice
+            b0 = self.let(I64, f"({pos} ? {d.offs}[{j.c}] : (i64)0)")
+            b1 = self.let(I64, f"({pos} ? {d.offs}[{j.c} + 1] : (i64)0)")
+            return VRef([f"({c} + {b0.c})" for c in d.vcols], f"({b1.c} - {b0.c})", d.vty.elem)
+        vks = leaves(d.vty)
+        vals = [self.let(k, f"({pos} ? ({col}[{j.c}] != 0) : false)" if k == BOOL else
+                         f"({pos} ? {col}[{j.c}] : ({CTYPE[k]})0)") for col, k in zip(d.vcols, vks)]
+        return _shape(d.vty, vals)
 
     # -- builders ------------------------------------------------------------
     def ex_NewBuilder(self, e, env):
@@ -2238,6 +2297,19 @@ def _capture_val(g: Gen, name, ty, val):
                     for l, k in enumerate(ks)]
             nn = g.param(f"c_{tag}_n", "i64", ("caplen", name) + tuple(path))
             return VRef(cols, nn, t.elem)
+        if isinstance(t, Dict):
+            kcols = [g.param(f"c_{tag}_k{l}", f"const {STYPE[k]}*", ("capdk", name) + tuple(path) + (l,))
+                     for l, k in enumerate(leaves(t.key))]
+            nn = g.param(f"c_{tag}_dn", "i64", ("capdn", name) + tuple(path))
+            if isinstance(t.value, Vec):
+                offs = g.param(f"c_{tag}_off", "const i64*", ("capdoff", name) + tuple(path))
+                vcols = [g.param(f"c_{tag}_v{l}", f"const {STYPE[k]}*", ("capdv", name) + tuple(path) + (l,))
+                         for l, k in enumerate(leaves(t.value.elem))]
+            else:
+                offs = None
+                vcols = [g.param(f"c_{tag}_v{l}", f"const {STYPE[k]}*", ("capdv", name) + tuple(path) + (l,))
+                         for l, k in enumerate(leaves(t.value))]
+            return DRef(kcols, vcols, offs, nn, t.key, t.value)
         if isinstance(t, Builder):
             return None
         raise DeviceUnsupported(f"captured value of type {t}")

@@ -495,6 +495,22 @@ __device__ __forceinline__ i64 wg_ht_findN(u64* table, int slot_words, u64 mask,
   return -1;
 }
 
+// order_key (builders.py:496-507) of one key leaf as an unsigned 64-bit
+// integer: signed ints ordered, floats in IEEE total order with -0.0 == 0.0
+// and every NaN after +inf.  Dictionary probes compare these.
+template <typename T> __device__ __forceinline__ u64 wg_okey(T v);
+template <> __device__ __forceinline__ u64 wg_okey<bool>(bool v) { return v ? 1ULL : 0ULL; }
+template <> __device__ __forceinline__ u64 wg_okey<i32>(i32 v) { return (u64)(i64)v ^ 0x8000000000000000ULL; }
+template <> __device__ __forceinline__ u64 wg_okey<i64>(i64 v) { return (u64)v ^ 0x8000000000000000ULL; }
+template <> __device__ __forceinline__ u64 wg_okey<double>(double v) {
+  if (v != v) return 0xffffffffffffffffULL;
+  if (v == 0.0) v = 0.0;
+  const u64 b = (u64)__double_as_longlong(v);
+  const u64 k = (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+  return k == 0xffffffffffffffffULL ? 0xfffffffffffffffeULL : k;
+}
+template <> __device__ __forceinline__ u64 wg_okey<float>(float v) { return wg_okey<double>((double)v); }
+
 // Canonical key words.  -0.0 and 0.0 are one dictionary key in the
 // reference (Python dict semantics); they map to the same word here.
 __device__ __forceinline__ u64 wg_key_f64(double v) { return v == 0.0 ? 0ULL : (u64)__double_as_longlong(v); }

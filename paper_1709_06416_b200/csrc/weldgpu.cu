@@ -480,6 +480,11 @@ __global__ void k_okey_minmax(const void* keys, int kind, uint64_t n, unsigned l
   if ((threadIdx.x & 31) == 0) { atomicMin(mm, lo); atomicMax(mm + 1, hi); }
 }
 
+// order keys relative to the minimum (same order, fewer varying bits)
+__global__ void k_sub_min(uint64_t* ok, uint64_t n, uint64_t kmin) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    ok[i] -= kmin;
+}
 }  // namespace
 
 // ===========================================================================
@@ -1034,8 +1039,17 @@ int wg_group_finish1(uint64_t keys, int key_kind, uint64_t vals, int val_width, 
   unsigned long long hmm[2];
   CK(cudaMemcpyAsync(hmm, mm, 16, cudaMemcpyDeviceToHost, g_stream));
   CK(cudaStreamSynchronize(g_stream));
-  const uint64_t diff = hmm[0] ^ hmm[1];
-  const int vbits = diff ? 64 - __builtin_clzll(diff) : 1;   // bits above vbits are equal in every key
+  const uint64_t diff = hmm[0] ^ hmm[1], span = hmm[1] - hmm[0];
+  int vbits = diff ? 64 - __builtin_clzll(diff) : 1;   // bits above vbits are equal in every key
+  const int rbits = span ? 64 - __builtin_clzll(span) : 1;
+  uint64_t kbase = 0;
+  if (rbits + 8 <= vbits) {
+    // a narrow range straddling a high bit (e.g. keys around 0): sort
+    // (okey - min) -- one extra pass, several radix passes saved
+    k_sub_min<<<g, 256, 0, g_stream>>>(k0, n, hmm[0]);
+    kbase = hmm[0];
+    vbits = rbits;
+  }
   const int begin_bit = vbits > 32 ? vbits - 32 : 0;
   cub::DoubleBuffer<uint64_t> dk(k0, k1), dv(v0, v1);
   size_t temp = 0;
@@ -1065,8 +1079,17 @@ int wg_group_finish1(uint64_t keys, int key_kind, uint64_t vals, int val_width, 
       CK(cudaMemcpyAsync(&hflag, flag, 4, cudaMemcpyDeviceToHost, g_stream));
       CK(cudaStreamSynchronize(g_stream));
     }
-    if (hflag)  // skewed buckets: finish with a full stable sort of the low bits
-      CK(cub::DeviceRadixSort::SortPairs(d_temp, temp, dk, dv, (int)n, 0, begin_bit, g_stream));
+    if (hflag) {
+      // skewed buckets: a full stable sort of every varying bit (sorting
+      // only the low bits now would undo the order of the high ones; ties
+      // keep the current -- input -- order of each key's rows)
+      size_t temp_full = 0;
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, temp_full, dk, dv, (int)n, 0, vbits, g_stream));
+      void* d_full = nullptr;
+      CK(cudaMallocAsync(&d_full, temp_full ? temp_full : 1, g_stream));
+      CK(cub::DeviceRadixSort::SortPairs(d_full, temp_full, dk, dv, (int)n, 0, vbits, g_stream));
+      CK(cudaFreeAsync(d_full, g_stream));
+    }
     CK(cudaFreeAsync(pos, g_stream));
   }
   uint8_t* heads;
@@ -1085,7 +1108,7 @@ int wg_group_finish1(uint64_t keys, int key_kind, uint64_t vals, int val_width, 
   int hK = 0;
   CK(cudaMemcpyAsync(&hK, d_cnt, 4, cudaMemcpyDeviceToHost, g_stream));
   CK(cudaStreamSynchronize(g_stream));
-  k_group_out<<<grid_for((uint64_t)hK + 1, 256), 256, 0, g_stream>>>(starts, (uint64_t)hK, n, dk.Current(), 0ULL,
+  k_group_out<<<grid_for((uint64_t)hK + 1, 256), 256, 0, g_stream>>>(starts, (uint64_t)hK, n, dk.Current(), kbase,
                                                                      key_kind,
                                                                      (int64_t*)(uintptr_t)offs_out,
                                                                      (void*)(uintptr_t)ukeys_out);

@@ -110,6 +110,7 @@ _fv_cache = {}
 
 class Ctx:
     def __init__(self, cfg: EngineConfig, externs, idx0=0):
+        self._host_dicts = {}
         self.cfg = cfg
         self.externs = externs or {}
         self.traversals = 0
@@ -681,6 +682,23 @@ class Ctx:
                    ty=Builder(st.kind))
         self.run_loop(loop, {"__rows": dv, "__b": st}, count_traversal=False)
 
+    def _dict_dev(self, v, ty, path):
+        """A dictionary captured by a loop body, as device columns sorted by
+        order_key (DDict / DGroups; a host dict payload is uploaded once)."""
+        if isinstance(v, (DDict, DGroups)):
+            return v
+        if isinstance(v, dict):
+            t = ty
+            for q in path:
+                t = t.fields[q]
+            cached = self._host_dicts.get(id(v))
+            if cached is not None and cached[0] is v:
+                return cached[1]
+            d = _host_dict_to_device(v, t)
+            self._host_dicts[id(v)] = (v, d)
+            return d
+        raise EvalError(f"captured value {type(v).__name__} is not a dictionary")
+
     def _acct_append(self, st, rows):
         if getattr(st, "hint", None) is None:
             nbytes = rows * sum(SIZE[k] for k in st.kinds)
@@ -744,6 +762,20 @@ class Ctx:
             return windows[key[1]][0]
         if k0 == "itstride":
             return windows[key[1]][1]
+        if k0 in ("capdk", "capdv", "capdn", "capdoff"):
+            name = key[1]
+            v = captures[name][1]
+            path = key[2:] if k0 in ("capdn", "capdoff") else key[2:-1]
+            for q in path:
+                v = v[q]
+            d = self._dict_dev(v, captures[name][0], path)
+            if k0 == "capdn":
+                return d.n
+            if k0 == "capdoff":
+                return d.offsets.ptr
+            if k0 == "capdk":
+                return d.keys.cols[key[-1]].ptr
+            return d.vals.cols[key[-1]].ptr
         if k0 in ("cap", "capcol", "caplen"):
             name = key[1]
             v = captures[name][1]
@@ -814,6 +846,27 @@ class Ctx:
                 if what == "oval":
                     return st.over[1][key[3]].ptr
         raise EvalError(f"internal: no value for kernel parameter {key}")
+
+
+def _host_dict_to_device(v, t):
+    """Reference dict payload -> DDict / DGroups with entries in order_key
+    order (builders.py:496-507)."""
+    from weldmill.engine.builders import order_key
+    from .columns import ListLayout, to_device
+    items = sorted(v.items(), key=lambda kv: order_key(kv[0]))
+    keys = to_device(Vec(t.key), [k for k, _ in items])
+    if isinstance(t.value, Vec):
+        flat, offs = [], [0]
+        for _, vv in items:
+            flat.extend(vv)
+            offs.append(len(flat))
+        vals = to_device(t.value, flat)
+        oc = Col.alloc(I64, len(offs))
+        arr = np.asarray(offs, dtype=np.int64)
+        rt.h2d(oc.ptr, arr.ctypes.data, arr.nbytes)
+        return DGroups(Dict(t.key, t.value), keys, oc, vals)
+    vals = to_device(Vec(t.value), [x for _, x in items])
+    return DDict(Dict(t.key, t.value), keys, vals)
 
 
 def _layout(t, cols):

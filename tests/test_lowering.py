@@ -121,3 +121,20 @@ def test_order_key_expression_matches_python():
     oks = [codegen.okey_py([I32, I32], w) for w in words]
     assert [p for _, p in sorted(zip(oks, pairs))] == sorted(pairs)
     assert codegen.rpart_ok([I64]) and codegen.rpart_ok([I32, I32]) and codegen.rpart_ok([BOOL])
+
+
+def test_dictionary_probes_lower_and_compile():
+    """lookup(d, k) in a loop body lowers to a binary search over the
+    dictionary's order-key-sorted key columns and compiles for sm_100a."""
+    from helpers import load_golden
+    from paper_1709_06416_b200 import codegen, runtime
+    seen = set()
+    for c in load_golden("lookup.json")["cases"]:
+        if c["name"] in seen:
+            continue
+        seen.add(c["name"])
+        plans = codegen.static_plans(_tree(c["source"], c["inputs"], "O3"))
+        probe = [p for p in plans if "WG_ERR_KEY_NOT_FOUND" in p.source]
+        assert probe, c["name"]
+        for p in probe:
+            assert runtime.compile_check(p.source) > 0
