@@ -1,6 +1,5 @@
-mkdir -p gpurun_out/t2
-for kp in 0 1; do
-WELDGPU_KPOOL=$kp timeout 600 python bench.py --workload blackscholes --steps 10 --warmup 3 --no-cpu --no-e2e 2>&1 | tail -1 > gpurun_out/t2/bs_kp$kp.log
-done
-WELDGPU_KPOOL=1 WELDGPU_MINBLOCKS=3 timeout 600 python bench.py --workload blackscholes --steps 10 --warmup 3 --no-cpu --no-e2e 2>&1 | tail -1 > gpurun_out/t2/bs_kp1_mb3.log
-WELDGPU_KPOOL=1 WELDGPU_MINBLOCKS=4 timeout 600 python bench.py --workload blackscholes --steps 10 --warmup 3 --no-cpu --no-e2e 2>&1 | tail -1 > gpurun_out/t2/bs_kp1_mb4.log
+mkdir -p gpurun_out/prof
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:wg_loop -s 2 -c 1 -o gpurun_out/prof/full_dict \
+   python bench.py --workload dict --steps 1 --warmup 3 --no-cpu --no-e2e --no-kernel-timing > gpurun_out/prof/ncu_dict.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:wg_dagg -s 1 -c 1 -o gpurun_out/prof/full_dict_dagg \
+   python bench.py --workload dict --steps 1 --warmup 3 --no-cpu --no-e2e --no-kernel-timing > /dev/null 2>&1

@@ -1,15 +1,21 @@
-# Round profile set: headline bench line, launch list of the default bench,
-# and one ncu --set full capture of each workload's loop kernel.
+# Round profile set: GPU tests, headline bench line, launch list of the
+# default bench and of one step per workload, one ncu --set full capture of
+# each workload's loop kernel, and a bench line per workload.
 mkdir -p gpurun_out/prof
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem --format=csv > gpurun_out/prof/gpu.txt
+timeout 1500 python -m pytest tests -q -m gpu 2>&1 | tail -5 > gpurun_out/prof/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/prof/smoke.log 2>&1
 timeout 900 python bench.py 2>&1 | tail -1 > gpurun_out/prof/bench_default.json
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches_default.csv \
   python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e --no-kernel-timing > /dev/null 2>&1
-for w in blackscholes q6 q1 dict group hist; do
+for w in blackscholes q6 q1 dict group hist filter map; do
   extra=""
   [ $w = q6 ] && extra="--n 600000000"
   skip=3; [ $w = dict ] && skip=8
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:wg_loop -s $skip -c 1 -o gpurun_out/prof/full_$w \
      python bench.py --workload $w --steps 1 --warmup 3 --no-cpu --no-e2e --no-kernel-timing $extra > gpurun_out/prof/ncu_$w.log 2>&1
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches_$w.csv \
+     python bench.py --workload $w --steps 1 --warmup 3 --no-cpu --no-e2e --no-kernel-timing $extra > /dev/null 2>&1
   timeout 600 python bench.py --workload $w --steps 10 --warmup 3 --no-cpu $extra 2>&1 | tail -1 > gpurun_out/prof/bench_$w.json
 done
+timeout 600 python bench.py --workload q6 --steps 20 --warmup 5 --no-cpu 2>&1 | tail -1 > gpurun_out/prof/bench_q6_1M.json

@@ -127,6 +127,38 @@ if os.path.exists(ll):
     with open(os.path.join(OUT, f"launches_default_{RND}.csv"), "w") as f:
         f.write(open(ll).read())
 
+# one step of each workload: every launch of the last evaluate (ncu launch list)
+step_lists = {}
+for ll in sorted(glob.glob(os.path.join(SRC, "launches_*.csv"))):
+    w = os.path.basename(ll)[len("launches_"):-len(".csv")]
+    if w == "default":
+        continue
+    rows = [r for r in csv.reader(open(ll)) if len(r) > 10]
+    if len(rows) < 2:
+        continue
+    h = rows[0]
+    ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    ks = [(r[ki], to_ms(r[vi], r[ui])) for r in rows[1:]]
+    starts = [i for i, (k, _) in enumerate(ks) if k.startswith("wg_loop") and (i == 0 or not ks[i - 1][0].startswith("wg_loop"))]
+    last = ks[starts[-1]:] if starts else ks
+    first = next((i for i, (k, _) in enumerate(ks) if k.startswith("wg_loop")), 0)
+    if all(k.startswith("wg_loop") for k, _ in ks[first:]):
+        last = ks[-1:]                  # one loop kernel per evaluate (the rest is input generation)
+    step_lists[w] = last
+    with open(os.path.join(OUT, f"launches_{w}_{RND}.csv"), "w") as f:
+        f.write(open(ll).read())
+if step_lists:
+    lines += ["", "## One evaluate() step per workload (ncu launch list, cold-cache, serialised)", ""]
+    for w, last in step_lists.items():
+        tot = sum(t for _, t in last)
+        lines += [f"### {w}: {len(last)} launches, {tot:.3f} ms", "", "| kernel | ms | share |", "|---|---|---|"]
+        for k, t in last:
+            lines.append(f"| `{k[:70]}` | {t:.3f} | {100 * t / tot:.1f}% |")
+        lines.append("")
+summary["step_launch_lists"] = {w: [[k[:70], round(t, 4)] for k, t in last] for w, last in step_lists.items()}
+with open(os.path.join(OUT, f"ncu_summary_{RND}.json"), "w") as f:
+    json.dump(summary, f, indent=1)
+
 with open(os.path.join(OUT, f"ncu_summary_{RND}.md"), "w") as f:
     f.write("\n".join(lines) + "\n")
 print("\n".join(lines))
