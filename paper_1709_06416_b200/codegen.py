@@ -663,7 +663,12 @@ class Gen:
             return bval
         if all(isinstance(d, VRef) for d in datas):
             if self._counts_outer(lam.body, env, {pb: bval}):
-                raise DeviceUnsupported("appends inside a data-dependent nested loop (two-pass sizing not lowered)")
+                # data-dependent append counts: fine for scan-mode appenders
+                # (counted in phase A, written in phase B, sized by a pre-pass)
+                cnt_ = merge_counts(lam.body, {**_benv_from(env), pb: bval})
+                if any(isinstance(b, BSpec) and isinstance(b.kind, (VecBuilder, GroupBuilder)) and mx > 0
+                       and b.mode != "scan" for b, (mn, mx) in cnt_.items()):
+                    raise DeviceUnsupported("appends inside a data-dependent nested loop into a non-scan builder")
             cnt = self.tmp("n")
             starts, strides = [], []
             for k, (it, d) in enumerate(zip(e.iters, datas)):
@@ -737,7 +742,7 @@ class Gen:
                 self.emit(f"c{b.bid} += 1;")
                 return
             if b.mode == "scan":
-                if self.phase == "A":
+                if self.phase in ("A", "count"):
                     self.emit(f"cnt{b.bid} += 1;")
                 else:
                     for f, (x, k) in enumerate(zip(vals, ks)):
@@ -1043,7 +1048,8 @@ def choose_items(iters):
     return max(2, min(8, p))
 
 
-def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_loop", items=None) -> KernelPlan:
+def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_loop", items=None,
+             count_only=False) -> KernelPlan:
     g = Gen(loop, iters, bstruct, captures, externs, strategy)
     lam = loop.func
     if not isinstance(lam, Lambda):
@@ -1111,7 +1117,12 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
             elif mx < INF:
                 b.mode, b.k = "scan", int(mx)
             else:
-                raise DeviceUnsupported("appends inside a data-dependent nested loop (two-pass sizing not lowered)")
+                # appends inside a data-dependent nested loop (flatmap): the
+                # scan schedule counts them in phase A and stores them in
+                # phase B; the executor sizes the output with a count-only
+                # pre-pass of the same body (generate(count_only=True))
+                b.mode, b.k = "scan", None
+                b.extra["unbounded"] = True
 
     scan_bs = [b for b in g.bspecs if b.mode == "scan"]
     if scan_bs and not (items or ITEMS_OVERRIDE):
@@ -1126,7 +1137,7 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
     staged_bytes = 0
     for b in scan_bs:
         b.extra["staged"] = False
-    if scan_bs and STAGE_SCAN:
+    if scan_bs and STAGE_SCAN and all(b.k is not None for b in scan_bs):
         need = sum(BLOCK * ITEMS * b.k * SIZE[k] for b in scan_bs for k in b.extra["kinds"])
         if need <= 40 * 1024:
             for b in scan_bs:
@@ -1174,6 +1185,9 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
         e[pi] = S("i", I64)
         e[pb] = bval
         return e
+
+    if count_only:
+        return _count_plan(g, lam, body_env, loads, iters, ITEMS, BLOCK, scan_bs, name)
 
     g.lines = []
     g.ind = 3
@@ -1593,6 +1607,61 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
                       smem=dyn_smem, builders=g.bspecs, scan_bids=[b.bid for b in scan_bs],
                       merger_bids=[b.bid for b in merger_bs])
     plan.pipe_stage_bytes = pipe_stage_bytes if pipe else 0
+    return plan
+
+
+def _count_plan(g, lam, body_env, loads, iters, ITEMS, BLOCK, scan_bs, name):
+    """Count-only pre-pass for appenders with data-dependent append counts
+    (flatmap): runs the body with every merge disabled except the scan
+    appenders' counters and adds the totals into one word per builder."""
+    g.lines = []
+    g.ind = 3
+    g.phase = "count"
+    g.ex(lam.body, body_env())
+    body = g.lines
+    unb = [b for b in scan_bs if b.extra.get("unbounded")]
+    for b in unb:
+        g.param(f"ct{b.bid}_total", "unsigned long long*", ("b", b.bid, "ctotal"))
+    src = ['#include "weld_device.cuh"', f"#define BLOCK {BLOCK}", f"#define ITEMS {ITEMS}",
+           "#define TILE (BLOCK * ITEMS)", "struct Params {"]
+    src += [f"  {p_.ctype} {p_.name};" for p_ in g.params]
+    src += ["};", f'extern "C" __global__ void __launch_bounds__(BLOCK) {name}(const Params p) {{',
+            "  const i64 n = p.n;", "  const i64 ntiles = (n + TILE - 1) / TILE;"]
+    src += [f"  i64 tc{b.bid} = 0;" for b in unb]
+    src.append("  for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {")
+    for (arr, st, kk, per, k, l, col) in loads:
+        cnt = f"ITEMS * {per}" if per > 1 else "ITEMS"
+        src.append(f"    alignas(16) {st} {arr}[{cnt}];")
+    src.append("    { const i64 lt0_ = tile * TILE + (i64)threadIdx.x * ITEMS;")
+    for (arr, st, kk, per, k, l, col) in loads:
+        cnt = f"ITEMS * {per}" if per > 1 else "ITEMS"
+        if iters[k].strided:
+            src.append(f"      for (int q = 0; q < ITEMS; ++q) {{ const i64 li_ = lt0_ + q; "
+                       f"{arr}[q] = (li_ < n) ? {col}[p.it{k}_start + li_ * p.it{k}_stride] : ({st})0; }}")
+        else:
+            src.append(f"      for (int q = 0; q < {cnt}; ++q) {{ const i64 e_ = lt0_ * {per} + q; "
+                       f"{arr}[q] = (e_ < n * {per}) ? {col}[e_] : ({st})0; }}")
+    src.append("    }")
+    src.append("    const i64 t0 = tile * TILE + (i64)threadIdx.x * ITEMS;")
+    src += [f"    i64 cnt{b.bid} = 0;" for b in scan_bs]
+    src.append("#pragma unroll")
+    src.append("    for (int j = 0; j < ITEMS; ++j) {")
+    src.append("      const i64 li = t0 + j;")
+    src.append("      if (li < n) {")
+    src.append("        const i64 i = p.idx0 + li;")
+    src.extend(body)
+    src.append("      }")
+    src.append("    }")
+    src += [f"    tc{b.bid} += cnt{b.bid};" for b in unb]
+    src.append("  }")
+    for b in unb:
+        src.append(f"  {{ i64 c_ = tc{b.bid};")
+        src.append("    for (int d = 16; d > 0; d >>= 1) c_ += __shfl_xor_sync(0xffffffffu, c_, d);")
+        src.append(f"    if ((threadIdx.x & 31) == 0 && c_) atomicAdd(p.ct{b.bid}_total, (unsigned long long)c_); }}")
+    src.append("}")
+    plan = KernelPlan(source="\n".join(src) + "\n", name=name, params=g.params, schedule="count", items=ITEMS,
+                      block=BLOCK, smem=0, builders=g.bspecs, scan_bids=[b.bid for b in scan_bs], merger_bids=[])
+    plan.pipe_stage_bytes = 0
     return plan
 
 
@@ -2325,7 +2394,8 @@ def _capture_val(g: Gen, name, ty, val):
 # suite to prove every loop of a program lowers and compiles for sm_100a.
 
 
-def static_plans(expr, env_types=None, externs=(), smem=True, lowcard=False, part=False, rpart=False):
+def static_plans(expr, env_types=None, externs=(), smem=True, lowcard=False, part=False, rpart=False,
+                 count_only=False):
     """Yield a KernelPlan per ``for`` loop in a typed program, deriving the
     iteration, builder and capture specs from types alone."""
     from weldmill.expr import walk, free_variables as _fv
@@ -2388,5 +2458,12 @@ def static_plans(expr, env_types=None, externs=(), smem=True, lowcard=False, par
             if isinstance(ty, Function):
                 continue
             caps[name] = (ty, None)
-        plans.append(generate(node, iters, bstruct, caps, ext, "local"))
+        plan = generate(node, iters, bstruct, caps, ext, "local")
+        if count_only:
+            # the count-only pre-pass of flatmap-shaped loops (fresh builder specs)
+            if any(b.extra.get("unbounded") for b in plan.builders):
+                counter[0] = 0
+                plans.append(generate(node, iters, mk(node.builders.ty), caps, ext, "local", count_only=True))
+            continue
+        plans.append(plan)
     return plans

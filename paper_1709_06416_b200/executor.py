@@ -533,8 +533,23 @@ class Ctx:
                     _plan_cache.clear()
                 _plan_cache[key] = cached
         plan, kern = cached[0], cached[1]
+        sizes = None
+        if any(b.extra.get("unbounded") for b in plan.builders):
+            # flatmap: appends inside data-dependent nested loops -- size the
+            # output with a count-only pre-pass of the same body
+            ckey = key + ("count",)
+            with _plan_lock:
+                cc = _plan_cache.get(ckey)
+            if cc is None:
+                cbs, _ = _bspecs(builders, strategy, count, loop_id=id(e))
+                cplan = generate(e if lam is e.func else _with_func(e, lam), specs, cbs, captures, self.externs,
+                                 strategy, count_only=True)
+                cc = (cplan, rt.get_kernel(cplan.source, cplan.name))
+                with _plan_lock:
+                    _plan_cache[ckey] = cc
+            sizes = self._count_pass(cc[0], cc[1], count, datas, windows, bmap, captures)
         try:
-            self.launch(plan, kern, count, datas, windows, builders, bmap, captures)
+            self.launch(plan, kern, count, datas, windows, builders, bmap, captures, sizes=sizes)
         except _RpartFallback:
             # skewed keys overflowed a partition: forget the merges and run
             # the loop again through the hash-table dictmerger
@@ -545,7 +560,26 @@ class Ctx:
             return self.run_loop(e, env, count_traversal=False)
         return builders
 
-    def launch(self, plan, kern, count, datas, windows, builders, bmap, captures):
+    def _count_pass(self, plan, kern, count, datas, windows, bmap, captures):
+        """Launch the count-only kernel; returns {builder id: appends}."""
+        tile = plan.block * plan.items
+        ntiles = (count + tile - 1) // tile
+        grid = max(1, min(ntiles, rt.sm_count() * kern.blocks_per_sm(plan.block, 0)))
+        unb = [b for b in plan.builders if b.extra.get("unbounded")]
+        tot = rt.alloc(8 * len(unb))
+        rt.memset(tot.ptr, 0, 8 * len(unb))
+        res = {b.bid: ("ctotal", tot.ptr + 8 * q) for q, b in enumerate(unb)}
+        vals = {p.name: self._param_value(p.key, count, datas, windows, bmap, res, captures, grid, None)
+                for p in plan.params}
+        kern.launch(grid, plan.block, b"".join(_pack(p.ctype, vals[p.name]) for p in plan.params), 0)
+        self.launches += 1
+        self.dirty = True
+        self.check_device()
+        arr = np.zeros(len(unb), dtype=np.int64)
+        rt.d2h(arr.ctypes.data, tot.ptr, arr.nbytes)
+        return {b.bid: int(x) for b, x in zip(unb, arr)}
+
+    def launch(self, plan, kern, count, datas, windows, builders, bmap, captures, sizes=None):
         items = plan.items
         tile = plan.block * items
         ntiles = (count + tile - 1) // tile
@@ -574,11 +608,12 @@ class Ctx:
                     res[b.bid] = seg
                     self._acct_append(st, count * b.k)
                 elif b.mode == "scan":
-                    seg = st.new_segment(count * b.k, False)
+                    cap = sizes[b.bid] if b.k is None else count * b.k
+                    seg = st.new_segment(cap, False)
                     status = rt.alloc(8 * max(ntiles, 1))
                     rt.memset(status.ptr, 0, 8 * max(ntiles, 1))
                     res[b.bid] = (seg, status)
-                    self._acct_append(st, count * b.k)
+                    self._acct_append(st, cap)
             elif isinstance(b.kind, DictMerger) and b.extra.get("rpart"):
                 st.ensure(1)            # (unused) table keeps the kernel's table parameters valid
                 st.hint_key = (plan.key_id, b.bid)
@@ -802,6 +837,8 @@ class Ctx:
                     return st.take_init_flag()
             if isinstance(st, (AppenderDev, GroupDev)):
                 r = res[bid]
+                if what == "ctotal":
+                    return r[1]
                 if what == "col":
                     seg = r if not isinstance(r, tuple) else r[0]
                     return seg.cols[key[3]].ptr

@@ -138,3 +138,24 @@ def test_dictionary_probes_lower_and_compile():
         assert probe, c["name"]
         for p in probe:
             assert runtime.compile_check(p.source) > 0
+
+
+def test_flatmap_loops_lower_and_compile():
+    """Appends inside data-dependent nested loops lower to the scan schedule
+    (unbounded appends, unstaged stores) plus a count-only pre-pass kernel;
+    both compile for sm_100a."""
+    from helpers import load_golden
+    from paper_1709_06416_b200 import codegen, runtime
+    seen = set()
+    for c in load_golden("flatmap.json")["cases"]:
+        if c["name"] in seen:
+            continue
+        seen.add(c["name"])
+        t = _tree(c["source"], c["inputs"], "O3")
+        plans = codegen.static_plans(t)
+        scan = [p for p in plans if p.schedule == "scan" and any(b.extra.get("unbounded") for b in p.builders)]
+        assert scan, c["name"]
+        counts = codegen.static_plans(t, count_only=True)
+        assert counts and all(p.schedule == "count" for p in counts)
+        for p in scan + counts:
+            assert runtime.compile_check(p.source) > 0
