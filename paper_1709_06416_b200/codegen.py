@@ -517,6 +517,35 @@ class Gen:
         self.emit("}")
         return out
 
+    def ex_Iterate(self, e, env):
+        """iterate(init, update) inside a loop body (run.py:668-686): a
+        device while-loop; IterationLimit after EngineConfig.max_iterations
+        steps without the continue flag dropping."""
+        lam = e.update
+        if not isinstance(lam, Lambda) or len(lam.params) != 1:
+            raise DeviceUnsupported("iterate update must be a one-parameter lambda literal")
+        init = self.ex(e.init, env)
+        state = self._declare_like(None, e.ty)
+        self._assign(state, init)
+        limit = self.param("maxit", "i64", ("maxit",))
+        steps = self.tmp("it")
+        self.emit(f"for (i64 {steps} = 1;; ++{steps}) {{")
+        self.ind += 1
+        env2 = dict(env)
+        env2[lam.params[0].name] = state
+        r = self.ex(lam.body, env2)
+        if not isinstance(r, T) or len(r.items) != 2:
+            raise DeviceUnsupported("iterate update must return {state, continue}")
+        nxt = self._declare_like(None, e.ty)
+        self._assign(nxt, r.items[0])
+        go = self.let(BOOL, r.items[1].c)
+        self._assign(state, nxt)
+        self.emit(f"if (!{go.c}) break;")
+        self.emit(f"if ({steps} >= {limit}) {{ wg_raise(p.err, WG_ERR_ITER_LIMIT, {steps}); break; }}")
+        self.ind -= 1
+        self.emit("}")
+        return state
+
     def ex_Len(self, e, env):
         v = self.ex(e.coll, env)
         if isinstance(v, VRef):

@@ -40,6 +40,7 @@ enum {
   WG_ERR_KEY_NOT_FOUND = 4, // KeyNotFound         run.py:704-710
   WG_ERR_INTERNAL = 5,
   WG_ERR_REMZERO = 6,       // DivideByZero (remainder)
+  WG_ERR_ITER_LIMIT = 7,    // IterationLimit      run.py:680-684
 };
 
 __device__ __forceinline__ void wg_raise(i64* err, i64 code, i64 info) {

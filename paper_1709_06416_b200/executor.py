@@ -44,10 +44,11 @@ class DeviceUnsupported(EvalError, _DU):
 
 
 ERR_CLASSES = {1: DivideByZero, 2: IndexOutOfBounds, 3: IndexOutOfBounds, 4: KeyNotFound, 5: EvalError,
-               6: DivideByZero}
+               6: DivideByZero, 7: IterationLimit}
 ERR_TEXT = {1: "integer division by zero", 2: "lookup index {info} outside vector",
             3: "vecmerger index {info} out of range", 4: "key not in dictionary",
-            5: "internal device error ({info})", 6: "integer remainder by zero"}
+            5: "internal device error ({info})", 6: "integer remainder by zero",
+            7: "iterate exceeded the iteration limit ({info} iterations)"}
 
 
 class HostVec:
@@ -780,6 +781,8 @@ class Ctx:
             return rt.error_ptr()
         if k0 == "ticket":
             return self.ticket()
+        if k0 == "maxit":
+            return self.cfg.max_iterations
         if k0 == "tilectr":
             return tilectr.ptr
         if k0 == "pipe_stages":

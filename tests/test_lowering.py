@@ -159,3 +159,18 @@ def test_flatmap_loops_lower_and_compile():
         assert counts and all(p.schedule == "count" for p in counts)
         for p in scan + counts:
             assert runtime.compile_check(p.source) > 0
+
+
+def test_iterate_in_loop_bodies_lowers_and_compiles():
+    from helpers import load_golden
+    from paper_1709_06416_b200 import codegen, runtime
+    seen = set()
+    for c in load_golden("iterate.json")["cases"]:
+        if c["name"] in seen:
+            continue
+        seen.add(c["name"])
+        plans = codegen.static_plans(_tree(c["source"], c["inputs"], "O3"))
+        body = [p for p in plans if "WG_ERR_ITER_LIMIT" in p.source]
+        assert body, c["name"]
+        for p in body:
+            assert runtime.compile_check(p.source) > 0
