@@ -90,6 +90,9 @@ int wg_dict_finish_small(uint64_t table, uint64_t nslots, int slot_words, int mo
                          uint64_t* count_out);
 int wg_order_key(uint64_t src, int kind, uint64_t n, uint64_t perm, uint64_t dst);
 int wg_iota_u32(uint64_t dst, uint64_t n);
+/* offsets[j] = j * step of vec[vec[T]] results built from fixed-length vectors
+ * (VecBuilderState.result, builders.py:274-283, for nested element types) */
+int wg_iota_i64(uint64_t dst, uint64_t n, int64_t step);
 int wg_sort_pairs(uint64_t keys_in, uint64_t vals_in, uint64_t keys_out, uint64_t vals_out, uint64_t n, int begin_bit,
                   int end_bit);
 int wg_gather(uint64_t src, uint64_t perm, uint64_t dst, uint64_t n, int width);

@@ -117,7 +117,12 @@ class Segment:
 
 
 class AppenderDev(BuilderBase):
-    """vecbuilder (and the row log of groupbuilder)."""
+    """vecbuilder (and the row log of groupbuilder).  A vecbuilder[vec[T]]
+    fed fixed-length vector literals keeps T's leaves here (nested=True) and
+    gets its offsets at result()."""
+
+    nested = False
+    nested_len = 1
 
     def __init__(self, kind, kinds, hint=None):
         super().__init__(kind)

@@ -754,8 +754,23 @@ class Gen:
             self.emit(f"m{b.bid}_h = 1;")
             return
         if isinstance(kind, (VecBuilder, GroupBuilder)):
-            vals = _flat(v)
             ks = b.extra["kinds"]
+            vals = _flat(v) if not b.extra.get("nested") else None
+            if b.mode == "direct" and b.extra.get("nested"):
+                if self.phase != "A":
+                    return
+                if not isinstance(v, SVec):
+                    raise DeviceUnsupported(f"vecbuilder[{kind.elem}] of a non-literal vector")
+                L = len(v.items)
+                if b.extra.setdefault("nested_len", L) != L:
+                    raise DeviceUnsupported(f"vecbuilder[{kind.elem}] of vectors with different lengths")
+                for q, item in enumerate(v.items):
+                    for f, (x, k) in enumerate(zip(_flat(item), ks)):
+                        val = f"(u8)({x.c})" if k == BOOL else x.c
+                        col = self.param(f"a{b.bid}_{f}", f"{STYPE[k]}*", ("b", b.bid, "col", f))
+                        self.emit(f"{col}[(li * {b.k} + c{b.bid}) * {L} + {q}] = {val};")
+                self.emit(f"c{b.bid} += 1;")
+                return
             if b.mode == "direct":
                 if self.phase != "A":
                     return
@@ -1134,15 +1149,24 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
                 # high / unknown cardinality: deferred merges, batched HBM probes
                 b.extra["deferred"] = True
         if isinstance(b.kind, (VecBuilder, GroupBuilder)):
-            if isinstance(b.kind, VecBuilder):
+            if isinstance(b.kind, VecBuilder) and isinstance(b.kind.elem, Vec):
+                # vecbuilder[vec[T]]: child leaves; the per-merge length is
+                # fixed by the merged vector literals (set in Gen.merge)
+                if not is_flat_type(b.kind.elem.elem):
+                    raise DeviceUnsupported(f"vecbuilder[{b.kind.elem}] (doubly nested) on the device")
+                b.extra["kinds"] = leaves(b.kind.elem.elem)
+                b.extra["nested"] = True
+            elif isinstance(b.kind, VecBuilder):
                 b.extra["kinds"] = leaves(b.kind.elem)
             else:
                 b.extra["kinds"] = leaves(b.kind.key) + leaves(b.kind.value)
+            if b.extra.get("nested") and not (mn == mx and mx > 0) and mx != 0:
+                raise DeviceUnsupported(f"vecbuilder[{b.kind.elem}] with data-dependent append counts")
             if mx == 0:
                 b.mode, b.k = "none", 0
             elif mn == mx:
                 b.mode, b.k = "direct", int(mn)
-                b.extra["buffered"] = ITEMS * b.k <= 32
+                b.extra["buffered"] = ITEMS * b.k <= 32 and not b.extra.get("nested")
             elif mx < INF:
                 b.mode, b.k = "scan", int(mx)
             else:
@@ -1160,7 +1184,7 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
         g.items = ITEMS
         for b in g.bspecs:
             if b.mode == "direct":
-                b.extra["buffered"] = ITEMS * b.k <= 32
+                b.extra["buffered"] = ITEMS * b.k <= 32 and not b.extra.get("nested")
     # order-preserving appenders stage their tile output in shared memory so
     # the global stores are contiguous per tile (coalesced)
     staged_bytes = 0
@@ -1692,6 +1716,14 @@ def _count_plan(g, lam, body_env, loads, iters, ITEMS, BLOCK, scan_bs, name):
                       block=BLOCK, smem=0, builders=g.bspecs, scan_bids=[b.bid for b in scan_bs], merger_bids=[])
     plan.pipe_stage_bytes = 0
     return plan
+
+
+def is_flat_type(t):
+    if isinstance(t, Scalar):
+        return True
+    if isinstance(t, Struct):
+        return all(is_flat_type(f) for f in t.fields)
+    return False
 
 
 def _dict_params(g, b):

@@ -485,6 +485,11 @@ __global__ void k_sub_min(uint64_t* ok, uint64_t n, uint64_t kmin) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
     ok[i] -= kmin;
 }
+// offsets of a vector of fixed-length vectors: dst[j] = j * step
+__global__ void k_iota_i64(int64_t* dst, uint64_t n, int64_t step) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = (int64_t)i * step;
+}
 }  // namespace
 
 // ===========================================================================
@@ -902,6 +907,14 @@ int wg_order_key(uint64_t src, int kind, uint64_t n, uint64_t perm, uint64_t dst
   if (!n) return 0;
   k_order_key<<<grid_for(n, 256), 256, 0, g_stream>>>((const void*)(uintptr_t)src, kind, n,
                                                        (const uint32_t*)(uintptr_t)perm, (uint64_t*)(uintptr_t)dst);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int wg_iota_i64(uint64_t dst, uint64_t n, int64_t step) {
+  NEED_INIT();
+  if (!n) return 0;
+  k_iota_i64<<<grid_for(n, 256), 256, 0, g_stream>>>((int64_t*)(uintptr_t)dst, n, step);
   CK(cudaGetLastError());
   return 0;
 }

@@ -307,7 +307,14 @@ class Ctx:
                 if hint < 0:
                     raise EvalError(f"negative vector size hint {hint}")
                 self.alloc(hint * _slot_bytes(kind.elem))
-            b = AppenderDev(kind, leaves(kind.elem) if is_flat(kind.elem) else None, hint)
+            if is_flat(kind.elem):
+                b = AppenderDev(kind, leaves(kind.elem), hint)
+            elif isinstance(kind.elem, Vec) and is_flat(kind.elem.elem):
+                # vec[vec[T]] from fixed-length vectors: child leaves + a length
+                b = AppenderDev(kind, leaves(kind.elem.elem), hint)
+                b.nested = True
+            else:
+                b = AppenderDev(kind, None, hint)
             b.acct = hint * _slot_bytes(kind.elem) if hint is not None else 0
             return b
         if isinstance(kind, Merger):
@@ -382,6 +389,16 @@ class Ctx:
             else:
                 cols, n = b.concat()
             self.free(getattr(b, "acct", 0))
+            if getattr(b, "nested", False):
+                # vec[vec[T]]: n child elements in fixed-length runs
+                L = getattr(b, "nested_len", 1)
+                nv = n // L if L else 0
+                offs = Col.alloc(I64, nv + 1)
+                rt.call("wg_iota_i64", offs.ptr, nv + 1, L)
+                from .columns import ListLayout, layout_from_cols
+                out = DVec(kind.elem, nv, ListLayout(offs, layout_from_cols(kind.elem.elem, cols), n))
+                self.materialized(out, 16 + nv * 16 + n * _slot_bytes(kind.elem.elem))
+                return out
             out = dvec_from_cols(kind.elem, n, cols)
             self.materialized(out, 16 + n * _slot_bytes(kind.elem))
             return out
@@ -605,9 +622,12 @@ class Ctx:
             st = bmap[b.bid]
             if isinstance(b.kind, (VecBuilder, GroupBuilder)):
                 if b.mode == "direct":
-                    seg = st.new_segment(count * b.k, True)
+                    per = b.k * b.extra.get("nested_len", 1)
+                    if b.extra.get("nested"):
+                        st.nested_len = b.extra["nested_len"]
+                    seg = st.new_segment(count * per, True)
                     res[b.bid] = seg
-                    self._acct_append(st, count * b.k)
+                    self._acct_append(st, count * per)
                 elif b.mode == "scan":
                     cap = sizes[b.bid] if b.k is None else count * b.k
                     seg = st.new_segment(cap, False)

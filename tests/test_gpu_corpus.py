@@ -15,8 +15,9 @@ from helpers import F64_TOL, approx_equal, first_diff, load_golden, norm
 pytestmark = pytest.mark.gpu
 
 CORPUS = load_golden("corpus.json")["programs"]
-# Known gaps of the device lowering (raise DeviceUnsupported, never a CPU fallback).
-UNSUPPORTED = {"vec-of-vec-0", "vec-of-vec-1", "vec-of-vec-2"}
+# Known gaps of the device lowering (raise DeviceUnsupported, never a CPU
+# fallback).  The whole reference corpus lowers now.
+UNSUPPORTED = set()
 LEVELS = ["O3", "none", "no-vectorize", "no-fuse", "no-predicate"]
 
 
@@ -76,13 +77,14 @@ def test_corpus_parity(front, level):
 
 
 def test_unsupported_programs_fail_loudly(front):
-    """No silent CPU fallback: IR outside the device lowering raises."""
+    """No silent CPU fallback: IR outside the device lowering raises
+    (here: nested appends of vectors whose lengths depend on the data)."""
     from weldmill.engine import Value
     from weldmill.optim import optimize
     import paper_1709_06416_b200 as wg
 
-    p = next(p for p in CORPUS if p["name"] == "vec-of-vec-0")
-    typed, env = front(p["source"], p["inputs"])
-    vals = {k: Value(env[k], v) for k, v in p["cases"][0]["inputs"].items()}
+    typed, env = front("result(for(v, vecbuilder[vec[i64]], (b, i, x) => merge(b, lookup(vv, x))))",
+                       {"v": "vec[i64]", "vv": "vec[vec[i64]]"})
+    vals = {"v": Value(env["v"], [0, 1]), "vv": Value(env["vv"], [[1, 2], [3]])}
     with pytest.raises(wg.DeviceUnsupported):
         wg.evaluate(optimize(typed)[0], vals)
