@@ -84,10 +84,12 @@ int wg_table_compact(uint64_t table, uint64_t nslots, int slot_words, int mode, 
 /* Small dictmerger result in one launch: occupied slots -> entries sorted by
  * the order_key tuple -> typed key/value columns (DictMergerState.result,
  * builders.py:380-392 + order_key :496-507).  key_desc = 4 ints per key leaf
- * (word, shift, width, kind); *count_out > 4096 means nothing was written. */
+ * (word, shift, width, kind); counters = the table's {distinct, spilled}
+ * words (device).  *count_out > 4096 means nothing was written; ~0 means
+ * spilled merges must be replayed first. */
 int wg_dict_finish_small(uint64_t table, uint64_t nslots, int slot_words, int mode, int nw, int nkl,
                          const int* key_desc, int nvl, const int* val_kinds, const uint64_t* outs,
-                         uint64_t* count_out);
+                         uint64_t counters, uint64_t* count_out);
 int wg_order_key(uint64_t src, int kind, uint64_t n, uint64_t perm, uint64_t dst);
 int wg_iota_u32(uint64_t dst, uint64_t n);
 /* offsets[j] = j * step of vec[vec[T]] results built from fixed-length vectors

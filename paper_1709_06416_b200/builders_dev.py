@@ -451,12 +451,13 @@ SMALL_DICT = 4096
 
 def _finish_small(d: DictDev, dict_ty):
     """Results of <= SMALL_DICT entries: one launch (wg_dict_finish_small)
-    instead of compaction + per-leaf radix sorts + gathers."""
-    distinct, spilled = d.read_counters()
+    instead of compaction + per-leaf radix sorts + gathers; the kernel also
+    checks the spill counter, so the host syncs once.  Returns None when the
+    general path (or a spill replay) is needed."""
     nkl, nvl = len(d.kks), len(d.vks)
-    if distinct > SMALL_DICT or spilled or nkl > 6 or nvl > 16:
+    if nkl > 6 or nvl > 16 or (d.hint_key is not None and _SIZE_HINTS.get(d.hint_key, 0) > SMALL_DICT):
         return None
-    n = distinct
+    n = SMALL_DICT
     kcols = [Col.alloc(k, max(n, 1)) for k in d.kks]
     vcols = [Col.alloc(k, max(n, 1)) for k in d.vks]
     desc = []
@@ -468,9 +469,13 @@ def _finish_small(d: DictDev, dict_ty):
     cnt = ctypes.c_uint64(0)
     mode = 1 if d.nw == 1 else 2
     rt.call("wg_dict_finish_small", d.table.ptr, d.cap, d.slot_words, mode, d.nw, nkl, kd, nvl, vk, outs,
-            ctypes.byref(cnt))
-    if cnt.value != n:
-        raise RuntimeError(f"dictmerger table holds {cnt.value} keys, counted {n}")
+            d.counters.ptr, ctypes.byref(cnt))
+    n = cnt.value
+    if n > SMALL_DICT:          # too many entries, or spilled merges to replay first
+        return None
+    d.distinct = n
+    if d.hint_key is not None:
+        _SIZE_HINTS[d.hint_key] = max(n, _SIZE_HINTS.get(d.hint_key, 0))
     return DDict(dict_ty, dvec_from_cols(dict_ty.key, n, kcols), dvec_from_cols(dict_ty.value, n, vcols))
 
 

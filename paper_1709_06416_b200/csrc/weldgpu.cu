@@ -381,10 +381,13 @@ __device__ __forceinline__ void wg_store_leaf(void* col, uint64_t i, uint64_t bi
 }
 
 __global__ void __launch_bounds__(1024) k_dict_finish_small(const uint64_t* table, uint64_t nslots, SmallDictDesc d,
+                                                            const unsigned long long* counters,
                                                             unsigned long long* count_out) {
   __shared__ uint32_t s_idx[WG_SMALL_DICT];
   __shared__ unsigned s_n;
   extern __shared__ uint64_t s_ok[];      // [WG_SMALL_DICT * nkl] order keys
+  // merges spilled past the table (counters[1]) must be replayed first
+  if (counters && counters[1] != 0ULL) { if (threadIdx.x == 0) *count_out = ~0ULL; return; }
   if (threadIdx.x == 0) s_n = 0;
   __syncthreads();
   const uint64_t total = nslots + (d.mode == 1 ? 1 : 0);
@@ -873,7 +876,7 @@ int wg_table_compact(uint64_t table, uint64_t nslots, int slot_words, int mode, 
 // WG_SMALL_DICT nothing is written and the caller uses the general path.
 int wg_dict_finish_small(uint64_t table, uint64_t nslots, int slot_words, int mode, int nw, int nkl,
                          const int* key_desc, int nvl, const int* val_kinds, const uint64_t* outs,
-                         uint64_t* count_out) {
+                         uint64_t counters, uint64_t* count_out) {
   NEED_INIT();
   if (nkl > 6 || nvl > 16) return fail("wg_dict_finish_small: too many key/value leaves");
   SmallDictDesc d;
@@ -893,7 +896,8 @@ int wg_dict_finish_small(uint64_t table, uint64_t nslots, int slot_words, int mo
     CK(cudaFuncSetAttribute(k_dict_finish_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 * WG_SMALL_DICT * 8));
     attr_set = true;
   }
-  k_dict_finish_small<<<1, 1024, smem, g_stream>>>((const uint64_t*)(uintptr_t)table, nslots, d, d_cnt);
+  k_dict_finish_small<<<1, 1024, smem, g_stream>>>((const uint64_t*)(uintptr_t)table, nslots, d,
+                                                   (const unsigned long long*)(uintptr_t)counters, d_cnt);
   CK(cudaGetLastError());
   unsigned long long h = 0;
   CK(cudaMemcpyAsync(&h, d_cnt, 8, cudaMemcpyDeviceToHost, g_stream));

@@ -31,7 +31,7 @@ from weldmill.expr import (Apply, BinaryOp, BitSelect, Broadcast, CastScalar, Ex
 
 from . import runtime as rt
 from . import semantics as sem
-from .builders_dev import (_RANGE_HINTS, AppenderDev, DDict, DGroups, DictDev, GroupDev, MergerDev, VecMergerDev,
+from .builders_dev import (_RANGE_HINTS, _finish_small, AppenderDev, DDict, DGroups, DictDev, GroupDev, MergerDev, VecMergerDev,
                            dict_payload, finish_dict, finish_groups, gather_cols, sort_perm, tovec)
 from .codegen import DEFER_DICT, PIPE_STAGES, BSpec, IterSpec, generate, rpart_ok, rpart_table_slots
 from .columns import Col, DVec, to_device, to_payload, dvec_from_cols
@@ -410,7 +410,10 @@ class Ctx:
         if isinstance(kind, DictMerger):
             if b.table is None:
                 b.ensure(1)
-            d = finish_dict(b, Dict(kind.key, kind.value))
+            d = _finish_small(b, Dict(kind.key, kind.value)) if b.rpart_out is None else None
+            if d is None:
+                self._settle(b)
+                d = finish_dict(b, Dict(kind.key, kind.value))
             self.materialized(d, 16 + d.n * (16 + _slot_bytes(kind.key) + _slot_bytes(kind.value)))
             return d
         if isinstance(kind, GroupBuilder):
@@ -519,6 +522,8 @@ class Ctx:
             b.check()
             if getattr(b, "rpart_out", None) is not None:
                 self._rpart_to_table(b)
+            if isinstance(b, DictDev):
+                self._settle(b)
             self.flush_pending(b)
         # loop-invariant captures
         fv = _fv_cache.get(id(lam))
@@ -663,14 +668,26 @@ class Ctx:
                 self._dict_aggregate(bmap[b.bid], b)
             if isinstance(b.kind, DictMerger) and b.extra.get("rpart"):
                 self._dict_rpart_aggregate(bmap[b.bid], b)
-        # dictmerger overflow: grow and replay spilled merges
+        # dictmerger overflow (merges spilled past the table) is settled
+        # lazily -- before the next launch into the builder or at result() --
+        # so a loop's launch does not wait on the device
         for b in plan.builders:
-            if isinstance(b.kind, DictMerger):
-                st = bmap[b.bid]
+            if isinstance(b.kind, DictMerger) and not b.extra.get("rpart"):
+                bmap[b.bid].spill_pending = True
+        self._keep = (tilectr, res)
+
+    def _settle(self, st):
+        """Grow the table and replay spilled merges, if the last launches
+        into this dictmerger spilled any."""
+        consumed, st.consumed = st.consumed, False    # result() may be finishing it: replay is internal
+        try:
+            while getattr(st, "spill_pending", False):
+                st.spill_pending = False
                 _, spilled = st.read_counters()
                 if spilled:
                     self._dict_regrow(st, spilled)
-        self._keep = (tilectr, res)
+        finally:
+            st.consumed = consumed
 
     def _dict_aggregate(self, st, b):
         from .codegen import dict_agg_source
@@ -722,7 +739,8 @@ class Ctx:
         its entries into a hash table first (all folds are commutative)."""
         kw, vw, n = st.rpart_out
         st.rpart_out = None
-        st.ensure(max(n, 1))
+        st.table, st.cap = None, 0         # drop the placeholder table of the partitioned launch
+        st.ensure(max(n, 1), hint_key=st.hint_key)
         if n == 0:
             return
         from .builders_dev import _words_to_cols, _value_words_to_cols

@@ -60,7 +60,7 @@ _SIGS = {
     "wg_table_init": (c_int, [u64, u64, c_int, ctypes.POINTER(u64)]),
     "wg_table_compact": (c_int, [u64, u64, c_int, c_int, ctypes.POINTER(u64), c_int, ctypes.POINTER(u64)]),
     "wg_dict_finish_small": (c_int, [u64, u64, c_int, c_int, c_int, c_int, ctypes.POINTER(c_int), c_int,
-                                     ctypes.POINTER(c_int), ctypes.POINTER(u64), ctypes.POINTER(u64)]),
+                                     ctypes.POINTER(c_int), ctypes.POINTER(u64), u64, ctypes.POINTER(u64)]),
     "wg_order_key": (c_int, [u64, c_int, u64, u64, u64]),
     "wg_iota_u32": (c_int, [u64, u64]),
     "wg_iota_i64": (c_int, [u64, u64, i64]),
