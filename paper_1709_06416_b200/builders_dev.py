@@ -77,17 +77,22 @@ class MergerDev(BuilderBase):
         self.launched = True
         return 1 if first else 0
 
-    def read_words(self):
-        """Slot words (values..., flag) or None if no loop ever ran."""
+    def read_words(self, err=None):
+        """Slot words (values..., flag) or None if no loop ever ran.  With
+        `err` (a list), the device error word is read in the same sync and
+        appended as (code, info)."""
         if not self.launched:
             return None
         F = len(self.ks)
         arr = np.empty(F + 1, dtype=np.uint64)
-        rt.d2h(arr.ctypes.data, self.slot.ptr, arr.nbytes)
+        if err is not None:
+            err.append(rt.d2h_checked(arr.ctypes.data, self.slot.ptr, arr.nbytes))
+        else:
+            rt.d2h(arr.ctypes.data, self.slot.ptr, arr.nbytes)
         return arr
 
-    def read(self):
-        arr = self.read_words()
+    def read(self, err=None):
+        arr = self.read_words(err)
         F = len(self.ks)
         if arr is None or not arr[F]:
             vals = [identity_value(self.kind.op, k) for k in self.ks]

@@ -585,6 +585,10 @@ int wg_alloc(uint64_t bytes, uint64_t* dptr) {
     }
   }
   *dptr = (uint64_t)(uintptr_t)p;
+  // WELDGPU_POISON=1: every block handed out is filled with 0xA5 bytes, so a
+  // kernel that relies on zeroed memory fails deterministically in tests
+  static const int poison = getenv("WELDGPU_POISON") && getenv("WELDGPU_POISON")[0] == '1';
+  if (poison) CK(cudaMemsetAsync(p, 0xA5, b, g_stream));
   std::lock_guard<std::mutex> lk(g_acct_mu);
   g_live += b;
   if (g_live > g_peak) g_peak = g_live;
@@ -694,6 +698,19 @@ int wg_error_ptr(uint64_t* p) { NEED_INIT(); *p = (uint64_t)(uintptr_t)g_err_wor
 
 int wg_read_error(int64_t* code, int64_t* info) {
   NEED_INIT();
+  CK(cudaMemcpyAsync(g_err_host, g_err_word, 16, cudaMemcpyDeviceToHost, g_stream));
+  CK(cudaStreamSynchronize(g_stream));
+  *code = g_err_host[0];
+  *info = g_err_host[1];
+  if (g_err_host[0] != 0) CK(cudaMemsetAsync(g_err_word, 0, 16, g_stream));
+  return 0;
+}
+
+// A result read-back and the error-word check in one synchronisation (the
+// common tail of an evaluate(): a merger's slot, then "did any kernel raise").
+int wg_d2h_checked(void* dst, uint64_t src, uint64_t bytes, int64_t* code, int64_t* info) {
+  NEED_INIT();
+  if (bytes) CK(cudaMemcpyAsync(dst, (const void*)(uintptr_t)src, bytes, cudaMemcpyDeviceToHost, g_stream));
   CK(cudaMemcpyAsync(g_err_host, g_err_word, 16, cudaMemcpyDeviceToHost, g_stream));
   CK(cudaStreamSynchronize(g_stream));
   *code = g_err_host[0];

@@ -15,6 +15,7 @@ from __future__ import annotations
 import math
 import struct as _struct
 import threading
+import weakref
 
 import numpy as np
 
@@ -114,6 +115,7 @@ class Ctx:
         self._host_dicts = {}
         self.cfg = cfg
         self.externs = externs or {}
+        self._ext_key = tuple(sorted(self.externs))
         self.traversals = 0
         self.allocs = 0
         self.tasks = 0
@@ -378,6 +380,16 @@ class Ctx:
         b.consume()
         kind = b.kind
         if isinstance(kind, Merger):
+            if self.dirty and b.launched:
+                # the merger's slot and the error word come back in one sync
+                err = []
+                v = b.read(err)
+                self.dirty = False
+                code, info = err[0]
+                if code:
+                    cls = ERR_CLASSES.get(code, EvalError)
+                    raise cls(ERR_TEXT.get(code, "device error {info}").format(info=info))
+                return v
             self.check_device()
             return b.read()
         if isinstance(kind, VecBuilder):
@@ -465,6 +477,7 @@ class Ctx:
         return self.run_loop(e, env)
 
     def run_loop(self, e, env, count_traversal=True):
+        _claim_loop_id(e)
         datas, specs, windows = [], [], []
         count = None
         for it in e.iters:
@@ -495,14 +508,19 @@ class Ctx:
                 raise ZipLengthMismatch(f"zipped iterations disagree: {count} vs {n}")
             datas.append(d)
             windows.append(win)
-            if not is_flat(elem):
+            ks = _leaves_of(elem)
+            if ks is None:
                 raise DeviceUnsupported(f"iterating vec[{elem}] on the device")
             aligned = False
             if win[1] == 1 and count:
                 dv = d.dev() if isinstance(d, HostVec) else d
-                aligned = all((c.ptr + win[0] * SIZE[c.kind]) % 16 == 0 for c in dv.cols)
-            specs.append(IterSpec(elem=elem, simd=it.simd, strided=(win[1] != 1), kinds=leaves(elem),
-                                  aligned=aligned))
+                off = win[0]
+                aligned = True
+                for c in dv.cols:
+                    if (c.ptr + off * SIZE[c.kind]) & 15:
+                        aligned = False
+                        break
+            specs.append(IterSpec(elem=elem, simd=it.simd, strided=(win[1] != 1), kinds=ks, aligned=aligned))
         builders = self.ev(e.builders, env)
         if count == 0:
             return builders
@@ -541,8 +559,7 @@ class Ctx:
         bstruct, bmap = _bspecs(builders, strategy, count, loop_id=id(e))
         # The expression identities fix every type in the loop; only the
         # runtime choices (strides, alignment, builder modes, externs) vary.
-        key = (id(e), id(lam), tuple((s.strided, s.aligned) for s in specs), _bsig(bstruct),
-               tuple(sorted(self.externs)))
+        key = (id(e), id(lam), tuple((s.strided, s.aligned) for s in specs), _bsig(bstruct), self._ext_key)
         with _plan_lock:
             cached = _plan_cache.get(key)
         if cached is None:
@@ -945,6 +962,46 @@ def _host_dict_to_device(v, t):
         return DGroups(Dict(t.key, t.value), keys, oc, vals)
     vals = to_device(Vec(t.value), [x for _, x in items])
     return DDict(Dict(t.key, t.value), keys, vals)
+
+
+_LOOP_REFS = {}     # id(loop expression) -> weakref: guards the id-keyed hints
+
+
+def _claim_loop_id(e):
+    """Per-loop hints (table sizes, key ranges, rpart fallbacks) are keyed by
+    id(loop).  When a loop expression dies and CPython reuses its id for a
+    new one, drop the dead loop's hints before the new loop reads them."""
+    lid = id(e)
+    r = _LOOP_REFS.get(lid)
+    if r is not None and r() is e:
+        return
+    if r is not None:
+        from .builders_dev import _SIZE_HINTS as _SH
+        for d in (_SH, _RANGE_HINTS):
+            for k in [k for k in d if k[0] == lid]:
+                del d[k]
+        for k in [k for k in _RPART_BAD if k[0] == lid]:
+            _RPART_BAD.discard(k)
+    try:
+        _LOOP_REFS[lid] = weakref.ref(e)
+    except TypeError:
+        pass
+
+
+_LEAVES = {}
+
+
+def _leaves_of(t):
+    """Scalar leaves of a flat element type (None if not flat), memoised:
+    loop element types repeat across every evaluate of a program."""
+    try:
+        return _LEAVES[t]
+    except KeyError:
+        ks = leaves(t) if is_flat(t) else None
+        _LEAVES[t] = ks
+        return ks
+    except TypeError:           # unhashable type object
+        return leaves(t) if is_flat(t) else None
 
 
 def _layout(t, cols):

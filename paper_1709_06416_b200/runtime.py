@@ -47,6 +47,7 @@ _SIGS = {
     "wg_host_unregister": (c_int, [c_void_p]),
     "wg_error_ptr": (c_int, [ctypes.POINTER(u64)]),
     "wg_read_error": (c_int, [ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+    "wg_d2h_checked": (c_int, [c_void_p, u64, u64, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
     "wg_compile": (c_int, [c_char_p, c_char_p, c_int, ctypes.POINTER(c_char_p), ctypes.POINTER(c_char_p), c_int,
                            ctypes.POINTER(c_char_p), ctypes.POINTER(u64), c_char_p, u64]),
     "wg_compile_check": (c_int, [c_char_p, c_char_p, c_int, ctypes.POINTER(c_char_p), ctypes.POINTER(c_char_p),
@@ -244,6 +245,14 @@ def d2h_async(host_ptr, src_ptr, nbytes):
 
 def d2d(dst_ptr, src_ptr, nbytes):
     _check(lib().wg_d2d(dst_ptr, src_ptr, nbytes))
+
+
+def d2h_checked(host_ptr, src_ptr, nbytes):
+    """Copy device -> host and read the error word; one synchronisation.
+    Returns (code, info)."""
+    c, i = i64(0), i64(0)
+    _check(lib().wg_d2h_checked(host_ptr, src_ptr, nbytes, ctypes.byref(c), ctypes.byref(i)))
+    return c.value, i.value
 
 
 def read_error():

@@ -1,2 +1,5 @@
 mkdir -p gpurun_out/t1
-timeout 600 python -m pytest tests/test_gpu_rpart.py -q -k reused 2>&1 | grep -E "assert|Error|Mismatch|^E " | head -30 > gpurun_out/t1/pytest.log
+: > gpurun_out/t1/pytest.log
+for r in 1 2; do
+timeout 1500 python -m pytest tests -q -m gpu 2>&1 | tail -4 >> gpurun_out/t1/pytest.log
+done

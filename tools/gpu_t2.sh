@@ -1,4 +1,4 @@
 mkdir -p gpurun_out/t2
-timeout 900 python -m pytest tests/test_gpu_configs.py tests/test_gpu_rpart.py -q -x -k "dict" 2>&1 | tail -3 > gpurun_out/t2/pytest.log
-timeout 300 python bench.py --workload dict --steps 10 --warmup 3 --no-cpu --no-e2e 2>&1 | tail -1 > gpurun_out/t2/bench_dict.log
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/t2/launches_dict.csv python bench.py --workload dict --steps 1 --warmup 3 --no-cpu --no-e2e --no-kernel-timing > /dev/null 2>&1
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 3 --warmup 3 > gpurun_out/t2/tr2.log 2>&1
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29512 bench.py --impl reference --gpus 2 --steps 2 --warmup 3 > gpurun_out/t2/tr2_ref.log 2>&1
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29513 bench.py --gpus 2 --workload q1 --steps 3 --warmup 3 --no-cpu > gpurun_out/t2/tr2_q1.log 2>&1
