@@ -68,6 +68,7 @@ SCAN_PREFETCH = _os.environ.get("WELDGPU_SCAN_PREFETCH", "0") == "1"
 LB_PER = int(_os.environ.get("WELDGPU_LB_PER", "1"))
 LB_SLEEP = int(_os.environ.get("WELDGPU_LB_SLEEP", "64"))
 SCAN_PIPE = _os.environ.get("WELDGPU_SCAN_PIPE", "0") == "1"
+PART_ITEMS = int(_os.environ.get("WELDGPU_PART_ITEMS", "8"))
 PIPE_STAGES = int(_os.environ.get("WELDGPU_PIPE_STAGES", "4"))
 PIPE_MAX_STAGES = 8
 PIPE_SMEM_BUDGET = int(_os.environ.get("WELDGPU_PIPE_SMEM", str(48 * 1024)))
@@ -1110,12 +1111,14 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
         if b.extra.get("rpart") and not (items or ITEMS_OVERRIDE):
             ITEMS = 2
         if b.extra.get("part"):
-            # the tile's records are staged in static shared memory (<= 40 KB)
+            # the tile's records are staged in dynamic shared memory; larger
+            # tiles mean longer per-partition runs and fewer global
+            # reservations per row
             rec = 8 + 8 * len(leaves(b.kind.value)) + 2
-            while ITEMS > 1 and BLOCK * ITEMS * rec > 40 * 1024:
+            ITEMS = PART_ITEMS
+            while ITEMS > 1 and BLOCK * ITEMS * rec > 96 * 1024:
                 ITEMS //= 2
-            ITEMS = min(ITEMS, 4)
-    if not (items or ITEMS_OVERRIDE) and PIPE:
+    if not (items or ITEMS_OVERRIDE) and PIPE and not any(b.extra.get("part") for b in g.bspecs):
         # keep >= 2 pipeline stages inside the shared-memory budget
         row = sum(SIZE[k] * (W if it.simd else 1) for it in iters for k in it.kinds)
         while ITEMS > 1 and 2 * BLOCK * ITEMS * row > PIPE_SMEM_BUDGET:
@@ -1294,6 +1297,16 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
                 smem_flush.append(
                     f"for (int q = threadIdx.x; q < {nb}; q += {BLOCK}) {{ const {CTYPE[kk]} v_ = (({CTYPE[kk]}*)(s_vm{b.bid} + {f * nb}))[q]; "
                     f"if (wg_to_bits<{CTYPE[kk]}>(v_) != wg_to_bits<{CTYPE[kk]}>({ident})) WgAtomicFold<{opc}, {CTYPE[kk]}>::f({col} + q, v_); }}")
+        if isinstance(b.kind, DictMerger) and b.extra.get("part"):
+            # hash-partitioned dictmerger: the tile's records, sorted by partition
+            B = b.bid
+            V_ = len(leaves(b.kind.value))
+            T_ = BLOCK * ITEMS
+            off = dyn_smem // 8
+            smem_decls.append(f"u64* s_rk{B} = wg_dyn_smem + {off};"
+                              + "".join(f" u64* s_rv{B}_{f} = wg_dyn_smem + {off + T_ * (1 + f)};" for f in range(V_))
+                              + f" unsigned short* s_rp{B} = (unsigned short*)(wg_dyn_smem + {off + T_ * (1 + V_)});")
+            dyn_smem += T_ * 8 * (1 + V_) + ((T_ * 2 + 7) // 8) * 8
         if isinstance(b.kind, DictMerger) and b.extra.get("rpart"):
             # per-partition tile counts, window cursors, tile bases (u32 x 4)
             NP = 1 << b.extra["pbits"]
@@ -2300,8 +2313,7 @@ def _deferred_dict_lines(g, b):
         # (shared arrays are declared once at kernel scope: this block can be
         # emitted twice -- main tile loop and tail tile)
         decl = [f"  __shared__ unsigned s_ph{B}[{NP}], s_po{B}[{NP}];", f"  __shared__ u64 s_pb{B}[{NP}];",
-                f"  __shared__ u64 s_rk{B}[TILE];"] + [f"  __shared__ u64 s_rv{B}_{f}[TILE];" for f in range(V)] + [
-                f"  __shared__ unsigned short s_rp{B}[TILE];", f"  __shared__ i64 s_sc{B}[33];"]
+                f"  __shared__ i64 s_sc{B}[33];"]
         b.extra["smem_decl"] = decl
         L.append(f"      unsigned pp_[ITEMS], pr_[ITEMS];")
         L.append(f"      for (int q = threadIdx.x; q < {NP}; q += BLOCK) s_ph{B}[q] = 0u;")

@@ -1375,7 +1375,7 @@ def evaluate_partials(loop, env, config=None, externs=None, idx0=0, rank=0):
 # Streaming path for host-resident inputs: copy/compute overlap.
 
 STREAM_MIN_ROWS = 1 << 22
-STREAM_CHUNK_ROWS = 1 << 23
+STREAM_CHUNK_ROWS = int(_os.environ.get("WELDGPU_STREAM_CHUNK", str(1 << 23)))
 
 
 def _stream_candidate(e, frame):
