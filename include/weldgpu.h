@@ -97,6 +97,9 @@ int wg_iota_u32(uint64_t dst, uint64_t n);
 /* offsets[j] = j * step of vec[vec[T]] results built from fixed-length vectors
  * (VecBuilderState.result, builders.py:274-283, for nested element types) */
 int wg_iota_i64(uint64_t dst, uint64_t n, int64_t step);
+/* exclusive scan of n i64 per-tile append counts -> tile offsets; *total (device) = sum
+ * (two-pass order-preserving appends: VecBuilderState.result order, builders.py:274-283) */
+int wg_exclusive_scan_i64(uint64_t src, uint64_t dst, uint64_t n, uint64_t total);
 int wg_sort_pairs(uint64_t keys_in, uint64_t vals_in, uint64_t keys_out, uint64_t vals_out, uint64_t n, int begin_bit,
                   int end_bit);
 int wg_gather(uint64_t src, uint64_t perm, uint64_t dst, uint64_t n, int width);

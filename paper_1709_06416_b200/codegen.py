@@ -68,6 +68,10 @@ SCAN_PREFETCH = _os.environ.get("WELDGPU_SCAN_PREFETCH", "0") == "1"
 LB_PER = int(_os.environ.get("WELDGPU_LB_PER", "1"))
 LB_SLEEP = int(_os.environ.get("WELDGPU_LB_SLEEP", "64"))
 SCAN_PIPE = _os.environ.get("WELDGPU_SCAN_PIPE", "0") == "1"
+# two-pass order-preserving appenders: a count-only pre-pass writes per-tile
+# append counts, an exclusive scan turns them into tile offsets, and the
+# main kernel stores without a decoupled look-back
+SCAN2 = _os.environ.get("WELDGPU_SCAN2", "0") == "1"
 PART_ITEMS = int(_os.environ.get("WELDGPU_PART_ITEMS", "8"))
 PIPE_STAGES = int(_os.environ.get("WELDGPU_PIPE_STAGES", "4"))
 PIPE_MAX_STAGES = 8
@@ -1275,6 +1279,8 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
         if b.mode == "scan":
             g.param(f"a{b.bid}_status", "u64*", ("b", b.bid, "status"))
             g.param(f"a{b.bid}_total", "i64*", ("b", b.bid, "total"))
+            if SCAN2:
+                g.param(f"a{b.bid}_tofs", "const i64*", ("b", b.bid, "tofs"))
     if schedule == "scan":
         g.param("tilectr", "unsigned long long*", ("tilectr",))
 
@@ -1480,10 +1486,16 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
             for si, b in enumerate(scan_bs):
                 out.append(f"    i64 agg{b.bid};")
                 out.append(f"    i64 wpos{b.bid} = wg_block_exclusive_scan(cnt{b.bid}, s_scan, &agg{b.bid});")
-                out.append("    if (threadIdx.x < 32) {")
-                out.append(f"      const i64 pre_ = wg_lookback(p.a{b.bid}_status, tile, agg{b.bid});")
-                out.append(f"      if (threadIdx.x == 0) {{ s_toff[{si}] = pre_; if (tile == ntiles - 1) *p.a{b.bid}_total = pre_ + agg{b.bid}; }}")
-                out.append("    }")
+                if SCAN2:
+                    # two-pass schedule: the tile's offset was computed by the
+                    # count pre-pass + exclusive scan (no look-back)
+                    out.append(f"    if (threadIdx.x == 0) {{ s_toff[{si}] = p.a{b.bid}_tofs[tile]; "
+                               f"if (tile == ntiles - 1) *p.a{b.bid}_total = s_toff[{si}] + agg{b.bid}; }}")
+                else:
+                    out.append("    if (threadIdx.x < 32) {")
+                    out.append(f"      const i64 pre_ = wg_lookback(p.a{b.bid}_status, tile, agg{b.bid});")
+                    out.append(f"      if (threadIdx.x == 0) {{ s_toff[{si}] = pre_; if (tile == ntiles - 1) *p.a{b.bid}_total = pre_ + agg{b.bid}; }}")
+                    out.append("    }")
             out.append("    __syncthreads();")
             out.extend(mid or [])
             for si, b in enumerate(scan_bs):
@@ -1508,7 +1520,24 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
                 out.append("    __syncthreads();")
         return out
 
-    if scan_bs and not pipe and not SCAN_PREFETCH:
+    if scan_bs and SCAN2:
+        # two-pass schedule: static grid-stride tiles, columns of the next
+        # tile in flight (register double buffering) -- tile offsets known
+        src.extend(decl_lines("", "  "))
+        src.append("  i64 tile = blockIdx.x;")
+        src.append("  if (tile < ntiles)")
+        src.extend(load_lines("tile", "", "  "))
+        src.append("  for (; tile < ntiles; tile += gridDim.x) {")
+        src.extend(decl_lines("_nx", "    "))
+        src.append("    const i64 ntile_ = tile + gridDim.x;")
+        src.append("    if (ntile_ < ntiles)")
+        src.extend(load_lines("ntile_", "_nx", "    "))
+        src.extend(tile_body())
+        for (arr, st, kk, per, k, l, col) in loads:
+            cnt = f"ITEMS * {per}" if per > 1 else "ITEMS"
+            src.append(f"#pragma unroll\n    for (int q = 0; q < {cnt}; ++q) {arr}[q] = {arr}_nx[q];")
+        src.append("  }")
+    elif scan_bs and not pipe and not SCAN_PREFETCH:
         # Dynamic tiles, claimed in order through an atomic counter (so every
         # predecessor a tile's look-back waits on is held by a running CTA).
         src.append("  while (true) {")
@@ -1688,6 +1717,9 @@ def _count_plan(g, lam, body_env, loads, iters, ITEMS, BLOCK, scan_bs, name):
     unb = [b for b in scan_bs if b.extra.get("unbounded")]
     for b in unb:
         g.param(f"ct{b.bid}_total", "unsigned long long*", ("b", b.bid, "ctotal"))
+    if SCAN2:
+        for b in scan_bs:
+            g.param(f"tc{b.bid}_counts", "i64*", ("b", b.bid, "tcounts"))
     src = ['#include "weld_device.cuh"', f"#define BLOCK {BLOCK}", f"#define ITEMS {ITEMS}",
            "#define TILE (BLOCK * ITEMS)", "struct Params {"]
     src += [f"  {p_.ctype} {p_.name};" for p_ in g.params]
@@ -1698,15 +1730,16 @@ def _count_plan(g, lam, body_env, loads, iters, ITEMS, BLOCK, scan_bs, name):
     for (arr, st, kk, per, k, l, col) in loads:
         cnt = f"ITEMS * {per}" if per > 1 else "ITEMS"
         src.append(f"    alignas(16) {st} {arr}[{cnt}];")
-    src.append("    { const i64 lt0_ = tile * TILE + (i64)threadIdx.x * ITEMS;")
+    src.append("    { const i64 lt0_ = tile * TILE + (i64)threadIdx.x * ITEMS; const bool lfull_ = (lt0_ + ITEMS <= n);")
     for (arr, st, kk, per, k, l, col) in loads:
         cnt = f"ITEMS * {per}" if per > 1 else "ITEMS"
         if iters[k].strided:
             src.append(f"      for (int q = 0; q < ITEMS; ++q) {{ const i64 li_ = lt0_ + q; "
                        f"{arr}[q] = (li_ < n) ? {col}[p.it{k}_start + li_ * p.it{k}_stride] : ({st})0; }}")
         else:
-            src.append(f"      for (int q = 0; q < {cnt}; ++q) {{ const i64 e_ = lt0_ * {per} + q; "
-                       f"{arr}[q] = (e_ < n * {per}) ? {col}[e_] : ({st})0; }}")
+            src.append(f"      if (lfull_) wg_load_contig<{st}, {cnt}>({col} + lt0_ * {per}, {arr});")
+            src.append(f"      else {{ for (int q = 0; q < {cnt}; ++q) {{ const i64 e_ = lt0_ * {per} + q; "
+                       f"{arr}[q] = (e_ < n * {per}) ? {col}[e_] : ({st})0; }} }}")
     src.append("    }")
     src.append("    const i64 t0 = tile * TILE + (i64)threadIdx.x * ITEMS;")
     src += [f"    i64 cnt{b.bid} = 0;" for b in scan_bs]
@@ -1719,6 +1752,11 @@ def _count_plan(g, lam, body_env, loads, iters, ITEMS, BLOCK, scan_bs, name):
     src.append("      }")
     src.append("    }")
     src += [f"    tc{b.bid} += cnt{b.bid};" for b in unb]
+    if SCAN2:
+        src.append("    __shared__ i64 s_sc_[33];")
+        for b in scan_bs:
+            src.append(f"    {{ i64 t_; (void)wg_block_exclusive_scan(cnt{b.bid}, s_sc_, &t_); "
+                       f"if (threadIdx.x == 0) p.tc{b.bid}_counts[tile] = t_; }}")
     src.append("  }")
     for b in unb:
         src.append(f"  {{ i64 c_ = tc{b.bid};")
@@ -2534,7 +2572,7 @@ def static_plans(expr, env_types=None, externs=(), smem=True, lowcard=False, par
         plan = generate(node, iters, bstruct, caps, ext, "local")
         if count_only:
             # the count-only pre-pass of flatmap-shaped loops (fresh builder specs)
-            if any(b.extra.get("unbounded") for b in plan.builders):
+            if any(b.extra.get("unbounded") for b in plan.builders) or (SCAN2 and plan.schedule == "scan"):
                 counter[0] = 0
                 plans.append(generate(node, iters, mk(node.builders.ty), caps, ext, "local", count_only=True))
             continue

@@ -493,6 +493,35 @@ __global__ void k_iota_i64(int64_t* dst, uint64_t n, int64_t step) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
     dst[i] = (int64_t)i * step;
 }
+// exclusive scan of n i64 counts by one CTA (tile offsets of the two-pass
+// order-preserving appender schedule); *total = sum
+__global__ void __launch_bounds__(1024) k_exscan_i64(const int64_t* src, int64_t* dst, uint64_t n, int64_t* total) {
+  __shared__ int64_t s_w[32];
+  __shared__ int64_t s_carry;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint64_t base = 0; base < n; base += 1024) {
+    const uint64_t i = base + threadIdx.x;
+    const int64_t x = i < n ? src[i] : 0;
+    int64_t incl = x;
+    for (int d = 1; d < 32; d <<= 1) { const int64_t o = __shfl_up_sync(0xffffffffu, incl, d); if (lane >= d) incl += o; }
+    if (lane == 31) s_w[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      int64_t w = s_w[lane], wi = w;
+      for (int d = 1; d < 32; d <<= 1) { const int64_t o = __shfl_up_sync(0xffffffffu, wi, d); if (lane >= d) wi += o; }
+      s_w[lane] = wi - w;
+    }
+    __syncthreads();
+    const int64_t carry = s_carry;
+    if (i < n) dst[i] = carry + s_w[warp] + incl - x;
+    __syncthreads();
+    if (threadIdx.x == 1023) s_carry = carry + s_w[31] + incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total = s_carry;
+}
 }  // namespace
 
 // ===========================================================================
@@ -928,6 +957,14 @@ int wg_order_key(uint64_t src, int kind, uint64_t n, uint64_t perm, uint64_t dst
   if (!n) return 0;
   k_order_key<<<grid_for(n, 256), 256, 0, g_stream>>>((const void*)(uintptr_t)src, kind, n,
                                                        (const uint32_t*)(uintptr_t)perm, (uint64_t*)(uintptr_t)dst);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int wg_exclusive_scan_i64(uint64_t src, uint64_t dst, uint64_t n, uint64_t total) {
+  NEED_INIT();
+  k_exscan_i64<<<1, 1024, 0, g_stream>>>((const int64_t*)(uintptr_t)src, (int64_t*)(uintptr_t)dst, n,
+                                         (int64_t*)(uintptr_t)total);
   CK(cudaGetLastError());
   return 0;
 }

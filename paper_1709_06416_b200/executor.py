@@ -34,7 +34,7 @@ from . import runtime as rt
 from . import semantics as sem
 from .builders_dev import (_RANGE_HINTS, _finish_small, AppenderDev, DDict, DGroups, DictDev, GroupDev, MergerDev, VecMergerDev,
                            dict_payload, finish_dict, finish_groups, gather_cols, sort_perm, tovec)
-from .codegen import DEFER_DICT, PIPE_STAGES, BSpec, IterSpec, generate, rpart_ok, rpart_table_slots
+from .codegen import DEFER_DICT, PIPE_STAGES, SCAN2, BSpec, IterSpec, generate, rpart_ok, rpart_table_slots
 from .columns import Col, DVec, to_device, to_payload, dvec_from_cols
 from .irtypes import (BOOL, F32, F64, I64, SIZE, identity_value, Builder, DeviceUnsupported as _DU, Dict, DictMerger, Function,
                       GroupBuilder, Merger, Scalar, Simd, Struct, Vec, VecBuilder, VecMerger, is_flat, leaves)
@@ -574,7 +574,7 @@ class Ctx:
                 _plan_cache[key] = cached
         plan, kern = cached[0], cached[1]
         sizes = None
-        if any(b.extra.get("unbounded") for b in plan.builders):
+        if any(b.extra.get("unbounded") for b in plan.builders) or (plan.schedule == "scan" and SCAN2):
             # flatmap: appends inside data-dependent nested loops -- size the
             # output with a count-only pre-pass of the same body
             ckey = key + ("count",)
@@ -601,23 +601,39 @@ class Ctx:
         return builders
 
     def _count_pass(self, plan, kern, count, datas, windows, bmap, captures):
-        """Launch the count-only kernel; returns {builder id: appends}."""
+        """Launch the count-only kernel.  Returns {builder id: appends}; with
+        the two-pass schedule also {builder id ("tofs", bid): tile offsets}."""
         tile = plan.block * plan.items
         ntiles = (count + tile - 1) // tile
         grid = max(1, min(ntiles, rt.sm_count() * kern.blocks_per_sm(plan.block, 0)))
         unb = [b for b in plan.builders if b.extra.get("unbounded")]
-        tot = rt.alloc(8 * len(unb))
+        scan = [b for b in plan.builders if b.mode == "scan"] if SCAN2 else []
+        tot = rt.alloc(8 * (len(unb) + len(scan)) + 8)
         rt.memset(tot.ptr, 0, 8 * len(unb))
         res = {b.bid: ("ctotal", tot.ptr + 8 * q) for q, b in enumerate(unb)}
+        tcounts = {b.bid: rt.alloc(8 * max(ntiles, 1)) for b in scan}
+        for b in scan:
+            r = res.get(b.bid, ("ctotal", 0))
+            res[b.bid] = (r[0], r[1], tcounts[b.bid].ptr)
         vals = {p.name: self._param_value(p.key, count, datas, windows, bmap, res, captures, grid, None)
                 for p in plan.params}
         kern.launch(grid, plan.block, b"".join(_pack(p.ctype, vals[p.name]) for p in plan.params), 0)
         self.launches += 1
+        out = {}
+        for q, b in enumerate(scan):
+            tofs = rt.alloc(8 * max(ntiles, 1))
+            rt.call("wg_exclusive_scan_i64", tcounts[b.bid].ptr, tofs.ptr, ntiles, tot.ptr + 8 * (len(unb) + q))
+            out[("tofs", b.bid)] = tofs
+            self.launches += 1
         self.dirty = True
         self.check_device()
-        arr = np.zeros(len(unb), dtype=np.int64)
+        arr = np.zeros(len(unb) + len(scan), dtype=np.int64)
         rt.d2h(arr.ctypes.data, tot.ptr, arr.nbytes)
-        return {b.bid: int(x) for b, x in zip(unb, arr)}
+        for q, b in enumerate(unb):
+            out[b.bid] = int(arr[q])
+        for q, b in enumerate(scan):
+            out[b.bid] = int(arr[len(unb) + q])
+        return out
 
     def launch(self, plan, kern, count, datas, windows, builders, bmap, captures, sizes=None):
         items = plan.items
@@ -651,11 +667,14 @@ class Ctx:
                     res[b.bid] = seg
                     self._acct_append(st, count * per)
                 elif b.mode == "scan":
-                    cap = sizes[b.bid] if b.k is None else count * b.k
+                    cap = sizes[b.bid] if (b.k is None or (sizes and b.bid in sizes)) else count * b.k
                     seg = st.new_segment(cap, False)
-                    status = rt.alloc(8 * max(ntiles, 1))
-                    rt.memset(status.ptr, 0, 8 * max(ntiles, 1))
-                    res[b.bid] = (seg, status)
+                    if sizes and ("tofs", b.bid) in sizes:
+                        res[b.bid] = (seg, None, sizes[("tofs", b.bid)])
+                    else:
+                        status = rt.alloc(8 * max(ntiles, 1))
+                        rt.memset(status.ptr, 0, 8 * max(ntiles, 1))
+                        res[b.bid] = (seg, status)
                     self._acct_append(st, cap)
             elif isinstance(b.kind, DictMerger) and b.extra.get("rpart"):
                 st.ensure(1)            # (unused) table keeps the kernel's table parameters valid
@@ -897,11 +916,15 @@ class Ctx:
                 r = res[bid]
                 if what == "ctotal":
                     return r[1]
+                if what == "tcounts":
+                    return r[2]
+                if what == "tofs":
+                    return r[2].ptr
                 if what == "col":
                     seg = r if not isinstance(r, tuple) else r[0]
                     return seg.cols[key[3]].ptr
                 if what == "status":
-                    return r[1].ptr
+                    return r[1].ptr if r[1] is not None else 0
                 if what == "total":
                     return r[0].total_buf.ptr
             if isinstance(st, VecMergerDev):

@@ -1,7 +1,3 @@
-mkdir -p gpurun_out/t2
-: > gpurun_out/t2/sweep_part.txt
-for it in 2 4 8 16; do
-  WELDGPU_PART_ITEMS=$it timeout 600 python -m pytest tests/test_gpu_configs.py -q -x -k "dict" 2>&1 | tail -1 >> gpurun_out/t2/sweep_part.txt
-  r=$(WELDGPU_PART_ITEMS=$it timeout 300 python bench.py --workload dict --steps 5 --warmup 3 --no-cpu --no-e2e 2>&1 | tail -1)
-  echo "part items=$it $(echo "$r" | python -c 'import sys,json; d=json.loads(sys.stdin.read()); r=d["roofline"]; print("dom %s %.3f ms step %.3f" % (r["kernel"], r["kernel_ms"], d["ms_per_step"]))' 2>&1 | tail -1)" >> gpurun_out/t2/sweep_part.txt
-done
+mkdir -p gpurun_out/prof
+timeout 900 ncu -f --set full --clock-control none --import-source on -k regex:wg_loop -s 2 -c 1 -o gpurun_out/prof/full_dict python bench.py --workload dict --steps 1 --warmup 3 --no-cpu --no-e2e --no-kernel-timing > gpurun_out/prof/ncu_dict.log 2>&1
+timeout 900 ncu -f --set full --clock-control none --import-source on -k regex:wg_dagg -s 1 -c 1 -o gpurun_out/prof/full_dict_dagg python bench.py --workload dict --steps 1 --warmup 3 --no-cpu --no-e2e --no-kernel-timing > /dev/null 2>&1
