@@ -505,9 +505,24 @@ def finish_dict(d: DictDev, dict_ty):
     kw, vw, n = d.compact()
     kcols = _words_to_cols(kw, d.kks, d.lay, n)
     vcols = _value_words_to_cols(vw, d.vks, n)
-    perm = sort_perm(kcols, n)
-    kcols = gather_cols(kcols, perm, n)
-    vcols = gather_cols(vcols, perm, n)
+    if len(kcols) == 1 and len(vcols) == 1 and d.kks[0] in (BOOL, I32, I64) and 1 < n < (1 << 32):
+        # one integer key leaf, one value leaf: the groupbuilder finisher's
+        # stable sort on the varying key bits carries the value through the
+        # radix passes (no permutation + gathers); keys are distinct, so the
+        # runs are the entries themselves
+        uk = Col.alloc(d.kks[0], n)
+        offs = Col.alloc(I64, n + 1)
+        vo = Col.alloc(vcols[0].kind, n)
+        K = ctypes.c_uint64(0)
+        rt.call("wg_group_finish1", kcols[0].ptr, KIND_CODE[d.kks[0]], vcols[0].ptr, SIZE[vcols[0].kind], n,
+                uk.ptr, offs.ptr, vo.ptr, ctypes.byref(K))
+        if K.value != n:
+            raise RuntimeError(f"dictmerger result has {K.value} distinct keys, expected {n}")
+        kcols, vcols = [uk], [vo]
+    else:
+        perm = sort_perm(kcols, n)
+        kcols = gather_cols(kcols, perm, n)
+        vcols = gather_cols(vcols, perm, n)
     if n and d.nw == 1:
         from .codegen import rpart_ok
         if d.hint_key is not None and rpart_ok(d.kks):
