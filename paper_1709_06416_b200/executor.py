@@ -816,6 +816,11 @@ class Ctx:
             st.acct = getattr(st, "acct", 0) + nbytes
 
     def _dict_regrow(self, st: DictDev, spilled):
+        global REGROWS
+        REGROWS += 1
+        self._dict_regrow_(st, spilled)
+
+    def _dict_regrow_(self, st: DictDev, spilled):
         """Grow the table 4x, re-insert existing entries and replay the
         spilled merges (all folds are commutative)."""
         import ctypes as _ct
@@ -1110,6 +1115,7 @@ RPART = _os.environ.get("WELDGPU_RPART", "0") == "1"
 RPART_MAX_PARTS = 4096
 _RPART_BAD = set()      # loops whose range-partitioned run overflowed once
 RPART_RUNS = 0
+REGROWS = 0         # dictmerger tables grown after spills (test instrumentation)
 
 
 class _RpartFallback(Exception):

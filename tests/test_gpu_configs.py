@@ -210,3 +210,46 @@ def test_group_skewed_windows_preserve_order(keys):
     np.testing.assert_array_equal(got[0], ks)
     np.testing.assert_array_equal(got[1].offsets, offs)
     np.testing.assert_array_equal(got[1].values, vs)
+
+
+def test_dict_partitioned_second_run_matches_oracle():
+    """The second evaluate of the C4a loop sees > 1M distinct keys from the
+    first and switches to the hash-partitioned two-kernel mode (2048-row
+    tiles bucketed in shared memory); the result must equal the oracle."""
+    import paper_1709_06416_b200 as wg
+    from oracle import weld_oracle
+    from paper_1709_06416_b200 import workloads as W
+    from weldmill.engine import EngineConfig, Value
+    wl = W.WORKLOADS["dict"]
+    tree = W.compile_program(wl)
+    types = W.input_types(wl)
+    cols = W.host_columns(wl, (4 << 20) + 11)
+    env = {c: Value(types[c], a) for c, a in cols.items()}
+    ks, vs = weld_oracle.dict_sum(cols)
+    for _ in range(2):
+        got = wg.evaluate(tree, env, EngineConfig(memory_limit=1 << 45), {}, result="numpy")[0].data
+        np.testing.assert_array_equal(got[0], ks)
+        np.testing.assert_array_equal(got[1], vs)
+
+
+def test_dict_table_regrows_when_keys_outgrow_the_hint():
+    """A loop sized from a small previous run spills past its table on a
+    much larger input: the spilled merges are replayed into a grown table
+    (settled lazily) and nothing is lost."""
+    import paper_1709_06416_b200 as wg
+    from oracle import weld_oracle
+    from paper_1709_06416_b200 import workloads as W
+    from weldmill.engine import EngineConfig, Value
+    wl = W.WORKLOADS["dict"]
+    tree = W.compile_program(wl)
+    types = W.input_types(wl)
+    from paper_1709_06416_b200 import executor
+    before = executor.REGROWS
+    for n in (5000, 900_000):
+        cols = W.host_columns(wl, n)
+        env = {c: Value(types[c], a) for c, a in cols.items()}
+        got = wg.evaluate(tree, env, EngineConfig(memory_limit=1 << 45), {}, result="numpy")[0].data
+        ks, vs = weld_oracle.dict_sum(cols)
+        np.testing.assert_array_equal(got[0], ks)
+        np.testing.assert_array_equal(got[1], vs)
+    assert executor.REGROWS > before
