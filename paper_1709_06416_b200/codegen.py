@@ -1368,7 +1368,7 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
     # the most stages that do not lower the kernel's occupancy.
     # Scan kernels use it too: with a persistent, fully resident grid the
     # static round-robin tile order is a valid look-back order.
-    pipe = bool(PIPE and (SCAN_PIPE or not scan_bs) and loads
+    pipe = bool(PIPE and (SCAN_PIPE or SCAN2 or not scan_bs) and loads
                 and all((not it.strided) and it.aligned for it in iters))
     pipe_off = pipe_stage_bytes = 0
     pipe_col_off = []
@@ -1520,7 +1520,7 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
                 out.append("    __syncthreads();")
         return out
 
-    if scan_bs and SCAN2:
+    if scan_bs and SCAN2 and not pipe:
         # two-pass schedule: static grid-stride tiles, columns of the next
         # tile in flight (register double buffering) -- tile offsets known
         src.extend(decl_lines("", "  "))
