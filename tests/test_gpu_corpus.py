@@ -88,3 +88,41 @@ def test_unsupported_programs_fail_loudly(front):
     vals = {"v": Value(env["v"], [0, 1]), "vv": Value(env["vv"], [[1, 2], [3]])}
     with pytest.raises(wg.DeviceUnsupported):
         wg.evaluate(optimize(typed)[0], vals)
+
+
+CORPUS2 = load_golden("corpus_s2.json")["programs"]
+
+
+@pytest.mark.parametrize("level", ["O3", "none"])
+def test_corpus_second_seed_parity(front, level):
+    """The same generator with another seed (tests/golden/make_corpus2.py):
+    different constants and three fresh input sets per program, expected
+    values (or runtime error classes) from the reference engine."""
+    from weldmill.engine import Value
+    from weldmill.optim import optimize
+    import paper_1709_06416_b200 as wg
+
+    failures = []
+    checked = 0
+    for p in CORPUS2:
+        typed, env = front(p["source"], p["inputs"])
+        tree = optimize(typed, _level(level))[0]
+        for case in p["cases"]:
+            vals = {k: Value(env[k], v) for k, v in case["inputs"].items()}
+            try:
+                got = norm(wg.evaluate(tree, vals)[0].data)
+            except Exception as exc:
+                if "error" in case and type(exc).__name__ == case["error"]:
+                    checked += 1
+                    continue
+                failures.append(f"{p['name']}: {type(exc).__name__}: {str(exc)[:200]}")
+                continue
+            if "error" in case:
+                failures.append(f"{p['name']}: expected {case['error']}, got a value")
+                continue
+            want = case["expected"]
+            ok = approx_equal(got, want, F64_TOL) if p["is_float"] else got == want
+            if not ok:
+                failures.append(f"{p['name']}: {first_diff(got, want, F64_TOL)}")
+            checked += 1
+    assert not failures, f"{len(failures)} failures ({checked} ok):\n" + "\n".join(failures[:40])
