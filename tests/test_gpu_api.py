@@ -33,10 +33,13 @@ def _run(src, inputs):
 @pytest.mark.parametrize("src,inputs", PROGRAMS, ids=[p[0][:40] for p in PROGRAMS])
 def test_public_api_bytes_match_reference(src, inputs):
     import paper_1709_06416_b200 as wg
+    from paper_1709_06416_b200 import runtime as rt
     want = _run(src, inputs)          # reference CPU engine
     wg.install()
     try:
+        before = rt.LAUNCHES[0]
         got = _run(src, inputs)       # same API, B200 executor underneath
+        assert rt.LAUNCHES[0] > before    # the device path ran
     finally:
         wg.uninstall()
     assert got == want
@@ -53,3 +56,39 @@ def test_public_api_staged_errors_match_reference():
     finally:
         wg.uninstall()
     assert want[0] is False and got == want
+
+
+def test_reference_cli_runs_on_the_gpu(tmp_path, capsys):
+    """weldmill's own CLI (`weldmill run prog --inputs manifest`, cli.py:188-213)
+    with install(): the known answers of the reference's CLI tests
+    (tests/test_cli.py: filter-sum 1300000; a struct of results [[2, 3, 4], 6])
+    and the same --out boundary bytes as the CPU engine."""
+    import json
+    import paper_1709_06416_b200 as wg
+    from weldmill import cli
+    (tmp_path / "prog.ir").write_text(
+        "result(for(v0, merger[i64, +], (b, i, x) => if (x > 500000, merge(b, x), b)))")
+    (tmp_path / "two.ir").write_text(
+        "data := [1, 2, 3];\nr1 := map(data, (x) => x + 1);\nr2 := reduce(data, 0, (x, y) => x + y);\n{r1, r2}\n")
+    (tmp_path / "m.json").write_text(json.dumps(
+        [{"name": "v0", "type": "vec[i64]", "value": [600000, 400000, 700000]}]))
+
+    def run(*argv):
+        capsys.readouterr()
+        assert cli.main(list(argv)) == 0
+        return json.loads(capsys.readouterr().out.strip().splitlines()[0])
+
+    cpu_out = tmp_path / "cpu.bin"
+    run("run", str(tmp_path / "prog.ir"), "--inputs", str(tmp_path / "m.json"), "--out", str(cpu_out))
+    from paper_1709_06416_b200 import runtime as rt
+    wg.install()
+    try:
+        before = rt.LAUNCHES[0]
+        gpu_out = tmp_path / "gpu.bin"
+        assert run("run", str(tmp_path / "prog.ir"), "--inputs", str(tmp_path / "m.json"),
+                   "--out", str(gpu_out)) == 1300000
+        assert run("run", str(tmp_path / "two.ir")) == [[2, 3, 4], 6]
+        assert rt.LAUNCHES[0] > before
+    finally:
+        wg.uninstall()
+    assert gpu_out.read_bytes() == cpu_out.read_bytes()
