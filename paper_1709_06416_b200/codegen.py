@@ -34,6 +34,7 @@ Per builder (reference state classes in engine/builders.py):
 from __future__ import annotations
 
 import math
+import re
 import struct as _struct
 from dataclasses import dataclass, field
 
@@ -68,6 +69,7 @@ SCAN_PREFETCH = _os.environ.get("WELDGPU_SCAN_PREFETCH", "0") == "1"
 LB_PER = int(_os.environ.get("WELDGPU_LB_PER", "1"))
 LB_SLEEP = int(_os.environ.get("WELDGPU_LB_SLEEP", "64"))
 SCAN_PIPE = _os.environ.get("WELDGPU_SCAN_PIPE", "0") == "1"
+SOA = _os.environ.get("WELDGPU_SOA", "1") == "1"      # statement-wise item loops for straight-line bodies
 # two-pass order-preserving appenders: a count-only pre-pass writes per-tile
 # append counts, an exclusive scan turns them into tile offsets, and the
 # main kernel stores without a decoupled look-back
@@ -440,7 +442,10 @@ class Gen:
             return Lanes([self.let(e.kind, self._cast_c(src.kind, e.kind, x.c)) for x in v.lanes], e.kind)
         return self.let(e.kind, self._cast_c(src.kind, e.kind, v.c))
 
+    ext_calls = 0
+
     def ex_ExternCall(self, e, env):
+        self.ext_calls += 1
         if e.name not in self.externs:
             from weldmill.errors import ExternCallUnknown
             raise ExternCallUnknown(f"no extern function {e.name!r} registered")
@@ -1464,6 +1469,17 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
                 out.append(f"#pragma unroll\n    for (int q = 0; q < ITEMS; ++q) dkf{b.bid}[q] = false;")
                 for f, kk in enumerate(leaves(b.kind.value)):
                     out.append(f"    {CTYPE[kk]} dkv{b.bid}_{f}[ITEMS];")
+        # (only for bodies with math-library calls: their long FP64 dependency
+        # chains are what interleaving hides; plain streaming bodies keep the
+        # per-item form, which schedules their loads/stores better)
+        soa = (_soa_body(body_a) if (SOA and ITEMS > 1 and not scan_bs and g.ext_calls) else None)
+        if soa is not None:
+            # full tiles: statement-by-statement over the thread's items, so
+            # the items' independent libdevice chains (erf, exp, log) sit
+            # side by side in straight-line code and interleave
+            out.append("    if (full) {")
+            out.extend(soa)
+            out.append("    } else {")
         out.append("#pragma unroll")
         out.append("    for (int j = 0; j < ITEMS; ++j) {")
         out.append("      const i64 li = t0 + j;")
@@ -1472,6 +1488,8 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
         out.extend(body_a)
         out.append("      }")
         out.append("    }")
+        if soa is not None:
+            out.append("    }")
         for b in g.bspecs:
             if b.mode == "direct" and b.extra.get("buffered"):
                 for f, kk in enumerate(b.extra["kinds"]):
@@ -1775,6 +1793,51 @@ def is_flat_type(t):
     if isinstance(t, Struct):
         return all(is_flat_type(f) for f in t.fields)
     return False
+
+
+_SOA_LET = re.compile(r"^\s*const (\w+) (t\d+) = (.*);$")
+_SOA_STORE = re.compile(r"^\s*(o\d+_\d+)\[j \* (\d+) \+ (c\d+)\] = (.*);$")
+_SOA_CINIT = re.compile(r"^\s*int (c\d+) = 0;$")
+_SOA_CINC = re.compile(r"^\s*(c\d+) \+= 1;$")
+
+
+def _soa_body(lines):
+    """Statement-wise form of a straight-line loop body (lets and buffered
+    direct appends only): every temporary becomes an ITEMS-array filled by
+    its own unrolled item loop.  Returns None for any other body shape."""
+    out = []
+    cval = {}
+    temps = set()
+
+    def sub(expr):
+        expr = re.sub(r"\b(t\d+)\b", lambda m: m.group(1) + "[j]" if m.group(1) in temps else m.group(1), expr)
+        expr = re.sub(r"\bli\b", "(t0 + j)", expr)
+        return re.sub(r"\bi\b", "(p.idx0 + t0 + j)", expr)
+
+    for ln in lines:
+        m = _SOA_LET.match(ln)
+        if m:
+            ty, name, expr = m.groups()
+            e2 = sub(expr)
+            temps.add(name)
+            out.append(f"      {ty} {name}[ITEMS];")
+            out.append(f"#pragma unroll\n      for (int j = 0; j < ITEMS; ++j) {name}[j] = {e2};")
+            continue
+        m = _SOA_CINIT.match(ln)
+        if m:
+            cval[m.group(1)] = 0
+            continue
+        m = _SOA_STORE.match(ln)
+        if m and m.group(3) in cval:
+            arr, k, c, val = m.groups()
+            out.append(f"#pragma unroll\n      for (int j = 0; j < ITEMS; ++j) {arr}[j * {k} + {cval[c]}] = {sub(val)};")
+            continue
+        m = _SOA_CINC.match(ln)
+        if m and m.group(1) in cval:
+            cval[m.group(1)] += 1
+            continue
+        return None
+    return out
 
 
 def _dict_params(g, b):
