@@ -52,7 +52,7 @@ from .irtypes import (
 
 W = 4  # SIMD_WIDTH (types.py:15)
 BLOCK = 256
-BLOCK_DEFAULT = BLOCK
+BLOCK_DEFAULT = int(__import__("os").environ.get("WELDGPU_BLOCK", str(BLOCK)))
 
 import os as _os
 
@@ -88,6 +88,16 @@ EXTERN_F64 = {
     "cbrt": "cbrt", "exp2": "exp2", "atan2": "atan2", "pow": "pow", "hypot": "hypot", "copysign": "copysign",
     "fmod": "fmod",
 }
+# WELDGPU_MATH: "tab" (default) -- erf from the shared-memory piecewise
+# polynomial table (weld_device.cuh wg_erf_tab, ~15 FP64 ops instead of ~43);
+# "estrin" -- exp/log/erf with libdevice's polynomials in Estrin form
+# (measured slower on Black-Scholes: more FP64 ops, more registers);
+# "libdevice" -- CUDA's own.
+MATH = _os.environ.get("WELDGPU_MATH", "tab")
+if MATH == "estrin":
+    EXTERN_F64.update({"exp": "wg_exp", "log": "wg_log", "erf": "wg_erf"})
+elif MATH == "tab":
+    EXTERN_F64.update({"erf": "wg_erf_tab"})
 
 
 # ---------------------------------------------------------------------------
@@ -443,6 +453,7 @@ class Gen:
         return self.let(e.kind, self._cast_c(src.kind, e.kind, v.c))
 
     ext_calls = 0
+    erf_tab = False
 
     def ex_ExternCall(self, e, env):
         self.ext_calls += 1
@@ -456,6 +467,8 @@ class Gen:
         args = [self.ex(a, env) for a in e.args]
         rk = e.ty.kind
         cargs = ", ".join(f"(double)({a.c})" for a in args)
+        if fn == "wg_erf_tab":
+            self.erf_tab = True             # kernel prologue copies the table to shared memory
         if rk == F64:
             return self.let(F64, f"{fn}({cargs})")
         if rk == F32:
@@ -1408,6 +1421,8 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
     lb = f"BLOCK, {MINBLOCKS}" if MINBLOCKS else "BLOCK"
     src.append(f'extern "C" __global__ void __launch_bounds__({lb}) {name}(const Params p) {{')
     src.append("  extern __shared__ __align__(16) u64 wg_dyn_smem[];")
+    if g.erf_tab:
+        smem_init.append("wg_erf_tab_init();")
     src.extend("  " + d for d in smem_decls)
     src.extend("  " + d for d in smem_init)
     if smem_init:
@@ -1743,6 +1758,8 @@ def _count_plan(g, lam, body_env, loads, iters, ITEMS, BLOCK, scan_bs, name):
     src += [f"  {p_.ctype} {p_.name};" for p_ in g.params]
     src += ["};", f'extern "C" __global__ void __launch_bounds__(BLOCK) {name}(const Params p) {{',
             "  const i64 n = p.n;", "  const i64 ntiles = (n + TILE - 1) / TILE;"]
+    if g.erf_tab:
+        src.append("  wg_erf_tab_init(); __syncthreads();")
     src += [f"  i64 tc{b.bid} = 0;" for b in unb]
     src.append("  for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {")
     for (arr, st, kk, per, k, l, col) in loads:

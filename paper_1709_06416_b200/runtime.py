@@ -290,10 +290,17 @@ def header_text():
     return _header_text
 
 
+_ERF_TAB_PATH = os.path.join(_HERE, "csrc", "wg_erf_table.h")
+_erf_tab_text = None
+
+
 def _nvrtc_args(src):
-    hdr = header_text().encode()
-    hs = (c_char_p * 1)(hdr)
-    hn = (c_char_p * 1)(b"weld_device.cuh")
+    global _erf_tab_text
+    if _erf_tab_text is None:
+        with open(_ERF_TAB_PATH) as f:
+            _erf_tab_text = f.read()
+    hs = (c_char_p * 2)(header_text().encode(), _erf_tab_text.encode())
+    hn = (c_char_p * 2)(b"weld_device.cuh", b"wg_erf_table.h")
     opts = [o.encode() for o in NVRTC_OPTS]
     oa = (c_char_p * len(opts))(*opts)
     return hs, hn, oa, len(opts)
@@ -306,7 +313,7 @@ def compile_check(src: str, name="weld_loop.cu"):
     hs, hn, oa, no = _nvrtc_args(src)
     sz = u64(0)
     log = ctypes.create_string_buffer(1 << 16)
-    rc = L.wg_compile_check(src.encode(), name.encode(), 1, hs, hn, no, oa, ctypes.byref(sz), log, 1 << 16)
+    rc = L.wg_compile_check(src.encode(), name.encode(), 2, hs, hn, no, oa, ctypes.byref(sz), log, 1 << 16)
     if rc != 0:
         raise WeldGpuError(L.wg_last_error().decode(errors="replace"))
     return sz.value
@@ -360,10 +367,10 @@ def compile_ptx(src: str, name="weld_loop.cu") -> str:
     hs, hn, oa, no = _nvrtc_args(src)
     size = u64(0)
     log = ctypes.create_string_buffer(1 << 16)
-    if L.wg_compile_ptx(src.encode(), name.encode(), 1, hs, hn, no, oa, None, 0, ctypes.byref(size), log, 1 << 16):
+    if L.wg_compile_ptx(src.encode(), name.encode(), 2, hs, hn, no, oa, None, 0, ctypes.byref(size), log, 1 << 16):
         raise WeldGpuError(L.wg_last_error().decode(errors="replace"))
     buf = ctypes.create_string_buffer(size.value)
-    _check(L.wg_compile_ptx(src.encode(), name.encode(), 1, hs, hn, no, oa, buf, size.value, ctypes.byref(size),
+    _check(L.wg_compile_ptx(src.encode(), name.encode(), 2, hs, hn, no, oa, buf, size.value, ctypes.byref(size),
                             log, 1 << 16))
     return buf.value.decode()
 
@@ -453,7 +460,7 @@ def get_kernel(src: str, name: str) -> Kernel:
                 _check(L.wg_module_load(const_pool_ptx(ptx).encode() + b"\0", ctypes.byref(m)))
                 rc = 0
             else:
-                rc = L.wg_compile(src.encode(), f"wg_{key[:12]}.cu".encode(), 1, hs, hn, no, oa, ctypes.byref(m),
+                rc = L.wg_compile(src.encode(), f"wg_{key[:12]}.cu".encode(), 2, hs, hn, no, oa, ctypes.byref(m),
                                   log, 1 << 16)
             if rc != 0:
                 raise WeldGpuError(L.wg_last_error().decode(errors="replace"))
