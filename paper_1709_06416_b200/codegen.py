@@ -69,7 +69,7 @@ SCAN_PREFETCH = _os.environ.get("WELDGPU_SCAN_PREFETCH", "0") == "1"
 LB_PER = int(_os.environ.get("WELDGPU_LB_PER", "1"))
 LB_SLEEP = int(_os.environ.get("WELDGPU_LB_SLEEP", "64"))
 SCAN_PIPE = _os.environ.get("WELDGPU_SCAN_PIPE", "0") == "1"
-SOA = _os.environ.get("WELDGPU_SOA", "1") == "1"      # statement-wise item loops for straight-line bodies
+SOA = _os.environ.get("WELDGPU_SOA", "0") == "1"      # statement-wise item loops for straight-line bodies
 # two-pass order-preserving appenders: a count-only pre-pass writes per-tile
 # append counts, an exclusive scan turns them into tile offsets, and the
 # main kernel stores without a decoupled look-back
@@ -77,6 +77,11 @@ SCAN2 = _os.environ.get("WELDGPU_SCAN2", "0") == "1"
 PART_ITEMS = int(_os.environ.get("WELDGPU_PART_ITEMS", "8"))
 PIPE_STAGES = int(_os.environ.get("WELDGPU_PIPE_STAGES", "4"))
 PIPE_MAX_STAGES = 8
+# Stage release in the bulk-async pipeline: 0 = __syncthreads after every
+# warp has read the stage; 1 = per-stage "empty" mbarriers (each warp arrives
+# after its reads; only the producer thread waits, before refilling);
+# 2 = as 1 with the refill of a stage deferred by one tile.
+PIPE_EMPTY = int(_os.environ.get("WELDGPU_PIPE_EMPTY", "0"))
 PIPE_SMEM_BUDGET = int(_os.environ.get("WELDGPU_PIPE_SMEM", str(48 * 1024)))
 
 # Extern names recognised as device intrinsics (the reference resolves
@@ -97,6 +102,8 @@ MATH = _os.environ.get("WELDGPU_MATH", "tab")
 if MATH == "estrin":
     EXTERN_F64.update({"exp": "wg_exp", "log": "wg_log", "erf": "wg_erf"})
 elif MATH == "tab":
+    EXTERN_F64.update({"erf": "wg_erf_tab", "log": "wg_log_tab"})
+elif MATH == "taberf":
     EXTERN_F64.update({"erf": "wg_erf_tab"})
 
 
@@ -453,7 +460,7 @@ class Gen:
         return self.let(e.kind, self._cast_c(src.kind, e.kind, v.c))
 
     ext_calls = 0
-    erf_tab = False
+    tabs = frozenset()
 
     def ex_ExternCall(self, e, env):
         self.ext_calls += 1
@@ -467,8 +474,8 @@ class Gen:
         args = [self.ex(a, env) for a in e.args]
         rk = e.ty.kind
         cargs = ", ".join(f"(double)({a.c})" for a in args)
-        if fn == "wg_erf_tab":
-            self.erf_tab = True             # kernel prologue copies the table to shared memory
+        if fn.endswith("_tab"):
+            self.tabs = self.tabs | {fn}    # kernel prologue copies the table to shared memory
         if rk == F64:
             return self.let(F64, f"{fn}({cargs})")
         if rk == F32:
@@ -1421,8 +1428,8 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
     lb = f"BLOCK, {MINBLOCKS}" if MINBLOCKS else "BLOCK"
     src.append(f'extern "C" __global__ void __launch_bounds__({lb}) {name}(const Params p) {{')
     src.append("  extern __shared__ __align__(16) u64 wg_dyn_smem[];")
-    if g.erf_tab:
-        smem_init.append("wg_erf_tab_init();")
+    for t in sorted(g.tabs):
+        smem_init.append(f"{t}_init();")
     src.extend("  " + d for d in smem_decls)
     src.extend("  " + d for d in smem_init)
     if smem_init:
@@ -1615,8 +1622,12 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
         src.append(f"  __shared__ __align__(8) u64 wg_bar[{PIPE_MAX_STAGES}];")
         src.append("  const i64 nfull = n / TILE;")
         src.append("  const i64 nmy = (nfull > (i64)blockIdx.x) ? (nfull - 1 - (i64)blockIdx.x) / gridDim.x + 1 : 0;")
+        if PIPE_EMPTY:
+            src.append(f"  __shared__ __align__(8) u64 wg_ebar[{PIPE_MAX_STAGES}];")
         src.append("  if (threadIdx.x == 0) {")
         src.append(f"    for (int s_ = 0; s_ < {pipe_stages}; ++s_) wg_mbar_init(&wg_bar[s_], 1);")
+        if PIPE_EMPTY:
+            src.append(f"    for (int s_ = 0; s_ < {pipe_stages}; ++s_) wg_mbar_init(&wg_ebar[s_], BLOCK / 32);")
         src.append("    wg_fence_mbar_init();")
         src.append("  }")
         src.append("  __syncthreads();")
@@ -1640,10 +1651,19 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
             cnt = f"ITEMS * {per}" if per > 1 else "ITEMS"
             src.append(f"      wg_lds_contig<{st}, {cnt}>((const {st}*)(sg_ + {off}) + threadIdx.x * {cnt}, {arr}); ")
         src.append("    }")
-        src.append("    __syncthreads();")
-        src.append(f"    if (threadIdx.x == 0 && kk_ + {pipe_stages} < nmy) {{")
-        src.append("      wg_fence_proxy_async();")
-        src.append(f"      const i64 k_ = kk_ + {pipe_stages};")
+        if PIPE_EMPTY:
+            dl = 1 if PIPE_EMPTY == 2 else 0
+            src.append(f"    __syncwarp(); if ((threadIdx.x & 31) == 0) wg_mbar_arrive(&wg_ebar[kk_ % {pipe_stages}]);")
+            src.append(f"    if (threadIdx.x == 0 && kk_ >= {dl} && kk_ - {dl} + {pipe_stages} < nmy) {{")
+            src.append(f"      const i64 kr_ = kk_ - {dl};")
+            src.append(f"      wg_mbar_wait(&wg_ebar[kr_ % {pipe_stages}], (unsigned)((kr_ / {pipe_stages}) & 1));")
+            src.append("      wg_fence_proxy_async();")
+            src.append(f"      const i64 k_ = kr_ + {pipe_stages};")
+        else:
+            src.append("    __syncthreads();")
+            src.append(f"    if (threadIdx.x == 0 && kk_ + {pipe_stages} < nmy) {{")
+            src.append("      wg_fence_proxy_async();")
+            src.append(f"      const i64 k_ = kk_ + {pipe_stages};")
         src.extend("  " + x for x in issue)
         src.append("    }")
         src.extend(tile_body())
@@ -1758,8 +1778,8 @@ def _count_plan(g, lam, body_env, loads, iters, ITEMS, BLOCK, scan_bs, name):
     src += [f"  {p_.ctype} {p_.name};" for p_ in g.params]
     src += ["};", f'extern "C" __global__ void __launch_bounds__(BLOCK) {name}(const Params p) {{',
             "  const i64 n = p.n;", "  const i64 ntiles = (n + TILE - 1) / TILE;"]
-    if g.erf_tab:
-        src.append("  wg_erf_tab_init(); __syncthreads();")
+    if g.tabs:
+        src.append("  " + " ".join(f"{t}_init();" for t in sorted(g.tabs)) + " __syncthreads();")
     src += [f"  i64 tc{b.bid} = 0;" for b in unb]
     src.append("  for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {")
     for (arr, st, kk, per, k, l, col) in loads:

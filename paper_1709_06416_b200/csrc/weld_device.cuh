@@ -666,6 +666,9 @@ __device__ __forceinline__ void wg_bulk_g2s(void* dst, const void* src, unsigned
       "l"(src), "r"(bytes), "r"(wg_saddr(bar))
       : "memory");
 }
+__device__ __forceinline__ void wg_mbar_arrive(u64* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(wg_saddr(bar)) : "memory");
+}
 __device__ __forceinline__ void wg_mbar_wait(u64* bar, unsigned phase) {
   asm volatile(
       "{\n .reg .pred P1;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n @!P1 bra WAIT_%=;\n}" ::"r"(
@@ -850,4 +853,51 @@ __device__ __forceinline__ double wg_erf_tab(double x) {
   res = (a >= 5.9215871957945) ? 1.0 : res;                  // erf rounds to 1 beyond here
   res = (a != a) ? x : res;
   return copysign(res, x);
+}
+
+// log from a 128-row shared-memory table (tools/gen_log_table.py): x = 2^k z,
+// row i = top 7 bits of bits(x) - OFF, r = z invc_i - 1 (|r| <= 2^-8, one fma),
+// log x = k ln2 + logc_i + log1p(r) with the large sums compensated; <= 1 ulp
+// (checked against mpmath by the generator and tests/test_gpu_math.py), 20
+// FP64 operations and no reciprocal iteration (libdevice: ~30 + MUFU.RCP64H).
+#include "wg_log_table.h"
+__shared__ __align__(16) double wg_log_s[2 * WG_LOG_ROWS];
+__shared__ double wg_log_lo_s[WG_LOG_ROWS];
+__device__ __forceinline__ void wg_log_tab_init() {
+  for (int q = threadIdx.x; q < 2 * WG_LOG_ROWS; q += blockDim.x) wg_log_s[q] = __longlong_as_double((long long)WG_LOG_TAB[q]);
+  for (int q = threadIdx.x; q < WG_LOG_ROWS; q += blockDim.x) wg_log_lo_s[q] = __longlong_as_double((long long)WG_LOG_LO[q]);
+}
+__device__ __forceinline__ double wg_log_tab(double x) {
+  unsigned long long ix = (unsigned long long)__double_as_longlong(x);
+  int hi = (int)(ix >> 32);
+  int kadj = 0;
+  if (__builtin_expect(hi < 0x00100000, 0)) {           // subnormal, zero or negative
+    x *= 18014398509481984.0;                           // 2^54
+    ix = (unsigned long long)__double_as_longlong(x);
+    hi = (int)(ix >> 32);
+    kadj = -54;
+  }
+  if (__builtin_expect((unsigned)(hi - 1) > 0x7FEFFFFEu, 0)) {   // <= 0, inf, nan
+    const double inf = __longlong_as_double(0x7FF0000000000000LL);
+    return (ix << 1) == 0 ? -inf : fma(x, inf, inf);
+  }
+  const unsigned long long tmp = ix - WG_LOG_OFF;
+  const int i = (int)(tmp >> 45) & (WG_LOG_ROWS - 1);
+  const int k = (int)((long long)tmp >> 52) + kadj;
+  const double z = __longlong_as_double((long long)(ix - (tmp & 0xFFF0000000000000ULL)));
+  const double2 ic = reinterpret_cast<const double2*>(wg_log_s)[i];
+  const double r = fma(z, ic.x, -1.0);
+  const double kd = __hiloint2double(0x43300000, k ^ 0x80000000) - __hiloint2double(0x43300000, 0x80000000);
+  const double l2hi = __longlong_as_double((long long)WG_LOG_LN2HI);
+  const double t1 = fma(kd, l2hi, ic.y);
+  const double e1 = fma(kd, l2hi, -t1) + ic.y;
+  const double t2 = t1 + r;
+  const double e2 = (t1 - t2) + r;
+  const double lo = fma(kd, __longlong_as_double((long long)WG_LOG_LN2LO), wg_log_lo_s[i]) + (e1 + e2);
+  double q = fma(1.0 / 7.0, r, -1.0 / 6.0);
+  q = fma(q, r, 1.0 / 5.0);
+  q = fma(q, r, -0.25);
+  q = fma(q, r, 1.0 / 3.0);
+  q = fma(q, r, -0.5);
+  return t2 + (lo + (r * r) * q);
 }
