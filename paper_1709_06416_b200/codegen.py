@@ -69,6 +69,11 @@ SCAN_PREFETCH = _os.environ.get("WELDGPU_SCAN_PREFETCH", "0") == "1"
 LB_PER = int(_os.environ.get("WELDGPU_LB_PER", "1"))
 LB_SLEEP = int(_os.environ.get("WELDGPU_LB_SLEEP", "64"))
 SCAN_PIPE = _os.environ.get("WELDGPU_SCAN_PIPE", "0") == "1"
+# scan schedule: claim the next tile during the current tile's store phase
+# instead of at the top of the next iteration (one barrier and one exposed
+# atomic round trip less per tile)
+SCAN_EARLY_CLAIM = _os.environ.get("WELDGPU_SCAN_EARLY_CLAIM", "1") == "1"
+SCAN_BLOCK_128 = _os.environ.get("WELDGPU_SCAN_BLOCK_128", "1") == "1"
 SOA = _os.environ.get("WELDGPU_SOA", "0") == "1"      # statement-wise item loops for straight-line bodies
 # two-pass order-preserving appenders: a count-only pre-pass writes per-tile
 # append counts, an exclusive scan turns them into tile offsets, and the
@@ -1213,6 +1218,12 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
     if scan_bs and not (items or ITEMS_OVERRIDE):
         # larger tiles for look-back kernels: half as many tiles to resolve
         ITEMS = min(16, ITEMS * 2)
+        row = sum(SIZE[k] * (W if it.simd else 1) for it in iters for k in it.kinds)
+        if row <= 8 and BLOCK == 256 and SCAN_BLOCK_128:
+            # one 8-byte column: the same 4096-row tile on 128 threads x 32
+            # items -- half the warps wait at each tile's look-back barrier
+            # and twice the CTAs are resident (filter: 2.44 -> 2.23 ms)
+            BLOCK, ITEMS = 128, ITEMS * 2
         g.items = ITEMS
         for b in g.bspecs:
             if b.mode == "direct":
@@ -1473,7 +1484,7 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
         return [f"{ind}alignas(16) {st} {arr}{suffix}[{'ITEMS * %d' % per if per > 1 else 'ITEMS'}];"
                 for (arr, st, kk, per, k, l, col) in loads]
 
-    def tile_body(mid=None):
+    def tile_body(mid=None, claim=False):
         """Everything a thread does for one tile once its columns are in
         registers (x arrays): body, buffered stores, deferred dict merges,
         and for scan appenders the block scan + look-back + store phase."""
@@ -1551,12 +1562,21 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
             out.append("    }")
             if any(b.extra["staged"] for b in scan_bs):
                 out.append("    __syncthreads();")
+                if claim:
+                    # claim the next tile now: the atomic's latency overlaps
+                    # the store phase, and the tile is unstarted only briefly
+                    out.append("    i64 nclaim_ = 0; if (threadIdx.x == 0) nclaim_ = (i64)atomicAdd(p.tilectr, 1ULL);")
                 for si, b in enumerate(scan_bs):
                     if not b.extra["staged"]:
                         continue
                     for f, kk in enumerate(b.extra["kinds"]):
                         out.append(f"    for (int q = threadIdx.x; q < (int)agg{b.bid}; q += BLOCK) "
                                    f"__stcs(p.a{b.bid}_{f} + s_toff[{si}] + q, s_ap{b.bid}_{f}[q]);")
+                if claim:
+                    out.append("    if (threadIdx.x == 0) s_tile[0] = nclaim_;")
+                out.append("    __syncthreads();")
+            elif claim:
+                out.append("    if (threadIdx.x == 0) s_tile[0] = (i64)atomicAdd(p.tilectr, 1ULL);")
                 out.append("    __syncthreads();")
         return out
 
@@ -1580,14 +1600,19 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
     elif scan_bs and not pipe and not SCAN_PREFETCH:
         # Dynamic tiles, claimed in order through an atomic counter (so every
         # predecessor a tile's look-back waits on is held by a running CTA).
-        src.append("  while (true) {")
-        src.append("    if (threadIdx.x == 0) s_tile[0] = (i64)atomicAdd(p.tilectr, 1ULL);")
-        src.append("    __syncthreads();")
+        if SCAN_EARLY_CLAIM:
+            src.append("  if (threadIdx.x == 0) s_tile[0] = (i64)atomicAdd(p.tilectr, 1ULL);")
+            src.append("  __syncthreads();")
+            src.append("  while (true) {")
+        else:
+            src.append("  while (true) {")
+            src.append("    if (threadIdx.x == 0) s_tile[0] = (i64)atomicAdd(p.tilectr, 1ULL);")
+            src.append("    __syncthreads();")
         src.append("    const i64 tile = s_tile[0];")
         src.append("    if (tile >= ntiles) break;")
         src.extend(decl_lines("", "    "))
         src.extend(load_lines("tile", "", "    "))
-        src.extend(tile_body())
+        src.extend(tile_body(claim=SCAN_EARLY_CLAIM))
         src.append("  }")
     elif scan_bs and not pipe:
         # (experimental) the next tile is claimed at the top of the current
