@@ -1476,6 +1476,7 @@ def _stream_evaluate(ctx, e, frame, cand):
         _STREAM_LOOPS[id(loop)] = loop2
     loop2 = loop2[1]
     outs = {}
+    scan_q, scan_off = [], {}
     ev_in = [rt.Event() for _ in range(nch)]
     ev_k = [rt.Event() for _ in range(nch)]
     try:
@@ -1509,13 +1510,20 @@ def _stream_evaluate(ctx, e, frame, cand):
                 if isinstance(st, AppenderDev) and st.segments:
                     seg = st.segments[-1]
                     if seg.n is None:
+                        # order-preserving (scan) appends: the count is on the
+                        # device; copy out one chunk later, when it is known
+                        scan_q.append((c, st, seg, m))
                         continue
                     if id(st) not in outs:
-                        outs[id(st)] = [pinned_empty(n * (seg.n // m if m else 1), {"bool": "u1", "i32": "<i4", "i64": "<i8", "f32": "<f4", "f64": "<f8"}[k])
-                                        for k in st.kinds]
+                        outs[id(st)] = [pinned_empty(n * (seg.n // m if m else 1), _NPK[k]) for k in st.kinds]
                     per = seg.n // m if m else 1
                     for arr, col in zip(outs[id(st)], seg.cols):
                         rt.d2h_async(arr.ctypes.data + lo * per * arr.itemsize, col.ptr, seg.n * arr.itemsize)
+            # the previous chunk's scan appends: waiting for its kernel costs
+            # nothing (the next input copy reuses its buffers and waits too)
+            _drain_scan(scan_q, outs, scan_off, n, before=c)
+        rt.stream_select(2)
+        _drain_scan(scan_q, outs, scan_off, n, before=nch)
     finally:
         rt.stream_select(0)
         ctx.idx0 = 0
@@ -1528,8 +1536,10 @@ def _stream_evaluate(ctx, e, frame, cand):
         st.consume()
         if isinstance(st, MergerDev):
             return st.read()
-        if id(st) in outs and all(s.n is not None for s in st.segments):
+        if outs.get(id(st)) is not None and all(s.n is not None for s in st.segments):
             o = outs[id(st)]
+            if id(st) in scan_off:
+                o = [a[:scan_off[id(st)]] for a in o]
             return o[0] if isinstance(st.kind.elem, Scalar) else tuple(o)
         cols, tot = st.concat() if st.segments else ([Col.alloc(k, 0) for k in st.kinds], 0)
         from .columns import to_numpy
@@ -1540,6 +1550,32 @@ def _stream_evaluate(ctx, e, frame, cand):
         return _shape_like(bval, lambda: build(None, it_))
     finally:
         del build   # no closure cycle may keep the pinned results' pool blocks alive
+
+
+_NPK = {"bool": "u1", "i32": "<i4", "i64": "<i8", "f32": "<f4", "f64": "<f8"}
+
+
+def _drain_scan(q, outs, offs, n, before):
+    """Copy out the scan-appender chunks queued before chunk `before`: read
+    each chunk's count (stream 2 already waits on that chunk's kernel), then
+    queue the copy of exactly that many rows at the running offset."""
+    from .columns import pinned_empty
+    while q and q[0][0] < before:
+        _, st, seg, m = q.pop(0)
+        cnt = seg.length()
+        if id(st) not in outs:
+            per = max(1, -(-seg.cap // m)) if m else 1
+            outs[id(st)] = [pinned_empty(n * per, _NPK[k]) for k in st.kinds]
+            offs[id(st)] = 0
+        if outs[id(st)] is None:
+            continue
+        off = offs[id(st)]
+        if off + cnt > len(outs[id(st)][0]):
+            outs[id(st)] = None      # more appends per row than the first chunk had: result() concatenates on device
+            continue
+        for arr, col in zip(outs[id(st)], seg.cols):
+            rt.d2h_async(arr.ctypes.data + off * arr.itemsize, col.ptr, cnt * arr.itemsize)
+        offs[id(st)] = off + cnt
 
 
 def _shape_like(v, leaf):

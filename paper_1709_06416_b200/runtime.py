@@ -144,6 +144,8 @@ def call(name, *args):
 def lib():
     """Library handle with the device initialised."""
     global _inited
+    if _inited:
+        return _lib
     L = load_library()
     if not _inited:
         with _lock:
@@ -158,10 +160,15 @@ def lib():
     return L
 
 
+_SM_COUNT = [0]
+
+
 def sm_count():
-    n = c_int(0)
-    _check(lib().wg_sm_count(ctypes.byref(n)))
-    return n.value
+    if not _SM_COUNT[0]:
+        n = c_int(0)
+        _check(lib().wg_sm_count(ctypes.byref(n)))
+        _SM_COUNT[0] = n.value
+    return _SM_COUNT[0]
 
 
 def stream_handle():
@@ -262,10 +269,16 @@ def read_error():
     return c.value, i.value
 
 
+_ERR_PTR = [0]
+
+
 def error_ptr():
-    p = u64(0)
-    _check(lib().wg_error_ptr(ctypes.byref(p)))
-    return p.value
+    """Device address of the error word (allocated once at library init)."""
+    if not _ERR_PTR[0]:
+        p = u64(0)
+        _check(lib().wg_error_ptr(ctypes.byref(p)))
+        _ERR_PTR[0] = p.value
+    return _ERR_PTR[0]
 
 
 def mem_stats():
