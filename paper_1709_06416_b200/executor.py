@@ -1416,9 +1416,20 @@ def _stream_candidate(e, frame):
     loop = e.builder
     if not isinstance(loop.func, Lambda):
         return None
+    tail = None
+    inner = loop.builders
+    if (len(loop.iters) == 1 and isinstance(inner, For) and isinstance(inner.func, Lambda)
+            and len(inner.iters) == 1 and inner.iters[0].simd and inner.iters[0].start is None
+            and isinstance(inner.iters[0].data, Ident) and isinstance(loop.iters[0].data, Ident)
+            and inner.iters[0].data.name == loop.iters[0].data.name
+            and loop.iters[0].start is not None and not loop.iters[0].simd):
+        # the vectorize pass's shape: simd main loop feeding a scalar tail
+        # loop over the last len(v) % 4 rows -- stream the simd loop, then
+        # run the tail on the device
+        tail, loop = loop, inner
     hvs = []
     for it in loop.iters:
-        if it.simd or it.start is not None or not isinstance(it.data, Ident):
+        if (it.simd and tail is None) or it.start is not None or not isinstance(it.data, Ident):
             return None
         hv = frame.get(it.data.name)
         if not isinstance(hv, HostVec) or hv._dev is not None:
@@ -1443,11 +1454,13 @@ def _stream_candidate(e, frame):
         return None
     # loop-invariant captures must be scalars (vectors would be re-uploaded per chunk)
     names = free_variables(loop.func) - {p.name for p in loop.func.params}
+    if tail is not None:
+        names |= free_variables(tail.func) - {p.name for p in tail.func.params}
     for nm in names:
         v = frame.get(nm)
         if isinstance(v, (HostVec, DVec)) or hasattr(v, "pending"):
             return None
-    return loop, hvs
+    return loop, hvs, tail
 
 
 def _stream_evaluate(ctx, e, frame, cand):
@@ -1457,9 +1470,13 @@ def _stream_evaluate(ctx, e, frame, cand):
     results).  The loop index stays global (idx0 = chunk start)."""
     from dataclasses import replace
     from .columns import Col, dvec_from_cols, pinned_empty
-    loop, hvs = cand
-    n = len(hvs[0])
+    loop, hvs, tail = cand
+    simd = tail is not None
+    n_all = len(hvs[0])
+    n = n_all - n_all % 4 if simd else n_all       # rows the streamed loop covers
     C = min(STREAM_CHUNK_ROWS, n)
+    if simd:
+        C -= C % 4
     nch = (n + C - 1) // C
     leaves_np = []
     for hv in hvs:
@@ -1500,7 +1517,7 @@ def _stream_evaluate(ctx, e, frame, cand):
             for it, hv, cols, ks in zip(loop.iters, hvs, sets[b], kinds):
                 f2[it.data.name] = dvec_from_cols(hv.ty.elem, m, [Col(cc.ptr, kk, cc.owner) for cc, kk in zip(cols, ks)])
             f2["__wg_sb"] = bval
-            ctx.idx0 = lo
+            ctx.idx0 = lo // 4 if simd else lo
             ctx.run_loop(loop2, f2, count_traversal=(c == 0))
             ev_k[c].record()
             # copy out (stream 2): this chunk's appended rows
@@ -1515,19 +1532,21 @@ def _stream_evaluate(ctx, e, frame, cand):
                         scan_q.append((c, st, seg, m))
                         continue
                     if id(st) not in outs:
-                        outs[id(st)] = [pinned_empty(n * (seg.n // m if m else 1), _NPK[k]) for k in st.kinds]
+                        outs[id(st)] = [pinned_empty(n_all * (seg.n // m if m else 1), _NPK[k]) for k in st.kinds]
                     per = seg.n // m if m else 1
                     for arr, col in zip(outs[id(st)], seg.cols):
                         rt.d2h_async(arr.ctypes.data + lo * per * arr.itemsize, col.ptr, seg.n * arr.itemsize)
             # the previous chunk's scan appends: waiting for its kernel costs
             # nothing (the next input copy reuses its buffers and waits too)
-            _drain_scan(scan_q, outs, scan_off, n, before=c)
+            _drain_scan(scan_q, outs, scan_off, n_all, before=c)
         rt.stream_select(2)
-        _drain_scan(scan_q, outs, scan_off, n, before=nch)
+        _drain_scan(scan_q, outs, scan_off, n_all, before=nch)
     finally:
         rt.stream_select(0)
         ctx.idx0 = 0
     rt.sync_all()
+    if simd and n_all > n:
+        _stream_tail(ctx, tail, frame, hvs, kinds, leaves_np, n, n_all, bval, blist, outs, scan_off)
     ctx.dirty = True
     ctx.check_device()
 
@@ -1553,6 +1572,47 @@ def _stream_evaluate(ctx, e, frame, cand):
 
 
 _NPK = {"bool": "u1", "i32": "<i4", "i64": "<i8", "f32": "<f4", "f64": "<f8"}
+_TAIL_LOOPS = {}
+
+
+def _stream_tail(ctx, tail, frame, hvs, kinds, leaves_np, n4, n, bval, blist, outs, offs):
+    """The vectorised shape's scalar tail (the last n % 4 rows): upload those
+    rows, run the tail loop on the device into the streamed builders, and
+    append its rows to the host results."""
+    from dataclasses import replace
+    from .columns import Col, dvec_from_cols
+    t = _TAIL_LOOPS.get(id(tail))
+    if t is None or t[0] is not tail:
+        t = (tail, replace(tail, builders=Ident("__wg_sb", ty=tail.builders.ty)))
+        _TAIL_LOOPS[id(tail)] = t
+    f2 = dict(frame)
+    f2["__wg_sb"] = bval
+    for it, hv, ks, arrs in zip(tail.iters, hvs, kinds, leaves_np):
+        cols = []
+        for kk, a in zip(ks, arrs):
+            buf = Col.alloc(kk, n - n4)
+            rt.h2d(buf.ptr, a.ctypes.data + n4 * a.itemsize, (n - n4) * a.itemsize)
+            # the tail loop reads only rows [n4, n): a base pointer n4 rows
+            # before the uploaded tail makes v's indices line up
+            cols.append(Col(buf.ptr - n4 * SIZE[kk], kk, buf))
+        f2[it.data.name] = dvec_from_cols(hv.ty.elem, n, cols)
+    seen = {id(st): len(st.segments) for st in blist if isinstance(st, AppenderDev)}
+    ctx.run_loop(t[1], f2, count_traversal=False)
+    rt.sync()
+    for st in blist:
+        if not isinstance(st, AppenderDev) or outs.get(id(st)) is None:
+            continue
+        off = offs.get(id(st), n4 * (len(outs[id(st)][0]) // n if n else 1))
+        for seg in st.segments[seen[id(st)]:]:
+            cnt = seg.length()
+            if off + cnt > len(outs[id(st)][0]):
+                outs[id(st)] = None
+                break
+            for arr, col in zip(outs[id(st)], seg.cols):
+                rt.d2h(arr.ctypes.data + off * arr.itemsize, col.ptr, cnt * arr.itemsize)
+            off += cnt
+        if id(st) in offs and outs.get(id(st)) is not None:
+            offs[id(st)] = off
 
 
 def _drain_scan(q, outs, offs, n, before):

@@ -157,7 +157,7 @@ def test_hist_large_conserves_weight():
     assert np.allclose(bins, ref, rtol=1e-9, atol=1e-9)
 
 
-@pytest.mark.parametrize("name", ["blackscholes", "q6", "filter"])
+@pytest.mark.parametrize("name", ["blackscholes", "q6", "filter", "map"])
 def test_streaming_host_inputs(name, monkeypatch):
     """Host numpy inputs take the chunked copy/compute-overlap path
     (several chunks + a ragged tail); results equal the oracle."""
@@ -179,8 +179,9 @@ def test_streaming_host_inputs(name, monkeypatch):
     if name == "q6":
         assert abs(got - want) <= 1e-9 * max(1.0, abs(want))
     elif isinstance(want, np.ndarray):
-        # order-preserving appends (filter): chunk counts are known only on
-        # the device, so each chunk is copied out one chunk behind
+        # filter: order-preserving appends, chunk counts known only on the
+        # device (copied out one chunk behind); map: the vectorised shape
+        # (simd loop streamed, scalar tail of n % 4 rows run afterwards)
         assert isinstance(got, np.ndarray) and got.shape == want.shape
         assert np.array_equal(got, want)
     else:
