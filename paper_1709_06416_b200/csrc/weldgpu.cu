@@ -328,14 +328,25 @@ __global__ void k_heads1(const uint64_t* k, uint64_t n, uint8_t* flags) {
     flags[i] = (i == 0 || k[i] != k[i - 1]) ? 1 : 0;
 }
 
+__global__ void k_heads1_u32(const uint32_t* k, uint64_t n, uint8_t* flags) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    flags[i] = (i == 0 || k[i] != k[i - 1]) ? 1 : 0;
+}
+// 32-bit sort keys: w = okey - base (every key's varying bits fit in 32)
+__global__ void k_key_u32(const uint64_t* ok, uint64_t n, uint64_t base, uint32_t* w) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    w[i] = (uint32_t)(ok[i] - base);
+}
+
 // offsets[j] = starts[j]; offsets[K] = n; ukeys[j] = inverse order key.
-__global__ void k_group_out(const uint32_t* starts, uint64_t K, uint64_t n, const uint64_t* sk, uint64_t kmin,
+template <typename KT>
+__global__ void k_group_out(const uint32_t* starts, uint64_t K, uint64_t n, const KT* sk, uint64_t kmin,
                             int kind, int64_t* offs, void* ukeys) {
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j <= K; j += (uint64_t)gridDim.x * blockDim.x) {
     if (j == K) { offs[K] = (int64_t)n; continue; }
     uint64_t s = starts[j];
     offs[j] = (int64_t)s;
-    uint64_t w = sk[s] + kmin;
+    uint64_t w = (uint64_t)sk[s] + kmin;
     if (kind == 0) ((uint8_t*)ukeys)[j] = (uint8_t)w;
     else if (kind == 1) ((int32_t*)ukeys)[j] = (int32_t)(int64_t)(w ^ 0x8000000000000000ULL);
     else ((int64_t*)ukeys)[j] = (int64_t)(w ^ 0x8000000000000000ULL);
@@ -1075,6 +1086,8 @@ int wg_run_starts(const uint64_t* key_words, int kw, uint64_t n, uint64_t starts
 // per-key input order).  Only the key bits that vary are sorted: a stable
 // radix sort on the top 24 varying bits, then a stable insertion sort
 // inside the (small) buckets; skewed data falls back to a full radix sort.
+static bool g_group_u32 = getenv("WELDGPU_GROUP_U32") == nullptr || getenv("WELDGPU_GROUP_U32")[0] != '0';
+
 int wg_group_finish1(uint64_t keys, int key_kind, uint64_t vals, int val_width, uint64_t n, uint64_t ukeys_out,
                      uint64_t offs_out, uint64_t vals_out, uint64_t* K_out) {
   NEED_INIT();
@@ -1122,6 +1135,59 @@ int wg_group_finish1(uint64_t keys, int key_kind, uint64_t vals, int val_width, 
     vbits = rbits;
   }
   const int begin_bit = vbits > 32 ? vbits - 32 : 0;
+  if (begin_bit == 0 && g_group_u32) {
+    // every key's varying bits fit in 32: sort (u32 key, u64 value) pairs --
+    // 12 instead of 16 bytes per row per radix pass -- and rebuild the keys
+    // from the common high bits
+    const uint64_t lowmask = vbits >= 64 ? ~0ULL : ((1ULL << vbits) - 1);
+    const uint64_t sub = kbase ? 0ULL : (hmm[0] & ~lowmask);   // k0 already holds okey - kbase when kbase != 0
+    const uint64_t recon = kbase ? kbase : sub;
+    uint32_t* w0 = (uint32_t*)k1;
+    uint32_t* w1 = w0 + n;
+    k_key_u32<<<g, 256, 0, g_stream>>>(k0, n, sub, w0);
+    cub::DoubleBuffer<uint32_t> dw(w0, w1);
+    cub::DoubleBuffer<uint64_t> dv(v0, (uint64_t*)k0);          // k0 is free once narrowed
+    size_t temp = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, temp, dw, dv, (int)n, 0, vbits, g_stream));
+    void* d_temp = nullptr;
+    CK(cudaMallocAsync(&d_temp, temp ? temp : 1, g_stream));
+    CK(cub::DeviceRadixSort::SortPairs(d_temp, temp, dw, dv, (int)n, 0, vbits, g_stream));
+    uint8_t* heads;
+    uint32_t* starts;
+    int* d_cnt;
+    CK(cudaMallocAsync((void**)&heads, n, g_stream));
+    CK(cudaMallocAsync((void**)&starts, n * 4, g_stream));
+    CK(cudaMallocAsync((void**)&d_cnt, 8, g_stream));
+    k_heads1_u32<<<g, 256, 0, g_stream>>>(dw.Current(), n, heads);
+    cub::CountingInputIterator<uint32_t> it(0);
+    size_t temp2 = 0;
+    CK(cub::DeviceSelect::Flagged(nullptr, temp2, it, heads, starts, d_cnt, (int)n, g_stream));
+    void* d_temp2 = nullptr;
+    CK(cudaMallocAsync(&d_temp2, temp2 ? temp2 : 1, g_stream));
+    CK(cub::DeviceSelect::Flagged(d_temp2, temp2, it, heads, starts, d_cnt, (int)n, g_stream));
+    int hK = 0;
+    CK(cudaMemcpyAsync(&hK, d_cnt, 4, cudaMemcpyDeviceToHost, g_stream));
+    CK(cudaStreamSynchronize(g_stream));
+    k_group_out<uint32_t><<<grid_for((uint64_t)hK + 1, 256), 256, 0, g_stream>>>(
+        starts, (uint64_t)hK, n, dw.Current(), recon, key_kind, (int64_t*)(uintptr_t)offs_out, (void*)(uintptr_t)ukeys_out);
+    if (val_width == 8)
+      CK(cudaMemcpyAsync((void*)(uintptr_t)vals_out, dv.Current(), n * 8, cudaMemcpyDeviceToDevice, g_stream));
+    else
+      k_narrow<<<g, 256, 0, g_stream>>>(dv.Current(), (void*)(uintptr_t)vals_out, val_width, n);
+    CK(cudaGetLastError());
+    CK(cudaFreeAsync(d_temp, g_stream));
+    CK(cudaFreeAsync(d_temp2, g_stream));
+    CK(cudaFreeAsync(heads, g_stream));
+    CK(cudaFreeAsync(starts, g_stream));
+    CK(cudaFreeAsync(d_cnt, g_stream));
+    CK(cudaFreeAsync(mm, g_stream));
+    CK(cudaFreeAsync(k0, g_stream));
+    if (own_v0) CK(cudaFreeAsync(v0, g_stream));
+    CK(cudaFreeAsync(k1, g_stream));
+    CK(cudaFreeAsync(v1, g_stream));
+    *K_out = (uint64_t)hK;
+    return 0;
+  }
   cub::DoubleBuffer<uint64_t> dk(k0, k1), dv(v0, v1);
   size_t temp = 0;
   CK(cub::DeviceRadixSort::SortPairs(nullptr, temp, dk, dv, (int)n, begin_bit, vbits, g_stream));
@@ -1179,7 +1245,7 @@ int wg_group_finish1(uint64_t keys, int key_kind, uint64_t vals, int val_width, 
   int hK = 0;
   CK(cudaMemcpyAsync(&hK, d_cnt, 4, cudaMemcpyDeviceToHost, g_stream));
   CK(cudaStreamSynchronize(g_stream));
-  k_group_out<<<grid_for((uint64_t)hK + 1, 256), 256, 0, g_stream>>>(starts, (uint64_t)hK, n, dk.Current(), kbase,
+  k_group_out<uint64_t><<<grid_for((uint64_t)hK + 1, 256), 256, 0, g_stream>>>(starts, (uint64_t)hK, n, dk.Current(), kbase,
                                                                      key_kind,
                                                                      (int64_t*)(uintptr_t)offs_out,
                                                                      (void*)(uintptr_t)ukeys_out);
