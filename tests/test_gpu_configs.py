@@ -190,12 +190,13 @@ def test_streaming_host_inputs(name, monkeypatch):
             np.testing.assert_allclose(g, w, rtol=1e-9, atol=1e-9)
 
 
-@pytest.mark.parametrize("keys", ["clustered", "narrow-around-zero"])
+@pytest.mark.parametrize("keys", ["clustered", "narrow-around-zero", "high-common-bits", "full-32-bits"])
 def test_group_skewed_windows_preserve_order(keys):
     """Key sets whose top 32 varying bits collide heavily (the bucket
-    fix-up overflows and a full stable sort takes over) and a narrow range
-    straddling zero (sorted as order_key - min): same groups, same per-key
-    input order as the oracle."""
+    fix-up overflows and a full stable sort takes over), a narrow range
+    straddling zero (sorted as order_key - min), and key sets whose varying
+    bits fit in 32 (sorted as u32 keys, high bits rebuilt): same groups,
+    same per-key input order as the oracle."""
     import paper_1709_06416_b200 as wg
     from oracle import weld_oracle
     from paper_1709_06416_b200 import workloads as W
@@ -204,8 +205,13 @@ def test_group_skewed_windows_preserve_order(keys):
     n = 200_003
     if keys == "clustered":
         k = rng.integers(0, 4, n).astype(np.int64) * (1 << 40) + rng.integers(0, 1000, n)
-    else:
+    elif keys == "narrow-around-zero":
         k = rng.integers(-700, 700, n).astype(np.int64)
+    elif keys == "high-common-bits":
+        k = (1 << 40) + rng.integers(0, 100_000, n).astype(np.int64)
+    else:
+        k = rng.integers(0, 1 << 32, n).astype(np.int64)
+        k[:1000] = k[1000:2000]                       # repeated keys
     v = np.arange(n, dtype=np.int64) * 7 - 3
     wl = W.WORKLOADS["group"]
     tree = W.compile_program(wl)
