@@ -104,3 +104,46 @@ def test_sample_against_mpmath(fn):
     f = getattr(mpmath, fn)
     want = np.array([float(f(mpmath.mpf(v))) for v in x.tolist()])
     assert _ulps(got, want).max() <= 2
+
+
+def _eval_prog(prog, xs, fns, extra=None):
+    import paper_1709_06416_b200 as wg
+    from weldmill.engine import EngineConfig, Value
+    from weldmill.optim import OptLevel, optimize
+    from weldmill.parser import parse, parse_type_text
+    from weldmill.sugar import expand
+    from weldmill.typecheck import infer
+    from weldmill.types import F64, Function, Scalar
+    ty = parse_type_text("vec[f64]")
+    env = {"v": ty}
+    vals = {"v": Value(ty, np.ascontiguousarray(xs, dtype=np.float64))}
+    for name, arr in (extra or {}).items():
+        env[name] = ty
+        vals[name] = Value(ty, np.ascontiguousarray(arr, dtype=np.float64))
+    env.update({f: Function((Scalar(F64),), Scalar(F64)) for f in fns})
+    tree = optimize(infer(expand(parse(prog)), env), OptLevel.none())[0]
+    val, _ = wg.evaluate(tree, vals, EngineConfig(memory_limit=1 << 40), {f: getattr(math, f) for f in fns},
+                         result="numpy")
+    return val.data
+
+
+def test_tables_in_scan_and_count_kernels():
+    """The table prologue is emitted in every kernel shape a body can land
+    in: the order-preserving scan schedule (filter on erf) and the count-only
+    pre-pass of a data-dependent flatmap (append count from log)."""
+    rng = np.random.default_rng(3)
+    x = rng.uniform(0.05, 3.0, 300_000)
+    e = np.array([math.erf(t) for t in x.tolist()])
+    x = x[np.abs(e - 0.5) > 1e-9]                     # no ties at the threshold
+    got = np.asarray(_eval_prog("filter(v, (x) => call(erf, x) > 0.5)", x, ["erf"]))
+    want = x[np.array([math.erf(t) for t in x.tolist()]) > 0.5]
+    np.testing.assert_array_equal(got, want)
+    # flatmap: row x appends x once per y in {0..5} with y < log(x) + 3
+    L = np.array([math.log(t) for t in x.tolist()]) + 3.0
+    xs = x[np.abs(L - np.round(L)) > 1e-9]            # no ties at integer boundaries
+    prog = ("result(for(v, vecbuilder[f64], (b, i, x) => "
+            "for(r, b, (c, j, y) => if (y < call(log, x) + 3.0, merge(c, x), c))))")
+    got = np.asarray(_eval_prog(prog, xs, ["log"], {"r": np.arange(6.0)}))
+    Ls = np.array([math.log(t) for t in xs.tolist()]) + 3.0
+    reps = (np.arange(6.0)[None, :] < Ls[:, None]).sum(axis=1)
+    np.testing.assert_array_equal(got, np.repeat(xs, reps))
