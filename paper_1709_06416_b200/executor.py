@@ -690,11 +690,22 @@ class Ctx:
             tilectr = rt.alloc(8)
             rt.memset(tilectr.ptr, 0, 8)
 
-        vals = {}
-        for p in plan.params:
-            vals[p.name] = self._param_value(p.key, count, datas, windows, bmap, res, captures, grid, tilectr)
-        vals["pipe_stages"] = stages
-        blob = b"".join(_pack(p.ctype, vals[p.name]) for p in plan.params)
+        packer = getattr(plan, "_packer", None)
+        if packer is None:
+            # every parameter is one 8-byte word (f64 or a masked integer)
+            dbl = [p.ctype == "double" for p in plan.params]
+            packer = plan._packer = (_struct.Struct("<" + "".join("d" if d else "Q" for d in dbl)), dbl)
+        words = []
+        for p, d in zip(plan.params, packer[1]):
+            v = stages if p.name == "pipe_stages" else \
+                self._param_value(p.key, count, datas, windows, bmap, res, captures, grid, tilectr)
+            if d:
+                words.append(float(v))
+            else:
+                if isinstance(v, float):
+                    raise EvalError(f"internal: float for {p.ctype} parameter")
+                words.append(int(v) & 0xFFFFFFFFFFFFFFFF)
+        blob = packer[0].pack(*words)
         kern.launch(grid, plan.block, blob, smem)
         self.launches += 1
         self.dirty = True

@@ -361,7 +361,7 @@ class Kernel:
         return v
 
     def launch(self, grid, block, params: bytes, smem=0):
-        buf = ctypes.create_string_buffer(params, len(params))
+        buf = params          # bytes: passed as a pointer, copied by cuLaunchKernel
         hook = LAUNCH_HOOK[0]
         if hook is not None:
             hook("before", self)
