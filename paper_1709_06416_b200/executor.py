@@ -160,11 +160,16 @@ class Ctx:
             raise cls(ERR_TEXT.get(code, "device error {info}").format(info=info))
 
     # -- evaluation ------------------------------------------------------------
+    _EV = {}
+
     def ev(self, e, env):
-        m = getattr(self, "ev_" + type(e).__name__, None)
-        if m is None:
-            raise DeviceUnsupported(f"cannot evaluate node {type(e).__name__}")
-        return m(e, env)
+        f = Ctx._EV.get(type(e))
+        if f is None:
+            f = getattr(Ctx, "ev_" + type(e).__name__, None)
+            if f is None:
+                raise DeviceUnsupported(f"cannot evaluate node {type(e).__name__}")
+            Ctx._EV[type(e)] = f
+        return f(self, e, env)
 
     def ev_Literal(self, e, env):
         return sem.literal(e.ty.kind, e.value)
