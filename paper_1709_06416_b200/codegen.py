@@ -73,7 +73,8 @@ SCAN_PIPE = _os.environ.get("WELDGPU_SCAN_PIPE", "0") == "1"
 # instead of at the top of the next iteration (one barrier and one exposed
 # atomic round trip less per tile)
 SCAN_EARLY_CLAIM = _os.environ.get("WELDGPU_SCAN_EARLY_CLAIM", "1") == "1"
-SCAN_BLOCK_128 = _os.environ.get("WELDGPU_SCAN_BLOCK_128", "1") == "1"
+SCAN_BLOCK_128 = _os.environ.get("WELDGPU_SCAN_BLOCK_128", "0") == "1"
+SCAN_MINBLOCKS = int(_os.environ.get("WELDGPU_SCAN_MINBLOCKS", "4"))   # in 256-thread CTAs per SM
 SOA = _os.environ.get("WELDGPU_SOA", "0") == "1"      # statement-wise item loops for straight-line bodies
 # two-pass order-preserving appenders: a count-only pre-pass writes per-tile
 # append counts, an exclusive scan turns them into tile offsets, and the
@@ -1436,7 +1437,13 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
     for p_ in g.params:
         src.append(f"  {p_.ctype} {p_.name};")
     src.append("};")
-    lb = f"BLOCK, {MINBLOCKS}" if MINBLOCKS else "BLOCK"
+    minb = MINBLOCKS
+    if scan_bs and not MINBLOCKS and SCAN_MINBLOCKS:
+        # scan schedule: resident CTAs hide each other's look-back waits;
+        # capping registers buys CTAs (filter: 78 -> 64 registers, 3 -> 4
+        # CTAs of 256 threads per SM)
+        minb = SCAN_MINBLOCKS * 256 // BLOCK
+    lb = f"BLOCK, {minb}" if minb else "BLOCK"
     src.append(f'extern "C" __global__ void __launch_bounds__({lb}) {name}(const Params p) {{')
     src.append("  extern __shared__ __align__(16) u64 wg_dyn_smem[];")
     for t in sorted(g.tabs):
