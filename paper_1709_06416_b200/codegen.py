@@ -99,8 +99,9 @@ EXTERN_F64 = {
     "cbrt": "cbrt", "exp2": "exp2", "atan2": "atan2", "pow": "pow", "hypot": "hypot", "copysign": "copysign",
     "fmod": "fmod",
 }
-# WELDGPU_MATH: "tab" (default) -- erf from the shared-memory piecewise
-# polynomial table (weld_device.cuh wg_erf_tab, ~15 FP64 ops instead of ~43);
+# WELDGPU_MATH: "tab" (default) -- erf, log and exp from shared-memory
+# tables (weld_device.cuh wg_erf_tab / wg_log_tab / wg_exp_tab: 11, 20 and
+# 12 FP64 ops instead of libdevice's ~43, ~30 and 15); "taberf" -- erf only;
 # "estrin" -- exp/log/erf with libdevice's polynomials in Estrin form
 # (measured slower on Black-Scholes: more FP64 ops, more registers);
 # "libdevice" -- CUDA's own.
@@ -108,7 +109,7 @@ MATH = _os.environ.get("WELDGPU_MATH", "tab")
 if MATH == "estrin":
     EXTERN_F64.update({"exp": "wg_exp", "log": "wg_log", "erf": "wg_erf"})
 elif MATH == "tab":
-    EXTERN_F64.update({"erf": "wg_erf_tab", "log": "wg_log_tab"})
+    EXTERN_F64.update({"erf": "wg_erf_tab", "log": "wg_log_tab", "exp": "wg_exp_tab"})
 elif MATH == "taberf":
     EXTERN_F64.update({"erf": "wg_erf_tab"})
 

@@ -901,3 +901,40 @@ __device__ __forceinline__ double wg_log_tab(double x) {
   q = fma(q, r, -0.5);
   return t2 + (lo + (r * r) * q);
 }
+
+// exp from a 64-entry shared-memory table of 2^(j/64) (tools/gen_exp_table.py):
+// k = round(64 x / ln2), r = x - k ln2/64 (Cody-Waite), exp(r) - 1 to r^6,
+// result 2^(k>>6) (T_hi + (T_lo + T_hi p)); <= 1 ulp, 12 FP64 operations
+// with a 9-deep chain (libdevice: 15, 15 deep).  Near over/underflow the
+// scaling is split in two steps, as libdevice does.
+#include "wg_exp_table.h"
+__shared__ __align__(16) double wg_exp_s[2 * WG_EXP_N];
+__device__ __forceinline__ void wg_exp_tab_init() {
+  for (int q = threadIdx.x; q < 2 * WG_EXP_N; q += blockDim.x) wg_exp_s[q] = __longlong_as_double((long long)WG_EXP_TAB[q]);
+}
+__device__ __forceinline__ double wg_exp_tab(double x) {
+  const double sh = fma(x, __longlong_as_double((long long)WG_EXP_INVL), 6755399441055744.0);
+  const int k = __double2loint(sh);
+  const double kf = sh - 6755399441055744.0;
+  double r = fma(kf, -__longlong_as_double((long long)WG_EXP_L2HI), x);
+  r = fma(kf, -__longlong_as_double((long long)WG_EXP_L2LO), r);
+  const double2 t = reinterpret_cast<const double2*>(wg_exp_s)[k & (WG_EXP_N - 1)];
+  const int e = k >> 6;
+  double q = fma(1.0 / 720.0, r, 1.0 / 120.0);
+  q = fma(q, r, 1.0 / 24.0);
+  q = fma(q, r, 1.0 / 6.0);
+  q = fma(q, r, 0.5);
+  const double p = fma(r * r, q, r);
+  const double y = t.x + fma(t.x, p, t.y);
+  double res = __hiloint2double(__double2hiint(y) + (e << 20), __double2loint(y));
+  const int ahi = __double2hiint(x) & 0x7fffffff;
+  if (__builtin_expect(ahi >= 0x4086232B, 0)) {          // |x| >= 708.39: over/underflow or subnormal
+    res = (x < 0.0) ? 0.0 : x + __longlong_as_double(0x7FF0000000000000LL);
+    if (ahi < 0x40874800) {                             // |x| < 745.0: scale in two steps
+      const int e1 = e / 2;
+      const double y1 = __hiloint2double(__double2hiint(y) + (e1 << 20), __double2loint(y));
+      res = y1 * __hiloint2double(((e - e1) << 20) + 0x3FF00000, 0);
+    }
+  }
+  return res;
+}

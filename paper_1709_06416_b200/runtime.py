@@ -303,7 +303,7 @@ def header_text():
     return _header_text
 
 
-_TABLES = ("wg_erf_table.h", "wg_log_table.h")     # generated by tools/gen_*_table.py
+_TABLES = ("wg_erf_table.h", "wg_log_table.h", "wg_exp_table.h")     # generated by tools/gen_*_table.py
 _table_texts = None
 
 
@@ -314,8 +314,8 @@ def _nvrtc_args(src):
         for t in _TABLES:
             with open(os.path.join(_HERE, "csrc", t)) as f:
                 _table_texts.append(f.read().encode())
-    hs = (c_char_p * 3)(header_text().encode(), *_table_texts)
-    hn = (c_char_p * 3)(b"weld_device.cuh", *(t.encode() for t in _TABLES))
+    hs = (c_char_p * (1 + len(_TABLES)))(header_text().encode(), *_table_texts)
+    hn = (c_char_p * (1 + len(_TABLES)))(b"weld_device.cuh", *(t.encode() for t in _TABLES))
     opts = [o.encode() for o in NVRTC_OPTS]
     oa = (c_char_p * len(opts))(*opts)
     return hs, hn, oa, len(opts)
@@ -328,7 +328,7 @@ def compile_check(src: str, name="weld_loop.cu"):
     hs, hn, oa, no = _nvrtc_args(src)
     sz = u64(0)
     log = ctypes.create_string_buffer(1 << 16)
-    rc = L.wg_compile_check(src.encode(), name.encode(), 3, hs, hn, no, oa, ctypes.byref(sz), log, 1 << 16)
+    rc = L.wg_compile_check(src.encode(), name.encode(), 1 + len(_TABLES), hs, hn, no, oa, ctypes.byref(sz), log, 1 << 16)
     if rc != 0:
         raise WeldGpuError(L.wg_last_error().decode(errors="replace"))
     return sz.value
@@ -382,10 +382,10 @@ def compile_ptx(src: str, name="weld_loop.cu") -> str:
     hs, hn, oa, no = _nvrtc_args(src)
     size = u64(0)
     log = ctypes.create_string_buffer(1 << 16)
-    if L.wg_compile_ptx(src.encode(), name.encode(), 3, hs, hn, no, oa, None, 0, ctypes.byref(size), log, 1 << 16):
+    if L.wg_compile_ptx(src.encode(), name.encode(), 1 + len(_TABLES), hs, hn, no, oa, None, 0, ctypes.byref(size), log, 1 << 16):
         raise WeldGpuError(L.wg_last_error().decode(errors="replace"))
     buf = ctypes.create_string_buffer(size.value)
-    _check(L.wg_compile_ptx(src.encode(), name.encode(), 3, hs, hn, no, oa, buf, size.value, ctypes.byref(size),
+    _check(L.wg_compile_ptx(src.encode(), name.encode(), 1 + len(_TABLES), hs, hn, no, oa, buf, size.value, ctypes.byref(size),
                             log, 1 << 16))
     return buf.value.decode()
 
@@ -475,7 +475,7 @@ def get_kernel(src: str, name: str) -> Kernel:
                 _check(L.wg_module_load(const_pool_ptx(ptx).encode() + b"\0", ctypes.byref(m)))
                 rc = 0
             else:
-                rc = L.wg_compile(src.encode(), f"wg_{key[:12]}.cu".encode(), 3, hs, hn, no, oa, ctypes.byref(m),
+                rc = L.wg_compile(src.encode(), f"wg_{key[:12]}.cu".encode(), 1 + len(_TABLES), hs, hn, no, oa, ctypes.byref(m),
                                   log, 1 << 16)
             if rc != 0:
                 raise WeldGpuError(L.wg_last_error().decode(errors="replace"))

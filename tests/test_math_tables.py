@@ -1,4 +1,4 @@
-"""The committed math tables (csrc/wg_erf_table.h, csrc/wg_log_table.h) are
+"""The committed math tables (csrc/wg_erf_table.h, wg_log_table.h, wg_exp_table.h) are
 exactly what their generators produce, and the generators' own accuracy
 checks pass (erf table <= 0.5 ulp evaluated exactly; the log algorithm,
 emulated with correctly rounded fma, <= 1 ulp from mpmath).  CPU only."""
@@ -17,7 +17,8 @@ def _load(name):
     return mod
 
 
-@pytest.mark.parametrize("gen,header", [("gen_erf_table", "wg_erf_table.h"), ("gen_log_table", "wg_log_table.h")])
+@pytest.mark.parametrize("gen,header", [("gen_erf_table", "wg_erf_table.h"), ("gen_log_table", "wg_log_table.h"),
+                                        ("gen_exp_table", "wg_exp_table.h")])
 def test_table_matches_generator(gen, header, tmp_path, monkeypatch):
     pytest.importorskip("mpmath")
     mod = _load(gen)
