@@ -242,41 +242,6 @@ class DictDev(BuilderBase):
             self.pv = [rt.alloc(8 * nparts * pcap) for _ in self.vks]
         rt.memset(self.pcount.ptr, 0, 8 * nparts)
 
-    # -- range-partitioned mode (codegen.dict_rpart_source) ------------------
-    def ensure_rpart(self, rows, nparts, grid, rng):
-        """Buckets for the range-partitioned mode: nparts x grid private
-        slices of scap records (1.3 x the mean share + 64).  `rng` is the
-        (min, max) order key seen last time: partition = top bits of
-        (order_key - min), clamped, so partitions are ordered key ranges."""
-        scap = (rows * 13) // (10 * nparts * grid) + 64
-        scap = (scap + 3) // 4 * 4
-        if getattr(self, "pcap", 0) < scap or getattr(self, "nparts", 0) != nparts or \
-                getattr(self, "nslices", 0) != grid:
-            self.pcap = scap
-            self.nparts = nparts
-            self.nslices = grid
-            self.pk = rt.alloc(8 * nparts * grid * scap)
-            self.pv = [rt.alloc(8 * nparts * grid * scap) for _ in self.vks]
-        self.pcount = rt.alloc(4 * nparts * grid)       # slice fill counts (written by the loop)
-        self.rcounters = rt.alloc(32)                   # [oflow, nout, ticket, pad]
-        rt.memset(self.rcounters.ptr, 0, 32)
-        lo, hi = rng
-        self.rlo = lo
-        self.rshift = max(0, (hi - lo).bit_length() - (nparts.bit_length() - 1))
-        self.rows_in = rows
-
-    def reset(self):
-        """Forget every merge (the range-partitioned fallback re-runs the loop)."""
-        self.table = None
-        self.cap = 0
-        rt.memset(self.counters.ptr, 0, 16)
-        self.over = None
-        self.ocap = 0
-        self.rpart_out = None
-        self.distinct = 0
-
-    rpart_out = None
-
     def _alloc_table(self, cap):
         self.cap = cap
         self.table = rt.alloc(8 * (cap + 1) * self.slot_words)
@@ -432,25 +397,6 @@ def gather_cols(cols, perm, n):
     return out
 
 
-_RANGE_HINTS = {}   # loop identity -> (min, max) order key of the last result
-
-
-def _record_range(d: DictDev, first_word, last_word):
-    from .codegen import okey_py, rpart_ok
-    if d.hint_key is not None and rpart_ok(d.kks):
-        _RANGE_HINTS[d.hint_key] = (okey_py(d.kks, first_word), okey_py(d.kks, last_word))
-
-
-def _pack_word(d: DictDev, cols, j):
-    """The packed one-word key of sorted entry j (for the range hint)."""
-    w = 0
-    for (wi, sh, width), c in zip(d.lay, cols):
-        arr = np.empty(1, dtype=np.uint64 if SIZE[c.kind] == 8 else (np.uint32 if SIZE[c.kind] == 4 else np.uint8))
-        rt.d2h(arr.ctypes.data, c.ptr + j * SIZE[c.kind], SIZE[c.kind])
-        w |= (int(arr[0]) & ((1 << width) - 1)) << sh
-    return w
-
-
 SMALL_DICT = 4096
 
 
@@ -485,20 +431,6 @@ def _finish_small(d: DictDev, dict_ty):
 
 
 def finish_dict(d: DictDev, dict_ty):
-    if d.rpart_out is not None:
-        # range-partitioned: the aggregation kernel wrote the entries sorted
-        kw, vw, n = d.rpart_out
-        d.rpart_out = None
-        if d.hint_key is not None:
-            _SIZE_HINTS[d.hint_key] = n
-        kcols = _words_to_cols(kw, d.kks, d.lay, n)
-        vcols = _value_words_to_cols(vw, d.vks, n)
-        if n:
-            ends = np.empty(2, dtype=np.uint64)
-            rt.d2h(ends.ctypes.data, kw[0].ptr, 8)
-            rt.d2h(ends[1:].ctypes.data, kw[0].ptr + 8 * (n - 1), 8)
-            _record_range(d, int(ends[0]), int(ends[1]))
-        return DDict(dict_ty, dvec_from_cols(dict_ty.key, n, kcols), dvec_from_cols(dict_ty.value, n, vcols))
     small = _finish_small(d, dict_ty)
     if small is not None:
         return small
@@ -523,10 +455,6 @@ def finish_dict(d: DictDev, dict_ty):
         perm = sort_perm(kcols, n)
         kcols = gather_cols(kcols, perm, n)
         vcols = gather_cols(vcols, perm, n)
-    if n and d.nw == 1:
-        from .codegen import rpart_ok
-        if d.hint_key is not None and rpart_ok(d.kks):
-            _record_range(d, _pack_word(d, kcols, 0), _pack_word(d, kcols, n - 1))
     return DDict(dict_ty, dvec_from_cols(dict_ty.key, n, kcols), dvec_from_cols(dict_ty.value, n, vcols))
 
 

@@ -65,29 +65,16 @@ AGG_MAX_GROUPS = int(_os.environ.get("WELDGPU_AGG_GROUPS", "8"))
 REGCACHE = int(_os.environ.get("WELDGPU_REGCACHE", "4"))
 PIPE = _os.environ.get("WELDGPU_PIPE", "1") == "1"
 STAGE_SCAN = _os.environ.get("WELDGPU_STAGE_SCAN", "1") == "1"
-SCAN_PREFETCH = _os.environ.get("WELDGPU_SCAN_PREFETCH", "0") == "1"
 LB_PER = int(_os.environ.get("WELDGPU_LB_PER", "1"))
 LB_SLEEP = int(_os.environ.get("WELDGPU_LB_SLEEP", "64"))
-SCAN_PIPE = _os.environ.get("WELDGPU_SCAN_PIPE", "0") == "1"
 # scan schedule: claim the next tile during the current tile's store phase
 # instead of at the top of the next iteration (one barrier and one exposed
 # atomic round trip less per tile)
 SCAN_EARLY_CLAIM = _os.environ.get("WELDGPU_SCAN_EARLY_CLAIM", "1") == "1"
-SCAN_BLOCK_128 = _os.environ.get("WELDGPU_SCAN_BLOCK_128", "0") == "1"
 SCAN_MINBLOCKS = int(_os.environ.get("WELDGPU_SCAN_MINBLOCKS", "4"))   # in 256-thread CTAs per SM
-SOA = _os.environ.get("WELDGPU_SOA", "0") == "1"      # statement-wise item loops for straight-line bodies
-# two-pass order-preserving appenders: a count-only pre-pass writes per-tile
-# append counts, an exclusive scan turns them into tile offsets, and the
-# main kernel stores without a decoupled look-back
-SCAN2 = _os.environ.get("WELDGPU_SCAN2", "0") == "1"
 PART_ITEMS = int(_os.environ.get("WELDGPU_PART_ITEMS", "8"))
 PIPE_STAGES = int(_os.environ.get("WELDGPU_PIPE_STAGES", "4"))
 PIPE_MAX_STAGES = 8
-# Stage release in the bulk-async pipeline: 0 = __syncthreads after every
-# warp has read the stage; 1 = per-stage "empty" mbarriers (each warp arrives
-# after its reads; only the producer thread waits, before refilling);
-# 2 = as 1 with the refill of a stage deferred by one tile.
-PIPE_EMPTY = int(_os.environ.get("WELDGPU_PIPE_EMPTY", "0"))
 PIPE_SMEM_BUDGET = int(_os.environ.get("WELDGPU_PIPE_SMEM", str(48 * 1024)))
 
 # Extern names recognised as device intrinsics (the reference resolves
@@ -99,16 +86,63 @@ EXTERN_F64 = {
     "cbrt": "cbrt", "exp2": "exp2", "atan2": "atan2", "pow": "pow", "hypot": "hypot", "copysign": "copysign",
     "fmod": "fmod",
 }
+EXTERN_IDS = {name: q for q, name in enumerate(sorted(EXTERN_F64))}
+
+
+def _extern_checks(name, a, r):
+    """C conditions under which Python's math.<name> raises for these
+    arguments / this result: [(condition, 1 if OverflowError else 0)]."""
+    x = a[0]
+    y = a[1] if len(a) > 1 else None
+    fin = lambda v: f"isfinite({v})"   # noqa: E731
+    if name in ("exp", "exp2", "expm1", "sinh", "cosh"):
+        return [(f"isinf({r}) && {fin(x)}", 1)]
+    if name in ("log", "log2", "log10"):
+        return [(f"{x} <= 0.0", 0)]
+    if name == "log1p":
+        return [(f"{x} <= -1.0", 0)]
+    if name == "sqrt":
+        return [(f"{x} < 0.0", 0)]
+    if name in ("sin", "cos", "tan"):
+        return [(f"isinf({x})", 0)]
+    if name in ("asin", "acos"):
+        return [(f"fabs({x}) > 1.0", 0)]
+    if name == "pow":
+        return [(f"(isnan({r}) && !isnan({x}) && !isnan({y})) || ({x} == 0.0 && {y} < 0.0 && {fin(y)})", 0),
+                (f"isinf({r}) && {fin(x)} && {fin(y)} && {x} != 0.0", 1)]
+    if name == "hypot":
+        return [(f"isinf({r}) && {fin(x)} && {fin(y)}", 1)]
+    if name == "fmod":
+        return [(f"({y} == 0.0 && !isnan({x})) || (isinf({x}) && !isnan({y}))", 0)]
+    return []
+
+
+# static shared-memory bytes of each table-driven math function
+# (weld_device.cuh: wg_erf_s 97 x 20 u32, wg_log_s + wg_log_lo_s 3 x 128 f64,
+# wg_exp_s 2 x 64 f64)
+TAB_BYTES = {"wg_erf_tab": 97 * 20 * 4, "wg_log_tab": 3 * 128 * 8, "wg_exp_tab": 2 * 64 * 8}
+
+
+def _table_bytes(body):
+    from weldmill.expr import walk
+    fns = {EXTERN_F64.get(n.name) for n in walk(body) if isinstance(n, ExternCall)}
+    return sum(TAB_BYTES.get(f, 0) for f in fns)
+
+
+def extern_error_text(info):
+    """Message of the EvalError a device extern failure raises (the
+    reference: f"extern {name!r} failed: {exc}", run.py:843-844)."""
+    names = sorted(EXTERN_F64)
+    name = names[info // 2] if 0 <= info // 2 < len(names) else "?"
+    return f"extern {name!r} failed: math {'range' if info % 2 else 'domain'} error"
+
+
 # WELDGPU_MATH: "tab" (default) -- erf, log and exp from shared-memory
 # tables (weld_device.cuh wg_erf_tab / wg_log_tab / wg_exp_tab: 11, 20 and
 # 12 FP64 ops instead of libdevice's ~43, ~30 and 15); "taberf" -- erf only;
-# "estrin" -- exp/log/erf with libdevice's polynomials in Estrin form
-# (measured slower on Black-Scholes: more FP64 ops, more registers);
 # "libdevice" -- CUDA's own.
 MATH = _os.environ.get("WELDGPU_MATH", "tab")
-if MATH == "estrin":
-    EXTERN_F64.update({"exp": "wg_exp", "log": "wg_log", "erf": "wg_erf"})
-elif MATH == "tab":
+if MATH == "tab":
     EXTERN_F64.update({"erf": "wg_erf_tab", "log": "wg_log_tab", "exp": "wg_exp_tab"})
 elif MATH == "taberf":
     EXTERN_F64.update({"erf": "wg_erf_tab"})
@@ -478,16 +512,33 @@ class Gen:
         if fn is None:
             from weldmill.errors import ExternCallUnknown
             raise ExternCallUnknown(f"extern {e.name!r} has no device implementation")
-        args = [self.ex(a, env) for a in e.args]
+        reg = self.externs[e.name]
+        if reg is not None and reg is not getattr(math, e.name, None):
+            # the reference calls whatever callable is registered (run.py:
+            # 836-844); only the math module's own functions have a device
+            # implementation -- anything else is not silently replaced
+            raise DeviceUnsupported(f"extern {e.name!r} is bound to {reg!r}, not math.{e.name}; "
+                                    "only the math module's functions run on the device")
+        args = [self.let(F64, f"(double)({a.c})") for a in self.ex_args(e.args, env)]
         rk = e.ty.kind
-        cargs = ", ".join(f"(double)({a.c})" for a in args)
+        cargs = ", ".join(a.c for a in args)
         if fn.endswith("_tab"):
             self.tabs = self.tabs | {fn}    # kernel prologue copies the table to shared memory
+        r = self.let(F64, f"{fn}({cargs})")
+        # Python's math raises where C returns NaN/inf (ValueError "math
+        # domain error", OverflowError "math range error"); the reference
+        # turns that into EvalError (run.py:841-844) -- so does the device
+        chk = _extern_checks(e.name, [a.c for a in args], r.c)
+        for cond, rng in chk:
+            self.emit(f"if ({cond}) wg_raise(p.err, WG_ERR_EXTERN, {2 * EXTERN_IDS[e.name] + rng});")
         if rk == F64:
-            return self.let(F64, f"{fn}({cargs})")
+            return r
         if rk == F32:
-            return self.let(F32, f"((float){fn}({cargs}))")
+            return self.let(F32, f"((float){r.c})")
         raise DeviceUnsupported(f"extern {e.name} returning {rk}")
+
+    def ex_args(self, args, env):
+        return [self.ex(a, env) for a in args]
 
     def _select(self, c, a, b):
         if isinstance(a, S):
@@ -735,24 +786,32 @@ class Gen:
                 if any(isinstance(b, BSpec) and isinstance(b.kind, (VecBuilder, GroupBuilder)) and mx > 0
                        and b.mode != "scan" for b, (mn, mx) in cnt_.items()):
                     raise DeviceUnsupported("appends inside a data-dependent nested loop into a non-scan builder")
+            # per-iter counts with the reference's checks, in its order
+            # (run.py:915-940): stride >= 1 (EvalError), window inside the
+            # vector (IndexOutOfBounds), then equal zipped counts
+            # (ZipLengthMismatch).  A failed check raises through the error
+            # word and runs the nested loop zero times (no out-of-range reads).
             cnt = self.tmp("n")
-            starts, strides = [], []
+            starts, strides, cs = [], [], []
+            ok = self.tmp("ok")
+            self.emit(f"bool {ok} = true;")
             for k, (it, d) in enumerate(zip(e.iters, datas)):
                 if it.start is not None:
-                    s = self.ex(it.start, env).c
-                    en = self.ex(it.end, env).c
-                    st = self.ex(it.stride, env).c
-                    self.emit(f"if (!({st} >= 1 && 0 <= {s} && {s} <= {en} && {en} <= {d.n})) "
-                              f"wg_raise(p.err, WG_ERR_LOOKUP_OOB, {s});")
-                    c = f"(({st} >= 1 && 0 <= {s} && {s} <= {en} && {en} <= {d.n}) ? (({en} - {s} + {st} - 1) / {st}) : 0)"
+                    s = self.let(I64, self.ex(it.start, env).c).c
+                    en = self.let(I64, self.ex(it.end, env).c).c
+                    st = self.let(I64, self.ex(it.stride, env).c).c
+                    self.emit(f"if ({ok} && {st} < 1) {{ wg_raise(p.err, WG_ERR_STRIDE, {st}); {ok} = false; }}")
+                    self.emit(f"if ({ok} && !(0 <= {s} && {s} <= {en} && {en} <= {d.n})) "
+                              f"{{ wg_raise(p.err, WG_ERR_LOOKUP_OOB, {s}); {ok} = false; }}")
+                    c = self.let(I64, f"({ok} ? (({en} - {s} + {st} - 1) / {st}) : 0)").c
                 else:
-                    s, st, c = "0", "1", d.n
+                    s, st, c = "0", "1", self.let(I64, d.n).c
                 starts.append(s)
                 strides.append(st)
-                if k == 0:
-                    self.emit(f"const i64 {cnt} = {c};")
-                else:
-                    self.emit(f"if ({c} != {cnt}) wg_raise(p.err, WG_ERR_INTERNAL, 0);")
+                if k > 0:
+                    self.emit(f"if ({ok} && {c} != {cs[0]}) {{ wg_raise(p.err, WG_ERR_ZIP, {c}); {ok} = false; }}")
+                cs.append(c)
+            self.emit(f"const i64 {cnt} = {ok} ? {cs[0]} : 0;")
             j = self.tmp("j")
             self.emit(f"for (i64 {j} = 0; {j} < {cnt}; ++{j}) {{")
             self.ind += 1
@@ -1137,15 +1196,11 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
         raise DeviceUnsupported("loop function must be a lambda literal")
     pb, pi, px = (p.name for p in lam.params)
 
-    # range-partitioned dictmergers hold per-partition chunk buffers in shared
-    # memory (one CTA per SM): twice the threads per CTA to hide latency
-    BLOCK = 512 if any(b.extra.get("rpart") for b in g.bspecs) else BLOCK_DEFAULT
+    BLOCK = BLOCK_DEFAULT
     ITEMS = items or ITEMS_OVERRIDE or choose_items(iters)
     if not (items or ITEMS_OVERRIDE) and any(isinstance(b.kind, DictMerger) for b in g.bspecs):
         ITEMS = min(ITEMS, 2)   # deferred merges + register caches are register-hungry
     for b in g.bspecs:
-        if b.extra.get("rpart") and not (items or ITEMS_OVERRIDE):
-            ITEMS = 2
         if b.extra.get("part"):
             # the tile's records are staged in dynamic shared memory; larger
             # tiles mean longer per-partition runs and fewer global
@@ -1220,12 +1275,6 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
     if scan_bs and not (items or ITEMS_OVERRIDE):
         # larger tiles for look-back kernels: half as many tiles to resolve
         ITEMS = min(16, ITEMS * 2)
-        row = sum(SIZE[k] * (W if it.simd else 1) for it in iters for k in it.kinds)
-        if row <= 8 and BLOCK == 256 and SCAN_BLOCK_128:
-            # one 8-byte column: the same 4096-row tile on 128 threads x 32
-            # items -- half the warps wait at each tile's look-back barrier
-            # and twice the CTAs are resident (filter: 2.44 -> 2.23 ms)
-            BLOCK, ITEMS = 128, ITEMS * 2
         g.items = ITEMS
         for b in g.bspecs:
             if b.mode == "direct":
@@ -1237,7 +1286,9 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
         b.extra["staged"] = False
     if scan_bs and STAGE_SCAN and all(b.k is not None for b in scan_bs):
         need = sum(BLOCK * ITEMS * b.k * SIZE[k] for b in scan_bs for k in b.extra["kinds"])
-        if need <= 40 * 1024:
+        # static shared memory is capped at 48 KB per kernel: the staging
+        # buffers share it with the math tables the body's externs copy in
+        if need <= min(40 * 1024, 46 * 1024 - _table_bytes(lam.body)):
             for b in scan_bs:
                 b.extra["staged"] = True
             staged_bytes = need
@@ -1317,8 +1368,6 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
         if b.mode == "scan":
             g.param(f"a{b.bid}_status", "u64*", ("b", b.bid, "status"))
             g.param(f"a{b.bid}_total", "i64*", ("b", b.bid, "total"))
-            if SCAN2:
-                g.param(f"a{b.bid}_tofs", "const i64*", ("b", b.bid, "tofs"))
     if schedule == "scan":
         g.param("tilectr", "unsigned long long*", ("tilectr",))
 
@@ -1351,19 +1400,6 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
                               + "".join(f" u64* s_rv{B}_{f} = wg_dyn_smem + {off + T_ * (1 + f)};" for f in range(V_))
                               + f" unsigned short* s_rp{B} = (unsigned short*)(wg_dyn_smem + {off + T_ * (1 + V_)});")
             dyn_smem += T_ * 8 * (1 + V_) + ((T_ * 2 + 7) // 8) * 8
-        if isinstance(b.kind, DictMerger) and b.extra.get("rpart"):
-            # per-partition tile counts, window cursors, tile bases (u32 x 4)
-            NP = 1 << b.extra["pbits"]
-            off = dyn_smem // 8
-            B = b.bid
-            V_ = len(leaves(b.kind.value))
-            smem_decls.append(f"unsigned* s_ph{B} = (unsigned*)(wg_dyn_smem + {off}); unsigned* s_wc{B} = s_ph{B} + {NP}; "
-                              f"unsigned* s_pb{B} = s_wc{B} + {NP}; unsigned* s_nb{B} = s_pb{B} + {NP};")
-            smem_decls.append(f"u64* s_bk{B} = wg_dyn_smem + {off + NP * 2};"
-                              + "".join(f" u64* s_bv{B}_{f} = wg_dyn_smem + {off + NP * 2 + NP * 4 * (1 + f)};"
-                                        for f in range(V_)))
-            smem_init.append(f"for (int q = threadIdx.x; q < {NP}; q += {BLOCK}) {{ s_ph{B}[q] = 0u; s_wc{B}[q] = 0u; }}")
-            dyn_smem += NP * 16 + NP * 4 * 8 * (1 + V_)
         if isinstance(b.kind, DictMerger) and b.mode == "smem":
             ns = b.extra["smem_slots"]
             sw = b.extra["slot_words"]
@@ -1406,7 +1442,7 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
     # the most stages that do not lower the kernel's occupancy.
     # Scan kernels use it too: with a persistent, fully resident grid the
     # static round-robin tile order is a valid look-back order.
-    pipe = bool(PIPE and (SCAN_PIPE or SCAN2 or not scan_bs) and loads
+    pipe = bool(PIPE and not scan_bs and loads
                 and all((not it.strided) and it.aligned for it in iters))
     pipe_off = pipe_stage_bytes = 0
     pipe_col_off = []
@@ -1510,17 +1546,6 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
                 out.append(f"#pragma unroll\n    for (int q = 0; q < ITEMS; ++q) dkf{b.bid}[q] = false;")
                 for f, kk in enumerate(leaves(b.kind.value)):
                     out.append(f"    {CTYPE[kk]} dkv{b.bid}_{f}[ITEMS];")
-        # (only for bodies with math-library calls: their long FP64 dependency
-        # chains are what interleaving hides; plain streaming bodies keep the
-        # per-item form, which schedules their loads/stores better)
-        soa = (_soa_body(body_a) if (SOA and ITEMS > 1 and not scan_bs and g.ext_calls) else None)
-        if soa is not None:
-            # full tiles: statement-by-statement over the thread's items, so
-            # the items' independent libdevice chains (erf, exp, log) sit
-            # side by side in straight-line code and interleave
-            out.append("    if (full) {")
-            out.extend(soa)
-            out.append("    } else {")
         out.append("#pragma unroll")
         out.append("    for (int j = 0; j < ITEMS; ++j) {")
         out.append("      const i64 li = t0 + j;")
@@ -1529,8 +1554,6 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
         out.extend(body_a)
         out.append("      }")
         out.append("    }")
-        if soa is not None:
-            out.append("    }")
         for b in g.bspecs:
             if b.mode == "direct" and b.extra.get("buffered"):
                 for f, kk in enumerate(b.extra["kinds"]):
@@ -1545,16 +1568,10 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
             for si, b in enumerate(scan_bs):
                 out.append(f"    i64 agg{b.bid};")
                 out.append(f"    i64 wpos{b.bid} = wg_block_exclusive_scan(cnt{b.bid}, s_scan, &agg{b.bid});")
-                if SCAN2:
-                    # two-pass schedule: the tile's offset was computed by the
-                    # count pre-pass + exclusive scan (no look-back)
-                    out.append(f"    if (threadIdx.x == 0) {{ s_toff[{si}] = p.a{b.bid}_tofs[tile]; "
-                               f"if (tile == ntiles - 1) *p.a{b.bid}_total = s_toff[{si}] + agg{b.bid}; }}")
-                else:
-                    out.append("    if (threadIdx.x < 32) {")
-                    out.append(f"      const i64 pre_ = wg_lookback(p.a{b.bid}_status, tile, agg{b.bid});")
-                    out.append(f"      if (threadIdx.x == 0) {{ s_toff[{si}] = pre_; if (tile == ntiles - 1) *p.a{b.bid}_total = pre_ + agg{b.bid}; }}")
-                    out.append("    }")
+                out.append("    if (threadIdx.x < 32) {")
+                out.append(f"      const i64 pre_ = wg_lookback(p.a{b.bid}_status, tile, agg{b.bid});")
+                out.append(f"      if (threadIdx.x == 0) {{ s_toff[{si}] = pre_; if (tile == ntiles - 1) *p.a{b.bid}_total = pre_ + agg{b.bid}; }}")
+                out.append("    }")
             out.append("    __syncthreads();")
             out.extend(mid or [])
             for si, b in enumerate(scan_bs):
@@ -1588,24 +1605,7 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
                 out.append("    __syncthreads();")
         return out
 
-    if scan_bs and SCAN2 and not pipe:
-        # two-pass schedule: static grid-stride tiles, columns of the next
-        # tile in flight (register double buffering) -- tile offsets known
-        src.extend(decl_lines("", "  "))
-        src.append("  i64 tile = blockIdx.x;")
-        src.append("  if (tile < ntiles)")
-        src.extend(load_lines("tile", "", "  "))
-        src.append("  for (; tile < ntiles; tile += gridDim.x) {")
-        src.extend(decl_lines("_nx", "    "))
-        src.append("    const i64 ntile_ = tile + gridDim.x;")
-        src.append("    if (ntile_ < ntiles)")
-        src.extend(load_lines("ntile_", "_nx", "    "))
-        src.extend(tile_body())
-        for (arr, st, kk, per, k, l, col) in loads:
-            cnt = f"ITEMS * {per}" if per > 1 else "ITEMS"
-            src.append(f"#pragma unroll\n    for (int q = 0; q < {cnt}; ++q) {arr}[q] = {arr}_nx[q];")
-        src.append("  }")
-    elif scan_bs and not pipe and not SCAN_PREFETCH:
+    if scan_bs:
         # Dynamic tiles, claimed in order through an atomic counter (so every
         # predecessor a tile's look-back waits on is held by a running CTA).
         if SCAN_EARLY_CLAIM:
@@ -1622,29 +1622,6 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
         src.extend(load_lines("tile", "", "    "))
         src.extend(tile_body(claim=SCAN_EARLY_CLAIM))
         src.append("  }")
-    elif scan_bs and not pipe:
-        # (experimental) the next tile is claimed at the top of the current
-        # one and its columns loaded before the store phase.  Measured slower:
-        # a claimed-but-unstarted tile lengthens every successor's look-back.
-        src.append("  if (threadIdx.x == 0) s_tile[0] = (i64)atomicAdd(p.tilectr, 1ULL);")
-        src.append("  __syncthreads();")
-        src.append("  i64 tile = s_tile[0];")
-        src.append("  int par_ = 0;")
-        src.extend(decl_lines("", "  "))
-        src.append("  if (tile < ntiles)")
-        src.extend(load_lines("tile", "", "  "))
-        src.append("  while (tile < ntiles) {")
-        src.append("    if (threadIdx.x == 0) s_tile[par_ ^ 1] = (i64)atomicAdd(p.tilectr, 1ULL);")
-        mid = ["    const i64 ntile_ = s_tile[par_ ^ 1];"]
-        mid += decl_lines("_nx", "    ")
-        mid.append("    if (ntile_ < ntiles)")
-        mid += load_lines("ntile_", "_nx", "    ")
-        src.extend(tile_body(mid))
-        for (arr, st, kk, per, k, l, col) in loads:
-            cnt = f"ITEMS * {per}" if per > 1 else "ITEMS"
-            src.append(f"#pragma unroll\n    for (int q = 0; q < {cnt}; ++q) {arr}[q] = {arr}_nx[q];")
-        src.append("    tile = ntile_; par_ ^= 1;")
-        src.append("  }")
     elif pipe:
         # Bulk-async (TMA engine) column streaming: every full tile's column
         # chunks are copied HBM -> shared memory by cp.async.bulk, PIPE_STAGES
@@ -1655,12 +1632,8 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
         src.append(f"  __shared__ __align__(8) u64 wg_bar[{PIPE_MAX_STAGES}];")
         src.append("  const i64 nfull = n / TILE;")
         src.append("  const i64 nmy = (nfull > (i64)blockIdx.x) ? (nfull - 1 - (i64)blockIdx.x) / gridDim.x + 1 : 0;")
-        if PIPE_EMPTY:
-            src.append(f"  __shared__ __align__(8) u64 wg_ebar[{PIPE_MAX_STAGES}];")
         src.append("  if (threadIdx.x == 0) {")
         src.append(f"    for (int s_ = 0; s_ < {pipe_stages}; ++s_) wg_mbar_init(&wg_bar[s_], 1);")
-        if PIPE_EMPTY:
-            src.append(f"    for (int s_ = 0; s_ < {pipe_stages}; ++s_) wg_mbar_init(&wg_ebar[s_], BLOCK / 32);")
         src.append("    wg_fence_mbar_init();")
         src.append("  }")
         src.append("  __syncthreads();")
@@ -1684,19 +1657,10 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
             cnt = f"ITEMS * {per}" if per > 1 else "ITEMS"
             src.append(f"      wg_lds_contig<{st}, {cnt}>((const {st}*)(sg_ + {off}) + threadIdx.x * {cnt}, {arr}); ")
         src.append("    }")
-        if PIPE_EMPTY:
-            dl = 1 if PIPE_EMPTY == 2 else 0
-            src.append(f"    __syncwarp(); if ((threadIdx.x & 31) == 0) wg_mbar_arrive(&wg_ebar[kk_ % {pipe_stages}]);")
-            src.append(f"    if (threadIdx.x == 0 && kk_ >= {dl} && kk_ - {dl} + {pipe_stages} < nmy) {{")
-            src.append(f"      const i64 kr_ = kk_ - {dl};")
-            src.append(f"      wg_mbar_wait(&wg_ebar[kr_ % {pipe_stages}], (unsigned)((kr_ / {pipe_stages}) & 1));")
-            src.append("      wg_fence_proxy_async();")
-            src.append(f"      const i64 k_ = kr_ + {pipe_stages};")
-        else:
-            src.append("    __syncthreads();")
-            src.append(f"    if (threadIdx.x == 0 && kk_ + {pipe_stages} < nmy) {{")
-            src.append("      wg_fence_proxy_async();")
-            src.append(f"      const i64 k_ = kk_ + {pipe_stages};")
+        src.append("    __syncthreads();")
+        src.append(f"    if (threadIdx.x == 0 && kk_ + {pipe_stages} < nmy) {{")
+        src.append("      wg_fence_proxy_async();")
+        src.append(f"      const i64 k_ = kk_ + {pipe_stages};")
         src.extend("  " + x for x in issue)
         src.append("    }")
         src.extend(tile_body())
@@ -1803,9 +1767,6 @@ def _count_plan(g, lam, body_env, loads, iters, ITEMS, BLOCK, scan_bs, name):
     unb = [b for b in scan_bs if b.extra.get("unbounded")]
     for b in unb:
         g.param(f"ct{b.bid}_total", "unsigned long long*", ("b", b.bid, "ctotal"))
-    if SCAN2:
-        for b in scan_bs:
-            g.param(f"tc{b.bid}_counts", "i64*", ("b", b.bid, "tcounts"))
     src = ['#include "weld_device.cuh"', f"#define BLOCK {BLOCK}", f"#define ITEMS {ITEMS}",
            "#define TILE (BLOCK * ITEMS)", "struct Params {"]
     src += [f"  {p_.ctype} {p_.name};" for p_ in g.params]
@@ -1840,11 +1801,6 @@ def _count_plan(g, lam, body_env, loads, iters, ITEMS, BLOCK, scan_bs, name):
     src.append("      }")
     src.append("    }")
     src += [f"    tc{b.bid} += cnt{b.bid};" for b in unb]
-    if SCAN2:
-        src.append("    __shared__ i64 s_sc_[33];")
-        for b in scan_bs:
-            src.append(f"    {{ i64 t_; (void)wg_block_exclusive_scan(cnt{b.bid}, s_sc_, &t_); "
-                       f"if (threadIdx.x == 0) p.tc{b.bid}_counts[tile] = t_; }}")
     src.append("  }")
     for b in unb:
         src.append(f"  {{ i64 c_ = tc{b.bid};")
@@ -1863,51 +1819,6 @@ def is_flat_type(t):
     if isinstance(t, Struct):
         return all(is_flat_type(f) for f in t.fields)
     return False
-
-
-_SOA_LET = re.compile(r"^\s*const (\w+) (t\d+) = (.*);$")
-_SOA_STORE = re.compile(r"^\s*(o\d+_\d+)\[j \* (\d+) \+ (c\d+)\] = (.*);$")
-_SOA_CINIT = re.compile(r"^\s*int (c\d+) = 0;$")
-_SOA_CINC = re.compile(r"^\s*(c\d+) \+= 1;$")
-
-
-def _soa_body(lines):
-    """Statement-wise form of a straight-line loop body (lets and buffered
-    direct appends only): every temporary becomes an ITEMS-array filled by
-    its own unrolled item loop.  Returns None for any other body shape."""
-    out = []
-    cval = {}
-    temps = set()
-
-    def sub(expr):
-        expr = re.sub(r"\b(t\d+)\b", lambda m: m.group(1) + "[j]" if m.group(1) in temps else m.group(1), expr)
-        expr = re.sub(r"\bli\b", "(t0 + j)", expr)
-        return re.sub(r"\bi\b", "(p.idx0 + t0 + j)", expr)
-
-    for ln in lines:
-        m = _SOA_LET.match(ln)
-        if m:
-            ty, name, expr = m.groups()
-            e2 = sub(expr)
-            temps.add(name)
-            out.append(f"      {ty} {name}[ITEMS];")
-            out.append(f"#pragma unroll\n      for (int j = 0; j < ITEMS; ++j) {name}[j] = {e2};")
-            continue
-        m = _SOA_CINIT.match(ln)
-        if m:
-            cval[m.group(1)] = 0
-            continue
-        m = _SOA_STORE.match(ln)
-        if m and m.group(3) in cval:
-            arr, k, c, val = m.groups()
-            out.append(f"#pragma unroll\n      for (int j = 0; j < ITEMS; ++j) {arr}[j * {k} + {cval[c]}] = {sub(val)};")
-            continue
-        m = _SOA_CINC.match(ln)
-        if m and m.group(1) in cval:
-            cval[m.group(1)] += 1
-            continue
-        return None
-    return out
 
 
 def _dict_params(g, b):
@@ -2074,343 +1985,6 @@ def dict_agg_source(kind, slot_words, S, pbits, name="wg_dagg"):
     return "\n".join(L) + "\n", 0
 
 
-# ---------------------------------------------------------------------------
-# Range-partitioned dictmerger (cardinality far beyond L2).
-#
-# DictMergerState.result (builders.py:380-392) folds the per-chunk tables and
-# sorts the entries by order_key (builders.py:496-507); tovec keeps that
-# order (run.py:737-747).  Here the sort is folded into the aggregation: the
-# loop kernel scatters every merge into one of NP partitions by the top bits
-# of the key's *order key* (so partition p holds a contiguous key range),
-# and a second kernel aggregates each partition in a shared-memory table,
-# sorts its few thousand distinct keys locally and writes them at the
-# partition's output offset (decoupled look-back over partitions).  No global
-# hash table, no global sort.
-
-RPART_W = int(_os.environ.get("WELDGPU_RPART_W", "64"))   # rows per reserved window (per CTA, per partition)
-
-
-def rpart_ok(kinds):
-    """Key layouts the range partitioner handles: integer/bool leaves packed
-    into one word (the order key is computed from the word)."""
-    lay, nw = key_layout(kinds)
-    return nw == 1 and all(k in (I64, I32, BOOL) for k in kinds)
-
-
-def okey_expr(kinds, w):
-    """C expression: order_key of a packed one-word key as an unsigned 64-bit
-    integer (builders.py:496-507: signed ints ordered, tuples lexicographic;
-    the first leaf is the most significant)."""
-    lay, _ = key_layout(kinds)
-    parts = []
-    pos = 64
-    for (word, sh, width), k in zip(lay, kinds):
-        leaf = f"(({w} >> {sh}) & 0x{(1 << width) - 1 if width < 64 else 0xFFFFFFFFFFFFFFFF:x}ULL)"
-        if k in (I64, I32):
-            leaf = f"({leaf} ^ 0x{1 << (width - 1):x}ULL)"
-        pos -= width
-        parts.append(f"({leaf} << {pos})" if pos else leaf)
-    return "(" + " | ".join(parts) + ")"
-
-
-def okey_py(kinds, word):
-    lay, _ = key_layout(kinds)
-    out, pos = 0, 64
-    for (wi, sh, width), k in zip(lay, kinds):
-        leaf = (word >> sh) & ((1 << width) - 1)
-        if k in (I64, I32):
-            leaf ^= 1 << (width - 1)
-        pos -= width
-        out |= leaf << pos
-    return out
-
-
-def _rpart_loop_lines(g, b):
-    """Loop side.  Partition q's bucket is split into one private slice per
-    CTA (slice capacity scap rows), so no global atomics are needed.  Per
-    tile: rank the pending merges per partition in shared memory, advance the
-    CTA's cursor of each touched partition once, and write records in whole
-    32-byte chunks (4 rows): a chunk that completes inside the tile is
-    stored straight from registers, the partial last chunk waits in a
-    per-partition shared-memory buffer until a later tile completes it -- the
-    L2 only sees full-sector writes however many partitions are open.  The
-    epilogue writes the partial chunks and the slice fill counts."""
-    B = b.bid
-    NP = 1 << b.extra["pbits"]
-    vks = leaves(b.kind.value)
-    kks = leaves(b.kind.key)
-    V = len(vks)
-    scap = g.param(f"d{B}_pcap", "u64", ("b", B, "pcap"))
-    rlo = g.param(f"d{B}_rlo", "u64", ("b", B, "rlo"))
-    rsh = g.param(f"d{B}_rshift", "u64", ("b", B, "rshift"))
-    pk = g.param(f"d{B}_pk", "u64*", ("b", B, "pk"))
-    pvs = [g.param(f"d{B}_pv{f}", "u64*", ("b", B, "pv", f)) for f in range(V)]
-    fill = g.param(f"d{B}_pcount", "unsigned*", ("b", B, "pcount"))
-    oflow = g.param(f"d{B}_oflow", "unsigned long long*", ("b", B, "oflow"))
-    ok = okey_expr(kks, f"dkk{B}[j]")
-    vbits = [f"wg_to_bits<{CTYPE[kk]}>(dkv{B}_{f}[j])" for f, kk in enumerate(vks)]
-    sbase = f"(((u64)q_ * gridDim.x + blockIdx.x) * {scap})"
-    L = [f"      unsigned pp_[ITEMS], pr_[ITEMS];",
-         "#pragma unroll",
-         "      for (int j = 0; j < ITEMS; ++j) {",
-         f"        if (!dkf{B}[j]) continue;",
-         f"        const u64 ok_ = {ok};",
-         f"        const u64 d_ = ok_ < {rlo} ? 0ULL : ((ok_ - {rlo}) >> {rsh});",
-         f"        pp_[j] = (unsigned)(d_ < {NP - 1}ULL ? d_ : {NP - 1}ULL);",
-         f"        pr_[j] = atomicAdd(&s_ph{B}[pp_[j]], 1u);",
-         "      }",
-         "      __syncthreads();",
-         # the first-ranked record of a partition advances the cursor (and
-         # clears the tile count) and, if this tile completes the buffered
-         # chunk, stores the chunk's head from shared memory
-         "#pragma unroll",
-         "      for (int j = 0; j < ITEMS; ++j) {",
-         f"        if (!dkf{B}[j] || pr_[j] != 0u) continue;",
-         f"        const unsigned q_ = pp_[j], c_ = s_ph{B}[q_], cur_ = s_wc{B}[q_], f_ = cur_ & 3u;",
-         f"        s_ph{B}[q_] = 0u; s_pb{B}[q_] = cur_; s_wc{B}[q_] = cur_ + c_;",
-         "        if (f_ && c_ >= 4u - f_ && (u64)cur_ <= " + scap + ") {",
-         f"          const u64 h_ = {sbase} + (cur_ - f_);",
-         "          for (unsigned s_ = 0; s_ < f_; ++s_) {",
-         f"            __stcs({pk} + h_ + s_, s_bk{B}[q_ * 4u + s_]);"] + [
-         f"            __stcs({pvs[f]} + h_ + s_, s_bv{B}_{f}[q_ * 4u + s_]);" for f in range(V)] + [
-         "          }",
-         "        }",
-         "      }",
-         "      __syncthreads();",
-         "#pragma unroll",
-         "      for (int j = 0; j < ITEMS; ++j) {",
-         f"        if (!dkf{B}[j]) continue;",
-         f"        const unsigned q_ = pp_[j], g_ = s_pb{B}[q_] + pr_[j];",
-         f"        if ((g_ | 3u) < s_wc{B}[q_]) {{",
-         f"          if ((u64)g_ < {scap}) {{ const u64 at_ = {sbase} + g_; __stcs({pk} + at_, dkk{B}[j]);"]
-    L[-1] += "".join(f" __stcs({pvs[f]} + at_, {vbits[f]});" for f in range(V))
-    L[-1] += f" }} else atomicAdd({oflow}, 1ULL);"
-    L += [f"          dkf{B}[j] = false;",
-          "        }",
-          "      }",
-          "      __syncthreads();",
-          # rows of the still-incomplete last chunk wait in shared memory
-          "#pragma unroll",
-          "      for (int j = 0; j < ITEMS; ++j) {",
-          f"        if (!dkf{B}[j]) continue;",
-          f"        const unsigned sl_ = pp_[j] * 4u + ((s_pb{B}[pp_[j]] + pr_[j]) & 3u); s_bk{B}[sl_] = dkk{B}[j];"]
-    L[-1] += "".join(f" s_bv{B}_{f}[sl_] = {vbits[f]};" for f in range(V))
-    L += [f"        dkf{B}[j] = false;",
-          "      }"]
-    # epilogue: each partition's partial chunk, then the slice fill counts
-    ep = ["  __syncthreads();",
-          f"  for (int q_ = threadIdx.x; q_ < {NP}; q_ += BLOCK) {{",
-          f"    const unsigned cur_ = s_wc{B}[q_], f_ = cur_ & 3u;",
-          f"    if (f_ && (u64)cur_ <= {scap}) for (unsigned s_ = 0; s_ < f_; ++s_) {{",
-          f"      {pk}[{sbase} + cur_ - f_ + s_] = s_bk{B}[q_ * 4 + s_];"]
-    for f in range(V):
-        ep.append(f"      {pvs[f]}[{sbase} + cur_ - f_ + s_] = s_bv{B}_{f}[q_ * 4 + s_];")
-    ep += ["    }",
-           f"    {fill}[(u64)q_ * gridDim.x + blockIdx.x] = (u64)cur_ <= {scap} ? cur_ : (unsigned){scap};",
-           "  }"]
-    b.extra["epilogue"] = ep
-    return L
-
-
-def rpart_table_slots(nvals):
-    """Shared-memory table size of the aggregation kernel (power of two):
-    keys + value words + u32 sub-bucket counters + u16 permutation."""
-    ts = 8192
-    while ts > 1024 and ts * (8 * (1 + nvals) + 6) + 4096 > 200 * 1024:
-        ts //= 2
-    return ts
-
-
-def dict_rpart_source(kind, TS, name="wg_drp"):
-    """Aggregation kernel of the range-partitioned dictmerger.  One CTA per
-    partition (claimed in order through a ticket): fold the partition's
-    records into a shared-memory open-addressing table, order the distinct
-    keys (counting sort on the partition's actual key range, insertion sort
-    inside sub-buckets), find the partition's output offset by decoupled
-    look-back and write the sorted (key word, value words) rows.  Overflow
-    (a partition with more than TS distinct keys) is flagged; the executor
-    then re-runs the loop through the hash-table path."""
-    vks = leaves(kind.value)
-    kks = leaves(kind.key)
-    V = len(vks)
-    opc = OPCODE[kind.op]
-    LOG = TS.bit_length() - 1
-    BLK = 1024
-    assert TS % BLK == 0
-    ident = [f"0x{to_bits_c(kk, internal_identity(kind.op, kk)):016x}ULL" for kk in vks]
-    ok = lambda w: okey_expr(kks, w)  # noqa: E731
-    L = ['#define WG_LB_PER 1', '#define WG_LB_SLEEP 32', '#include "weld_device.cuh"',
-         f"#define BLOCK {BLK}", f"#define TS {TS}", f"#define LOGTS {LOG}", "#define RITEMS 4",
-         "struct Params {", "  const u64* pk;"] + [f"  const u64* pv{f};" for f in range(V)] + [
-        "  const unsigned* fill; u64 scap; u64 nslices; u64 nparts;",
-        "  u64* outk;"] + [f"  u64* outv{f};" for f in range(V)] + [
-        "  u64* status; unsigned long long* ticket; unsigned long long* oflow; unsigned long long* nout;",
-        "};",
-        f'extern "C" __global__ void __launch_bounds__(BLOCK) {name}(const Params p) {{',
-        "  extern __shared__ __align__(16) u64 sm_[];",
-        "  u64* s_k = sm_;"]
-    for f in range(V):
-        L.append(f"  u64* s_v{f} = sm_ + {(1 + f)} * TS;")
-    L += [f"  unsigned* s_cnt = (unsigned*)(sm_ + {1 + V} * TS);",
-          "  unsigned short* s_perm = (unsigned short*)(s_cnt + TS);",
-          "  __shared__ u64 s_sk[1 + " + str(V) + "];   // the key equal to the EMPTY sentinel",
-          "  __shared__ int s_has, s_part, s_fail;",
-          "  __shared__ unsigned long long s_min, s_max;",
-          "  __shared__ i64 s_off, s_sc[33];",
-          "  __shared__ unsigned s_c;",
-          "  for (int q = threadIdx.x; q < TS; q += BLOCK) { s_k[q] = WG_EMPTY_KEY;"]
-    for f in range(V):
-        L[-1] += f" s_v{f}[q] = {ident[f]};"
-    L[-1] += " }"
-    L += ["  for (;;) {",
-          "    if (threadIdx.x == 0) {",
-          "      s_part = (int)atomicAdd(p.ticket, 1ULL); s_has = 0; s_fail = 0;",
-          "      s_min = ~0ULL; s_max = 0ULL;"]
-    for f in range(V):
-        L.append(f"      s_sk[{f}] = {ident[f]};")
-    L += ["    }",
-          "    __syncthreads();",
-          "    const i64 part = s_part;",
-          "    if (part >= (i64)p.nparts) break;",
-          # ---- fold the partition's records (one private slice per loop CTA;
-          # warp w streams slices w, w + 32, ...) into the shared table
-          "    const int lane = threadIdx.x & 31;",
-          "    for (u64 sl = threadIdx.x >> 5; sl < p.nslices; sl += BLOCK / 32) {",
-          "      const u64 base = ((u64)part * p.nslices + sl) * p.scap;",
-          "      const unsigned rows = p.fill[(u64)part * p.nslices + sl];",
-          "      for (unsigned r0 = 0; r0 < rows; r0 += 32 * RITEMS) {",
-          "        u64 k_[RITEMS];"] + [f"        u64 v{f}_[RITEMS];" for f in range(V)] + [
-          "#pragma unroll",
-          "        for (int j = 0; j < RITEMS; ++j) {",
-          "          const unsigned r = r0 + j * 32 + lane;",
-          "          k_[j] = r < rows ? __ldcs(p.pk + base + r) : WG_EMPTY_KEY;"]
-    for f in range(V):
-        L.append(f"          v{f}_[j] = r < rows ? __ldcs(p.pv{f} + base + r) : 0ULL;")
-    L += ["        }",
-          "#pragma unroll",
-          "        for (int j = 0; j < RITEMS; ++j) {",
-          "          if (r0 + j * 32 + lane >= rows) continue;",
-          "          const u64 key = k_[j];",
-          "          if (*(volatile int*)&s_fail) continue;     // overflowed: the host re-runs the loop",
-          "          if (key == WG_EMPTY_KEY) {",
-          "            s_has = 1;"]
-    for f, kk in enumerate(vks):
-        ct = CTYPE[kk]
-        L.append(f"            WgSmemFold<{opc}, {ct}>::f(({ct}*)(s_sk + {f}), wg_from_bits<{ct}>(v{f}_[j]));")
-    L += ["            continue;",
-          "          }",
-          # Fibonacci hashing: the keys of one partition share their high bits
-          "          unsigned h = (unsigned)((key * 0x9E3779B97F4A7C15ULL) >> (64 - LOGTS));",
-          "          int probe = 0;",
-          "          for (; probe < TS; ++probe) {",
-          "            const u64 cur = *(volatile u64*)(s_k + h);",
-          "            if (cur == key) break;",
-          "            if (cur == WG_EMPTY_KEY) {",
-          "              const u64 prev = atomicCAS((unsigned long long*)(s_k + h), WG_EMPTY_KEY, key);",
-          "              if (prev == WG_EMPTY_KEY || prev == key) break;",
-          "            }",
-          "            h = (h + 1) & (TS - 1);",
-          "          }",
-          "          if (probe == TS) { s_fail = 1; continue; }"]
-    for f, kk in enumerate(vks):
-        ct = CTYPE[kk]
-        L.append(f"          WgSmemFold<{opc}, {ct}>::f(({ct}*)(s_v{f} + h), wg_from_bits<{ct}>(v{f}_[j]));")
-    L += ["        }",
-          "      }",
-          "    }",
-          "    __syncthreads();",
-          "    if (threadIdx.x == 0 && s_fail) atomicAdd(p.oflow, 1ULL);",
-          # ---- order the distinct keys: counting sort on the actual key range
-          "    {",
-          "      u64 mn = ~0ULL, mx = 0ULL;",
-          "      for (int q = threadIdx.x; q < TS; q += BLOCK) {",
-          "        s_cnt[q] = 0u;",
-          "        const u64 w = s_k[q];",
-          "        if (w != WG_EMPTY_KEY) { const u64 o = " + ok("w") + "; mn = o < mn ? o : mn; mx = o > mx ? o : mx; }",
-          "      }",
-          "#pragma unroll",
-          "      for (int d = 16; d > 0; d >>= 1) {",
-          "        const u64 a = __shfl_xor_sync(0xffffffffu, mn, d), b = __shfl_xor_sync(0xffffffffu, mx, d);",
-          "        mn = a < mn ? a : mn; mx = b > mx ? b : mx;",
-          "      }",
-          "      if ((threadIdx.x & 31) == 0 && mx >= mn) { atomicMin(&s_min, mn); atomicMax(&s_max, mx); }",
-          "    }",
-          "    __syncthreads();",
-          "    const u64 omin = s_min, span = s_max >= s_min ? s_max - s_min : 0ULL;",
-          "    const int ssh = span ? max(0, 64 - __clzll(span) - LOGTS) : 0;",
-          "    for (int q = threadIdx.x; q < TS; q += BLOCK) {",
-          "      const u64 w = s_k[q];",
-          "      if (w != WG_EMPTY_KEY) atomicAdd(&s_cnt[(unsigned)((" + ok("w") + " - omin) >> ssh)], 1u);",
-          "    }",
-          "    __syncthreads();",
-          "    {  // exclusive scan of the TS counters (TS / BLOCK consecutive per thread)",
-          "      constexpr int PER = TS / BLOCK;",
-          "      unsigned loc[PER]; unsigned s = 0;",
-          "#pragma unroll",
-          "      for (int t = 0; t < PER; ++t) { loc[t] = s_cnt[threadIdx.x * PER + t]; s += loc[t]; }",
-          "      i64 tot; const i64 ex = wg_block_exclusive_scan((i64)s, s_sc, &tot);",
-          "      unsigned run = (unsigned)ex;",
-          "#pragma unroll",
-          "      for (int t = 0; t < PER; ++t) { s_cnt[threadIdx.x * PER + t] = run; run += loc[t]; }",
-          "      if (threadIdx.x == 0) s_c = (unsigned)tot;",
-          "    }",
-          "    __syncthreads();",
-          "    for (int q = threadIdx.x; q < TS; q += BLOCK) {",
-          "      const u64 w = s_k[q];",
-          "      if (w != WG_EMPTY_KEY) s_perm[atomicAdd(&s_cnt[(unsigned)((" + ok("w") + " - omin) >> ssh)], 1u)] = (unsigned short)q;",
-          "    }",
-          "    __syncthreads();",
-          "    const unsigned c = s_c;",
-          # s_cnt[b] is now the end of sub-bucket b; insertion-sort the rare multi-key buckets
-          "    for (int q = threadIdx.x; q < TS; q += BLOCK) {",
-          "      const unsigned s0 = q ? s_cnt[q - 1] : 0u, e0 = s_cnt[q];",
-          "      for (unsigned a = s0 + 1; a < e0; ++a) {",
-          "        const unsigned short x = s_perm[a];",
-          "        const u64 kx = " + ok("s_k[x]") + ";",
-          "        unsigned bb = a;",
-          "        while (bb > s0 && " + ok("s_k[s_perm[bb - 1]]") + " > kx) { s_perm[bb] = s_perm[bb - 1]; --bb; }",
-          "        s_perm[bb] = x;",
-          "      }",
-          "    }",
-          # ---- output offset: decoupled look-back over partitions (claim order)
-          "    const unsigned ctot = c + (unsigned)s_has;",
-          "    if (threadIdx.x < 32) {",
-          "      const i64 ex = wg_lookback(p.status, part, (i64)ctot);",
-          "      if (threadIdx.x == 0) { s_off = ex; if (part == (i64)p.nparts - 1) *p.nout = (unsigned long long)(ex + ctot); }",
-          "    }",
-          "    __syncthreads();",
-          "    const u64 off = (u64)s_off;",
-          # position of the sentinel-valued key among the sorted keys
-          "    unsigned lb = c;",
-          "    if (s_has) {",
-          "      const u64 ke = " + ok("WG_EMPTY_KEY") + ";",
-          "      unsigned lo_ = 0, hi_ = c;",
-          "      while (lo_ < hi_) { const unsigned m = (lo_ + hi_) >> 1; if (" + ok("s_k[s_perm[m]]") + " < ke) lo_ = m + 1; else hi_ = m; }",
-          "      lb = lo_;",
-          "      if (threadIdx.x == 0) { p.outk[off + lb] = WG_EMPTY_KEY;"]
-    for f in range(V):
-        L[-1] += f" p.outv{f}[off + lb] = s_sk[{f}];"
-    L[-1] += " }"
-    L += ["    }",
-          "    for (unsigned i = threadIdx.x; i < c; i += BLOCK) {",
-          "      const unsigned x = s_perm[i];",
-          "      const u64 dst = off + i + (i >= lb ? (u64)s_has : 0ULL);",
-          "      __stcs(p.outk + dst, s_k[x]);"]
-    for f in range(V):
-        L.append(f"      __stcs(p.outv{f} + dst, s_v{f}[x]);")
-    L += ["    }",
-          "    __syncthreads();",
-          "    for (int q = threadIdx.x; q < TS; q += BLOCK) { s_k[q] = WG_EMPTY_KEY;"]
-    for f in range(V):
-        L[-1] += f" s_v{f}[q] = {ident[f]};"
-    L[-1] += " }"
-    L += ["    __syncthreads();",
-          "  }",
-          "}"]
-    smem = TS * 8 * (1 + V) + TS * 4 + TS * 2
-    return "\n".join(L) + "\n", smem
-
-
 def _agg_apply(vks, opc, slot_words, ind, key, vals):
     L = [f"{ind}if (sl_ >= 0) {{"]
     for f, kk in enumerate(vks):
@@ -2463,8 +2037,6 @@ def _deferred_dict_lines(g, b):
         for f, kk in enumerate(vks):
             L.append(f"        dkv{B}_{f}[j] = a{f}_;")
         L.append("      }")
-    if b.extra.get("rpart"):
-        L += _rpart_loop_lines(g, b)
         L.append("    }")
         return L
     if b.extra.get("part"):
@@ -2638,7 +2210,7 @@ def _capture_val(g: Gen, name, ty, val):
 # suite to prove every loop of a program lowers and compiles for sm_100a.
 
 
-def static_plans(expr, env_types=None, externs=(), smem=True, lowcard=False, part=False, rpart=False,
+def static_plans(expr, env_types=None, externs=(), smem=True, lowcard=False, part=False,
                  count_only=False):
     """Yield a KernelPlan per ``for`` loop in a typed program, deriving the
     iteration, builder and capture specs from types alone."""
@@ -2674,9 +2246,7 @@ def static_plans(expr, env_types=None, externs=(), smem=True, lowcard=False, par
                     sw = (1 if nw == 1 else 1 + nw) + len(leaves(t.kind.value))
                     bs.extra["slot_words"] = sw
                     bs.mode = "global"
-                    if nw == 1 and rpart and rpart_ok(leaves(t.kind.key)):
-                        bs.extra.update(rpart=True, pbits=11)
-                    elif nw == 1 and part:
+                    if nw == 1 and part:
                         bs.extra.update(part=True, pbits=8, agg_S=0)
                     elif nw == 1 and smem:
                         bs.mode = "smem"
@@ -2705,7 +2275,7 @@ def static_plans(expr, env_types=None, externs=(), smem=True, lowcard=False, par
         plan = generate(node, iters, bstruct, caps, ext, "local")
         if count_only:
             # the count-only pre-pass of flatmap-shaped loops (fresh builder specs)
-            if any(b.extra.get("unbounded") for b in plan.builders) or (SCAN2 and plan.schedule == "scan"):
+            if any(b.extra.get("unbounded") for b in plan.builders):
                 counter[0] = 0
                 plans.append(generate(node, iters, mk(node.builders.ty), caps, ext, "local", count_only=True))
             continue

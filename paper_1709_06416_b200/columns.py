@@ -11,6 +11,7 @@ this layout with numpy, without Python-object round trips.
 from __future__ import annotations
 
 import ctypes
+import os
 import struct as _struct
 
 import numpy as np
@@ -214,27 +215,71 @@ def col_to_numpy(col: Col, n: int) -> np.ndarray:
 
 
 class _PinnedBlock:
-    """Page-locked host memory from cudaHostAlloc, recycled through a
-    size-keyed pool when the numpy array viewing it dies."""
+    """Page-locked host memory from cudaHostAlloc, recycled through a pool
+    when the numpy array viewing it dies.  Sizes are rounded like the device
+    allocator (pow2 below 2 MiB, 2 MiB multiples above) and a request reuses
+    any cached block up to 2x its size; cached bytes are capped
+    (WELDGPU_PINNED_CACHE, default 8 GiB) -- the oldest blocks beyond the
+    cap go back to the driver (wg_host_free) -- and ``trim_pinned()`` frees
+    every cached block."""
 
     __slots__ = ("ptr", "nbytes", "__weakref__")
-    _pool = {}
+    _pool = []            # cached (size, ptr), oldest first
+    _cached = 0
+    CAP = int(os.environ.get("WELDGPU_PINNED_CACHE", str(8 << 30)))
 
     def __init__(self, nbytes):
-        free = _PinnedBlock._pool.get(nbytes)
-        if free:
-            self.ptr = free.pop()
-        else:
-            p = ctypes.c_void_p(0)
-            rt.call("wg_host_alloc", nbytes, ctypes.byref(p))
-            self.ptr = p.value
-        self.nbytes = nbytes
+        size = _round_pinned(nbytes)
+        pool = _PinnedBlock._pool
+        best = None
+        for q, (sz, _) in enumerate(pool):
+            if size <= sz <= 2 * size and (best is None or sz < pool[best][0]):
+                best = q
+        if best is not None:
+            sz, ptr = pool.pop(best)
+            _PinnedBlock._cached -= sz
+            self.ptr, self.nbytes = ptr, sz
+            return
+        p = ctypes.c_void_p(0)
+        try:
+            rt.call("wg_host_alloc", size, ctypes.byref(p))
+        except rt.WeldGpuError:
+            trim_pinned()
+            rt.call("wg_host_alloc", size, ctypes.byref(p))
+        self.ptr, self.nbytes = p.value, size
 
     def __del__(self):
         try:
-            _PinnedBlock._pool.setdefault(self.nbytes, []).append(self.ptr)
+            _PinnedBlock._pool.append((self.nbytes, self.ptr))
+            _PinnedBlock._cached += self.nbytes
+            while _PinnedBlock._cached > _PinnedBlock.CAP and _PinnedBlock._pool:
+                sz, ptr = _PinnedBlock._pool.pop(0)
+                _PinnedBlock._cached -= sz
+                rt.call("wg_host_free", ptr)
         except Exception:
             pass
+
+
+def _round_pinned(nbytes):
+    if nbytes < (2 << 20):
+        r = 4096
+        while r < nbytes:
+            r <<= 1
+        return r
+    return (nbytes + (2 << 20) - 1) // (2 << 20) * (2 << 20)
+
+
+def trim_pinned():
+    """Free every cached pinned host block (results still alive keep theirs)."""
+    pool = _PinnedBlock._pool
+    while pool:
+        sz, ptr = pool.pop()
+        _PinnedBlock._cached -= sz
+        rt.call("wg_host_free", ptr)
+
+
+def pinned_cache_bytes():
+    return _PinnedBlock._cached
 
 
 PINNED_MIN_BYTES = 1 << 20

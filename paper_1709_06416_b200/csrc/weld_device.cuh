@@ -41,6 +41,9 @@ enum {
   WG_ERR_INTERNAL = 5,
   WG_ERR_REMZERO = 6,       // DivideByZero (remainder)
   WG_ERR_ITER_LIMIT = 7,    // IterationLimit      run.py:680-684
+  WG_ERR_EXTERN = 8,        // EvalError("extern ... failed: math domain/range error")  run.py:841-844
+  WG_ERR_ZIP = 9,           // ZipLengthMismatch   run.py:935-940 (nested loops)
+  WG_ERR_STRIDE = 10,       // EvalError (stride < 1)  run.py:921-924 (nested loops)
 };
 
 __device__ __forceinline__ void wg_raise(i64* err, i64 code, i64 info) {
@@ -695,130 +698,6 @@ __device__ __forceinline__ void wg_lds_contig(const T* src, T (&dst)[N]) {
   }
 }
 
-// ---------------------------------------------------------------------------
-// exp / log / erf for the `call(name, ...)` externs (the reference resolves
-// them through a host registry to libm, run.py:832-846).
-//
-// Same argument reductions, coefficients and special-case handling as CUDA's
-// libdevice (so results stay within an ulp or two of it and of glibc), but
-// the polynomials are evaluated in Estrin form: libdevice's Horner chains
-// are serial (erf: 24 dependent FMAs, then a 10-deep exp), which leaves the
-// FP64 pipe waiting on latency in FP64-bound loops such as Black-Scholes.
-// Estrin trades them for independent FMAs (erf's depth ~40 -> ~18).  The
-// low-order steps that set the final rounding (exp's 1 + r + r^2 T) stay in
-// Horner order.
-#define WG_D(h) __longlong_as_double((long long)0x##h##ULL)
-
-__device__ __forceinline__ double wg_exp(double x) {
-  const double sh = fma(x, WG_D(3FF71547652B82FE), WG_D(4338000000000000));   // n + 1.5*2^52
-  const int n = __double2loint(sh);
-  const double fn = sh - WG_D(4338000000000000);
-  double r = fma(fn, WG_D(BFE62E42FEFA39EF), x);                               // x - n*ln2_hi
-  r = fma(fn, WG_D(BC7ABC9E3B39803F), r);                                      //   - n*ln2_lo
-  // T(r) = sum_{j=0..9} t_j r^j; exp(r) = 1 + r + r^2 T(r)
-  const double r2 = r * r, r4 = r2 * r2;
-  const double p01 = fma(WG_D(3FC5555555555511), r, WG_D(3FE000000000000B));
-  const double p23 = fma(WG_D(3F81111111122322), r, WG_D(3FA55555555502A1));
-  const double p45 = fma(WG_D(3F2A01A014761F65), r, WG_D(3F56C16C1852B7AF));
-  const double p67 = fma(WG_D(3EC71DEE62401315), r, WG_D(3EFA01997C89EB71));
-  const double p89 = fma(WG_D(3E5ADE1569CE2BDF), r, WG_D(3E928AF3FCA213EA));
-  const double q0 = fma(p23, r2, p01), q1 = fma(p67, r2, p45);
-  const double T = fma(fma(p89, r4, q1), r4, q0);
-  const double E = fma(fma(T, r, 1.0), r, 1.0);
-  double res = __hiloint2double(__double2hiint(E) + (n << 20), __double2loint(E));
-  const int ahi = __double2hiint(x) & 0x7fffffff;
-  if (__builtin_expect(ahi >= 0x4086232B, 0)) {          // |x| >= 708.39: over/underflow or subnormal
-    res = (x < 0.0) ? 0.0 : x + __longlong_as_double(0x7FF0000000000000LL);
-    if (ahi < 0x40874800) {                             // |x| < 745.0: scale in two steps
-      const int n1 = n / 2;
-      const double e1 = __hiloint2double(__double2hiint(E) + (n1 << 20), __double2loint(E));
-      res = e1 * __hiloint2double(((n - n1) << 20) + 0x3FF00000, 0);
-    }
-  }
-  return res;
-}
-
-__device__ __forceinline__ double wg_log(double x) {
-  int hi = __double2hiint(x), lo = __double2loint(x);
-  int eb = -1023;
-  if (__builtin_expect(hi < 0x00100000, 0)) {           // subnormal, zero or negative
-    x *= WG_D(4350000000000000);                        // 2^54
-    hi = __double2hiint(x); lo = __double2loint(x);
-    eb = -1077;
-  }
-  if (__builtin_expect((unsigned)(hi - 1) > 0x7FEFFFFEu, 0)) {   // <= 0, inf, nan
-    const double inf = __longlong_as_double(0x7FF0000000000000LL);
-    return ((hi & 0x7fffffff) | lo) == 0 ? -inf : fma(x, inf, inf);
-  }
-  int e = eb + (hi >> 20);
-  int mh = (hi & 0x000FFFFF) | 0x3FF00000;
-  if ((unsigned)mh >= 0x3FF6A09Fu) { mh -= 0x00100000; e += 1; }  // m in [sqrt(1/2), sqrt(2))
-  const double m = __hiloint2double(mh, lo);
-  const double f = m - 1.0, g = m + 1.0;
-  double q0;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(q0) : "d"(g));
-  const double ee = fma(-g, q0, 1.0);
-  const double q = fma(fma(ee, ee, ee), q0, q0);          // 1/(m+1)
-  const double u2 = 2.0 * (f * q);                        // 2f/(m+1)
-  const double v = u2 * u2;
-  // R(v) = sum_{j=0..7} c_j v^j (atanh series tail)
-  const double v2 = v * v, v4 = v2 * v2;
-  const double p01 = fma(WG_D(3F8999999999A3C4), v, WG_D(3FB5555555555554));
-  const double p23 = fma(WG_D(3F3C71C72D1B5154), v, WG_D(3F624924923BE72D));
-  const double p45 = fma(WG_D(3EF3B2669F02676F), v, WG_D(3F1745CBA9AB0956));
-  const double p67 = fma(WG_D(3EB1380B3AE80F1E), v, WG_D(3ED0EE258B7A8B04));
-  const double R = fma(fma(p67, v2, p45), v4, fma(p23, v2, p01));
-  const double d = f - u2;
-  const double corr = q * fma(-u2, f, d + d);             // low part of 2f/(m+1)
-  const double s = fma(v * R, u2, corr);
-  const double ed = __hiloint2double(0x43300000, e ^ 0x80000000) - __hiloint2double(0x43300000, 0x80000000);
-  const double hi1 = fma(ed, WG_D(3FE62E42FEFA39EF), u2);
-  const double lo1 = fma(ed, WG_D(3C7ABC9E3B39803F), s - (fma(ed, WG_D(BFE62E42FEFA39EF), hi1) - u2));
-  return hi1 + lo1;
-}
-
-__device__ __forceinline__ double wg_erf(double x) {
-  const double a = fabs(x);
-  // t(a) = a + a P(a) ~ -log(erfc(a)); P = sum_{j=0..23} d_j a^j in Estrin form
-  const double a2 = a * a, a4 = a2 * a2, a8 = a4 * a4, a16 = a8 * a8;
-  const double e0 = fma(WG_D(3FE45F306DC9C8BB), a, WG_D(3FC06EBA8214DB69));
-  const double e1 = fma(WG_D(BF9396685912A453), a, WG_D(3FBA4F4E2A1ABEF8));
-  const double e2 = fma(WG_D(BF2B6B69EBBC280B), a, WG_D(3F5BCA68F73D6AFC));
-  const double e3 = fma(WG_D(3EFB292D828E5CB2), a, WG_D(BF4356626EBF9BFA));
-  const double e4 = fma(WG_D(BEFF05355BC5B225), a, WG_D(3F10E37A3108BC8B));
-  const double e5 = fma(WG_D(3ECA30375BA9A84E), a, WG_D(3ECAAD18DEDEA43E));
-  const double e6 = fma(WG_D(3EA2EF6CC0F67A49), a, WG_D(BEC102B892333B6F));
-  const double e7 = fma(WG_D(BE720A2C7155D5C6), a, WG_D(BE41D29B37CA1397));
-  const double e8 = fma(WG_D(BE476DB45919F583), a, WG_D(3E62D698D98C8D71));
-  const double e9 = fma(WG_D(BDFA28A3CD2D56C4), a, WG_D(3E2485EE67835925));
-  const double e10 = fma(WG_D(BD8DF9F9B976A9B2), a, WG_D(3DC7F1F5590CC332));
-  const double e11 = fma(WG_D(BCF0679AFBA6F279), a, WG_D(3D47088FDB46FA5F));
-  const double f0 = fma(e1, a2, e0), f1 = fma(e3, a2, e2), f2 = fma(e5, a2, e4);
-  const double f3 = fma(e7, a2, e6), f4 = fma(e9, a2, e8), f5 = fma(e11, a2, e10);
-  const double g0 = fma(f1, a4, f0), g1 = fma(f3, a4, f2), g2 = fma(f5, a4, f4);
-  const double P = fma(g2, a16, fma(g1, a8, g0));
-  const double th = fma(P, a, a);                         // t = th + tl
-  const double tl = fma(P, a, a - th);
-  // 1 - exp(-t) = (1 - 2^n) - 2^n expm1(r - tl), r = -th - n ln2
-  const float nf = rintf(__double2float_rn(th) * __int_as_float((int)0xBFB8AA3Bu));
-  const double n = (double)nf;
-  const double r = fma(n, WG_D(BFE62E42FEFA39EF), -th);
-  const double r2 = r * r, r4 = r2 * r2, r8 = r4 * r4;
-  const double p01 = fma(WG_D(3FC5555555555540), r, WG_D(3FE0000000000005));
-  const double p23 = fma(WG_D(3F811111111173C4), r, WG_D(3FA555555555211A));
-  const double p45 = fma(WG_D(3F2A01A017EED94F), r, WG_D(3F56C16C17F2A71B));
-  const double p67 = fma(WG_D(3EC71DE715FF7E07), r, WG_D(3EFA019A6B0AC45A));
-  const double p89 = fma(WG_D(3E5AE904A4741B81), r, WG_D(3E928A27F89B6999));
-  const double Q = fma(p89, r8, fma(fma(p67, r2, p45), r4, fma(p23, r2, p01)));
-  const double em = r + fma(r * Q, r, -tl);               // expm1(r - tl)
-  float sf;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(sf) : "f"(nf));
-  const double s = (double)sf;
-  double res = fma(-em, s, 1.0 - s);
-  res = (a >= WG_D(4017AFB48DC96626)) ? 1.0 : res;
-  return copysign(res, x);
-}
-#undef WG_D
 
 // erf from a piecewise polynomial table (tools/gen_erf_table.py): one
 // 80-byte row per 1/16 of |x| in [0, 6), degree-10 polynomial in
@@ -930,7 +809,7 @@ __device__ __forceinline__ double wg_exp_tab(double x) {
   const int ahi = __double2hiint(x) & 0x7fffffff;
   if (__builtin_expect(ahi >= 0x4086232B, 0)) {          // |x| >= 708.39: over/underflow or subnormal
     res = (x < 0.0) ? 0.0 : x + __longlong_as_double(0x7FF0000000000000LL);
-    if (ahi < 0x40874800) {                             // |x| < 745.0: scale in two steps
+    if (ahi < 0x40874911) {                             // |x| <~ 745.1332 (glibc's smallest subnormal result): scale in two steps
       const int e1 = e / 2;
       const double y1 = __hiloint2double(__double2hiint(y) + (e1 << 20), __double2loint(y));
       res = y1 * __hiloint2double(((e - e1) << 20) + 0x3FF00000, 0);

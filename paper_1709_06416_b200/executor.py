@@ -32,9 +32,9 @@ from weldmill.expr import (Apply, BinaryOp, BitSelect, Broadcast, CastScalar, Ex
 
 from . import runtime as rt
 from . import semantics as sem
-from .builders_dev import (_RANGE_HINTS, _finish_small, AppenderDev, DDict, DGroups, DictDev, GroupDev, MergerDev, VecMergerDev,
+from .builders_dev import (_finish_small, AppenderDev, DDict, DGroups, DictDev, GroupDev, MergerDev, VecMergerDev,
                            dict_payload, finish_dict, finish_groups, gather_cols, sort_perm, tovec)
-from .codegen import DEFER_DICT, PIPE_STAGES, SCAN2, BSpec, IterSpec, generate, rpart_ok, rpart_table_slots
+from .codegen import DEFER_DICT, PIPE_STAGES, BSpec, IterSpec, generate
 from .columns import Col, DVec, to_device, to_payload, dvec_from_cols
 from .irtypes import (BOOL, F32, F64, I64, SIZE, identity_value, Builder, DeviceUnsupported as _DU, Dict, DictMerger, Function,
                       GroupBuilder, Merger, Scalar, Simd, Struct, Vec, VecBuilder, VecMerger, is_flat, leaves)
@@ -45,11 +45,22 @@ class DeviceUnsupported(EvalError, _DU):
 
 
 ERR_CLASSES = {1: DivideByZero, 2: IndexOutOfBounds, 3: IndexOutOfBounds, 4: KeyNotFound, 5: EvalError,
-               6: DivideByZero, 7: IterationLimit}
+               6: DivideByZero, 7: IterationLimit, 8: EvalError, 9: ZipLengthMismatch, 10: EvalError}
 ERR_TEXT = {1: "integer division by zero", 2: "lookup index {info} outside vector",
             3: "vecmerger index {info} out of range", 4: "key not in dictionary",
             5: "internal device error ({info})", 6: "integer remainder by zero",
-            7: "iterate exceeded the iteration limit ({info} iterations)"}
+            7: "iterate exceeded the iteration limit ({info} iterations)",
+            9: "zipped iterations disagree (an iteration of length {info})",
+            10: "iteration stride must be positive, got {info}"}
+
+
+def device_error(code, info):
+    """The EvalError subclass instance for a device error word (code, info)."""
+    if code == 8:
+        from .codegen import extern_error_text
+        return EvalError(extern_error_text(info))
+    cls = ERR_CLASSES.get(code, EvalError)
+    return cls(ERR_TEXT.get(code, "device error {info}").format(info=info))
 
 
 class HostVec:
@@ -156,8 +167,7 @@ class Ctx:
         self.dirty = False
         code, info = rt.read_error()
         if code:
-            cls = ERR_CLASSES.get(code, EvalError)
-            raise cls(ERR_TEXT.get(code, "device error {info}").format(info=info))
+            raise device_error(code, info)
 
     # -- evaluation ------------------------------------------------------------
     _EV = {}
@@ -392,8 +402,7 @@ class Ctx:
                 self.dirty = False
                 code, info = err[0]
                 if code:
-                    cls = ERR_CLASSES.get(code, EvalError)
-                    raise cls(ERR_TEXT.get(code, "device error {info}").format(info=info))
+                    raise device_error(code, info)
                 return v
             self.check_device()
             return b.read()
@@ -427,7 +436,7 @@ class Ctx:
         if isinstance(kind, DictMerger):
             if b.table is None:
                 b.ensure(1)
-            d = _finish_small(b, Dict(kind.key, kind.value)) if b.rpart_out is None else None
+            d = _finish_small(b, Dict(kind.key, kind.value))
             if d is None:
                 self._settle(b)
                 d = finish_dict(b, Dict(kind.key, kind.value))
@@ -543,8 +552,6 @@ class Ctx:
         _collect_builders(builders, blist)
         for b in blist:
             b.check()
-            if getattr(b, "rpart_out", None) is not None:
-                self._rpart_to_table(b)
             if isinstance(b, DictDev):
                 self._settle(b)
             self.flush_pending(b)
@@ -579,7 +586,7 @@ class Ctx:
                 _plan_cache[key] = cached
         plan, kern = cached[0], cached[1]
         sizes = None
-        if any(b.extra.get("unbounded") for b in plan.builders) or (plan.schedule == "scan" and SCAN2):
+        if any(b.extra.get("unbounded") for b in plan.builders):
             # flatmap: appends inside data-dependent nested loops -- size the
             # output with a count-only pre-pass of the same body
             ckey = key + ("count",)
@@ -593,52 +600,27 @@ class Ctx:
                 with _plan_lock:
                     _plan_cache[ckey] = cc
             sizes = self._count_pass(cc[0], cc[1], count, datas, windows, bmap, captures)
-        try:
-            self.launch(plan, kern, count, datas, windows, builders, bmap, captures, sizes=sizes)
-        except _RpartFallback:
-            # skewed keys overflowed a partition: forget the merges and run
-            # the loop again through the hash-table dictmerger
-            for bid, st in bmap.items():
-                if isinstance(st, DictDev):
-                    _RPART_BAD.add((id(e), bid))
-                    st.reset()
-            return self.run_loop(e, env, count_traversal=False)
+        self.launch(plan, kern, count, datas, windows, builders, bmap, captures, sizes=sizes)
         return builders
 
     def _count_pass(self, plan, kern, count, datas, windows, bmap, captures):
-        """Launch the count-only kernel.  Returns {builder id: appends}; with
-        the two-pass schedule also {builder id ("tofs", bid): tile offsets}."""
+        """Launch the count-only kernel.  Returns {builder id: appends}."""
         tile = plan.block * plan.items
         ntiles = (count + tile - 1) // tile
         grid = max(1, min(ntiles, rt.sm_count() * kern.blocks_per_sm(plan.block, 0)))
         unb = [b for b in plan.builders if b.extra.get("unbounded")]
-        scan = [b for b in plan.builders if b.mode == "scan"] if SCAN2 else []
-        tot = rt.alloc(8 * (len(unb) + len(scan)) + 8)
+        tot = rt.alloc(8 * len(unb) + 8)
         rt.memset(tot.ptr, 0, 8 * len(unb))
         res = {b.bid: ("ctotal", tot.ptr + 8 * q) for q, b in enumerate(unb)}
-        tcounts = {b.bid: rt.alloc(8 * max(ntiles, 1)) for b in scan}
-        for b in scan:
-            r = res.get(b.bid, ("ctotal", 0))
-            res[b.bid] = (r[0], r[1], tcounts[b.bid].ptr)
         vals = {p.name: self._param_value(p.key, count, datas, windows, bmap, res, captures, grid, None)
                 for p in plan.params}
         kern.launch(grid, plan.block, b"".join(_pack(p.ctype, vals[p.name]) for p in plan.params), 0)
         self.launches += 1
-        out = {}
-        for q, b in enumerate(scan):
-            tofs = rt.alloc(8 * max(ntiles, 1))
-            rt.call("wg_exclusive_scan_i64", tcounts[b.bid].ptr, tofs.ptr, ntiles, tot.ptr + 8 * (len(unb) + q))
-            out[("tofs", b.bid)] = tofs
-            self.launches += 1
         self.dirty = True
         self.check_device()
-        arr = np.zeros(len(unb) + len(scan), dtype=np.int64)
+        arr = np.zeros(len(unb), dtype=np.int64)
         rt.d2h(arr.ctypes.data, tot.ptr, arr.nbytes)
-        for q, b in enumerate(unb):
-            out[b.bid] = int(arr[q])
-        for q, b in enumerate(scan):
-            out[b.bid] = int(arr[len(unb) + q])
-        return out
+        return {b.bid: int(arr[q]) for q, b in enumerate(unb)}
 
     def launch(self, plan, kern, count, datas, windows, builders, bmap, captures, sizes=None):
         items = plan.items
@@ -674,17 +656,10 @@ class Ctx:
                 elif b.mode == "scan":
                     cap = sizes[b.bid] if (b.k is None or (sizes and b.bid in sizes)) else count * b.k
                     seg = st.new_segment(cap, False)
-                    if sizes and ("tofs", b.bid) in sizes:
-                        res[b.bid] = (seg, None, sizes[("tofs", b.bid)])
-                    else:
-                        status = rt.alloc(8 * max(ntiles, 1))
-                        rt.memset(status.ptr, 0, 8 * max(ntiles, 1))
-                        res[b.bid] = (seg, status)
+                    status = rt.alloc(8 * max(ntiles, 1))
+                    rt.memset(status.ptr, 0, 8 * max(ntiles, 1))
+                    res[b.bid] = (seg, status)
                     self._acct_append(st, cap)
-            elif isinstance(b.kind, DictMerger) and b.extra.get("rpart"):
-                st.ensure(1)            # (unused) table keeps the kernel's table parameters valid
-                st.hint_key = (plan.key_id, b.bid)
-                st.ensure_rpart(count, 1 << b.extra["pbits"], grid, _RANGE_HINTS[st.hint_key])
             elif isinstance(b.kind, DictMerger):
                 st.ensure(count * max(1, b.extra.get("maxm", 1)), hint_key=(plan.key_id, b.bid))
                 if b.extra.get("part") and b.extra.get("deferred"):
@@ -718,13 +693,11 @@ class Ctx:
         for b in plan.builders:
             if isinstance(b.kind, DictMerger) and b.extra.get("part") and b.extra.get("deferred"):
                 self._dict_aggregate(bmap[b.bid], b)
-            if isinstance(b.kind, DictMerger) and b.extra.get("rpart"):
-                self._dict_rpart_aggregate(bmap[b.bid], b)
         # dictmerger overflow (merges spilled past the table) is settled
         # lazily -- before the next launch into the builder or at result() --
         # so a loop's launch does not wait on the device
         for b in plan.builders:
-            if isinstance(b.kind, DictMerger) and not b.extra.get("rpart"):
+            if isinstance(b.kind, DictMerger):
                 bmap[b.bid].spill_pending = True
         self._keep = (tilectr, res)
 
@@ -754,59 +727,6 @@ class Ctx:
         kern.launch(grid, 256, blob, smem)
         self.launches += 1
         self.dirty = True
-
-    def _dict_rpart_aggregate(self, st, b):
-        """Second kernel of the range-partitioned dictmerger: per-partition
-        shared-memory aggregation + local sort, written at look-back
-        offsets.  Leaves the sorted entries in st.rpart_out."""
-        from .codegen import dict_rpart_source
-        V = len(st.vks)
-        ts = rpart_table_slots(V)
-        src, smem = dict_rpart_source(st.kind, ts)
-        kern = rt.get_kernel(src, "wg_drp")
-        P = st.nparts
-        cap = min(st.rows_in, P * ts) + 1
-        outk = rt.alloc(8 * cap)
-        outv = [rt.alloc(8 * cap) for _ in range(V)]
-        status = rt.alloc(8 * P)
-        rt.memset(status.ptr, 0, 8 * P)
-        grid = max(1, min(P, rt.sm_count() * max(1, kern.blocks_per_sm(1024, smem))))
-        rc = st.rcounters.ptr
-        words = [st.pk.ptr] + [v.ptr for v in st.pv] + [st.pcount.ptr, st.pcap, st.nslices, P, outk.ptr]
-        words += [o.ptr for o in outv]
-        words += [status.ptr, rc + 16, rc, rc + 8]
-        blob = b"".join(_pack("u64", w) for w in words)
-        kern.launch(grid, 1024, blob, smem)
-        self.launches += 1
-        global RPART_RUNS
-        RPART_RUNS += 1
-        cnt = np.empty(2, dtype=np.uint64)
-        rt.d2h(cnt.ctypes.data, rc, 16)
-        if int(cnt[0]):
-            raise _RpartFallback()
-        st.rpart_out = ([outk], outv, int(cnt[1]))
-
-    def _rpart_to_table(self, st):
-        """A range-partitioned result that receives further merges: replay
-        its entries into a hash table first (all folds are commutative)."""
-        kw, vw, n = st.rpart_out
-        st.rpart_out = None
-        st.table, st.cap = None, 0         # drop the placeholder table of the partitioned launch
-        st.ensure(max(n, 1), hint_key=st.hint_key)
-        if n == 0:
-            return
-        from .builders_dev import _words_to_cols, _value_words_to_cols
-        kcols = _words_to_cols(kw, st.kks, st.lay, n)
-        vcols = _value_words_to_cols(vw, st.vks, n)
-        kty, vty = st.kind.key, st.kind.value
-        elem = Struct((kty, vty))
-        dv = DVec(elem, n, (_layout(kty, kcols), _layout(vty, vcols)))
-        x = Ident("x", ty=elem)
-        body = Merge(Ident("b", ty=Builder(st.kind)), x, ty=Builder(st.kind))
-        lam = Lambda((XParam("b"), XParam("i"), XParam("x")), body)
-        loop = For((XIterSpec(Ident("__rows", ty=Vec(elem))),), Ident("__b", ty=Builder(st.kind)), lam,
-                   ty=Builder(st.kind))
-        self.run_loop(loop, {"__rows": dv, "__b": st}, count_traversal=False)
 
     def _dict_dev(self, v, ty, path):
         """A dictionary captured by a loop body, as device columns sorted by
@@ -937,10 +857,6 @@ class Ctx:
                 r = res[bid]
                 if what == "ctotal":
                     return r[1]
-                if what == "tcounts":
-                    return r[2]
-                if what == "tofs":
-                    return r[2].ptr
                 if what == "col":
                     seg = r if not isinstance(r, tuple) else r[0]
                     return seg.cols[key[3]].ptr
@@ -966,12 +882,6 @@ class Ctx:
                     return st.ocap
                 if what == "okey":
                     return st.over[0][key[3]].ptr
-                if what == "rlo":
-                    return st.rlo
-                if what == "rshift":
-                    return st.rshift
-                if what == "oflow":
-                    return st.rcounters.ptr
                 if what == "pcount":
                     return st.pcount.ptr
                 if what == "pcap":
@@ -1012,7 +922,7 @@ _LOOP_REFS = {}     # id(loop expression) -> weakref: guards the id-keyed hints
 
 
 def _claim_loop_id(e):
-    """Per-loop hints (table sizes, key ranges, rpart fallbacks) are keyed by
+    """Per-loop hints (table sizes) are keyed by
     id(loop).  When a loop expression dies and CPython reuses its id for a
     new one, drop the dead loop's hints before the new loop reads them."""
     lid = id(e)
@@ -1021,11 +931,8 @@ def _claim_loop_id(e):
         return
     if r is not None:
         from .builders_dev import _SIZE_HINTS as _SH
-        for d in (_SH, _RANGE_HINTS):
-            for k in [k for k in d if k[0] == lid]:
-                del d[k]
-        for k in [k for k in _RPART_BAD if k[0] == lid]:
-            _RPART_BAD.discard(k)
+        for k in [k for k in _SH if k[0] == lid]:
+            del _SH[k]
     try:
         _LOOP_REFS[lid] = weakref.ref(e)
     except TypeError:
@@ -1122,21 +1029,7 @@ STREAMING = _os.environ.get("WELDGPU_STREAM", "1") == "1"
 PART_MIN_KEYS = 1 << 20
 
 
-# Range-partitioned dictmerger (codegen.dict_rpart_source): correct for every
-# key distribution (overflow re-runs the loop), but on B200 its per-CTA
-# partition slices turn the bucket writes into isolated 32-byte DRAM writes;
-# at 2048 partitions the hash-partitioned path is faster, so it
-# is opt-in.
-RPART = _os.environ.get("WELDGPU_RPART", "0") == "1"
-RPART_MAX_PARTS = 4096
-_RPART_BAD = set()      # loops whose range-partitioned run overflowed once
-RPART_RUNS = 0
 REGROWS = 0         # dictmerger tables grown after spills (test instrumentation)
-
-
-class _RpartFallback(Exception):
-    """A range-partitioned dictmerger overflowed (skewed keys): re-run the
-    loop through the hash-table path."""
 
 
 def _bspecs(builders, strategy, count, loop_id=None):
@@ -1164,23 +1057,10 @@ def _bspecs(builders, strategy, count, loop_id=None):
             # Cardinality seen the last time this loop ran decides the
             # variant: low -> register cache + shared table, otherwise (or
             # unknown) -> deferred merges with batched HBM probes.
-            from .builders_dev import _SIZE_HINTS, _RANGE_HINTS
+            from .builders_dev import _SIZE_HINTS
             seen = _SIZE_HINTS.get((loop_id, bid))
             lowcard = seen is not None and seen <= LOWCARD_MAX
-            rng = _RANGE_HINTS.get((loop_id, bid))
-            if (seen is not None and seen > PART_MIN_KEYS and strategy != "global" and v.nw == 1 and DEFER_DICT
-                    and RPART and single and rng is not None and rpart_ok(v.kks) and v.table is None
-                    and v.rpart_out is None and not v.pending and (loop_id, bid) not in _RPART_BAD):
-                # cardinality far beyond L2: range-partitioned aggregation, the
-                # key order falls out of the partitioning (no global sort)
-                ts = rpart_table_slots(len(v.vks))
-                nparts = 1 << max(6, int(-(-seen * 5 // (3 * ts)) - 1).bit_length())
-                loop_smem = nparts * (16 + 32 * (1 + len(v.vks)))      # chunk buffers + cursors
-                if (ts * (8 * (1 + len(v.vks)) + 6) + 4096 <= 200 * 1024 and nparts <= RPART_MAX_PARTS
-                        and loop_smem <= 168 * 1024):
-                    bs.extra["rpart"] = True
-                    bs.extra["pbits"] = int(_os.environ.get("WELDGPU_RPART_PBITS", nparts.bit_length() - 1))
-            if (not bs.extra.get("rpart") and seen is not None and seen > PART_MIN_KEYS and strategy != "global"
+            if (seen is not None and seen > PART_MIN_KEYS and strategy != "global"
                     and v.nw == 1 and DEFER_DICT):
                 # cardinality far beyond L2: partitioned two-kernel aggregation
                 bs.extra["part"] = True
@@ -1211,7 +1091,7 @@ def _bsig(bs):
     if isinstance(bs, tuple):
         return tuple(_bsig(x) for x in bs)
     return (bs.mode, bs.extra.get("nbins"), bs.extra.get("smem_slots"), bs.extra.get("lowcard"),
-            bs.extra.get("part"), bs.extra.get("pbits"), bs.extra.get("rpart"))
+            bs.extra.get("part"), bs.extra.get("pbits"))
 
 
 def _type_of(v, lam, name):

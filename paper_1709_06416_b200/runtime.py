@@ -7,7 +7,6 @@ from __future__ import annotations
 
 import ctypes
 import hashlib
-import re
 import os
 import threading
 
@@ -374,9 +373,6 @@ class Kernel:
             hook("after", self)
 
 
-KPOOL = os.environ.get("WELDGPU_KPOOL", "0") == "1"
-
-
 def compile_ptx(src: str, name="weld_loop.cu") -> str:
     L = load_library()
     hs, hn, oa, no = _nvrtc_args(src)
@@ -390,75 +386,6 @@ def compile_ptx(src: str, name="weld_loop.cu") -> str:
     return buf.value.decode()
 
 
-_IMM = re.compile(r"0d([0-9A-Fa-f]{16})")
-_ARITH = re.compile(r"^\s*(fma|mul|add|sub|min|max)\.[a-z.]*f64\b")
-
-
-def const_pool_ptx(ptx: str) -> str:
-    """Move the 64-bit FP immediates of f64 arithmetic (the polynomial
-    coefficients of libdevice exp/log/erf) into a shared-memory pool.
-
-    ptxas materialises each such immediate with two UMOVs at every use inside
-    the tile loop (116 issue slots per Black-Scholes option).  From a .const
-    pool it hoists them into 58 extra registers (half the occupancy); from
-    shared memory it cannot hoist them across the loop's barriers, so each
-    use becomes a (128-bit, paired) LDS at no register cost.  The pool is
-    copied const -> shared by the first threads at kernel entry."""
-    pool = {}
-    out = []
-    nreg = 0
-    for line in ptx.split("\n"):
-        if _ARITH.match(line):
-            loads = []
-
-            def rep(m):
-                nonlocal nreg
-                h = m.group(1).upper()
-                if int(h, 16) & 0xFFFFFFFF == 0:
-                    return m.group(0)          # encodable as a 32-bit immediate
-                idx = pool.setdefault(h, len(pool))
-                r = f"%wgk{nreg}"
-                nreg += 1
-                loads.append(f"\tld.shared.f64 \t{r}, [wg_kpool_s+{8 * idx}];")
-                return r
-            line = _IMM.sub(rep, line)
-            out.extend(loads)
-        out.append(line)
-    if not pool:
-        return ptx
-    n = len(pool)
-    txt = "\n".join(out)
-    decl = (".const .align 8 .b64 wg_kpool[%d] = {%s};\n.shared .align 8 .b64 wg_kpool_s[%d];\n"
-            % (n, ", ".join("0x" + h for h in sorted(pool, key=pool.get)), n))
-    txt = re.sub(r"(\.address_size \d+\n)", lambda m: m.group(1) + decl, txt, count=1)
-    prologue = [f"\t.reg .f64 \t%wgk<{nreg}>;", "\t.reg .u32 %wgkt;", "\t.reg .pred %wgkp;",
-                "\t.reg .u64 %wgka, %wgkb, %wgkc, %wgkv;",
-                "\tmov.u32 %wgkt, %tid.x;", f"\tsetp.lt.u32 %wgkp, %wgkt, {n};",
-                "\tmul.wide.u32 %wgka, %wgkt, 8;", "\tmov.u64 %wgkb, wg_kpool;", "\tadd.u64 %wgkb, %wgkb, %wgka;",
-                "\tmov.u64 %wgkc, wg_kpool_s;", "\tadd.u64 %wgkc, %wgkc, %wgka;",
-                "\t@%wgkp ld.const.u64 %wgkv, [%wgkb];", "\t@%wgkp st.shared.u64 [%wgkc], %wgkv;",
-                "\tbar.sync 0;"]
-    lines = txt.split("\n")
-    res = []
-    i = 0
-    while i < len(lines):
-        res.append(lines[i])
-        if lines[i].startswith(".entry") or lines[i].startswith(".visible .entry"):
-            # copy through the parameter list and the body's declarations
-            while not lines[i].strip().startswith("{"):
-                i += 1
-                res.append(lines[i])
-            i += 1
-            while i < len(lines) and (lines[i].strip().startswith((".reg", ".shared", ".local", "//"))
-                                      or not lines[i].strip()):
-                res.append(lines[i])
-                i += 1
-            res.extend(prologue)
-            continue
-        i += 1
-    return "\n".join(res)
-
-
 def get_kernel(src: str, name: str) -> Kernel:
     """Compile (cached by source hash) and return the named kernel."""
     key = hashlib.sha1(src.encode()).hexdigest()
@@ -469,14 +396,8 @@ def get_kernel(src: str, name: str) -> Kernel:
             hs, hn, oa, no = _nvrtc_args(src)
             m = u64(0)
             log = ctypes.create_string_buffer(1 << 16)
-            if KPOOL and "double" in src:
-                # NVRTC -> PTX -> constant-pool pass -> driver JIT
-                ptx = compile_ptx(src, f"wg_{key[:12]}.cu")
-                _check(L.wg_module_load(const_pool_ptx(ptx).encode() + b"\0", ctypes.byref(m)))
-                rc = 0
-            else:
-                rc = L.wg_compile(src.encode(), f"wg_{key[:12]}.cu".encode(), 1 + len(_TABLES), hs, hn, no, oa, ctypes.byref(m),
-                                  log, 1 << 16)
+            rc = L.wg_compile(src.encode(), f"wg_{key[:12]}.cu".encode(), 1 + len(_TABLES), hs, hn, no, oa, ctypes.byref(m),
+                              log, 1 << 16)
             if rc != 0:
                 raise WeldGpuError(L.wg_last_error().decode(errors="replace"))
             mod = _modules[key] = (m.value, {})

@@ -164,13 +164,4 @@ def literal(kind, v):
     return int(v)
 
 
-def order_key(payload):
-    """Total order used by sort/tovec (builders.py:496-507)."""
-    if isinstance(payload, float):
-        return (payload != payload, payload if payload == payload else 0.0)
-    if isinstance(payload, tuple):
-        return tuple(order_key(p) for p in payload)
-    return (False, payload)
-
-
-__all__ = ["wrap", "fold", "binop", "neg", "cast", "literal", "fmin", "fmax", "order_key", "F64"]
+__all__ = ["wrap", "fold", "binop", "neg", "cast", "literal", "fmin", "fmax", "F64"]

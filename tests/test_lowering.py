@@ -93,38 +93,6 @@ def test_generated_literals_are_exact():
     assert c_literal("f64", float("inf")).endswith("0x7ff0000000000000LL)")
 
 
-def test_range_partitioned_dict_kernels_compile():
-    """Loop side (range digit + windowed bucket writes) and the shared-memory
-    aggregation/sort kernel, for each fold op and a two-field value."""
-    from paper_1709_06416_b200 import codegen, runtime, workloads as W
-    from paper_1709_06416_b200.irtypes import DictMerger, leaves
-    plans = codegen.static_plans(W.compile_program(W.WORKLOADS["dict"]), rpart=True)
-    assert any("d0_rlo" in p.source for p in plans)
-    for plan in plans:
-        assert runtime.compile_check(plan.source) > 0
-    kind = plans[0].builders[0].kind
-    for op in ("+", "*", "min", "max"):
-        k = DictMerger(kind.key, kind.value, op)
-        src, smem = codegen.dict_rpart_source(k, codegen.rpart_table_slots(len(leaves(k.value))))
-        assert smem <= 200 * 1024
-        assert runtime.compile_check(src, "drp.cu") > 0
-
-
-def test_order_key_expression_matches_python():
-    """okey_expr (device) and okey_py (host) agree with the reference's
-    order_key on packed integer keys: signed order, first leaf major."""
-    from paper_1709_06416_b200 import codegen
-    from paper_1709_06416_b200.irtypes import I32, I64, BOOL
-    vals = [-(1 << 63), -5, -1, 0, 1, 7, (1 << 63) - 1]
-    oks = [codegen.okey_py([I64], v & 0xFFFFFFFFFFFFFFFF) for v in vals]
-    assert oks == sorted(oks) and len(set(oks)) == len(oks)
-    pairs = [(a, b) for a in (-3, 0, 2) for b in (-(1 << 31), -1, 0, (1 << 31) - 1)]
-    words = [(a & 0xFFFFFFFF) | ((b & 0xFFFFFFFF) << 32) for a, b in pairs]
-    oks = [codegen.okey_py([I32, I32], w) for w in words]
-    assert [p for _, p in sorted(zip(oks, pairs))] == sorted(pairs)
-    assert codegen.rpart_ok([I64]) and codegen.rpart_ok([I32, I32]) and codegen.rpart_ok([BOOL])
-
-
 def test_dictionary_probes_lower_and_compile():
     """lookup(d, k) in a loop body lowers to a binary search over the
     dictionary's order-key-sorted key columns and compiles for sm_100a."""
@@ -176,3 +144,60 @@ def test_iterate_in_loop_bodies_lowers_and_compiles():
         assert body, c["name"]
         for p in body:
             assert runtime.compile_check(p.source) > 0
+
+
+def _typed_with_externs(src, inputs, names):
+    import paper_1709_06416_b200  # noqa: F401
+    from weldmill.optim import OptLevel, optimize
+    from weldmill.parser import parse, parse_type_text
+    from weldmill.sugar import expand
+    from weldmill.typecheck import check_linearity, infer
+    from weldmill.types import F64, Function, Scalar
+    env = {k: parse_type_text(t) for k, t in inputs.items()}
+    for nm in names:
+        env[nm] = Function((Scalar(F64),), Scalar(F64))
+    typed = infer(expand(parse(src)), env)
+    check_linearity(typed)
+    return optimize(typed, OptLevel.none())[0]
+
+
+def test_staged_filter_with_math_tables_fits_static_shared_memory():
+    """Regression (advisor, round 1): an order-preserving filter over a
+    13-byte row whose predicate calls erf and log used to stage 40 KB of
+    appends next to 11 KB of math tables (> 48 KB static shared memory):
+    ptxas rejected it.  The staging budget now subtracts the tables."""
+    from paper_1709_06416_b200 import codegen, runtime
+    src = "filter(v, (x) => call(erf, x.0) + call(log, x.0) > 0.0)"
+    tree = _typed_with_externs(src, {"v": "vec[{f64, bool, bool}]"}, ("erf", "log"))
+    plans = codegen.static_plans(tree, externs=("erf", "log"))
+    assert plans and any("wg_erf_tab_init" in p.source for p in plans)
+    for p in plans:
+        assert runtime.compile_check(p.source) > 0
+
+
+def test_extern_bound_to_custom_callable_is_not_replaced():
+    """The reference calls whatever callable is registered (run.py:836-844);
+    the device lowers only the math module's functions and refuses others
+    instead of silently substituting libm."""
+    import math
+    from paper_1709_06416_b200 import codegen
+    from paper_1709_06416_b200.irtypes import DeviceUnsupported
+    tree = _typed_with_externs("map(v, (x) => call(exp, x))", {"v": "vec[f64]"}, ("exp",))
+    from weldmill.expr import For, walk
+    loop = next(n for n in walk(tree) if isinstance(n, For))
+    from paper_1709_06416_b200.codegen import IterSpec, BSpec
+    from paper_1709_06416_b200.irtypes import leaves
+    iters = [IterSpec(elem=it.data.ty.elem, simd=it.simd, strided=it.start is not None,
+                      kinds=leaves(it.data.ty.elem)) for it in loop.iters]
+    bs = BSpec(bid=0, kind=loop.builders.ty.kind)
+    codegen.generate(loop, iters, bs, {}, {"exp": math.exp}, "local")
+    with pytest.raises(DeviceUnsupported):
+        codegen.generate(loop, iters, BSpec(bid=0, kind=loop.builders.ty.kind), {}, {"exp": lambda x: x + 1}, "local")
+
+
+def test_extern_error_text_matches_the_reference_form():
+    from paper_1709_06416_b200 import codegen
+    i = codegen.EXTERN_IDS["log"]
+    assert codegen.extern_error_text(2 * i) == "extern 'log' failed: math domain error"
+    i = codegen.EXTERN_IDS["exp"]
+    assert codegen.extern_error_text(2 * i + 1) == "extern 'exp' failed: math range error"
