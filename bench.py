@@ -1,34 +1,45 @@
 #!/usr/bin/env python
-"""Benchmark: one Weld IR program end to end on N B200s (one process per GPU).
+"""Benchmark: the Weld IR programs of BASELINE.json on N B200s (one process per GPU).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--n ROWS]
     python bench.py --impl reference ...      # the reference's CPU engine arm
 
-A "step" is one evaluate() of the workload's IR program (BASELINE.json
-configs; default configs[1] = Black-Scholes over 64M options) over one
-batch of synthetic rows:
+A "step" is one evaluate() of a workload's IR program (BASELINE.json
+configs) over one batch of synthetic rows.  The headline line is
+configs[1], Black-Scholes over 64M options; the same line carries a
+``per_config`` block with every other config measured the same way
+(C1 Q6 at 1M and 600M rows, C3 Q1, C4a dictmerger, C4b groupbuilder,
+C5 vecmerger histogram, plus the two appender scans).
 
-* value    -- rows/s over the whole job, inputs resident in HBM, results left
-              in HBM; device time from CUDA events on the executor's stream,
-              max over ranks.  Inputs are far larger than L2 (126 MB), so no
-              flush is needed between steps (config.l2).
-* e2e      -- the same metric through the public API with host inputs:
-              pinned numpy columns -> evaluate(...) -> numpy results, host<->
-              device copies inside the timed region.
-* roofline -- algorithmic bytes of the dominant generated
-              kernel / its event-timed duration, against MEASURED_PEAKS.json.
-* cpu_baseline -- the reference engine (weldmill.engine.evaluate) on a
-              bounded sample of the same rows, rank 0 at N=1 only.
+Per workload:
+* value        rows/s over the whole job, inputs resident in HBM, results
+               left in HBM; device time from CUDA events on the executor's
+               stream around the K steps, max over ranks.  Inputs >> L2
+               (126 MB), except C1 at 1M rows, which flushes L2 (512 MB
+               write) before every step, outside the per-step events.
+* roofline     algorithmic bytes per step / the device time
+               of ALL kernels of the step (every launch bracketed by events
+               inside libweldgpu, wg_prof_*), against MEASURED_PEAKS.json;
+               the dominant kernel and its share are named; step_frac uses
+               the whole step (host gaps included).
+* e2e          the same metric through the public API with HOST buffers:
+               pinned numpy columns -> evaluate(..., result="numpy") ->
+               numpy results; host<->device copies inside the timed region.
+* cpu_baseline the reference engine (weldmill.engine.evaluate) on a bounded
+               sample of the same generator rows, rank 0 at N=1 only.
 
-Multi-GPU: rows are partitioned across ranks (rank r gets rows [r*n,
-(r+1)*n)); the per-builder combine is exercised by paper_1709_06416_b200.
-distributed.  Black-Scholes appends have no exchange step (the ordered
-gather is a per-rank D2H into its offset), so the default workload is weak
-scaling with no data-path collective.
+Multi-GPU (--gpus N; re-launches itself under torch.distributed.run when
+WORLD_SIZE is not set): STRONG scaling -- the config's global rows are split
+into contiguous shards (distributed.shard_bounds), each rank evaluates its
+shard and the per-builder combine runs inside the timed region
+(distributed.evaluate_sharded_device: merger all-gather + rank-order fold,
+appender count all-gather, vecmerger all-reduce, dictmerger / groupbuilder
+hash-partitioned all-to-all + device merge).
 """
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -41,6 +52,19 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "rows/sec and achieved HBM GB/s (fraction of roofline) per IR program at 1/2/4/8 B200"
+
+# (label, workload, rows or 0 = the config's own size, e2e row cap)
+PER_CONFIG = [
+    ("C1_q6_1M", "q6", 0, None),
+    ("C1_q6_600M", "q6", 600_000_000, 200_000_000),
+    ("C2_blackscholes_64M", "blackscholes", 0, None),
+    ("C3_q1_60M", "q1", 0, None),
+    ("C4a_dict_200M", "dict", 0, None),
+    ("C4b_group_200M", "group", 0, None),
+    ("C5_hist_1B", "hist", 0, 200_000_000),
+    ("appender_filter_500M", "filter", 0, 200_000_000),
+    ("appender_map_500M", "map", 0, 200_000_000),
+]
 
 
 def _dist():
@@ -107,28 +131,35 @@ def _peaks():
     try:
         with open(path) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def _traffic(workload):
-    """dram bytes per launch of the dominant kernel from the committed ncu
-    capture summary (profiles/), or None."""
+def _traffic(workload, n):
+    """DRAM bytes per step from the committed ncu capture summary
+    (profiles/ncu_summary_r*.json, latest round wins), scaled to n rows."""
     import glob
     best = None
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_summary_r*.json"))):
         try:
             with open(path) as f:
                 d = json.load(f)
-            if workload in d and d[workload].get("dram_bytes") is not None:
-                best = d[workload]
+            e = d.get(workload)
+            if e and e.get("dram_bytes_step") is not None:
+                best = e["dram_bytes_step"] * (n / e["n"])
+            elif e and e.get("dram_bytes") is not None:
+                best = e["dram_bytes"] * (n / e["n"])
         except Exception:
             pass
     return best
 
 
-def cpu_reference_rate(workload, target_s=10.0, threads=1):
+# ---------------------------------------------------------------------------
+# reference CPU engine
+
+
+def cpu_reference_rate(workload, target_s=10.0, threads=1, cap=3_000_000):
     """Reference engine rows/s on a bounded sample of the same rows."""
     import paper_1709_06416_b200  # noqa: F401  (front end on sys.path)
     from paper_1709_06416_b200 import workloads as W
@@ -148,7 +179,7 @@ def cpu_reference_rate(workload, target_s=10.0, threads=1):
     probe = 20000
     dt = run(probe)
     rate = probe / max(dt, 1e-9)
-    n = int(min(max(rate * target_s, probe), 3_000_000))
+    n = int(min(max(rate * target_s, probe), cap))
     dt = run(n)
     return n / dt, n, dt
 
@@ -186,7 +217,7 @@ def reference_arm(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": "rows/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic",
         "config": {"workload": args.workload, "rows_per_step": n, "program": wl.title},
         "cpu_baseline": {"value": rate, "unit": "rows/s", "cores": th, "kind": "reference",
                          "sample": f"weldmill.engine.evaluate, threads={th} (best of 1 and {threads}), "
@@ -196,211 +227,188 @@ def reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="blackscholes")
-    ap.add_argument("--n", type=int, default=0, help="rows per GPU (default: the config's size)")
-    ap.add_argument("--impl", default="weldgpu")
-    ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-kernel-timing", action="store_true")
-    args = ap.parse_args()
-    args.warmup = max(args.warmup, 3)
+# ---------------------------------------------------------------------------
+# one workload on this rank
 
-    if args.impl == "reference":
-        reference_arm(args)
-        return
 
-    rank, world = _dist()
-    dist = None
-    if world > 1:
+class Runner:
+    def __init__(self, dist, rank, world):
+        self.dist = dist
+        self.rank = rank
+        self.world = world
+        import paper_1709_06416_b200 as wg
+        from paper_1709_06416_b200 import distributed as D, runtime as rt, workloads as W
+        self.wg, self.D, self.rt, self.W = wg, D, rt, W
+        self.comm = D.device_comm() if world > 1 else None
+
+    def barrier(self):
+        if self.dist is not None:
+            self.dist.barrier()
+
+    def max_over_ranks(self, *vals):
+        if self.dist is None:
+            return vals
         import torch
-        import torch.distributed as tdist
-        local = int(os.environ.get("LOCAL_RANK", "0"))
-        ngpu = torch.cuda.device_count()
-        torch.cuda.set_device(local % max(ngpu, 1))
-        # one process per GPU over NCCL; more ranks than GPUs (a single-GPU
-        # smoke of the multi-rank path) falls back to gloo for the barrier /
-        # timing reductions -- the timed data path has no collective either way
-        tdist.init_process_group("nccl" if ngpu >= world else "gloo")
-        dist = tdist
+        t = torch.tensor(list(vals), dtype=torch.float64, device=_coll_dev(self.dist))
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return tuple(float(x) for x in t.tolist())
 
-    import numpy as np
-    import paper_1709_06416_b200 as wg
-    from paper_1709_06416_b200 import runtime as rt
-    from paper_1709_06416_b200 import workloads as W
-    from weldmill.engine import EngineConfig, Value
+    def evaluate(self, tree, env, cfg, ext, result):
+        if self.world == 1:
+            return self.wg.evaluate(tree, env, cfg, ext, result=result)[0].data
+        return self.D.evaluate_sharded_device(tree, env, cfg, ext, comm=self.comm, row0=self.row0,
+                                              n_total=self.n_total, result=result)
 
-    wl = W.WORKLOADS[args.workload]
-    n = args.n or wl.n
-    tree = W.compile_program(wl)
-    types = W.input_types(wl)
-    ext = W.externs_for(wl)
-    cfg = EngineConfig(memory_limit=1 << 46)
-    row0 = rank * n
+    def run(self, name, n_total, steps, warmup, e2e_cap=None, e2e_steps=3, do_e2e=True, do_cpu=True,
+            kernel_timing=True, clocks=None):
+        from weldmill.engine import EngineConfig, Value
+        W, rt = self.W, self.rt
+        wl = W.WORKLOADS[name]
+        n_total = n_total or wl.n
+        lo, hi = self.D.shard_bounds(n_total, self.rank, self.world)
+        self.row0, self.n_total = lo, n_total
+        n = hi - lo
+        tree = W.compile_program(wl)
+        types = W.input_types(wl)
+        ext = W.externs_for(wl)
+        cfg = EngineConfig(memory_limit=1 << 46)
+        dev_cols = W.device_columns(wl, n, lo)
+        env = {k: Value(types[k], v) for k, v in dev_cols.items()}
 
-    dev_cols = W.device_columns(wl, n, row0)
-    env = {k: Value(types[k], v) for k, v in dev_cols.items()}
-
-    # per-launch timing of generated kernels (dominant kernel = most time)
-    kern_times = {}
-    pending = []
-
-    ev_pool = [rt.Event() for _ in range(4 * args.steps + 16)]
-
-    def hook(when, kern):
-        ev = ev_pool.pop() if ev_pool else rt.Event()
-        ev.record()
-        if when == "before":
-            pending.append((kern.name + ":" + str(kern.fn), ev))
+        out = None
+        for _ in range(warmup):
+            out = self.evaluate(tree, env, cfg, ext, "device")
+        rt.sync()
+        alg = W.algorithmic_bytes(wl, n_total)
+        flush = alg < (1 << 30)
+        flush_buf = rt.alloc(512 << 20) if flush else None
+        gc.collect()
+        gc.disable()          # no collector pauses inside the timed region
+        if clocks:
+            clocks.start()
+            time.sleep(0.3)
+        self.barrier()
+        rt.sync()
+        if flush:
+            evs = [(rt.Event(), rt.Event()) for _ in range(steps)]
+            for k in range(steps):
+                rt.call("wg_flush_l2", flush_buf.ptr, 512 << 20, k + 1)
+                evs[k][0].record()
+                out = self.evaluate(tree, env, cfg, ext, "device")
+                evs[k][1].record()
+            rt.sync()
+            ms = sum(a.elapsed_ms(b) for a, b in evs) / steps
         else:
-            key, ev0 = pending.pop()
-            kern_times.setdefault(key, []).append((ev0, ev))
+            e0, e1 = rt.Event(), rt.Event()
+            e0.record()
+            for _ in range(steps):
+                out = self.evaluate(tree, env, cfg, ext, "device")
+            e1.record()
+            rt.sync()
+            ms = e0.elapsed_ms(e1) / steps
+        self.barrier()
+        clk = clocks.stop() if clocks else None
+        # Per-kernel device time in a second pass over the same steps (the
+        # per-launch events would otherwise sit inside the headline region).
+        kern = {}
+        launches = None
+        if kernel_timing:
+            for k in range(steps):
+                if flush:
+                    rt.call("wg_flush_l2", flush_buf.ptr, 512 << 20, 100 + k)
+                rt.prof_enable(True)
+                out = self.evaluate(tree, env, cfg, ext, "device")
+                rt.prof_enable(False)
+                recs = rt.prof_records()
+                for nm, t in recs:
+                    a = kern.setdefault(nm, [0.0, 0])
+                    a[0] += t
+                    a[1] += 1
+            launches = sum(c for nm, (t, c) in kern.items() if nm not in ("memset", "memcpy_d2d")) / steps
+        gc.enable()
+        del out
+        step_kern_ms = sum(t for t, c in kern.values()) / steps if kern else None
+        dom = max(kern.items(), key=lambda kv: kv[1][0]) if kern else None
+        ms, step_kern_ms_max = self.max_over_ranks(ms, step_kern_ms or 0.0)
+        if step_kern_ms is not None:
+            step_kern_ms = step_kern_ms_max
+        value = n_total / (ms / 1e3)
+        peak, peak_src = _peaks()
+        achieved = alg / (step_kern_ms / 1e3) / 1e9 if step_kern_ms else None
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None,
+                "traffic": _traffic(name, n_total), "peak_source": peak_src,
+                "basis": "algorithmic bytes / device time of every kernel in the step (wg_prof events)",
+                "algorithmic_bytes": alg, "step_kernel_ms": step_kern_ms,
+                "step_frac": alg / (ms / 1e3) / 1e9 / peak}
+        if dom:
+            roof["kernel"] = dom[0]
+            roof["kernel_ms"] = dom[1][0] / steps
+            roof["kernel_share"] = dom[1][0] / steps / step_kern_ms if step_kern_ms else None
+            roof["kernels"] = [{"name": nm, "ms_per_step": t / steps, "launches_per_step": c / steps}
+                               for nm, (t, c) in sorted(kern.items(), key=lambda kv: -kv[1][0])[:8]]
+        del env, dev_cols
+        if flush_buf is not None:
+            del flush_buf
+        gc.collect()
+        rt.call("wg_mem_trim")
 
-    def barrier():
-        if dist is not None:
-            dist.barrier()
+        res = {"value": value, "unit": "rows/s", "ms_per_step": ms, "rows": n_total, "rows_per_gpu": n,
+               "roofline": roof, "gpu_launches": launches, "clocks": clk,
+               "l2": ("L2 flushed (512 MB write) before every step, outside the per-step events" if flush
+                      else "inputs >> L2 (126 MB); no flush needed")}
 
-    # Warm-up mirrors the timed loop exactly (the previous step's result is
-    # still alive while the next one allocates), so the allocator cache is
-    # in steady state before timing starts.
-    out = None
-    for _ in range(args.warmup):
-        out = wg.evaluate(tree, env, cfg, ext, result="device")
-    rt.sync()
+        # ---- e2e through the public API with host buffers ----------------
+        if do_e2e:
+            ne = min(n_total, e2e_cap) if e2e_cap else n_total
+            elo, ehi = self.D.shard_bounds(ne, self.rank, self.world)
+            self.row0, self.n_total = elo, ne
+            host = host_columns_pinned(W, wl, ehi - elo, elo)
+            henv = {k: Value(types[k], v) for k, v in host.items()}
+            h2d = sum(a.nbytes for a in host.values())
+            r = None
+            for _ in range(max(2, warmup)):
+                r = self.evaluate(tree, henv, cfg, ext, "numpy")
+            del r
+            self.barrier()
+            t0 = time.perf_counter()
+            for _ in range(e2e_steps):
+                r = self.evaluate(tree, henv, cfg, ext, "numpy")
+            el = (time.perf_counter() - t0) / e2e_steps
+            d2h = _nbytes(r)
+            del r
+            (el,) = self.max_over_ranks(el)
+            res["e2e"] = {"value": ne / el, "unit": "rows/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                          "ms_per_step": el * 1e3, "rows": ne,
+                          "inputs": "pinned host numpy columns (the step copies them in and the result out)"}
+            del host, henv
+            gc.collect()
+            rt.call("wg_mem_trim")
+        if do_cpu and self.rank == 0 and self.world == 1:
+            rate, ncpu, dt = cpu_reference_rate(name, target_s=3.0 if n_total != wl.n or name != "blackscholes"
+                                                else 10.0, threads=1)
+            res["cpu_baseline"] = {"value": rate, "unit": "rows/s", "cores": 1, "kind": "reference",
+                                   "sample": f"weldmill.engine.evaluate (threads=1; its GIL-bound pool does not "
+                                             f"scale, BASELINE.md) on the first {ncpu} generator rows of the same "
+                                             f"workload, {dt:.1f} s"}
+        return res
 
-    clocks = Clocks(int(os.environ.get("LOCAL_RANK", "0"))) if rank == 0 else None
-    if clocks:
-        clocks.start()
-        time.sleep(0.5)
-    import gc
-    gc.collect()
-    gc.disable()          # no collector pauses inside the timed region
-    # Inputs smaller than L2 (e.g. Q6 at its 1M-row config) would be served
-    # from a warm L2: flush it (write 512 MB) between steps, outside the
-    # per-step event pairs.
-    alg_bytes = W.algorithmic_bytes(wl, n)
-    flush = alg_bytes < (1 << 30)
-    flush_buf = rt.alloc(512 << 20) if flush else None
-    launches0 = rt.LAUNCHES[0]
-    barrier()
-    rt.sync()
-    if flush:
-        evs = [(rt.Event(), rt.Event()) for _ in range(args.steps)]
-        for k in range(args.steps):
-            rt.call("wg_flush_l2", flush_buf.ptr, 512 << 20, k + 1)
-            evs[k][0].record()
-            out = wg.evaluate(tree, env, cfg, ext, result="device")
-            evs[k][1].record()
-        rt.sync()
-        ms = sum(a.elapsed_ms(b) for a, b in evs) / args.steps
-        launches = rt.LAUNCHES[0] - launches0 - args.steps   # minus the flush kernels
-    else:
-        e0, e1 = rt.Event(), rt.Event()
-        e0.record()
-        for _ in range(args.steps):
-            out = wg.evaluate(tree, env, cfg, ext, result="device")
-        e1.record()
-        rt.sync()
-        launches = rt.LAUNCHES[0] - launches0
-        ms = e0.elapsed_ms(e1) / args.steps
-    # Per-kernel event timing in a second pass over the same steps (the
-    # bracketing events would otherwise sit inside the headline region).
-    if not args.no_kernel_timing:
-        for k in range(args.steps):
-            if flush:
-                rt.call("wg_flush_l2", flush_buf.ptr, 512 << 20, 100 + k)
-            rt.LAUNCH_HOOK[0] = hook
-            out = wg.evaluate(tree, env, cfg, ext, result="device")
-            rt.LAUNCH_HOOK[0] = None
-        rt.sync()
-    clk = clocks.stop() if clocks else None
-    gc.enable()
 
-    # dominant generated kernel
-    dom_tot, dom_ms, dom_name = 0.0, 0.0, None
-    for key, evs in kern_times.items():
-        tot = sum(a.elapsed_ms(b) for a, b in evs)
-        if tot > dom_tot:
-            dom_tot, dom_ms, dom_name = tot, tot / len(evs), key
-    del kern_times
-
-    if dist is not None:
-        import torch
-        t = torch.tensor([ms, dom_ms], dtype=torch.float64, device=_coll_dev(dist))
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, dom_ms = float(t[0]), float(t[1])
-
-    rows = n * world
-    value = rows / (ms / 1e3)
-    peak, peak_kind = _peaks()
-    alg = W.algorithmic_bytes(wl, n)
-    achieved = alg / (dom_ms / 1e3) / 1e9 if dom_ms else None
-    tr = _traffic(args.workload)
-
-    # ---- e2e through the public API with host buffers ----------------------
-    e2e = None
-    if not args.no_e2e:
-        host = W.host_columns(wl, n, row0)
-        for arr in host.values():
-            rt.host_register(arr)
-        henv = {k: Value(types[k], v) for k, v in host.items()}
-        h2d = sum(a.nbytes for a in host.values())
-        d2h = 0
-        # same warm-up discipline as the device loop: keep the previous result
-        # alive so the pinned result pool reaches steady state before timing
-        res = None
-        for _ in range(max(3, args.warmup)):
-            res = wg.evaluate(tree, henv, cfg, ext, result="numpy")[0].data
-        barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.e2e_steps):
-            res = wg.evaluate(tree, henv, cfg, ext, result="numpy")[0].data
-        el = (time.perf_counter() - t0) / args.e2e_steps
-        d2h = _nbytes(res)
-        if dist is not None:
-            import torch
-            t = torch.tensor([el], dtype=torch.float64, device=_coll_dev(dist))
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            el = float(t[0])
-        e2e = {"value": rows / el, "unit": "rows/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "ms_per_step": el * 1e3}
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        rate, ncpu, dt = cpu_reference_rate(args.workload, target_s=10.0, threads=1)
-        cpu = {"value": rate, "unit": "rows/s", "cores": 1, "kind": "reference",
-               "sample": f"weldmill.engine.evaluate (threads=1; its GIL-bound pool does not scale, "
-                         f"BASELINE.md) on the first {ncpu} generator rows of the same workload, {dt:.1f} s"}
-
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic",
-            "config": {"workload": args.workload, "program": wl.title, "rows_per_gpu": n,
-                       "global_rows": rows, "parallelism": f"row-partitioned x{world}",
-                       "l2": "inputs >> L2 (126 MB); no flush needed" if not flush else
-                             "L2 flushed (512 MB write) before every step, outside the per-step events"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": (achieved / peak) if achieved else None,
-                         "traffic": (tr["dram_bytes"] * (n / tr["n"]) if tr else None),
-                         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-                         "kernel": dom_name.split(":")[0] if dom_name else None, "kernel_ms": dom_ms,
-                         "algorithmic_bytes": alg},
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": launches,
-            "clocks": clk,
-        }
-        print(json.dumps(line), flush=True)
-    if dist is not None:
-        dist.barrier()
-        dist.destroy_process_group()
+def host_columns_pinned(W, wl, n, row0):
+    """The workload's columns in pinned host memory: generated on the device
+    (identical bits to the numpy generator) and copied down once."""
+    from paper_1709_06416_b200.columns import pinned_empty
+    from paper_1709_06416_b200.irtypes import NPTYPE
+    from paper_1709_06416_b200 import runtime as rt
+    dev = W.device_columns(wl, n, row0)
+    out = {}
+    for k, dv in dev.items():
+        c = dv.cols[0]
+        a = pinned_empty(dv.n, NPTYPE[c.kind])
+        if dv.n:
+            rt.d2h(a.ctypes.data, c.ptr, a.nbytes)
+        out[k] = a
+    return out
 
 
 def _coll_dev(dist):
@@ -410,10 +418,101 @@ def _coll_dev(dist):
 def _nbytes(v):
     import numpy as np
     if isinstance(v, np.ndarray) or hasattr(v, "offsets"):
+        if hasattr(v, "offsets"):
+            return v.offsets.nbytes + _nbytes(v.values)
         return v.nbytes
     if isinstance(v, (tuple, list)):
         return sum(_nbytes(x) for x in v)
     return 8
+
+
+def _relaunch(args):
+    """--gpus N without a torchrun environment: re-launch this script as N
+    ranks (one process per GPU) and pass rank 0's JSON line through."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={29500 + os.getpid() % 1000}", os.path.abspath(__file__)]
+    cmd += [a for a in sys.argv[1:]]
+    rc = subprocess.call(cmd)
+    sys.exit(rc)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="blackscholes")
+    ap.add_argument("--n", type=int, default=0, help="global rows (default: the config's size)")
+    ap.add_argument("--impl", default="weldgpu")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-kernel-timing", action="store_true")
+    ap.add_argument("--per-config", default="all", help="all | none | comma list of PER_CONFIG labels")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        reference_arm(args)
+        return
+
+    rank, world = _dist()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        _relaunch(args)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one process per GPU")
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        ngpu = torch.cuda.device_count()
+        torch.cuda.set_device(local % max(ngpu, 1))
+        tdist.init_process_group("nccl" if ngpu >= world else "gloo")
+        dist = tdist
+
+    runner = Runner(dist, rank, world)
+    wl = runner.W.WORKLOADS[args.workload]
+    clocks = Clocks(int(os.environ.get("LOCAL_RANK", "0"))) if rank == 0 else None
+    head = runner.run(args.workload, args.n or wl.n, args.steps, args.warmup, e2e_steps=args.e2e_steps,
+                      do_e2e=not args.no_e2e, do_cpu=not args.no_cpu, kernel_timing=not args.no_kernel_timing,
+                      clocks=clocks)
+    per = {}
+    if args.per_config != "none" and world == 1:
+        want = None if args.per_config == "all" else set(args.per_config.split(","))
+        for label, name, rows, cap in PER_CONFIG:
+            if want is not None and label not in want:
+                continue
+            if name == args.workload and (rows or runner.W.WORKLOADS[name].n) == (args.n or wl.n):
+                per[label] = {k: v for k, v in head.items() if k != "clocks"}
+                per[label]["workload"] = name
+                continue
+            r = runner.run(name, rows, args.steps, args.warmup, e2e_cap=cap, e2e_steps=args.e2e_steps,
+                           do_e2e=not args.no_e2e, do_cpu=not args.no_cpu,
+                           kernel_timing=not args.no_kernel_timing)
+            r["workload"] = name
+            r["program"] = runner.W.WORKLOADS[name].title
+            per[label] = r
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": head["value"], "unit": "rows/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": wl.dtype, "data": "synthetic",
+            "config": {"workload": args.workload, "program": wl.title, "global_rows": head["rows"],
+                       "rows_per_gpu": head["rows_per_gpu"], "parallelism": f"row-partitioned x{world}",
+                       "l2": head["l2"]},
+            "roofline": head["roofline"],
+            "cpu_baseline": head.get("cpu_baseline"),
+            "e2e": head.get("e2e"),
+            "gpu_launches": head["gpu_launches"],
+            "clocks": head["clocks"],
+            "per_config": per,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

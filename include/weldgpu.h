@@ -119,6 +119,12 @@ int wg_event_create(uint64_t* ev);
 int wg_event_record(uint64_t ev);
 int wg_event_elapsed_ms(uint64_t start, uint64_t stop, float* ms);
 int wg_event_destroy(uint64_t ev);
+/* Per-launch device timing: while enabled, every kernel the library launches
+ * (fixed-function and NVRTC loop kernels) is bracketed by CUDA events on its
+ * stream and recorded under its name; enabling clears the records. */
+int wg_prof_enable(int on);
+int wg_prof_count(int* n);
+int wg_prof_record(int i, char* name, int cap, float* ms);
 /* Copy/compute overlap for host-resident inputs (executor streaming path). */
 int wg_stream_select(int which);
 int wg_stream_wait_event(uint64_t ev);

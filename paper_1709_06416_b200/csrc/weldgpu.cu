@@ -48,6 +48,46 @@ int fail(const std::string& msg) {
   return -1;
 }
 
+// ---- per-launch device timing (wg_prof_*) ----------------------------------
+// When enabled, every kernel this library launches -- fixed-function
+// kernels and NVRTC loop kernels alike -- is bracketed by a pair of CUDA
+// events on the stream it is launched on, tagged with the kernel's name.
+// bench.py reads the records back to find the dominant kernel and the
+// whole-step kernel time (no profiler attached, no extra synchronisation
+// inside the step).
+struct ProfRec { const char* name; cudaEvent_t a, b; };
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+std::vector<cudaEvent_t> g_prof_free;
+std::mutex g_prof_mu;
+std::unordered_map<uint64_t, std::string> g_fn_names;   // CUfunction -> kernel name
+
+cudaEvent_t prof_event() {
+  if (!g_prof_free.empty()) { cudaEvent_t e = g_prof_free.back(); g_prof_free.pop_back(); return e; }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct ProfScope {
+  const char* name;
+  cudaEvent_t a = nullptr;
+  explicit ProfScope(const char* n) : name(n) {
+    if (!g_prof_on) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    a = prof_event();
+    cudaEventRecord(a, g_stream);
+  }
+  ~ProfScope() {
+    if (!a) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    cudaEvent_t b = prof_event();
+    cudaEventRecord(b, g_stream);
+    g_prof.push_back({name, a, b});
+  }
+};
+#define WG_PROF(name) ProfScope wg_prof_scope_(name)
+
 // Driver API entry points are resolved through cudart at wg_init() so the
 // library loads (for symbol checks and NVRTC compile checks) on hosts with
 // no GPU driver at all.
@@ -676,6 +716,7 @@ int wg_mem_reset_peak(void) {
 int wg_memset(uint64_t dptr, int value, uint64_t bytes) {
   NEED_INIT();
   if (!bytes) return 0;
+  WG_PROF("memset");
   CK(cudaMemsetAsync((void*)(uintptr_t)dptr, value, bytes, g_stream));
   return 0;
 }
@@ -705,6 +746,7 @@ int wg_d2h_async(void* dst, uint64_t src, uint64_t bytes) {
 int wg_d2d(uint64_t dst, uint64_t src, uint64_t bytes) {
   NEED_INIT();
   if (!bytes) return 0;
+  WG_PROF("memcpy_d2d");
   CK(cudaMemcpyAsync((void*)(uintptr_t)dst, (const void*)(uintptr_t)src, bytes, cudaMemcpyDeviceToDevice, g_stream));
   return 0;
 }
@@ -863,6 +905,8 @@ int wg_module_function(uint64_t module, const char* name, uint64_t* fn) {
   CUfunction f;
   CKD(p_cuModuleGetFunction(&f, (CUmodule)(uintptr_t)module, name));
   *fn = (uint64_t)(uintptr_t)f;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_fn_names[*fn] = name;
   return 0;
 }
 
@@ -882,6 +926,13 @@ int wg_launch(uint64_t fn, uint32_t grid, uint32_t block, uint32_t dyn_smem, con
   size_t sz = (size_t)params_size;
   void* extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, const_cast<void*>(params), CU_LAUNCH_PARAM_BUFFER_SIZE, &sz,
                    CU_LAUNCH_PARAM_END};
+  const char* pname = "nvrtc_kernel";
+  if (g_prof_on) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    auto it = g_fn_names.find(fn);
+    if (it != g_fn_names.end()) pname = it->second.c_str();
+  }
+  WG_PROF(pname);
   CKD(p_cuLaunchKernel(f, grid, 1, 1, block, 1, 1, dyn_smem, (CUstream)g_stream, nullptr, extra));
   return 0;
 }
@@ -894,7 +945,7 @@ int wg_table_init(uint64_t table, uint64_t nslots, int slot_words, const uint64_
   CK(cudaMallocAsync((void**)&pat, 64 * 8, g_stream));
   CK(cudaMemcpyAsync(pat, pattern, slot_words * 8, cudaMemcpyHostToDevice, g_stream));
   uint64_t total = nslots * (uint64_t)slot_words;
-  k_table_init<<<grid_for(total, 256), 256, 0, g_stream>>>((uint64_t*)(uintptr_t)table, nslots, slot_words, pat);
+  { WG_PROF("k_table_init"); k_table_init<<<grid_for(total, 256), 256, 0, g_stream>>>((uint64_t*)(uintptr_t)table, nslots, slot_words, pat); }
   CK(cudaGetLastError());
   CK(cudaFreeAsync(pat, g_stream));
   return 0;
@@ -909,12 +960,12 @@ int wg_table_compact(uint64_t table, uint64_t nslots, int slot_words, int mode, 
   CK(cudaMallocAsync((void**)&d_cnt, 8, g_stream));
   CK(cudaMemcpyAsync(d_out, out_words, sizeof(uint64_t) * nout, cudaMemcpyHostToDevice, g_stream));
   CK(cudaMemsetAsync(d_cnt, 0, 8, g_stream));
-  k_table_compact<<<grid_for(nslots, 256), 256, 0, g_stream>>>((const uint64_t*)(uintptr_t)table, nslots,
-                                                                slot_words, mode, d_out, nout, d_cnt);
+  { WG_PROF("k_table_compact"); k_table_compact<<<grid_for(nslots, 256), 256, 0, g_stream>>>((const uint64_t*)(uintptr_t)table, nslots,
+                                                                slot_words, mode, d_out, nout, d_cnt); }
   CK(cudaGetLastError());
   if (mode == 1) {
-    k_table_compact_sentinel<<<1, 32, 0, g_stream>>>((const uint64_t*)(uintptr_t)table, nslots, slot_words, d_out,
-                                                     nout, d_cnt);
+    { WG_PROF("k_table_compact_sentinel"); k_table_compact_sentinel<<<1, 32, 0, g_stream>>>((const uint64_t*)(uintptr_t)table, nslots, slot_words, d_out,
+                                                     nout, d_cnt); }
     CK(cudaGetLastError());
   }
   unsigned long long h = 0;
@@ -953,8 +1004,8 @@ int wg_dict_finish_small(uint64_t table, uint64_t nslots, int slot_words, int mo
     CK(cudaFuncSetAttribute(k_dict_finish_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 * WG_SMALL_DICT * 8));
     attr_set = true;
   }
-  k_dict_finish_small<<<1, 1024, smem, g_stream>>>((const uint64_t*)(uintptr_t)table, nslots, d,
-                                                   (const unsigned long long*)(uintptr_t)counters, d_cnt);
+  { WG_PROF("k_dict_finish_small"); k_dict_finish_small<<<1, 1024, smem, g_stream>>>((const uint64_t*)(uintptr_t)table, nslots, d,
+                                                   (const unsigned long long*)(uintptr_t)counters, d_cnt); }
   CK(cudaGetLastError());
   unsigned long long h = 0;
   CK(cudaMemcpyAsync(&h, d_cnt, 8, cudaMemcpyDeviceToHost, g_stream));
@@ -966,16 +1017,16 @@ int wg_dict_finish_small(uint64_t table, uint64_t nslots, int slot_words, int mo
 int wg_order_key(uint64_t src, int kind, uint64_t n, uint64_t perm, uint64_t dst) {
   NEED_INIT();
   if (!n) return 0;
-  k_order_key<<<grid_for(n, 256), 256, 0, g_stream>>>((const void*)(uintptr_t)src, kind, n,
-                                                       (const uint32_t*)(uintptr_t)perm, (uint64_t*)(uintptr_t)dst);
+  { WG_PROF("k_order_key"); k_order_key<<<grid_for(n, 256), 256, 0, g_stream>>>((const void*)(uintptr_t)src, kind, n,
+                                                       (const uint32_t*)(uintptr_t)perm, (uint64_t*)(uintptr_t)dst); }
   CK(cudaGetLastError());
   return 0;
 }
 
 int wg_exclusive_scan_i64(uint64_t src, uint64_t dst, uint64_t n, uint64_t total) {
   NEED_INIT();
-  k_exscan_i64<<<1, 1024, 0, g_stream>>>((const int64_t*)(uintptr_t)src, (int64_t*)(uintptr_t)dst, n,
-                                         (int64_t*)(uintptr_t)total);
+  { WG_PROF("k_exscan_i64"); k_exscan_i64<<<1, 1024, 0, g_stream>>>((const int64_t*)(uintptr_t)src, (int64_t*)(uintptr_t)dst, n,
+                                         (int64_t*)(uintptr_t)total); }
   CK(cudaGetLastError());
   return 0;
 }
@@ -983,7 +1034,7 @@ int wg_exclusive_scan_i64(uint64_t src, uint64_t dst, uint64_t n, uint64_t total
 int wg_iota_i64(uint64_t dst, uint64_t n, int64_t step) {
   NEED_INIT();
   if (!n) return 0;
-  k_iota_i64<<<grid_for(n, 256), 256, 0, g_stream>>>((int64_t*)(uintptr_t)dst, n, step);
+  { WG_PROF("k_iota_i64"); k_iota_i64<<<grid_for(n, 256), 256, 0, g_stream>>>((int64_t*)(uintptr_t)dst, n, step); }
   CK(cudaGetLastError());
   return 0;
 }
@@ -991,7 +1042,7 @@ int wg_iota_i64(uint64_t dst, uint64_t n, int64_t step) {
 int wg_iota_u32(uint64_t dst, uint64_t n) {
   NEED_INIT();
   if (!n) return 0;
-  k_iota_u32<<<grid_for(n, 256), 256, 0, g_stream>>>((uint32_t*)(uintptr_t)dst, n);
+  { WG_PROF("k_iota_u32"); k_iota_u32<<<grid_for(n, 256), 256, 0, g_stream>>>((uint32_t*)(uintptr_t)dst, n); }
   CK(cudaGetLastError());
   return 0;
 }
@@ -1010,9 +1061,9 @@ int wg_sort_pairs(uint64_t keys_in, uint64_t vals_in, uint64_t keys_out, uint64_
                                      (uint32_t*)(uintptr_t)vals_out, (int)n, begin_bit, end_bit, g_stream));
   void* d_temp = nullptr;
   CK(cudaMallocAsync(&d_temp, temp ? temp : 1, g_stream));
-  CK(cub::DeviceRadixSort::SortPairs(d_temp, temp, (const uint64_t*)(uintptr_t)keys_in,
+  { WG_PROF("cub::DeviceRadixSort::SortPairs"); CK(cub::DeviceRadixSort::SortPairs(d_temp, temp, (const uint64_t*)(uintptr_t)keys_in,
                                      (uint64_t*)(uintptr_t)keys_out, (const uint32_t*)(uintptr_t)vals_in,
-                                     (uint32_t*)(uintptr_t)vals_out, (int)n, begin_bit, end_bit, g_stream));
+                                     (uint32_t*)(uintptr_t)vals_out, (int)n, begin_bit, end_bit, g_stream)); }
   CK(cudaFreeAsync(d_temp, g_stream));
   return 0;
 }
@@ -1023,9 +1074,9 @@ int wg_gather(uint64_t src, uint64_t perm, uint64_t dst, uint64_t n, int width) 
   unsigned g = grid_for(n, 256);
   const uint32_t* pm = (const uint32_t*)(uintptr_t)perm;
   switch (width) {
-    case 8: k_gather<uint64_t><<<g, 256, 0, g_stream>>>((const uint64_t*)(uintptr_t)src, pm, (uint64_t*)(uintptr_t)dst, n); break;
-    case 4: k_gather<uint32_t><<<g, 256, 0, g_stream>>>((const uint32_t*)(uintptr_t)src, pm, (uint32_t*)(uintptr_t)dst, n); break;
-    case 1: k_gather<uint8_t><<<g, 256, 0, g_stream>>>((const uint8_t*)(uintptr_t)src, pm, (uint8_t*)(uintptr_t)dst, n); break;
+    case 8: { WG_PROF("k_gather"); k_gather<uint64_t><<<g, 256, 0, g_stream>>>((const uint64_t*)(uintptr_t)src, pm, (uint64_t*)(uintptr_t)dst, n); } break;
+    case 4: { WG_PROF("k_gather"); k_gather<uint32_t><<<g, 256, 0, g_stream>>>((const uint32_t*)(uintptr_t)src, pm, (uint32_t*)(uintptr_t)dst, n); } break;
+    case 1: { WG_PROF("k_gather"); k_gather<uint8_t><<<g, 256, 0, g_stream>>>((const uint8_t*)(uintptr_t)src, pm, (uint8_t*)(uintptr_t)dst, n); } break;
     default: return fail("wg_gather: width must be 1, 4 or 8");
   }
   CK(cudaGetLastError());
@@ -1035,7 +1086,7 @@ int wg_gather(uint64_t src, uint64_t perm, uint64_t dst, uint64_t n, int width) 
 int wg_narrow(uint64_t src, uint64_t dst, int width, uint64_t n) {
   NEED_INIT();
   if (!n) return 0;
-  k_narrow<<<grid_for(n, 256), 256, 0, g_stream>>>((const uint64_t*)(uintptr_t)src, (void*)(uintptr_t)dst, width, n);
+  { WG_PROF("k_narrow"); k_narrow<<<grid_for(n, 256), 256, 0, g_stream>>>((const uint64_t*)(uintptr_t)src, (void*)(uintptr_t)dst, width, n); }
   CK(cudaGetLastError());
   return 0;
 }
@@ -1043,7 +1094,7 @@ int wg_narrow(uint64_t src, uint64_t dst, int width, uint64_t n) {
 int wg_widen(uint64_t src, uint64_t dst, int width, uint64_t n) {
   NEED_INIT();
   if (!n) return 0;
-  k_widen<<<grid_for(n, 256), 256, 0, g_stream>>>((const void*)(uintptr_t)src, (uint64_t*)(uintptr_t)dst, width, n);
+  { WG_PROF("k_widen"); k_widen<<<grid_for(n, 256), 256, 0, g_stream>>>((const void*)(uintptr_t)src, (uint64_t*)(uintptr_t)dst, width, n); }
   CK(cudaGetLastError());
   return 0;
 }
@@ -1061,14 +1112,14 @@ int wg_run_starts(const uint64_t* key_words, int kw, uint64_t n, uint64_t starts
   CK(cudaMemcpyAsync(d_words, key_words, sizeof(uint64_t) * kw, cudaMemcpyHostToDevice, g_stream));
   CK(cudaMallocAsync((void**)&flags, n, g_stream));
   CK(cudaMallocAsync((void**)&d_cnt, 8, g_stream));
-  k_heads<<<grid_for(n, 256), 256, 0, g_stream>>>((const uint64_t* const*)d_words, kw, n, flags);
+  { WG_PROF("k_heads"); k_heads<<<grid_for(n, 256), 256, 0, g_stream>>>((const uint64_t* const*)d_words, kw, n, flags); }
   CK(cudaGetLastError());
   cub::CountingInputIterator<uint32_t> it(0);
   size_t temp = 0;
   CK(cub::DeviceSelect::Flagged(nullptr, temp, it, flags, (uint32_t*)(uintptr_t)starts_out, d_cnt, (int)n, g_stream));
   void* d_temp = nullptr;
   CK(cudaMallocAsync(&d_temp, temp ? temp : 1, g_stream));
-  CK(cub::DeviceSelect::Flagged(d_temp, temp, it, flags, (uint32_t*)(uintptr_t)starts_out, d_cnt, (int)n, g_stream));
+  { WG_PROF("cub::DeviceSelect::Flagged"); CK(cub::DeviceSelect::Flagged(d_temp, temp, it, flags, (uint32_t*)(uintptr_t)starts_out, d_cnt, (int)n, g_stream)); }
   int h = 0;
   CK(cudaMemcpyAsync(&h, d_cnt, 4, cudaMemcpyDeviceToHost, g_stream));
   CK(cudaStreamSynchronize(g_stream));
@@ -1118,8 +1169,8 @@ int wg_group_finish1(uint64_t keys, int key_kind, uint64_t vals, int val_width, 
   flag = (int*)(mm + 2);
   uint64_t init[4] = {~0ULL, 0ULL, 0ULL, 0ULL};
   CK(cudaMemcpyAsync(mm, init, 32, cudaMemcpyHostToDevice, g_stream));
-  k_okey_minmax<<<g, 256, 0, g_stream>>>((const void*)(uintptr_t)keys, key_kind, n, mm, k0);
-  if (own_v0) k_widen<<<g, 256, 0, g_stream>>>((const void*)(uintptr_t)vals, v0, val_width, n);
+  { WG_PROF("k_okey_minmax"); k_okey_minmax<<<g, 256, 0, g_stream>>>((const void*)(uintptr_t)keys, key_kind, n, mm, k0); }
+  if (own_v0) { WG_PROF("k_widen"); k_widen<<<g, 256, 0, g_stream>>>((const void*)(uintptr_t)vals, v0, val_width, n); }
   unsigned long long hmm[2];
   CK(cudaMemcpyAsync(hmm, mm, 16, cudaMemcpyDeviceToHost, g_stream));
   CK(cudaStreamSynchronize(g_stream));
@@ -1130,7 +1181,7 @@ int wg_group_finish1(uint64_t keys, int key_kind, uint64_t vals, int val_width, 
   if (rbits + 8 <= vbits) {
     // a narrow range straddling a high bit (e.g. keys around 0): sort
     // (okey - min) -- one extra pass, several radix passes saved
-    k_sub_min<<<g, 256, 0, g_stream>>>(k0, n, hmm[0]);
+    { WG_PROF("k_sub_min"); k_sub_min<<<g, 256, 0, g_stream>>>(k0, n, hmm[0]); }
     kbase = hmm[0];
     vbits = rbits;
   }
@@ -1144,36 +1195,36 @@ int wg_group_finish1(uint64_t keys, int key_kind, uint64_t vals, int val_width, 
     const uint64_t recon = kbase ? kbase : sub;
     uint32_t* w0 = (uint32_t*)k1;
     uint32_t* w1 = w0 + n;
-    k_key_u32<<<g, 256, 0, g_stream>>>(k0, n, sub, w0);
+    { WG_PROF("k_key_u32"); k_key_u32<<<g, 256, 0, g_stream>>>(k0, n, sub, w0); }
     cub::DoubleBuffer<uint32_t> dw(w0, w1);
     cub::DoubleBuffer<uint64_t> dv(v0, (uint64_t*)k0);          // k0 is free once narrowed
     size_t temp = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, temp, dw, dv, (int)n, 0, vbits, g_stream));
     void* d_temp = nullptr;
     CK(cudaMallocAsync(&d_temp, temp ? temp : 1, g_stream));
-    CK(cub::DeviceRadixSort::SortPairs(d_temp, temp, dw, dv, (int)n, 0, vbits, g_stream));
+    { WG_PROF("cub::DeviceRadixSort::SortPairs"); CK(cub::DeviceRadixSort::SortPairs(d_temp, temp, dw, dv, (int)n, 0, vbits, g_stream)); }
     uint8_t* heads;
     uint32_t* starts;
     int* d_cnt;
     CK(cudaMallocAsync((void**)&heads, n, g_stream));
     CK(cudaMallocAsync((void**)&starts, n * 4, g_stream));
     CK(cudaMallocAsync((void**)&d_cnt, 8, g_stream));
-    k_heads1_u32<<<g, 256, 0, g_stream>>>(dw.Current(), n, heads);
+    { WG_PROF("k_heads1_u32"); k_heads1_u32<<<g, 256, 0, g_stream>>>(dw.Current(), n, heads); }
     cub::CountingInputIterator<uint32_t> it(0);
     size_t temp2 = 0;
     CK(cub::DeviceSelect::Flagged(nullptr, temp2, it, heads, starts, d_cnt, (int)n, g_stream));
     void* d_temp2 = nullptr;
     CK(cudaMallocAsync(&d_temp2, temp2 ? temp2 : 1, g_stream));
-    CK(cub::DeviceSelect::Flagged(d_temp2, temp2, it, heads, starts, d_cnt, (int)n, g_stream));
+    { WG_PROF("cub::DeviceSelect::Flagged"); CK(cub::DeviceSelect::Flagged(d_temp2, temp2, it, heads, starts, d_cnt, (int)n, g_stream)); }
     int hK = 0;
     CK(cudaMemcpyAsync(&hK, d_cnt, 4, cudaMemcpyDeviceToHost, g_stream));
     CK(cudaStreamSynchronize(g_stream));
-    k_group_out<uint32_t><<<grid_for((uint64_t)hK + 1, 256), 256, 0, g_stream>>>(
-        starts, (uint64_t)hK, n, dw.Current(), recon, key_kind, (int64_t*)(uintptr_t)offs_out, (void*)(uintptr_t)ukeys_out);
+    { WG_PROF("k_group_out"); k_group_out<uint32_t><<<grid_for((uint64_t)hK + 1, 256), 256, 0, g_stream>>>(
+        starts, (uint64_t)hK, n, dw.Current(), recon, key_kind, (int64_t*)(uintptr_t)offs_out, (void*)(uintptr_t)ukeys_out); }
     if (val_width == 8)
-      CK(cudaMemcpyAsync((void*)(uintptr_t)vals_out, dv.Current(), n * 8, cudaMemcpyDeviceToDevice, g_stream));
+      { WG_PROF("memcpy_d2d"); CK(cudaMemcpyAsync((void*)(uintptr_t)vals_out, dv.Current(), n * 8, cudaMemcpyDeviceToDevice, g_stream)); }
     else
-      k_narrow<<<g, 256, 0, g_stream>>>(dv.Current(), (void*)(uintptr_t)vals_out, val_width, n);
+      { WG_PROF("k_narrow"); k_narrow<<<g, 256, 0, g_stream>>>(dv.Current(), (void*)(uintptr_t)vals_out, val_width, n); }
     CK(cudaGetLastError());
     CK(cudaFreeAsync(d_temp, g_stream));
     CK(cudaFreeAsync(d_temp2, g_stream));
@@ -1193,7 +1244,7 @@ int wg_group_finish1(uint64_t keys, int key_kind, uint64_t vals, int val_width, 
   CK(cub::DeviceRadixSort::SortPairs(nullptr, temp, dk, dv, (int)n, begin_bit, vbits, g_stream));
   void* d_temp = nullptr;
   CK(cudaMallocAsync(&d_temp, temp ? temp : 1, g_stream));
-  CK(cub::DeviceRadixSort::SortPairs(d_temp, temp, dk, dv, (int)n, begin_bit, vbits, g_stream));
+  { WG_PROF("cub::DeviceRadixSort::SortPairs"); CK(cub::DeviceRadixSort::SortPairs(d_temp, temp, dk, dv, (int)n, begin_bit, vbits, g_stream)); }
   if (begin_bit > 0) {
     uint64_t cap = n / 8 + 1024;
     uint32_t* pos;
@@ -1201,7 +1252,7 @@ int wg_group_finish1(uint64_t keys, int key_kind, uint64_t vals, int val_width, 
     CK(cudaMallocAsync((void**)&pos, cap * 4, g_stream));
     CK(cudaMemsetAsync(npos, 0, 8, g_stream));
     CK(cudaMemsetAsync(flag, 0, 4, g_stream));
-    k_disorder<<<g, 256, 0, g_stream>>>(dk.Current(), n, begin_bit, pos, npos, cap);
+    { WG_PROF("k_disorder"); k_disorder<<<g, 256, 0, g_stream>>>(dk.Current(), n, begin_bit, pos, npos, cap); }
     unsigned long long hn = 0;
     CK(cudaMemcpyAsync(&hn, npos, 8, cudaMemcpyDeviceToHost, g_stream));
     CK(cudaStreamSynchronize(g_stream));
@@ -1210,8 +1261,8 @@ int wg_group_finish1(uint64_t keys, int key_kind, uint64_t vals, int val_width, 
       unsigned* claimed;
       CK(cudaMallocAsync((void**)&claimed, (n / 32 + 1) * 4, g_stream));
       CK(cudaMemsetAsync(claimed, 0, (n / 32 + 1) * 4, g_stream));
-      k_fix_buckets<<<grid_for(hn, 128), 128, 0, g_stream>>>(dk.Current(), dv.Current(), n, begin_bit, pos, hn, 512,
-                                                             flag, claimed);
+      { WG_PROF("k_fix_buckets"); k_fix_buckets<<<grid_for(hn, 128), 128, 0, g_stream>>>(dk.Current(), dv.Current(), n, begin_bit, pos, hn, 512,
+                                                             flag, claimed); }
       CK(cudaFreeAsync(claimed, g_stream));
       CK(cudaMemcpyAsync(&hflag, flag, 4, cudaMemcpyDeviceToHost, g_stream));
       CK(cudaStreamSynchronize(g_stream));
@@ -1224,7 +1275,7 @@ int wg_group_finish1(uint64_t keys, int key_kind, uint64_t vals, int val_width, 
       CK(cub::DeviceRadixSort::SortPairs(nullptr, temp_full, dk, dv, (int)n, 0, vbits, g_stream));
       void* d_full = nullptr;
       CK(cudaMallocAsync(&d_full, temp_full ? temp_full : 1, g_stream));
-      CK(cub::DeviceRadixSort::SortPairs(d_full, temp_full, dk, dv, (int)n, 0, vbits, g_stream));
+      { WG_PROF("cub::DeviceRadixSort::SortPairs"); CK(cub::DeviceRadixSort::SortPairs(d_full, temp_full, dk, dv, (int)n, 0, vbits, g_stream)); }
       CK(cudaFreeAsync(d_full, g_stream));
     }
     CK(cudaFreeAsync(pos, g_stream));
@@ -1235,24 +1286,24 @@ int wg_group_finish1(uint64_t keys, int key_kind, uint64_t vals, int val_width, 
   CK(cudaMallocAsync((void**)&heads, n, g_stream));
   CK(cudaMallocAsync((void**)&starts, n * 4, g_stream));
   CK(cudaMallocAsync((void**)&d_cnt, 8, g_stream));
-  k_heads1<<<g, 256, 0, g_stream>>>(dk.Current(), n, heads);
+  { WG_PROF("k_heads1"); k_heads1<<<g, 256, 0, g_stream>>>(dk.Current(), n, heads); }
   cub::CountingInputIterator<uint32_t> it(0);
   size_t temp2 = 0;
   CK(cub::DeviceSelect::Flagged(nullptr, temp2, it, heads, starts, d_cnt, (int)n, g_stream));
   void* d_temp2 = nullptr;
   CK(cudaMallocAsync(&d_temp2, temp2 ? temp2 : 1, g_stream));
-  CK(cub::DeviceSelect::Flagged(d_temp2, temp2, it, heads, starts, d_cnt, (int)n, g_stream));
+  { WG_PROF("cub::DeviceSelect::Flagged"); CK(cub::DeviceSelect::Flagged(d_temp2, temp2, it, heads, starts, d_cnt, (int)n, g_stream)); }
   int hK = 0;
   CK(cudaMemcpyAsync(&hK, d_cnt, 4, cudaMemcpyDeviceToHost, g_stream));
   CK(cudaStreamSynchronize(g_stream));
-  k_group_out<uint64_t><<<grid_for((uint64_t)hK + 1, 256), 256, 0, g_stream>>>(starts, (uint64_t)hK, n, dk.Current(), kbase,
+  { WG_PROF("k_group_out"); k_group_out<uint64_t><<<grid_for((uint64_t)hK + 1, 256), 256, 0, g_stream>>>(starts, (uint64_t)hK, n, dk.Current(), kbase,
                                                                      key_kind,
                                                                      (int64_t*)(uintptr_t)offs_out,
-                                                                     (void*)(uintptr_t)ukeys_out);
+                                                                     (void*)(uintptr_t)ukeys_out); }
   if (val_width == 8)
-    CK(cudaMemcpyAsync((void*)(uintptr_t)vals_out, dv.Current(), n * 8, cudaMemcpyDeviceToDevice, g_stream));
+    { WG_PROF("memcpy_d2d"); CK(cudaMemcpyAsync((void*)(uintptr_t)vals_out, dv.Current(), n * 8, cudaMemcpyDeviceToDevice, g_stream)); }
   else
-    k_narrow<<<g, 256, 0, g_stream>>>(dv.Current(), (void*)(uintptr_t)vals_out, val_width, n);
+    { WG_PROF("k_narrow"); k_narrow<<<g, 256, 0, g_stream>>>(dv.Current(), (void*)(uintptr_t)vals_out, val_width, n); }
   CK(cudaGetLastError());
   CK(cudaFreeAsync(d_temp, g_stream));
   CK(cudaFreeAsync(d_temp2, g_stream));
@@ -1280,7 +1331,7 @@ int wg_gen_column(uint64_t dst, uint64_t n, uint64_t row0, int dist, int width, 
   g.flo = flo; g.fhi = fhi; g.div = div; g.ncat = ncat;
   if (ncat > 8) return fail("wg_gen_column: at most 8 categories");
   for (int c = 0; c < ncat; ++c) { g.cum[c] = cum[c]; g.vals[c] = vals[c]; }
-  k_gen<<<grid_for(n, 256), 256, 0, g_stream>>>((void*)(uintptr_t)dst, n, row0, g);
+  { WG_PROF("k_gen"); k_gen<<<grid_for(n, 256), 256, 0, g_stream>>>((void*)(uintptr_t)dst, n, row0, g); }
   CK(cudaGetLastError());
   return 0;
 }
@@ -1288,7 +1339,7 @@ int wg_gen_column(uint64_t dst, uint64_t n, uint64_t row0, int dist, int width, 
 int wg_mul_inplace_f64(uint64_t a, uint64_t b, uint64_t n) {
   NEED_INIT();
   if (!n) return 0;
-  k_mul_inplace<<<grid_for(n, 256), 256, 0, g_stream>>>((double*)(uintptr_t)a, (const double*)(uintptr_t)b, n);
+  { WG_PROF("k_mul_inplace"); k_mul_inplace<<<grid_for(n, 256), 256, 0, g_stream>>>((double*)(uintptr_t)a, (const double*)(uintptr_t)b, n); }
   CK(cudaGetLastError());
   return 0;
 }
@@ -1296,7 +1347,7 @@ int wg_mul_inplace_f64(uint64_t a, uint64_t b, uint64_t n) {
 int wg_flush_l2(uint64_t buf, uint64_t bytes, uint32_t salt) {
   NEED_INIT();
   uint64_t n16 = bytes / 16;
-  k_flush<<<grid_for(n16, 512), 512, 0, g_stream>>>((uint4*)(uintptr_t)buf, n16, salt);
+  { WG_PROF("k_flush"); k_flush<<<grid_for(n16, 512), 512, 0, g_stream>>>((uint4*)(uintptr_t)buf, n16, salt); }
   CK(cudaGetLastError());
   return 0;
 }
@@ -1342,6 +1393,38 @@ int wg_stream_wait_event(uint64_t ev) {
 int wg_sync_all(void) {
   NEED_INIT();
   for (int i = 0; i < 3; ++i) CK(cudaStreamSynchronize(g_streams[i]));
+  return 0;
+}
+
+// ---- per-launch timing ---------------------------------------------------------
+int wg_prof_enable(int on) {
+  NEED_INIT();
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (on) {
+    for (auto& r : g_prof) { g_prof_free.push_back(r.a); g_prof_free.push_back(r.b); }
+    g_prof.clear();
+  }
+  g_prof_on = on != 0;
+  return 0;
+}
+
+int wg_prof_count(int* n) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  *n = (int)g_prof.size();
+  return 0;
+}
+
+int wg_prof_record(int i, char* name, int cap, float* ms) {
+  NEED_INIT();
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (i < 0 || i >= (int)g_prof.size()) return fail("wg_prof_record: index out of range");
+  const ProfRec& r = g_prof[i];
+  CK(cudaEventSynchronize(r.b));
+  CK(cudaEventElapsedTime(ms, r.a, r.b));
+  if (name && cap > 0) {
+    strncpy(name, r.name, cap - 1);
+    name[cap - 1] = 0;
+  }
   return 0;
 }
 

@@ -79,6 +79,9 @@ _SIGS = {
     "wg_event_record": (c_int, [u64]),
     "wg_event_elapsed_ms": (c_int, [u64, u64, ctypes.POINTER(ctypes.c_float)]),
     "wg_event_destroy": (c_int, [u64]),
+    "wg_prof_enable": (c_int, [c_int]),
+    "wg_prof_count": (c_int, [ctypes.POINTER(c_int)]),
+    "wg_prof_record": (c_int, [c_int, c_char_p, c_int, ctypes.POINTER(ctypes.c_float)]),
     "wg_stream_select": (c_int, [c_int]),
     "wg_stream_wait_event": (c_int, [u64]),
     "wg_sync_all": (c_int, []),
@@ -446,3 +449,25 @@ class Event:
                 _lib.wg_event_destroy(self.h)
         except Exception:
             pass
+
+
+# ---------------------------------------------------------------------------
+# Per-launch device timing (wg_prof_*): every kernel the library launches,
+# bracketed by events on its own stream.
+
+
+def prof_enable(on=True):
+    _check(lib().wg_prof_enable(1 if on else 0))
+
+
+def prof_records():
+    """[(kernel name, ms)] for every launch since prof_enable(True)."""
+    n = c_int(0)
+    _check(lib().wg_prof_count(ctypes.byref(n)))
+    out = []
+    buf = ctypes.create_string_buffer(256)
+    ms = ctypes.c_float(0)
+    for i in range(n.value):
+        _check(lib().wg_prof_record(i, buf, 256, ctypes.byref(ms)))
+        out.append((buf.value.decode(), ms.value))
+    return out
