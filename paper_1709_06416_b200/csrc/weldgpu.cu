@@ -13,7 +13,6 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <nvrtc.h>
-#include <cub/cub.cuh>
 
 #include <cstdint>
 #include <cstdio>
@@ -149,6 +148,8 @@ inline unsigned grid_for(uint64_t n, unsigned block) {
   return (unsigned)g;
 }
 
+#include "wg_radix.cuh"
+
 // ---------------------------------------------------------------------------
 // Fixed-function kernels.
 
@@ -265,14 +266,6 @@ __global__ void k_widen(const void* src, uint64_t* dst, int width, uint64_t n) {
 }
 
 // Segment heads over sorted multi-word keys: flag[i] = (i == 0) || key(i) != key(i-1).
-__global__ void k_heads(const uint64_t* const* words, int kw, uint64_t n, uint8_t* flags) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    bool h = (i == 0);
-    if (!h) for (int k = 0; k < kw; ++k) if (words[k][i] != words[k][i - 1]) { h = true; break; }
-    flags[i] = h ? 1 : 0;
-  }
-}
-
 // ---------------------------------------------------------------------------
 // Counter-based synthetic columns: h = splitmix64(seed ^
 // (col << 56) ^ row); u = (h >> 11) * 2^-53; ints = lo + h mod span.
@@ -363,15 +356,6 @@ __global__ void k_fix_buckets(uint64_t* k, uint64_t* v, uint64_t n, int shift, c
   }
 }
 
-__global__ void k_heads1(const uint64_t* k, uint64_t n, uint8_t* flags) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-    flags[i] = (i == 0 || k[i] != k[i - 1]) ? 1 : 0;
-}
-
-__global__ void k_heads1_u32(const uint32_t* k, uint64_t n, uint8_t* flags) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-    flags[i] = (i == 0 || k[i] != k[i - 1]) ? 1 : 0;
-}
 // 32-bit sort keys: w = okey - base (every key's varying bits fit in 32)
 __global__ void k_key_u32(const uint64_t* ok, uint64_t n, uint64_t base, uint32_t* w) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
@@ -1047,25 +1031,101 @@ int wg_iota_u32(uint64_t dst, uint64_t n) {
   return 0;
 }
 
-// Stable LSD radix sort of (u64 key, u32 value) pairs over key bits
-// [begin_bit, end_bit).  Stability is what makes multi-field lexicographic
-// sorts (last field first) and order-preserving grouping correct.
+}  // extern "C"
+
+namespace {
+
+// Stable LSD radix sort of (key, value) pairs over key bits [begin_bit,
+// end_bit) with the onesweep kernels of wg_radix.cuh.  The first pass reads
+// (kin, vin); the result lands in (kA, vA); (kB, vB) are ping-pong scratch.
+// Stability is what makes multi-field lexicographic sorts (last field first)
+// and order-preserving grouping correct.
+template <typename K, typename V>
+int radix_sort(const K* kin, const V* vin, K* kA, K* kB, V* vA, V* vB, uint64_t n, int begin_bit, int end_bit) {
+  if (n > 0xffffffffULL) return fail("radix sort: more than 2^32 items");
+  if (!n) return 0;
+  const int npass = end_bit > begin_bit ? (end_bit - begin_bit + 7) / 8 : 0;
+  if (npass == 0) {
+    if ((const void*)kA != (const void*)kin) CK(cudaMemcpyAsync(kA, kin, n * sizeof(K), cudaMemcpyDeviceToDevice, g_stream));
+    if ((const void*)vA != (const void*)vin) CK(cudaMemcpyAsync(vA, vin, n * sizeof(V), cudaMemcpyDeviceToDevice, g_stream));
+    return 0;
+  }
+  constexpr int ITEMS = 8, TILE = 512 * ITEMS;
+  constexpr int SMEM = wgr::onesweep_smem<K, V, ITEMS>();
+  static bool attr_set = false;   // per template instance
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(wgr::k_onesweep<K, V, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    attr_set = true;
+  }
+  const uint64_t tiles = (n + TILE - 1) / TILE;
+  uint32_t* hist;
+  unsigned long long* status;
+  CK(cudaMallocAsync((void**)&hist, (npass * wgr::RADIX + npass) * 4, g_stream));
+  uint32_t* ctr = hist + npass * wgr::RADIX;
+  CK(cudaMemsetAsync(hist, 0, (npass * wgr::RADIX + npass) * 4, g_stream));
+  CK(cudaMallocAsync((void**)&status, tiles * wgr::RADIX * 8, g_stream));
+  { WG_PROF("k_radix_hist"); wgr::k_radix_hist<K><<<grid_for(n, 256), 256, 0, g_stream>>>(kin, n, begin_bit, end_bit, npass, hist); }
+  { WG_PROF("k_radix_offsets"); wgr::k_radix_offsets<<<npass, wgr::RADIX, 0, g_stream>>>(hist); }
+  const K* ki = kin;
+  const V* vi = vin;
+  for (int p = 0; p < npass; ++p) {
+    const bool toA = ((npass - 1 - p) & 1) == 0;
+    K* ko = toA ? kA : kB;
+    V* vo = toA ? vA : vB;
+    const int shift = begin_bit + 8 * p;
+    const int wbits = end_bit - shift < 8 ? end_bit - shift : 8;
+    CK(cudaMemsetAsync(status, 0, tiles * wgr::RADIX * 8, g_stream));
+    { WG_PROF("k_onesweep"); wgr::k_onesweep<K, V, ITEMS><<<(unsigned)tiles, 512, SMEM, g_stream>>>(
+        ki, vi, ko, vo, (uint32_t)n, shift, (1u << wbits) - 1u, hist + p * wgr::RADIX, status, ctr + p); }
+    CK(cudaGetLastError());
+    ki = ko;
+    vi = vo;
+  }
+  CK(cudaFreeAsync(status, g_stream));
+  CK(cudaFreeAsync(hist, g_stream));
+  return 0;
+}
+
+// Run starts of sorted keys (u32 positions) and their count (host).
+template <typename EQ>
+int run_heads(EQ eq, uint64_t n, uint32_t* starts, uint64_t* count) {
+  if (!n) { *count = 0; return 0; }
+  constexpr int ITEMS = 16, TILE = 256 * ITEMS;
+  const uint64_t tiles = (n + TILE - 1) / TILE;
+  unsigned long long* st;
+  CK(cudaMallocAsync((void**)&st, tiles * 8 + 16, g_stream));
+  CK(cudaMemsetAsync(st, 0, tiles * 8 + 16, g_stream));
+  unsigned long long* total = st + tiles;
+  uint32_t* ctr = (uint32_t*)(st + tiles + 1);
+  { WG_PROF("k_run_heads"); wgr::k_run_heads<EQ, ITEMS><<<(unsigned)tiles, 256, 0, g_stream>>>(eq, n, starts, st, ctr, total); }
+  CK(cudaGetLastError());
+  unsigned long long h = 0;
+  CK(cudaMemcpyAsync(&h, total, 8, cudaMemcpyDeviceToHost, g_stream));
+  CK(cudaStreamSynchronize(g_stream));
+  CK(cudaFreeAsync(st, g_stream));
+  *count = h;
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
 int wg_sort_pairs(uint64_t keys_in, uint64_t vals_in, uint64_t keys_out, uint64_t vals_out, uint64_t n,
                   int begin_bit, int end_bit) {
   NEED_INIT();
   if (!n) return 0;
   if (n > 0xffffffffULL) return fail("wg_sort_pairs: more than 2^32 items");
-  size_t temp = 0;
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, temp, (const uint64_t*)(uintptr_t)keys_in,
-                                     (uint64_t*)(uintptr_t)keys_out, (const uint32_t*)(uintptr_t)vals_in,
-                                     (uint32_t*)(uintptr_t)vals_out, (int)n, begin_bit, end_bit, g_stream));
-  void* d_temp = nullptr;
-  CK(cudaMallocAsync(&d_temp, temp ? temp : 1, g_stream));
-  { WG_PROF("cub::DeviceRadixSort::SortPairs"); CK(cub::DeviceRadixSort::SortPairs(d_temp, temp, (const uint64_t*)(uintptr_t)keys_in,
-                                     (uint64_t*)(uintptr_t)keys_out, (const uint32_t*)(uintptr_t)vals_in,
-                                     (uint32_t*)(uintptr_t)vals_out, (int)n, begin_bit, end_bit, g_stream)); }
-  CK(cudaFreeAsync(d_temp, g_stream));
-  return 0;
+  uint64_t* kB;
+  uint32_t* vB;
+  CK(cudaMallocAsync((void**)&kB, n * 8, g_stream));
+  CK(cudaMallocAsync((void**)&vB, n * 4, g_stream));
+  int rc = radix_sort<uint64_t, uint32_t>((const uint64_t*)(uintptr_t)keys_in, (const uint32_t*)(uintptr_t)vals_in,
+                                          (uint64_t*)(uintptr_t)keys_out, kB, (uint32_t*)(uintptr_t)vals_out, vB, n,
+                                          begin_bit, end_bit);
+  CK(cudaFreeAsync(kB, g_stream));
+  CK(cudaFreeAsync(vB, g_stream));
+  return rc;
 }
 
 int wg_gather(uint64_t src, uint64_t perm, uint64_t dst, uint64_t n, int width) {
@@ -1106,36 +1166,18 @@ int wg_run_starts(const uint64_t* key_words, int kw, uint64_t n, uint64_t starts
   if (!n) { *nruns = 0; return 0; }
   if (n > 0xffffffffULL) return fail("wg_run_starts: more than 2^32 items");
   uint64_t** d_words = nullptr;
-  uint8_t* flags = nullptr;
-  int* d_cnt = nullptr;
   CK(cudaMallocAsync((void**)&d_words, sizeof(uint64_t*) * kw, g_stream));
   CK(cudaMemcpyAsync(d_words, key_words, sizeof(uint64_t) * kw, cudaMemcpyHostToDevice, g_stream));
-  CK(cudaMallocAsync((void**)&flags, n, g_stream));
-  CK(cudaMallocAsync((void**)&d_cnt, 8, g_stream));
-  { WG_PROF("k_heads"); k_heads<<<grid_for(n, 256), 256, 0, g_stream>>>((const uint64_t* const*)d_words, kw, n, flags); }
-  CK(cudaGetLastError());
-  cub::CountingInputIterator<uint32_t> it(0);
-  size_t temp = 0;
-  CK(cub::DeviceSelect::Flagged(nullptr, temp, it, flags, (uint32_t*)(uintptr_t)starts_out, d_cnt, (int)n, g_stream));
-  void* d_temp = nullptr;
-  CK(cudaMallocAsync(&d_temp, temp ? temp : 1, g_stream));
-  { WG_PROF("cub::DeviceSelect::Flagged"); CK(cub::DeviceSelect::Flagged(d_temp, temp, it, flags, (uint32_t*)(uintptr_t)starts_out, d_cnt, (int)n, g_stream)); }
-  int h = 0;
-  CK(cudaMemcpyAsync(&h, d_cnt, 4, cudaMemcpyDeviceToHost, g_stream));
-  CK(cudaStreamSynchronize(g_stream));
-  CK(cudaFreeAsync(d_temp, g_stream));
-  CK(cudaFreeAsync(flags, g_stream));
-  CK(cudaFreeAsync(d_cnt, g_stream));
+  int rc = run_heads(wgr::EqWords{(const uint64_t* const*)d_words, kw}, n, (uint32_t*)(uintptr_t)starts_out, nruns);
   CK(cudaFreeAsync(d_words, g_stream));
-  *nruns = (uint64_t)h;
-  return 0;
+  return rc;
 }
 
 // GroupBuilderState.result (builders.py:478-493) for one integer/bool key
 // leaf and one value leaf: a stable sort of the appended {key, value} rows
 // by key, then run starts -> (sorted unique keys, offsets[K+1], values in
 // per-key input order).  Only the key bits that vary are sorted: a stable
-// radix sort on the top 24 varying bits, then a stable insertion sort
+// radix sort on the top 32 varying bits, then a stable insertion sort
 // inside the (small) buckets; skewed data falls back to a full radix sort.
 static bool g_group_u32 = getenv("WELDGPU_GROUP_U32") == nullptr || getenv("WELDGPU_GROUP_U32")[0] != '0';
 
@@ -1157,14 +1199,17 @@ int wg_group_finish1(uint64_t keys, int key_kind, uint64_t vals, int val_width, 
   // but the value/key gather afterwards is a random permutation -- 11 ms at
   // 200M rows on B200 vs 4.5 ms saved; carrying the payload through the
   // passes is cheaper.)
-  uint64_t *k0, *k1, *v0, *v1;
+  uint64_t *k0, *kA, *kB, *v0, *vA, *vB;
   unsigned long long* mm;
   int* flag;
   const bool own_v0 = val_width != 8;
   CK(cudaMallocAsync((void**)&k0, n * 8, g_stream));
   if (own_v0) CK(cudaMallocAsync((void**)&v0, n * 8, g_stream)); else v0 = (uint64_t*)(uintptr_t)vals;
-  CK(cudaMallocAsync((void**)&k1, n * 8, g_stream));
-  CK(cudaMallocAsync((void**)&v1, n * 8, g_stream));
+  CK(cudaMallocAsync((void**)&kA, n * 8, g_stream));
+  CK(cudaMallocAsync((void**)&kB, n * 8, g_stream));
+  CK(cudaMallocAsync((void**)&vB, n * 8, g_stream));
+  // the last radix pass writes the values straight into vals_out when they are 8 bytes wide
+  if (own_v0) CK(cudaMallocAsync((void**)&vA, n * 8, g_stream)); else vA = (uint64_t*)(uintptr_t)vals_out;
   CK(cudaMallocAsync((void**)&mm, 32, g_stream));
   flag = (int*)(mm + 2);
   uint64_t init[4] = {~0ULL, 0ULL, 0ULL, 0ULL};
@@ -1186,6 +1231,9 @@ int wg_group_finish1(uint64_t keys, int key_kind, uint64_t vals, int val_width, 
     vbits = rbits;
   }
   const int begin_bit = vbits > 32 ? vbits - 32 : 0;
+  uint32_t* starts;
+  CK(cudaMallocAsync((void**)&starts, n * 4, g_stream));
+  uint64_t hK = 0;
   if (begin_bit == 0 && g_group_u32) {
     // every key's varying bits fit in 32: sort (u32 key, u64 value) pairs --
     // 12 instead of 16 bytes per row per radix pass -- and rebuild the keys
@@ -1193,129 +1241,65 @@ int wg_group_finish1(uint64_t keys, int key_kind, uint64_t vals, int val_width, 
     const uint64_t lowmask = vbits >= 64 ? ~0ULL : ((1ULL << vbits) - 1);
     const uint64_t sub = kbase ? 0ULL : (hmm[0] & ~lowmask);   // k0 already holds okey - kbase when kbase != 0
     const uint64_t recon = kbase ? kbase : sub;
-    uint32_t* w0 = (uint32_t*)k1;
-    uint32_t* w1 = w0 + n;
+    uint32_t* w0 = (uint32_t*)kB;
+    uint32_t* wA = (uint32_t*)kA;
+    uint32_t* wB = w0 + n;                                      // kB holds w0 and wB (2 x 4n bytes)
     { WG_PROF("k_key_u32"); k_key_u32<<<g, 256, 0, g_stream>>>(k0, n, sub, w0); }
-    cub::DoubleBuffer<uint32_t> dw(w0, w1);
-    cub::DoubleBuffer<uint64_t> dv(v0, (uint64_t*)k0);          // k0 is free once narrowed
-    size_t temp = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, temp, dw, dv, (int)n, 0, vbits, g_stream));
-    void* d_temp = nullptr;
-    CK(cudaMallocAsync(&d_temp, temp ? temp : 1, g_stream));
-    { WG_PROF("cub::DeviceRadixSort::SortPairs"); CK(cub::DeviceRadixSort::SortPairs(d_temp, temp, dw, dv, (int)n, 0, vbits, g_stream)); }
-    uint8_t* heads;
-    uint32_t* starts;
-    int* d_cnt;
-    CK(cudaMallocAsync((void**)&heads, n, g_stream));
-    CK(cudaMallocAsync((void**)&starts, n * 4, g_stream));
-    CK(cudaMallocAsync((void**)&d_cnt, 8, g_stream));
-    { WG_PROF("k_heads1_u32"); k_heads1_u32<<<g, 256, 0, g_stream>>>(dw.Current(), n, heads); }
-    cub::CountingInputIterator<uint32_t> it(0);
-    size_t temp2 = 0;
-    CK(cub::DeviceSelect::Flagged(nullptr, temp2, it, heads, starts, d_cnt, (int)n, g_stream));
-    void* d_temp2 = nullptr;
-    CK(cudaMallocAsync(&d_temp2, temp2 ? temp2 : 1, g_stream));
-    { WG_PROF("cub::DeviceSelect::Flagged"); CK(cub::DeviceSelect::Flagged(d_temp2, temp2, it, heads, starts, d_cnt, (int)n, g_stream)); }
-    int hK = 0;
-    CK(cudaMemcpyAsync(&hK, d_cnt, 4, cudaMemcpyDeviceToHost, g_stream));
-    CK(cudaStreamSynchronize(g_stream));
-    { WG_PROF("k_group_out"); k_group_out<uint32_t><<<grid_for((uint64_t)hK + 1, 256), 256, 0, g_stream>>>(
-        starts, (uint64_t)hK, n, dw.Current(), recon, key_kind, (int64_t*)(uintptr_t)offs_out, (void*)(uintptr_t)ukeys_out); }
-    if (val_width == 8)
-      { WG_PROF("memcpy_d2d"); CK(cudaMemcpyAsync((void*)(uintptr_t)vals_out, dv.Current(), n * 8, cudaMemcpyDeviceToDevice, g_stream)); }
-    else
-      { WG_PROF("k_narrow"); k_narrow<<<g, 256, 0, g_stream>>>(dv.Current(), (void*)(uintptr_t)vals_out, val_width, n); }
-    CK(cudaGetLastError());
-    CK(cudaFreeAsync(d_temp, g_stream));
-    CK(cudaFreeAsync(d_temp2, g_stream));
-    CK(cudaFreeAsync(heads, g_stream));
-    CK(cudaFreeAsync(starts, g_stream));
-    CK(cudaFreeAsync(d_cnt, g_stream));
-    CK(cudaFreeAsync(mm, g_stream));
-    CK(cudaFreeAsync(k0, g_stream));
-    if (own_v0) CK(cudaFreeAsync(v0, g_stream));
-    CK(cudaFreeAsync(k1, g_stream));
-    CK(cudaFreeAsync(v1, g_stream));
-    *K_out = (uint64_t)hK;
-    return 0;
-  }
-  cub::DoubleBuffer<uint64_t> dk(k0, k1), dv(v0, v1);
-  size_t temp = 0;
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, temp, dk, dv, (int)n, begin_bit, vbits, g_stream));
-  void* d_temp = nullptr;
-  CK(cudaMallocAsync(&d_temp, temp ? temp : 1, g_stream));
-  { WG_PROF("cub::DeviceRadixSort::SortPairs"); CK(cub::DeviceRadixSort::SortPairs(d_temp, temp, dk, dv, (int)n, begin_bit, vbits, g_stream)); }
-  if (begin_bit > 0) {
-    uint64_t cap = n / 8 + 1024;
-    uint32_t* pos;
-    unsigned long long* npos = mm + 3;
-    CK(cudaMallocAsync((void**)&pos, cap * 4, g_stream));
-    CK(cudaMemsetAsync(npos, 0, 8, g_stream));
-    CK(cudaMemsetAsync(flag, 0, 4, g_stream));
-    { WG_PROF("k_disorder"); k_disorder<<<g, 256, 0, g_stream>>>(dk.Current(), n, begin_bit, pos, npos, cap); }
-    unsigned long long hn = 0;
-    CK(cudaMemcpyAsync(&hn, npos, 8, cudaMemcpyDeviceToHost, g_stream));
-    CK(cudaStreamSynchronize(g_stream));
-    int hflag = hn > cap;
-    if (!hflag && hn) {
-      unsigned* claimed;
-      CK(cudaMallocAsync((void**)&claimed, (n / 32 + 1) * 4, g_stream));
-      CK(cudaMemsetAsync(claimed, 0, (n / 32 + 1) * 4, g_stream));
-      { WG_PROF("k_fix_buckets"); k_fix_buckets<<<grid_for(hn, 128), 128, 0, g_stream>>>(dk.Current(), dv.Current(), n, begin_bit, pos, hn, 512,
-                                                             flag, claimed); }
-      CK(cudaFreeAsync(claimed, g_stream));
-      CK(cudaMemcpyAsync(&hflag, flag, 4, cudaMemcpyDeviceToHost, g_stream));
+    if (radix_sort<uint32_t, uint64_t>(w0, v0, wA, wB, vA, vB, n, 0, vbits)) return -1;
+    if (run_heads(wgr::EqU32{wA}, n, starts, &hK)) return -1;
+    { WG_PROF("k_group_out"); k_group_out<uint32_t><<<grid_for(hK + 1, 256), 256, 0, g_stream>>>(
+        starts, hK, n, wA, recon, key_kind, (int64_t*)(uintptr_t)offs_out, (void*)(uintptr_t)ukeys_out); }
+  } else {
+    if (radix_sort<uint64_t, uint64_t>(k0, v0, kA, kB, vA, vB, n, begin_bit, vbits)) return -1;
+    if (begin_bit > 0) {
+      uint64_t cap = n / 8 + 1024;
+      uint32_t* pos = starts;             // scratch until the run starts are computed
+      unsigned long long* npos = mm + 3;
+      CK(cudaMemsetAsync(npos, 0, 8, g_stream));
+      CK(cudaMemsetAsync(flag, 0, 4, g_stream));
+      { WG_PROF("k_disorder"); k_disorder<<<g, 256, 0, g_stream>>>(kA, n, begin_bit, pos, npos, cap); }
+      unsigned long long hn = 0;
+      CK(cudaMemcpyAsync(&hn, npos, 8, cudaMemcpyDeviceToHost, g_stream));
       CK(cudaStreamSynchronize(g_stream));
+      int hflag = hn > cap;
+      if (!hflag && hn) {
+        unsigned* claimed;
+        CK(cudaMallocAsync((void**)&claimed, (n / 32 + 1) * 4, g_stream));
+        CK(cudaMemsetAsync(claimed, 0, (n / 32 + 1) * 4, g_stream));
+        { WG_PROF("k_fix_buckets"); k_fix_buckets<<<grid_for(hn, 128), 128, 0, g_stream>>>(kA, vA, n, begin_bit, pos, hn, 512,
+                                                                                             flag, claimed); }
+        CK(cudaFreeAsync(claimed, g_stream));
+        CK(cudaMemcpyAsync(&hflag, flag, 4, cudaMemcpyDeviceToHost, g_stream));
+        CK(cudaStreamSynchronize(g_stream));
+      }
+      if (hflag) {
+        // skewed buckets: a full stable sort of every varying bit (sorting
+        // only the low bits now would undo the order of the high ones; ties
+        // keep the current -- input -- order of each key's rows)
+        uint64_t *kt, *vt;
+        CK(cudaMallocAsync((void**)&kt, n * 8, g_stream));
+        CK(cudaMallocAsync((void**)&vt, n * 8, g_stream));
+        CK(cudaMemcpyAsync(kt, kA, n * 8, cudaMemcpyDeviceToDevice, g_stream));
+        CK(cudaMemcpyAsync(vt, vA, n * 8, cudaMemcpyDeviceToDevice, g_stream));
+        if (radix_sort<uint64_t, uint64_t>(kt, vt, kA, kB, vA, vB, n, 0, vbits)) return -1;
+        CK(cudaFreeAsync(kt, g_stream));
+        CK(cudaFreeAsync(vt, g_stream));
+      }
     }
-    if (hflag) {
-      // skewed buckets: a full stable sort of every varying bit (sorting
-      // only the low bits now would undo the order of the high ones; ties
-      // keep the current -- input -- order of each key's rows)
-      size_t temp_full = 0;
-      CK(cub::DeviceRadixSort::SortPairs(nullptr, temp_full, dk, dv, (int)n, 0, vbits, g_stream));
-      void* d_full = nullptr;
-      CK(cudaMallocAsync(&d_full, temp_full ? temp_full : 1, g_stream));
-      { WG_PROF("cub::DeviceRadixSort::SortPairs"); CK(cub::DeviceRadixSort::SortPairs(d_full, temp_full, dk, dv, (int)n, 0, vbits, g_stream)); }
-      CK(cudaFreeAsync(d_full, g_stream));
-    }
-    CK(cudaFreeAsync(pos, g_stream));
+    if (run_heads(wgr::EqU64{kA}, n, starts, &hK)) return -1;
+    { WG_PROF("k_group_out"); k_group_out<uint64_t><<<grid_for(hK + 1, 256), 256, 0, g_stream>>>(
+        starts, hK, n, kA, kbase, key_kind, (int64_t*)(uintptr_t)offs_out, (void*)(uintptr_t)ukeys_out); }
   }
-  uint8_t* heads;
-  uint32_t* starts;
-  int* d_cnt;
-  CK(cudaMallocAsync((void**)&heads, n, g_stream));
-  CK(cudaMallocAsync((void**)&starts, n * 4, g_stream));
-  CK(cudaMallocAsync((void**)&d_cnt, 8, g_stream));
-  { WG_PROF("k_heads1"); k_heads1<<<g, 256, 0, g_stream>>>(dk.Current(), n, heads); }
-  cub::CountingInputIterator<uint32_t> it(0);
-  size_t temp2 = 0;
-  CK(cub::DeviceSelect::Flagged(nullptr, temp2, it, heads, starts, d_cnt, (int)n, g_stream));
-  void* d_temp2 = nullptr;
-  CK(cudaMallocAsync(&d_temp2, temp2 ? temp2 : 1, g_stream));
-  { WG_PROF("cub::DeviceSelect::Flagged"); CK(cub::DeviceSelect::Flagged(d_temp2, temp2, it, heads, starts, d_cnt, (int)n, g_stream)); }
-  int hK = 0;
-  CK(cudaMemcpyAsync(&hK, d_cnt, 4, cudaMemcpyDeviceToHost, g_stream));
-  CK(cudaStreamSynchronize(g_stream));
-  { WG_PROF("k_group_out"); k_group_out<uint64_t><<<grid_for((uint64_t)hK + 1, 256), 256, 0, g_stream>>>(starts, (uint64_t)hK, n, dk.Current(), kbase,
-                                                                     key_kind,
-                                                                     (int64_t*)(uintptr_t)offs_out,
-                                                                     (void*)(uintptr_t)ukeys_out); }
-  if (val_width == 8)
-    { WG_PROF("memcpy_d2d"); CK(cudaMemcpyAsync((void*)(uintptr_t)vals_out, dv.Current(), n * 8, cudaMemcpyDeviceToDevice, g_stream)); }
-  else
-    { WG_PROF("k_narrow"); k_narrow<<<g, 256, 0, g_stream>>>(dv.Current(), (void*)(uintptr_t)vals_out, val_width, n); }
+  if (own_v0) { WG_PROF("k_narrow"); k_narrow<<<g, 256, 0, g_stream>>>(vA, (void*)(uintptr_t)vals_out, val_width, n); }
   CK(cudaGetLastError());
-  CK(cudaFreeAsync(d_temp, g_stream));
-  CK(cudaFreeAsync(d_temp2, g_stream));
-  CK(cudaFreeAsync(heads, g_stream));
   CK(cudaFreeAsync(starts, g_stream));
-  CK(cudaFreeAsync(d_cnt, g_stream));
   CK(cudaFreeAsync(mm, g_stream));
   CK(cudaFreeAsync(k0, g_stream));
-  if (own_v0) CK(cudaFreeAsync(v0, g_stream));
-  CK(cudaFreeAsync(k1, g_stream));
-  CK(cudaFreeAsync(v1, g_stream));
-  *K_out = (uint64_t)hK;
+  if (own_v0) { CK(cudaFreeAsync(v0, g_stream)); CK(cudaFreeAsync(vA, g_stream)); }
+  CK(cudaFreeAsync(kA, g_stream));
+  CK(cudaFreeAsync(kB, g_stream));
+  CK(cudaFreeAsync(vB, g_stream));
+  *K_out = hK;
   return 0;
 }
 
