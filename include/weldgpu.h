@@ -130,6 +130,29 @@ int wg_stream_select(int which);
 int wg_stream_wait_event(uint64_t ev);
 int wg_sync_all(void);
 
+/* ---- multi-GPU combine (row-partitioned evaluation) -------
+ * The reference folds per-chunk builder partials at result() --
+ * merger builders.py:314-328, dictmerger :380-392, vecmerger :435-450,
+ * groupbuilder :478-493 -- on one host.  Across GPUs each rank's partial is
+ * exchanged with these entry points (NCCL over NVLink, libnccl.so.2 loaded
+ * at wg_nccl_init) and folded by device kernels.
+ *
+ * wg_partition: stable split of n rows into nsplit+1 destinations by the
+ *   order key (builders.py:496-507) of the first key leaf against ascending
+ *   splitter order keys; every column is scattered so each destination's rows
+ *   are contiguous and in input order; counts_out (host) gets the
+ *   per-destination row counts. */
+int wg_partition(uint64_t key_col, int key_kind, const uint64_t* splitters, int nsplit, int ncols,
+                 const uint64_t* cols_in, const uint64_t* cols_out, const int* widths, uint64_t n,
+                 uint64_t* counts_out);
+int wg_nccl_unique_id(char* out, int cap);
+int wg_nccl_init(int rank, int world, const char* id_bytes);
+int wg_nccl_finalize(void);
+int wg_nccl_allgather(uint64_t send, uint64_t recv, uint64_t bytes);
+int wg_nccl_allreduce(uint64_t send, uint64_t recv, uint64_t count, int kind, int op);
+int wg_nccl_sendrecv(int nsend, const uint64_t* send_ptr, const uint64_t* send_bytes, const int* send_peer,
+                     int nrecv, const uint64_t* recv_ptr, const uint64_t* recv_bytes, const int* recv_peer);
+
 #ifdef __cplusplus
 }
 #endif

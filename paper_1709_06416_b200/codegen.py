@@ -2281,3 +2281,53 @@ def static_plans(expr, env_types=None, externs=(), smem=True, lowcard=False, par
             continue
         plans.append(plan)
     return plans
+
+
+# ---------------------------------------------------------------------------
+# Multi-GPU combine kernels (distributed.py): the reference folds builder
+# partials in (step, chunk) key order at result() (builders.py:314-328,
+# 435-450); across ranks the partials are folded in rank order with the same
+# device fold functions the loop kernels use.
+
+
+def combine_source(op, kinds):
+    """Kernels folding G per-rank partials in rank order, for a builder of
+    merge op `op` over leaves `kinds`:
+
+    wg_fold_slots      merger slots (F value words + merged flag per rank)
+                       -> one slot; a rank that merged nothing is skipped,
+                       so an all-empty result keeps flag 0 (identity)
+    wg_fold_chunks<f>  vecmerger leaf f: out[i] = fold over s of
+                       chunks[s * L + i] (chunk s = rank s's slice)."""
+    F = len(kinds)
+    st = OPSTRUCT[op]
+    L = ['#include "weld_device.cuh"',
+         "struct SlotParams { const u64* parts; u64 G; u64* out; };",
+         "struct ChunkParams { u64 out; u64 chunks; u64 L; u64 G; };",
+         'extern "C" __global__ void wg_fold_slots(const SlotParams p) {',
+         "  if (threadIdx.x != 0 || blockIdx.x != 0) return;",
+         "  bool has = false;"]
+    for f, k in enumerate(kinds):
+        L.append(f"  {CTYPE[k]} a{f} = {CTYPE[k]}();")
+    L += [f"  for (u64 r = 0; r < p.G; ++r) {{",
+          f"    const u64* w = p.parts + r * {F + 1};",
+          f"    if (!w[{F}]) continue;"]
+    for f, k in enumerate(kinds):
+        ct = CTYPE[k]
+        L.append(f"    a{f} = has ? {st}<{ct}>::f(a{f}, wg_from_bits<{ct}>(w[{f}])) : wg_from_bits<{ct}>(w[{f}]);")
+    L += ["    has = true;", "  }"]
+    for f, k in enumerate(kinds):
+        L.append(f"  p.out[{f}] = wg_to_bits<{CTYPE[k]}>(a{f});")
+    L += [f"  p.out[{F}] = has ? 1ULL : 0ULL;", "}"]
+    for f, k in enumerate(kinds):
+        ct = CTYPE[k]
+        L += [f'extern "C" __global__ void wg_fold_chunks{f}(const ChunkParams p) {{',
+              f"  {ct}* out = ({ct}*)p.out;",
+              f"  const {ct}* c = (const {ct}*)p.chunks;",
+              "  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < p.L; i += (u64)gridDim.x * blockDim.x) {",
+              f"    {ct} a = c[i];",
+              f"    for (u64 s = 1; s < p.G; ++s) a = {st}<{ct}>::f(a, c[s * p.L + i]);",
+              "    out[i] = a;",
+              "  }",
+              "}"]
+    return "\n".join(L) + "\n"

@@ -13,6 +13,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <nvrtc.h>
+#include <nccl.h>   // types only: libnccl.so.2 is dlopen()ed at wg_nccl_init
+#include <dlfcn.h>
 
 #include <cstdint>
 #include <cstdio>
@@ -231,6 +233,144 @@ __global__ void k_order_key(const void* src, int kind, uint64_t n, const uint32_
       }
     }
     dst[i] = k;
+  }
+}
+
+// ---- row partitioning for the multi-GPU combine --------------------------
+// dest(row) = number of splitters <= order_key(key[row]) (range partition
+// of the first key leaf: equal keys always meet on one rank, and rank-order
+// concatenation of the per-rank results is globally sorted).
+__device__ __forceinline__ uint64_t okey_at(const void* src, int kind, uint64_t j) {
+  switch (kind) {
+    case 0: return ((const uint8_t*)src)[j];
+    case 1: return (uint64_t)(int64_t)((const int32_t*)src)[j] ^ 0x8000000000000000ULL;
+    case 2: return (uint64_t)((const int64_t*)src)[j] ^ 0x8000000000000000ULL;
+    default: {
+      double v = (kind == 3) ? (double)((const float*)src)[j] : ((const double*)src)[j];
+      if (v != v) return 0xffffffffffffffffULL;
+      if (v == 0.0) v = 0.0;
+      uint64_t b = (uint64_t)__double_as_longlong(v);
+      uint64_t k = (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+      return k == 0xffffffffffffffffULL ? 0xfffffffffffffffeULL : k;
+    }
+  }
+}
+
+#define WG_PART_MAX 64
+struct PartSpec {
+  int G, nsplit, ncols, kind;
+  const void* key;
+  uint64_t split[WG_PART_MAX];
+  const void* in[16];
+  void* out[16];
+  int width[16];
+};
+
+__device__ __forceinline__ int part_dest(const PartSpec& p, uint64_t row) {
+  const uint64_t k = okey_at(p.key, p.kind, row);
+  int lo = 0, hi = p.nsplit;   // first splitter > k
+  while (lo < hi) { const int m = (lo + hi) >> 1; if (p.split[m] <= k) lo = m + 1; else hi = m; }
+  return lo;
+}
+
+// per-tile destination counts: cnt[d * ntiles + t]
+__global__ void __launch_bounds__(256) k_part_count(PartSpec p, uint64_t n, uint32_t* cnt, uint32_t ntiles) {
+  __shared__ uint32_t c[WG_PART_MAX];
+  if (threadIdx.x < WG_PART_MAX) c[threadIdx.x] = 0;
+  __syncthreads();
+  const uint64_t t0 = (uint64_t)blockIdx.x * 4096;
+  for (int i = threadIdx.x; i < 4096; i += 256) {
+    const uint64_t r = t0 + i;
+    if (r < n) atomicAdd(&c[part_dest(p, r)], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < p.G) cnt[(uint64_t)threadIdx.x * ntiles + blockIdx.x] = c[threadIdx.x];
+}
+
+// one CTA per destination: exclusive scan of its per-tile counts (in
+// place), the destination's total into tot[d]
+__global__ void __launch_bounds__(1024) k_part_scan(uint32_t* cnt, uint32_t ntiles, uint64_t* tot) {
+  __shared__ uint32_t ws[32];
+  __shared__ uint64_t carry;
+  uint32_t* c = cnt + (uint64_t)blockIdx.x * ntiles;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (uint32_t b = 0; b < ntiles; b += 1024) {
+    const uint32_t i = b + threadIdx.x;
+    const uint32_t v = i < ntiles ? c[i] : 0;
+    uint32_t x = v;
+    for (int s = 1; s < 32; s <<= 1) { const uint32_t y = __shfl_up_sync(0xffffffffu, x, s); if (lane >= s) x += y; }
+    if (lane == 31) ws[w] = x;
+    __syncthreads();
+    uint32_t before = 0, all = 0;
+    for (int j = 0; j < 32; ++j) { if (j < w) before += ws[j]; all += ws[j]; }
+    const uint64_t base = carry;
+    if (i < ntiles) c[i] = (uint32_t)(base + before + x - v);
+    __syncthreads();
+    if (threadIdx.x == 0) carry = base + all;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) tot[blockIdx.x] = carry;
+}
+
+// stable scatter of every column: rows keep their input order inside each
+// destination segment (warp rounds of 32 consecutive rows, ballot ranks)
+__global__ void __launch_bounds__(256) k_part_scatter(PartSpec p, uint64_t n, const uint32_t* cnt, uint32_t ntiles,
+                                                      const uint64_t* tot) {
+  constexpr int ITEMS = 16;
+  __shared__ uint32_t wc[8][WG_PART_MAX];
+  __shared__ uint64_t base[WG_PART_MAX];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  for (int i = tid; i < 8 * WG_PART_MAX; i += 256) (&wc[0][0])[i] = 0;
+  if (tid < p.G) {
+    uint64_t b = 0;
+    for (int d = 0; d < tid; ++d) b += tot[d];
+    base[tid] = b + cnt[(uint64_t)tid * ntiles + blockIdx.x];
+  }
+  __syncthreads();
+  const uint64_t wrow = (uint64_t)blockIdx.x * 4096 + (uint64_t)w * 512 + lane;
+  int dd[ITEMS];
+  uint32_t rk[ITEMS];
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const uint64_t r = wrow + i * 32;
+    const int d = r < n ? part_dest(p, r) : WG_PART_MAX;
+    unsigned pm = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < 7; ++b) {
+      const bool bit = (d >> b) & 1;
+      const unsigned bm = __ballot_sync(0xffffffffu, bit);
+      pm &= bit ? bm : ~bm;
+    }
+    const uint32_t below = __popc(pm & lt);
+    const uint32_t prev = d < WG_PART_MAX ? wc[w][d] : 0u;
+    __syncwarp();
+    if (d < WG_PART_MAX && below == 0) wc[w][d] = prev + __popc(pm);
+    __syncwarp();
+    dd[i] = d;
+    rk[i] = prev + below;
+  }
+  __syncthreads();
+  if (tid < p.G) {   // warp offsets within the tile's segment of each destination
+    uint32_t run = 0;
+    for (int j = 0; j < 8; ++j) { const uint32_t c = wc[j][tid]; wc[j][tid] = run; run += c; }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int d = dd[i];
+    if (d >= WG_PART_MAX) continue;
+    const uint64_t src = wrow + i * 32;
+    const uint64_t dst = base[d] + wc[w][d] + rk[i];
+    for (int c = 0; c < p.ncols; ++c) {
+      switch (p.width[c]) {
+        case 1: ((uint8_t*)p.out[c])[dst] = ((const uint8_t*)p.in[c])[src]; break;
+        case 4: ((uint32_t*)p.out[c])[dst] = ((const uint32_t*)p.in[c])[src]; break;
+        default: ((uint64_t*)p.out[c])[dst] = ((const uint64_t*)p.in[c])[src]; break;
+      }
+    }
   }
 }
 
@@ -1415,6 +1555,161 @@ int wg_prof_record(int i, char* name, int cap, float* ms) {
 int wg_event_destroy(uint64_t ev) {
   NEED_INIT();
   CK(cudaEventDestroy((cudaEvent_t)(uintptr_t)ev));
+  return 0;
+}
+
+
+// ---- multi-GPU: row partitioning + NCCL (libnccl.so.2, dlopen'ed) ---------
+// The combine step of row-partitioned evaluation.  The
+// reference folds its per-chunk partials at result()
+// (builders.py:314-328, 380-392, 435-450, 478-493); across GPUs the partials
+// are exchanged with these collectives on the library's stream.
+int wg_partition(uint64_t key_col, int key_kind, const uint64_t* splitters, int nsplit, int ncols,
+                 const uint64_t* cols_in, const uint64_t* cols_out, const int* widths, uint64_t n,
+                 uint64_t* counts_out) {
+  NEED_INIT();
+  if (nsplit + 1 > WG_PART_MAX) return fail("wg_partition: at most 64 destinations");
+  if (ncols > 16) return fail("wg_partition: at most 16 columns");
+  if (n > 0xffffffffULL) return fail("wg_partition: more than 2^32 rows");
+  const int G = nsplit + 1;
+  if (n == 0) { for (int d = 0; d < G; ++d) counts_out[d] = 0; return 0; }
+  PartSpec p;
+  memset(&p, 0, sizeof(p));
+  p.G = G; p.nsplit = nsplit; p.ncols = ncols; p.kind = key_kind;
+  p.key = (const void*)(uintptr_t)key_col;
+  for (int i = 0; i < nsplit; ++i) p.split[i] = splitters[i];
+  for (int c = 0; c < ncols; ++c) {
+    p.in[c] = (const void*)(uintptr_t)cols_in[c];
+    p.out[c] = (void*)(uintptr_t)cols_out[c];
+    p.width[c] = widths[c];
+    if (widths[c] != 1 && widths[c] != 4 && widths[c] != 8) return fail("wg_partition: column width must be 1, 4 or 8");
+  }
+  const uint32_t ntiles = (uint32_t)((n + 4095) / 4096);
+  uint32_t* cnt;
+  uint64_t* tot;
+  CK(cudaMallocAsync((void**)&cnt, (uint64_t)G * ntiles * 4, g_stream));
+  CK(cudaMallocAsync((void**)&tot, G * 8, g_stream));
+  { WG_PROF("k_part_count"); k_part_count<<<ntiles, 256, 0, g_stream>>>(p, n, cnt, ntiles); }
+  { WG_PROF("k_part_scan"); k_part_scan<<<G, 1024, 0, g_stream>>>(cnt, ntiles, tot); }
+  { WG_PROF("k_part_scatter"); k_part_scatter<<<ntiles, 256, 0, g_stream>>>(p, n, cnt, ntiles, tot); }
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(counts_out, tot, G * 8, cudaMemcpyDeviceToHost, g_stream));
+  CK(cudaStreamSynchronize(g_stream));
+  CK(cudaFreeAsync(cnt, g_stream));
+  CK(cudaFreeAsync(tot, g_stream));
+  return 0;
+}
+
+}  // extern "C"
+
+namespace {
+struct Nccl {
+  void* h = nullptr;
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+} g_nccl;
+
+int nccl_load() {
+  if (g_nccl.h) return 0;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return fail(std::string("wg_nccl: cannot load libnccl.so.2: ") + dlerror());
+#define WG_NSYM(f)                                                              \
+  g_nccl.f = reinterpret_cast<decltype(g_nccl.f)>(dlsym(h, "nccl" #f));          \
+  if (!g_nccl.f) return fail("wg_nccl: libnccl.so.2 lacks nccl" #f);
+  WG_NSYM(GetUniqueId) WG_NSYM(CommInitRank) WG_NSYM(CommDestroy) WG_NSYM(AllGather) WG_NSYM(AllReduce)
+  WG_NSYM(Send) WG_NSYM(Recv) WG_NSYM(GroupStart) WG_NSYM(GroupEnd) WG_NSYM(GetErrorString)
+#undef WG_NSYM
+  g_nccl.h = h;
+  return 0;
+}
+}  // namespace
+
+#define CKNC(x)                                                                        \
+  do {                                                                                 \
+    ncclResult_t r_ = (x);                                                             \
+    if (r_ != ncclSuccess) return fail(std::string(#x) + ": " + g_nccl.GetErrorString(r_)); \
+  } while (0)
+#define NEED_NCCL() \
+  do { if (!g_nccl.comm) return fail("wg_nccl: wg_nccl_init() has not been called"); } while (0)
+
+extern "C" {
+
+int wg_nccl_unique_id(char* out, int cap) {
+  if (cap < (int)sizeof(ncclUniqueId)) return fail("wg_nccl_unique_id: buffer smaller than 128 bytes");
+  if (nccl_load()) return -1;
+  ncclUniqueId id;
+  CKNC(g_nccl.GetUniqueId(&id));
+  memcpy(out, &id, sizeof(id));
+  return 0;
+}
+
+int wg_nccl_init(int rank, int world, const char* id_bytes) {
+  NEED_INIT();
+  if (nccl_load()) return -1;
+  if (g_nccl.comm) return fail("wg_nccl_init: already initialised");
+  ncclUniqueId id;
+  memcpy(&id, id_bytes, sizeof(id));
+  CKNC(g_nccl.CommInitRank(&g_nccl.comm, world, id, rank));
+  g_nccl.rank = rank;
+  g_nccl.world = world;
+  return 0;
+}
+
+int wg_nccl_finalize(void) {
+  if (!g_nccl.comm) return 0;
+  CK(cudaStreamSynchronize(g_stream));
+  CKNC(g_nccl.CommDestroy(g_nccl.comm));
+  g_nccl.comm = nullptr;
+  return 0;
+}
+
+int wg_nccl_allgather(uint64_t send, uint64_t recv, uint64_t bytes) {
+  NEED_INIT(); NEED_NCCL();
+  WG_PROF("ncclAllGather");
+  CKNC(g_nccl.AllGather((const void*)(uintptr_t)send, (void*)(uintptr_t)recv, bytes, ncclUint8, g_nccl.comm, g_stream));
+  return 0;
+}
+
+// kind: KIND_CODE (1 i32, 2 i64, 3 f32, 4 f64); op: 0 sum 1 prod 2 min 3 max
+int wg_nccl_allreduce(uint64_t send, uint64_t recv, uint64_t count, int kind, int op) {
+  NEED_INIT(); NEED_NCCL();
+  ncclDataType_t t;
+  switch (kind) {
+    case 1: t = ncclInt32; break;
+    case 2: t = ncclInt64; break;
+    case 3: t = ncclFloat32; break;
+    case 4: t = ncclFloat64; break;
+    default: return fail("wg_nccl_allreduce: unsupported kind");
+  }
+  const ncclRedOp_t ops[4] = {ncclSum, ncclProd, ncclMin, ncclMax};
+  if (op < 0 || op > 3) return fail("wg_nccl_allreduce: unsupported op");
+  WG_PROF("ncclAllReduce");
+  CKNC(g_nccl.AllReduce((const void*)(uintptr_t)send, (void*)(uintptr_t)recv, count, t, ops[op], g_nccl.comm, g_stream));
+  return 0;
+}
+
+// Grouped point-to-point: an all-to-all-v of one or more columns is one
+// group of sends and receives (NCCL has no alltoallv).
+int wg_nccl_sendrecv(int nsend, const uint64_t* send_ptr, const uint64_t* send_bytes, const int* send_peer,
+                     int nrecv, const uint64_t* recv_ptr, const uint64_t* recv_bytes, const int* recv_peer) {
+  NEED_INIT(); NEED_NCCL();
+  WG_PROF("ncclSendRecv");
+  CKNC(g_nccl.GroupStart());
+  for (int i = 0; i < nsend; ++i)
+    if (send_bytes[i]) CKNC(g_nccl.Send((const void*)(uintptr_t)send_ptr[i], send_bytes[i], ncclUint8, send_peer[i], g_nccl.comm, g_stream));
+  for (int i = 0; i < nrecv; ++i)
+    if (recv_bytes[i]) CKNC(g_nccl.Recv((void*)(uintptr_t)recv_ptr[i], recv_bytes[i], ncclUint8, recv_peer[i], g_nccl.comm, g_stream));
+  CKNC(g_nccl.GroupEnd());
   return 0;
 }
 

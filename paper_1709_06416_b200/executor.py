@@ -37,7 +37,8 @@ from .builders_dev import (_finish_small, AppenderDev, DDict, DGroups, DictDev, 
 from .codegen import DEFER_DICT, PIPE_STAGES, BSpec, IterSpec, generate
 from .columns import Col, DVec, to_device, to_payload, dvec_from_cols
 from .irtypes import (BOOL, F32, F64, I64, SIZE, identity_value, Builder, DeviceUnsupported as _DU, Dict, DictMerger, Function,
-                      GroupBuilder, Merger, Scalar, Simd, Struct, Vec, VecBuilder, VecMerger, is_flat, leaves)
+                      GroupBuilder, Merger, NPTYPE, Scalar, Simd, Struct, Vec, VecBuilder, VecMerger, is_flat, leaves,
+                      to_bits)
 
 
 class DeviceUnsupported(EvalError, _DU):
@@ -568,7 +569,40 @@ class Ctx:
             captures[name] = (cty, lenv[name])
 
         strategy = self.cfg.strategy
-        bstruct, bmap = _bspecs(builders, strategy, count, loop_id=id(e))
+        # dictmerger variant chosen from the data on a loop's first run: the
+        # first SKETCH_ROWS rows run as a launch of their own (low-
+        # cardinality variant, correct for any cardinality), the distinct
+        # count they produced picks the variant -- and the table size -- for
+        # the remaining rows (all builders accept a loop split into
+        # consecutive launches: merges are commutative, appends land in order)
+        dicts = [(q, b) for q, b in enumerate(_builder_order(builders)) if isinstance(b, DictDev)]
+        from .builders_dev import _SIZE_HINTS
+        if (dicts and strategy != "global" and count >= 4 * SKETCH_ROWS and not any(s.simd for s in specs)
+                and any(_SIZE_HINTS.get((id(e), q)) is None for q, _ in dicts)):
+            self._launch_loop(e, lam, specs, datas, windows, SKETCH_ROWS, builders, captures, strategy,
+                              assume_lowcard=True)
+            for q, st in dicts:
+                if _SIZE_HINTS.get((id(e), q)) is not None:
+                    continue
+                self._settle(st)
+                d, _ = st.read_counters()
+                est = d if d * 32 <= SKETCH_ROWS else min(1 << 24, max(d, (d * count) // SKETCH_ROWS))
+                _SIZE_HINTS[(id(e), q)] = est
+                if est * 2 > st.cap:
+                    self._dict_regrow_(st, 0, want=est)
+            rest = [(s0 + SKETCH_ROWS * st_, st_) for s0, st_ in windows]
+            saved = self.idx0
+            self.idx0 = saved + SKETCH_ROWS
+            try:
+                self._launch_loop(e, lam, specs, datas, rest, count - SKETCH_ROWS, builders, captures, strategy)
+            finally:
+                self.idx0 = saved
+            return builders
+        self._launch_loop(e, lam, specs, datas, windows, count, builders, captures, strategy)
+        return builders
+
+    def _launch_loop(self, e, lam, specs, datas, windows, count, builders, captures, strategy, assume_lowcard=False):
+        bstruct, bmap = _bspecs(builders, strategy, count, loop_id=id(e), assume_lowcard=assume_lowcard)
         # The expression identities fix every type in the loop; only the
         # runtime choices (strides, alignment, builder modes, externs) vary.
         key = (id(e), id(lam), tuple((s.strided, s.aligned) for s in specs), _bsig(bstruct), self._ext_key)
@@ -593,7 +627,7 @@ class Ctx:
             with _plan_lock:
                 cc = _plan_cache.get(ckey)
             if cc is None:
-                cbs, _ = _bspecs(builders, strategy, count, loop_id=id(e))
+                cbs, _ = _bspecs(builders, strategy, count, loop_id=id(e), assume_lowcard=assume_lowcard)
                 cplan = generate(e if lam is e.func else _with_func(e, lam), specs, cbs, captures, self.externs,
                                  strategy, count_only=True)
                 cc = (cplan, rt.get_kernel(cplan.source, cplan.name))
@@ -601,7 +635,6 @@ class Ctx:
                     _plan_cache[ckey] = cc
             sizes = self._count_pass(cc[0], cc[1], count, datas, windows, bmap, captures)
         self.launch(plan, kern, count, datas, windows, builders, bmap, captures, sizes=sizes)
-        return builders
 
     def _count_pass(self, plan, kern, count, datas, windows, bmap, captures):
         """Launch the count-only kernel.  Returns {builder id: appends}."""
@@ -756,13 +789,15 @@ class Ctx:
         REGROWS += 1
         self._dict_regrow_(st, spilled)
 
-    def _dict_regrow_(self, st: DictDev, spilled):
-        """Grow the table 4x, re-insert existing entries and replay the
-        spilled merges (all folds are commutative)."""
-        import ctypes as _ct
+    def _dict_regrow_(self, st: DictDev, spilled, want=0):
+        """Grow the table 4x (or to hold `want` keys at load 1/2), re-insert
+        existing entries and replay the spilled merges (all folds are
+        commutative)."""
         kw, vw, n = st.compact()
         old_over, old_cnt = st.over, spilled
         newcap = max(4 * st.cap, 1 << int(max(2 * n, 1) - 1).bit_length())
+        if want:
+            newcap = max(st.cap, 1 << int(max(2 * max(want, n), 1) - 1).bit_length())
         st._alloc_table(newcap)
         rt.memset(st.ocount.ptr, 0, 8)
         # replay: entries from the old table then the spill list, as a device loop
@@ -1032,7 +1067,23 @@ PART_MIN_KEYS = 1 << 20
 REGROWS = 0         # dictmerger tables grown after spills (test instrumentation)
 
 
-def _bspecs(builders, strategy, count, loop_id=None):
+SKETCH_ROWS = 1 << 16   # rows of a loop's first run that choose its dictmerger variants
+
+
+def _builder_order(builders):
+    """Builders in _bspecs' id order (depth-first over builder structs)."""
+    out = []
+    stack = [builders]
+    while stack:                 # iterative: a recursive closure would pin the builders until GC
+        v = stack.pop()
+        if isinstance(v, tuple):
+            stack.extend(reversed(v))
+        else:
+            out.append(v)
+    return out
+
+
+def _bspecs(builders, strategy, count, loop_id=None, assume_lowcard=False):
     bmap = {}
     counter = [0]
     single = not isinstance(builders, tuple)
@@ -1059,6 +1110,8 @@ def _bspecs(builders, strategy, count, loop_id=None):
             # unknown) -> deferred merges with batched HBM probes.
             from .builders_dev import _SIZE_HINTS
             seen = _SIZE_HINTS.get((loop_id, bid))
+            if seen is None and assume_lowcard:
+                seen = 1
             lowcard = seen is not None and seen <= LOWCARD_MAX
             if (seen is not None and seen > PART_MIN_KEYS and strategy != "global"
                     and v.nw == 1 and DEFER_DICT):
@@ -1230,14 +1283,11 @@ def _infer_free_type(e, name):
     return None
 
 
-def evaluate_partials(loop, env, config=None, externs=None, idx0=0, rank=0):
-    """Run one ``for`` loop over this rank's row shard and return each
-    builder's *partial* state as host arrays (for distributed.combine_*).
-    Vecmerger bins on ranks > 0 start from the fold identity so ``init`` is
-    counted once."""
+def _run_partial_loop(loop, env, config, externs, idx0, rank):
+    """Run one ``for`` loop over this rank's row shard; return (ctx, builders)
+    with the builders NOT finalised.  Vecmerger bins on ranks > 0 start from
+    the fold identity so ``init`` is counted once (rank 0 folds it)."""
     from dataclasses import replace
-    from .builders_dev import _value_words_to_cols, _words_to_cols
-    from .columns import col_to_numpy
     from .irtypes import internal_identity as _iid
     cfg = config or EngineConfig(memory_limit=1 << 46)
     ctx = Ctx(cfg, externs, idx0=idx0)
@@ -1252,48 +1302,71 @@ def evaluate_partials(loop, env, config=None, externs=None, idx0=0, rank=0):
     for b in blist:
         if isinstance(b, VecMergerDev) and rank > 0:
             for c, k in zip(b.cols, b.ks):
-                arr = np.full(b.n, _iid(b.kind.op, k), dtype=np.dtype(
-                    {"i32": "<i4", "i64": "<i8", "f32": "<f4", "f64": "<f8"}[k]))
-                rt.h2d(c.ptr, arr.ctypes.data, arr.nbytes)
+                ident = _iid(b.kind.op, k)
+                if b.n and to_bits(k, ident) == 0:
+                    rt.memset(c.ptr, 0, b.n * SIZE[k])
+                elif b.n:
+                    arr = np.full(b.n, ident, dtype=NPTYPE[k])
+                    rt.h2d(c.ptr, arr.ctypes.data, arr.nbytes)
     frame["__wg_b"] = bval
-    ctx.run_loop(replace(loop, builders=Ident("__wg_b", ty=loop.builders.ty)), frame)
+    hit = _PARTIAL_LOOPS.get(id(loop))
+    if hit is None or hit[0] is not loop:
+        # one rewritten loop per program, so plans and dictmerger hints are reused across calls
+        hit = _PARTIAL_LOOPS[id(loop)] = (loop, replace(loop, builders=Ident("__wg_b", ty=loop.builders.ty)))
+    ctx.run_loop(hit[1], frame)
     ctx.check_device()
-    out = []
     for b in blist:
         b.consume()
+    return ctx, blist
+
+
+_PARTIAL_LOOPS = {}
+
+
+def evaluate_partials_device(loop, env, config=None, externs=None, idx0=0, rank=0):
+    """Per-builder partial states of one loop over this rank's row shard,
+    left in HBM for the device combine (distributed.evaluate_sharded):
+
+      merger     {"slot": F+1 words (values, merged flag)}
+      appender   {"cols": leaf Cols, "n"}
+      vecmerger  {"cols": bin Cols, "n"}
+      dict       {"keys", "vals": typed leaf Cols of the compacted table, "n"}
+      group      {"keys", "vals": leaf Cols of the row log (input order), "n"}
+    """
+    from .builders_dev import _value_words_to_cols, _words_to_cols
+    ctx, blist = _run_partial_loop(loop, env, config, externs, idx0, rank)
+    out = []
+    for b in blist:
         kind = b.kind
         if isinstance(kind, Merger):
             F = len(b.ks)
-            w = b.read_words()
-            from .irtypes import from_bits
-            if w is None:
-                out.append({"kind": "merger", "op": kind.op, "kinds": b.ks, "has": False,
-                            "values": [identity_value(kind.op, k) for k in b.ks]})
-            else:
-                out.append({"kind": "merger", "op": kind.op, "kinds": b.ks, "has": bool(w[F]),
-                            "values": [from_bits(k, int(x)) for k, x in zip(b.ks, w[:F])]})
+            if not b.launched:         # no rows on this rank: merged flag 0
+                rt.memset(b.slot.ptr, 0, 8 * (F + 1))
+            out.append({"kind": "merger", "op": kind.op, "kinds": b.ks, "slot": b.slot, "b": b})
         elif isinstance(kind, VecBuilder):
-            cols, n = b.concat() if b.segments else ([], 0)
-            out.append({"kind": "appender", "cols": [col_to_numpy(c, n) for c in cols] if cols else
-                        [np.zeros(0, dtype={"bool": "u1", "i32": "<i4", "i64": "<i8", "f32": "<f4",
-                                            "f64": "<f8"}[k]) for k in b.kinds]})
+            if b.segments:
+                cols, n = b.concat()
+            else:
+                cols, n = [Col.alloc(k, 0) for k in b.kinds], 0
+            out.append({"kind": "appender", "kinds": b.kinds, "cols": cols, "n": n, "b": b})
         elif isinstance(kind, VecMerger):
-            out.append({"kind": "vecmerger", "op": kind.op, "kinds": b.ks,
-                        "cols": [col_to_numpy(c, b.n) for c in b.cols]})
+            out.append({"kind": "vecmerger", "op": kind.op, "kinds": b.ks, "cols": b.cols, "n": b.n, "b": b})
         elif isinstance(kind, DictMerger):
             if b.table is None:
                 b.ensure(1)
             kw, vw, n = b.compact()
-            kc = _words_to_cols(kw, b.kks, b.lay, n)
-            vc = _value_words_to_cols(vw, b.vks, n)
-            out.append({"kind": "dict", "op": kind.op, "vkinds": b.vks,
-                        "keys": [col_to_numpy(c, n) for c in kc], "vals": [col_to_numpy(c, n) for c in vc]})
+            out.append({"kind": "dict", "op": kind.op, "kks": b.kks, "vks": b.vks, "type": kind,
+                        "keys": _words_to_cols(kw, b.kks, b.lay, n), "vals": _value_words_to_cols(vw, b.vks, n),
+                        "n": n})
         elif isinstance(kind, GroupBuilder):
-            cols, n = b.concat() if b.segments else ([Col.alloc(k, 0) for k in b.kinds], 0)
+            if b.segments:
+                cols, n = b.concat()
+            else:
+                cols, n = [Col.alloc(k, 0) for k in b.kinds], 0
             nk = len(b.kks)
-            arrs = [col_to_numpy(c, n) for c in cols]
-            out.append({"kind": "group", "keys": arrs[:nk], "vals": arrs[nk:]})
-    return out
+            out.append({"kind": "group", "kks": b.kks, "vks": b.vks, "type": kind, "keys": cols[:nk],
+                        "vals": cols[nk:], "n": n})
+    return out, ctx
 
 
 # ---------------------------------------------------------------------------

@@ -85,6 +85,15 @@ _SIGS = {
     "wg_stream_select": (c_int, [c_int]),
     "wg_stream_wait_event": (c_int, [u64]),
     "wg_sync_all": (c_int, []),
+    "wg_partition": (c_int, [u64, c_int, ctypes.POINTER(u64), c_int, c_int, ctypes.POINTER(u64), ctypes.POINTER(u64),
+                             ctypes.POINTER(c_int), u64, ctypes.POINTER(u64)]),
+    "wg_nccl_unique_id": (c_int, [c_char_p, c_int]),
+    "wg_nccl_init": (c_int, [c_int, c_int, c_char_p]),
+    "wg_nccl_finalize": (c_int, []),
+    "wg_nccl_allgather": (c_int, [u64, u64, u64]),
+    "wg_nccl_allreduce": (c_int, [u64, u64, u64, c_int, c_int]),
+    "wg_nccl_sendrecv": (c_int, [c_int, ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(c_int), c_int,
+                                 ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(c_int)]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -1,6 +1,3 @@
-mkdir -p gpurun_out
-timeout 120 ./tools/sort_ab | tee gpurun_out/sort_ab.txt
-timeout 900 python -m pytest tests/test_gpu_sort.py tests/test_gpu_math.py tests/test_gpu_configs.py -x -q 2>&1 | tail -3
-timeout 600 python bench.py --workload group --steps 10 --warmup 3 --per-config none --no-cpu --no-e2e > gpurun_out/bench_group.json 2>gpurun_out/bench_group.err; echo bench_rc=$?
-python -c "
-import json;d=json.loads(open('gpurun_out/bench_group.json').read().strip().splitlines()[-1]);print(d['ms_per_step'], d['roofline']['frac']); print(d['roofline']['kernels'])"
+python tools/prof_host_q1.py q1 2>&1 | head -1
+for w in q1 dict group; do timeout 600 python bench.py --workload $w --steps 10 --warmup 3 --per-config none --no-cpu --no-e2e 2>&1 | tail -1 | python -c "
+import json,sys;d=json.loads(sys.stdin.read());print(d['config']['workload'], 'ms', round(d['ms_per_step'],3), 'cold', round(d['cold_ms_per_step'],3), [(k['name'], round(k['ms_per_step'],3)) for k in d['roofline']['kernels']])"; done
