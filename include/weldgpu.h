@@ -100,6 +100,13 @@ int wg_iota_i64(uint64_t dst, uint64_t n, int64_t step);
 /* exclusive scan of n i64 per-tile append counts -> tile offsets; *total (device) = sum
  * (two-pass order-preserving appends: VecBuilderState.result order, builders.py:274-283) */
 int wg_exclusive_scan_i64(uint64_t src, uint64_t dst, uint64_t n, uint64_t total);
+/* reallocation accounting of an unhinted vecbuilder's scan-mode launch
+ * (VecBuilderState.merge, builders.py:256-272): coff[c] = output position of
+ * chunk c's first append (nch grain-wide chunks), *total = the launch's
+ * appends (device).  out (device u64[4]): sum of doublings and of final
+ * capacities over interior chunks 1..nch-2, then the first and last chunk's
+ * append counts. */
+int wg_seg_stats(uint64_t coff, uint64_t nch, uint64_t total, uint64_t out);
 int wg_sort_pairs(uint64_t keys_in, uint64_t vals_in, uint64_t keys_out, uint64_t vals_out, uint64_t n, int begin_bit,
                   int end_bit);
 int wg_gather(uint64_t src, uint64_t perm, uint64_t dst, uint64_t n, int width);

@@ -200,11 +200,12 @@ class DRef:
 
 class SVec:
     """A small vector literal built inside the body (registers)."""
-    __slots__ = ("items", "elem")
+    __slots__ = ("items", "elem", "node")
 
-    def __init__(self, items, elem):
+    def __init__(self, items, elem, node=None):
         self.items = list(items)
         self.elem = elem
+        self.node = node
 
 
 class BRef:
@@ -266,6 +267,10 @@ class KernelPlan:
     merger_bids: list
     key: str = ""
     pipe_stage_bytes: int = 0
+    count_nodes: list = field(default_factory=list)   # count_evals: loop-local node ordinals
+    stat_nodes: list = field(default_factory=list)    # ("alloc" | "trav", node): body EvalStats events
+    lit_nodes: dict = field(default_factory=dict)     # nested appender bid -> ids of literals it keeps
+    seg_bids: list = field(default_factory=list)      # unhinted scan appenders with chunk offsets
 
 
 def _hex_f64(v):
@@ -325,6 +330,17 @@ class Gen:
         self.bspecs = []
         self._collect(bstruct)
         self.items = items
+        # count_evals (EngineConfig.count_evals, run.py:544-557): every node
+        # evaluation in phase A bumps a per-node device counter; the host
+        # maps these loop-local ordinals back to the program's nodes
+        self.counting = False
+        self.count_nodes = []
+        self._count_ord = {}
+        # EvalStats events inside the body: literal vectors materialised
+        # ("alloc") and nested loops that read at least one element ("trav")
+        self.stat_nodes = []
+        self._stat_ord = {}
+        self.lit_nodes = {}
 
     # -- helpers -----------------------------------------------------------
     def _collect(self, bs):
@@ -353,10 +369,26 @@ class Gen:
         return S(name, kind)
 
     # -- expressions -------------------------------------------------------
+    def stat(self, what, e, cond=None):
+        if self.phase != "A":
+            return
+        k = self._stat_ord.get((what, id(e)))
+        if k is None:
+            k = self._stat_ord[(what, id(e))] = len(self.stat_nodes)
+            self.stat_nodes.append((what, e))
+        self.param("scnt", "unsigned long long*", ("scnt",))
+        self.emit(f"wg_count(p.scnt + {k});" if cond is None else f"if ({cond}) wg_count(p.scnt + {k});")
+
     def ex(self, e, env):
         m = getattr(self, "ex_" + type(e).__name__, None)
         if m is None:
             raise DeviceUnsupported(f"{type(e).__name__} inside a loop body is not lowered to the device")
+        if self.counting and self.phase == "A":
+            k = self._count_ord.get(id(e))
+            if k is None:
+                k = self._count_ord[id(e)] = len(self.count_nodes)
+                self.count_nodes.append(e)
+            self.emit(f"wg_count(p.cnt + {k});")
         return m(e, env)
 
     def ex_Literal(self, e, env):
@@ -391,7 +423,11 @@ class Gen:
         raise DeviceUnsupported("field access on a non-struct value")
 
     def ex_MakeVector(self, e, env):
-        return SVec([self.ex(x, env) for x in e.items], e.ty.elem)
+        items = [self.ex(x, env) for x in e.items]
+        # the reference materialises every literal it evaluates (run.py:781-789):
+        # an allocation per execution, counted for EvalStats
+        self.stat("alloc", e)
+        return SVec(items, e.ty.elem, e)
 
     def ex_Broadcast(self, e, env):
         v = self.ex(e.value, env)
@@ -772,6 +808,8 @@ class Gen:
             if any(len(d.items) != n for d in datas):
                 from weldmill.errors import ZipLengthMismatch
                 raise ZipLengthMismatch("zipped iterations disagree")
+            if n:
+                self.stat("trav", e)
             for j in range(n):
                 elem = datas[0].items[j] if len(datas) == 1 else T([d.items[j] for d in datas])
                 env2 = dict(env)
@@ -812,6 +850,7 @@ class Gen:
                     self.emit(f"if ({ok} && {c} != {cs[0]}) {{ wg_raise(p.err, WG_ERR_ZIP, {c}); {ok} = false; }}")
                 cs.append(c)
             self.emit(f"const i64 {cnt} = {ok} ? {cs[0]} : 0;")
+            self.stat("trav", e, f"{cnt} > 0")
             j = self.tmp("j")
             self.emit(f"for (i64 {j} = 0; {j} < {cnt}; ++{j}) {{")
             self.ind += 1
@@ -857,6 +896,8 @@ class Gen:
                     return
                 if not isinstance(v, SVec):
                     raise DeviceUnsupported(f"vecbuilder[{kind.elem}] of a non-literal vector")
+                if v.node is not None:
+                    self.lit_nodes.setdefault(b.bid, set()).add(id(v.node))
                 L = len(v.items)
                 if b.extra.setdefault("nested_len", L) != L:
                     raise DeviceUnsupported(f"vecbuilder[{kind.elem}] of vectors with different lengths")
@@ -977,8 +1018,9 @@ class Gen:
             chain = " else ".join(f"if (rk{b.bid}_{r} == {kc}) {{ {fold(r)} }}" for r in range(R))
             claim = " else ".join(f"if (rk{b.bid}_{r} == WG_EMPTY_KEY) {{ rk{b.bid}_{r} = {kc}; {fold(r)} }}"
                                   for r in range(R))
-            self.emit(f"{chain} else if ({kc} != WG_EMPTY_KEY) {{ {claim} else {{ {hit} = false; }} }} "
-                      f"else {{ {hit} = false; }}")
+            # the sentinel-valued key bypasses the cache (an unclaimed slot
+            # holds the sentinel too and would absorb its merges)
+            self.emit(f"if ({kc} == WG_EMPTY_KEY) {{ {hit} = false; }} else {chain} else {{ {claim} else {{ {hit} = false; }} }}")
             self.emit(f"if (!{hit}) {{")
             self.ind += 1
         if b.mode == "smem" and nw == 1:
@@ -1189,8 +1231,9 @@ def choose_items(iters):
 
 
 def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_loop", items=None,
-             count_only=False) -> KernelPlan:
+             count_only=False, counting=False) -> KernelPlan:
     g = Gen(loop, iters, bstruct, captures, externs, strategy)
+    g.counting = counting and not count_only
     lam = loop.func
     if not isinstance(lam, Lambda):
         raise DeviceUnsupported("loop function must be a lambda literal")
@@ -1309,6 +1352,18 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
         if it.strided:
             g.param(f"it{k}_start", "i64", ("itstart", k))
             g.param(f"it{k}_stride", "i64", ("itstride", k))
+
+    if g.counting:
+        g.param("cnt", "unsigned long long*", ("cnt",))
+    seg_bs = [b for b in scan_bs if b.extra.get("segstats")] if not count_only else []
+    if seg_bs:
+        # chunk-start output positions of unhinted appenders (the
+        # reference's per-(step, chunk) segments, builders.py:256-272)
+        g.param("cgrain", "i64", ("cgrain",))
+        g.param("cgmask", "i64", ("cgmask",))
+        g.param("cbase", "i64", ("cbase",))
+        for b in seg_bs:
+            g.param(f"a{b.bid}_coff", "i64*", ("b", b.bid, "coff"))
 
     def elem_val(k, it):
         """Element value of iter k at item j (C arrays indexed by j)."""
@@ -1577,11 +1632,24 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
             for si, b in enumerate(scan_bs):
                 if not b.extra["staged"]:
                     out.append(f"    wpos{b.bid} += s_toff[{si}];")
+            if seg_bs:
+                # first item of this thread that starts a grain-wide chunk
+                out.append("    i64 sgn_ = (p.cgmask >= 0) ? ((p.cbase + t0) & p.cgmask) : ((p.cbase + t0) % p.cgrain);")
+                out.append("    sgn_ = sgn_ ? p.cgrain - sgn_ : 0;")
             out.append("#pragma unroll")
             out.append("    for (int j = 0; j < ITEMS; ++j) {")
             out.append("      const i64 li = t0 + j;")
             out.append("      if (li < n) {")
             out.append("        const i64 i = p.idx0 + li;")
+            if seg_bs:
+                out.append("        if (j == sgn_) {")
+                out.append("          const i64 ci_ = (p.cbase + li) / p.cgrain - p.cbase / p.cgrain;")
+                for b in seg_bs:
+                    si = scan_bs.index(b)
+                    pos = f"wpos{b.bid} + s_toff[{si}]" if b.extra["staged"] else f"wpos{b.bid}"
+                    out.append(f"          p.a{b.bid}_coff[ci_] = {pos};")
+                out.append("          sgn_ += p.cgrain;")
+                out.append("        }")
             out.extend(body_b)
             out.append("      }")
             out.append("    }")
@@ -1752,6 +1820,10 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
                       smem=dyn_smem, builders=g.bspecs, scan_bids=[b.bid for b in scan_bs],
                       merger_bids=[b.bid for b in merger_bs])
     plan.pipe_stage_bytes = pipe_stage_bytes if pipe else 0
+    plan.count_nodes = g.count_nodes
+    plan.stat_nodes = g.stat_nodes
+    plan.lit_nodes = {bid: set(v) for bid, v in g.lit_nodes.items()}
+    plan.seg_bids = [b.bid for b in seg_bs]
     return plan
 
 
@@ -1858,16 +1930,18 @@ def _regcache_lines(b, R, ind="    "):
         return " ".join(f"rv{B}_{r}_{f} = {op}<{CTYPE[kk]}>::f(rv{B}_{r}_{f}, dkv{B}_{f}[j]);"
                         for f, kk in enumerate(vks))
 
+    # the sentinel-valued key (all ones) never enters the cache: an unclaimed
+    # slot holds the sentinel too and would absorb its merges
     L = [f"{ind}#pragma unroll", f"{ind}for (int j = 0; j < ITEMS; ++j) {{",
-         f"{ind}  if (!dkf{B}[j]) continue;", f"{ind}  const u64 k_ = dkk{B}[j];"]
+         f"{ind}  if (!dkf{B}[j]) continue;", f"{ind}  const u64 k_ = dkk{B}[j];",
+         f"{ind}  if (k_ == WG_EMPTY_KEY) continue;"]
     chain = []
     for r in range(R):
         chain.append(f"if (rk{B}_{r} == k_) {{ {fold(r)} }}")
     claim = []
     for r in range(R):
         claim.append(f"if (rk{B}_{r} == WG_EMPTY_KEY) {{ rk{B}_{r} = k_; {fold(r)} }}")
-    L.append(f"{ind}  " + " else ".join(chain) + " else if (k_ != WG_EMPTY_KEY) { "
-             + " else ".join(claim) + " else { continue; } } else { continue; }")
+    L.append(f"{ind}  " + " else ".join(chain) + " else { " + " else ".join(claim) + " else { continue; } }")
     L.append(f"{ind}  dkf{B}[j] = false;")
     L.append(f"{ind}}}")
     return L
@@ -2211,7 +2285,7 @@ def _capture_val(g: Gen, name, ty, val):
 
 
 def static_plans(expr, env_types=None, externs=(), smem=True, lowcard=False, part=False,
-                 count_only=False):
+                 count_only=False, counting=False, segstats=False):
     """Yield a KernelPlan per ``for`` loop in a typed program, deriving the
     iteration, builder and capture specs from types alone."""
     from weldmill.expr import walk, free_variables as _fv
@@ -2255,6 +2329,8 @@ def static_plans(expr, env_types=None, externs=(), smem=True, lowcard=False, par
                         bs.extra["lowcard"] = lowcard
                 if isinstance(t.kind, VecMerger):
                     bs.mode = "global"
+                if isinstance(t.kind, VecBuilder) and segstats:
+                    bs.extra["segstats"] = True
                 return bs
             if isinstance(t, Struct):
                 return tuple(mk(f) for f in t.fields)
@@ -2272,7 +2348,7 @@ def static_plans(expr, env_types=None, externs=(), smem=True, lowcard=False, par
             if isinstance(ty, Function):
                 continue
             caps[name] = (ty, None)
-        plan = generate(node, iters, bstruct, caps, ext, "local")
+        plan = generate(node, iters, bstruct, caps, ext, "local", counting=counting)
         if count_only:
             # the count-only pre-pass of flatmap-shaped loops (fresh builder specs)
             if any(b.extra.get("unbounded") for b in plan.builders):

@@ -52,6 +52,14 @@ __device__ __forceinline__ void wg_raise(i64* err, i64 code, i64 info) {
   }
 }
 
+// count_evals (run.py:544-557): one node evaluation per active lane.  All
+// lanes reaching this statement bump the same counter, so the warp's active
+// lanes are counted with one atomic by the lowest of them.
+__device__ __forceinline__ void wg_count(unsigned long long* c) {
+  const unsigned m = __activemask();
+  if ((threadIdx.x & 31) == (unsigned)(__ffs(m) - 1)) atomicAdd(c, (unsigned long long)__popc(m));
+}
+
 // ---------------------------------------------------------------------------
 // Integer arithmetic: wraps at the width (computed unsigned, no UB).
 __device__ __forceinline__ i64 wg_add_i64(i64 a, i64 b) { return (i64)((u64)a + (u64)b); }

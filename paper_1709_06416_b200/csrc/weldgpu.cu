@@ -697,6 +697,34 @@ __global__ void __launch_bounds__(1024) k_exscan_i64(const int64_t* src, int64_t
   }
   if (threadIdx.x == 0) *total = s_carry;
 }
+// Reallocation accounting of an unhinted vecbuilder (builders.py:256-272):
+// coff[c] = output position where chunk c of the launch starts (coff[0] = 0),
+// *total = the launch's appends.  A segment of k appends starts at capacity
+// 16 and doubles while full: cap(k) = 16 << dbl(k), dbl(k) = ceil(log2(k)) - 4
+// for k > 16.  out[0..1] += sum dbl / sum cap over the interior chunks
+// 1..nch-2; out[2], out[3] = appends of the first and last chunk (segments a
+// neighbouring launch of the same loop may share; the host folds those).
+__global__ void k_seg_stats(const int64_t* coff, uint64_t nch, const int64_t* total, unsigned long long* out) {
+  unsigned long long d = 0, c = 0;
+  const int64_t tot = *total;
+  for (uint64_t i = 1 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i + 1 < nch; i += (uint64_t)gridDim.x * blockDim.x) {
+    const int64_t k = coff[i + 1] - coff[i];
+    if (k > 0) {
+      const int db = k <= 16 ? 0 : (64 - __clzll((unsigned long long)(k - 1))) - 4;
+      d += (unsigned long long)db;
+      c += 16ULL << db;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    d += __shfl_xor_sync(0xffffffffu, d, o);
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+  }
+  if ((threadIdx.x & 31) == 0 && (d | c)) { atomicAdd(out, d); atomicAdd(out + 1, c); }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    out[2] = (unsigned long long)((nch > 1 ? coff[1] : tot) - coff[0]);
+    out[3] = (unsigned long long)(nch > 1 ? tot - coff[nch - 1] : 0);
+  }
+}
 }  // namespace
 
 // ===========================================================================
@@ -1143,6 +1171,16 @@ int wg_order_key(uint64_t src, int kind, uint64_t n, uint64_t perm, uint64_t dst
   if (!n) return 0;
   { WG_PROF("k_order_key"); k_order_key<<<grid_for(n, 256), 256, 0, g_stream>>>((const void*)(uintptr_t)src, kind, n,
                                                        (const uint32_t*)(uintptr_t)perm, (uint64_t*)(uintptr_t)dst); }
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int wg_seg_stats(uint64_t coff, uint64_t nch, uint64_t total, uint64_t out) {
+  NEED_INIT();
+  CK(cudaMemsetAsync((void*)(uintptr_t)out, 0, 2 * sizeof(uint64_t), g_stream));
+  const unsigned grid = nch > 2 ? grid_for(nch - 2, 256) : 1;
+  { WG_PROF("k_seg_stats"); k_seg_stats<<<grid, 256, 0, g_stream>>>((const int64_t*)(uintptr_t)coff, nch,
+                                         (const int64_t*)(uintptr_t)total, (unsigned long long*)(uintptr_t)out); }
   CK(cudaGetLastError());
   return 0;
 }

@@ -138,6 +138,100 @@ class Ctx:
         self.launches = 0
         self._ticket = None
         self.dirty = False
+        # the reference's loop step (run.py:958-981): +1 before and after
+        # every claimed top-level loop; appender segments are keyed by
+        # (step, chunk) and the chunk is the loop row // grain_size
+        self.step = 0
+        self.cbase = 0
+        self.reallocs = 0
+        self._seg_pending = []
+        self.counting = bool(cfg.count_evals)
+        if self.counting:
+            self._cnt_ord = {}
+            self._cnt_text = []
+            self._cnt = []
+            self._cnt_nodes = []
+            self.ev = self._ev_counting
+
+    # -- count_evals (run.py:544-557, 1055-1060) ---------------------------
+    def count_program(self, root):
+        """Ordinals for every node the reference's _compile would wrap."""
+        from weldmill.printer import print_expr
+        for node in _compiled_nodes(root):
+            if id(node) not in self._cnt_ord:
+                self._cnt_ord[id(node)] = len(self._cnt)
+                self._cnt.append(0)
+                self._cnt_nodes.append(node)
+                self._cnt_text.append(print_expr(node))
+
+    def _ev_counting(self, e, env):
+        k = self._cnt_ord.get(id(e))
+        if k is not None:
+            self._cnt[k] += 1
+        return Ctx.ev(self, e, env)
+
+    def count_extra(self, e, times):
+        k = self._cnt_ord.get(id(e))
+        if k is not None:
+            self._cnt[k] += times
+
+    def node_evals(self):
+        totals = {}
+        for text, n in zip(self._cnt_text, self._cnt):
+            totals[text] = totals.get(text, 0) + n
+        return totals
+
+    # -- unhinted vecbuilder segments (builders.py:256-272) -----------------
+    def seg_add(self, b, key, m):
+        """m more appends into b's segment `key`: capacity doublings count as
+        reallocations, capacity growth is charged to the builder."""
+        if m <= 0:
+            return
+        old = b.segk.get(key, 0)
+        new = old + m
+        b.segk[key] = new
+        self.reallocs += _seg_dbl(new) - _seg_dbl(old)
+        grow = (_seg_cap(new) - _seg_cap(old)) * b.eb
+        if grow:
+            b.acct += grow
+            self.alloc(grow)
+
+    def seg_rows(self, b, lo, hi, k, claimed):
+        """Appends of a launch that merges exactly k times per loop row, rows
+        [lo, hi) of the loop."""
+        if hi <= lo or k <= 0:
+            return
+        if not claimed:
+            self.seg_add(b, (self.step, 0), (hi - lo) * k)
+            return
+        g = self.cfg.grain_size
+        c0, c1 = lo // g, (hi - 1) // g
+        if c0 == c1:
+            self.seg_add(b, (self.step, c0), (hi - lo) * k)
+            return
+        self.seg_add(b, (self.step, c0), ((c0 + 1) * g - lo) * k)
+        mid = c1 - c0 - 1
+        if mid:
+            self.reallocs += mid * _seg_dbl(g * k)
+            grow = mid * _seg_cap(g * k) * b.eb
+            b.acct += grow
+            self.alloc(grow)
+        self.seg_add(b, (self.step, c1), (hi - c1 * g) * k)
+
+    def settle_segs(self):
+        """Apply the device-side chunk statistics of scan-mode launches."""
+        pend, self._seg_pending = self._seg_pending, []
+        for b, step, k0, k1, out in pend:
+            w = np.zeros(4, dtype=np.uint64)
+            rt.d2h(w.ctypes.data, out.ptr, 32)
+            self.reallocs += int(w[0])
+            grow = int(w[1]) * b.eb
+            if grow:
+                b.acct += grow
+                self.alloc(grow)
+            self.seg_add(b, k0, int(w[2]))
+            if k1 != k0:
+                self.seg_add(b, k1, int(w[3]))
 
     # -- memory accounting (run.py:208-228) --------------------------------
     def alloc(self, n):
@@ -148,11 +242,15 @@ class Ctx:
             raise MemoryLimitExceeded(f"engine memory {self.live} bytes exceeds limit {self.cfg.memory_limit}")
 
     def free(self, n):
+        if self._seg_pending:
+            self.settle_segs()
         self.live -= n
 
-    def materialized(self, obj, nbytes):
+    def materialized(self, obj, nbytes, extra=(0, 0)):
+        """extra = (objects, bytes) allocated earlier that live or die with
+        obj (literal vectors a vecbuilder[vec[T]] result holds)."""
         self.alloc(nbytes)
-        self.registry.append((obj, nbytes))
+        self.registry.append((obj, nbytes + extra[1], 1 + extra[0]))
         self.allocs += 1
 
     def ticket(self):
@@ -263,7 +361,8 @@ class Ctx:
     def ev_MakeVector(self, e, env):
         items = [self.ev(x, env) for x in e.items]
         hv = HostVec(e.ty, items)
-        self.materialized(hv, payload_bytes(e.ty, items) if is_flat(e.ty.elem) else 16)
+        self.materialized(hv, payload_bytes(e.ty, items) if is_flat(e.ty.elem)
+                          else 16 + sum(_value_bytes(e.ty.elem, x) for x in items))
         return hv
 
     def ev_Len(self, e, env):
@@ -296,15 +395,19 @@ class Ctx:
         upd = self.ev(e.update, env)
         limit = self.cfg.max_iterations
         steps = 0
-        while True:
-            env2 = dict(upd.env)
-            env2[upd.lam.params[0].name] = state
-            state, go = self.ev(upd.lam.body, env2)
-            steps += 1
-            if not go:
-                return state
-            if steps >= limit:
-                raise IterationLimit(f"iterate exceeded {limit} iterations")
+        try:
+            while True:
+                env2 = dict(upd.env)
+                env2[upd.lam.params[0].name] = state
+                state, go = self.ev(upd.lam.body, env2)
+                steps += 1
+                if not go:
+                    return state
+                if steps >= limit:
+                    raise IterationLimit(f"iterate exceeded {limit} iterations")
+        finally:
+            if self.counting and not isinstance(e.update, Lambda):
+                self.count_extra(e.update, steps - 1)    # run.py:875-882: evaluated per step
 
     def ev_ExternCall(self, e, env):
         fn = self.externs.get(e.name)
@@ -334,6 +437,8 @@ class Ctx:
             else:
                 b = AppenderDev(kind, None, hint)
             b.acct = hint * _slot_bytes(kind.elem) if hint is not None else 0
+            b.eb = _slot_bytes(kind.elem)
+            b.segk = {} if hint is None else None
             return b
         if isinstance(kind, Merger):
             return MergerDev(kind)
@@ -362,6 +467,8 @@ class Ctx:
             b.pending.extend(v)
         else:
             b.pending.append(v)
+        if getattr(b, "segk", None) is not None:
+            self.seg_add(b, (self.step, 0), len(v) if isinstance(e.value.ty, Simd) else 1)
         b.pending_ty = e.value.ty.kind if isinstance(e.value.ty, Simd) else e.value.ty
         if isinstance(b.pending_ty, str):
             b.pending_ty = Scalar(b.pending_ty)
@@ -408,6 +515,8 @@ class Ctx:
             self.check_device()
             return b.read()
         if isinstance(kind, VecBuilder):
+            if self._seg_pending:
+                self.settle_segs()
             if b.kinds is None:
                 raise DeviceUnsupported(f"vecbuilder[{kind.elem}] (nested element types) on the device")
             if not b.segments:
@@ -424,7 +533,7 @@ class Ctx:
                 rt.call("wg_iota_i64", offs.ptr, nv + 1, L)
                 from .columns import ListLayout, layout_from_cols
                 out = DVec(kind.elem, nv, ListLayout(offs, layout_from_cols(kind.elem.elem, cols), n))
-                self.materialized(out, 16 + nv * 16 + n * _slot_bytes(kind.elem.elem))
+                self.materialized(out, 16 + nv * 16 + n * _slot_bytes(kind.elem.elem), getattr(b, "lit_acct", (0, 0)))
                 return out
             out = dvec_from_cols(kind.elem, n, cols)
             self.materialized(out, 16 + n * _slot_bytes(kind.elem))
@@ -444,6 +553,7 @@ class Ctx:
             self.materialized(d, 16 + d.n * (16 + _slot_bytes(kind.key) + _slot_bytes(kind.value)))
             return d
         if isinstance(kind, GroupBuilder):
+            self.free(getattr(b, "acct", 0))     # GroupBuilderState.result releases its rows (builders.py:480)
             g = finish_groups(b, Dict(kind.key, Vec(kind.value)))
             self.materialized(g, 16 + g.n * (16 + _slot_bytes(kind.key) + 16) + g.vals.n * _slot_bytes(kind.value))
             return g
@@ -484,14 +594,18 @@ class Ctx:
             kcols, _ = kb.concat()
             perm = sort_perm(kcols, n)
             out = dvec_from_cols(dv.elem, n, gather_cols(dv.cols, perm, n))
-        self.materialized(out, 16 + n * _slot_bytes(dv.elem))
+        self.materialized(out, payload_bytes_dvec(Vec(dv.elem), out))
         return out
 
     # -- loops ---------------------------------------------------------------------
     def ev_For(self, e, env):
         return self.run_loop(e, env)
 
-    def run_loop(self, e, env, count_traversal=True):
+    def run_loop(self, e, env, count_traversal=True, part=None):
+        """Run one `for` loop.  count_traversal=False marks a synthetic loop
+        (pending merges, dict regrowth, sort keys).  part=(lo, total, first,
+        last): this launch covers iterations [lo, lo + count) of a loop of
+        `total` iterations run in slices (the streaming path)."""
         _claim_loop_id(e)
         datas, specs, windows = [], [], []
         count = None
@@ -539,9 +653,32 @@ class Ctx:
         builders = self.ev(e.builders, env)
         if count == 0:
             return builders
-        if count_traversal:
+        # synthetic loops (pending merges, dict regrowth, sort keys) are not
+        # loops of the program: no traversal, no step, no segment accounting
+        if part is not None:
+            lo, total, first, last = part
+            synthetic = False
+        else:
+            lo, total, first, last = 0, count, True, True
+            synthetic = not count_traversal
+        if first and not synthetic:
             self.traversals += len(e.iters)
+        claimed = not synthetic and total > 1
+        if claimed and first:
+            self.step += 1
+        saved = (self._synthetic, self._claimed, self.cbase)
+        self._synthetic, self._claimed, self.cbase = synthetic, claimed, lo
+        try:
+            return self._run_loop(e, env, builders, specs, datas, windows, count)
+        finally:
+            self._synthetic, self._claimed, self.cbase = saved
+            if claimed and last:
+                self.step += 1
 
+    _synthetic = False
+    _claimed = False
+
+    def _run_loop(self, e, env, builders, specs, datas, windows, count):
         lam = e.func
         lenv = env
         if not isinstance(lam, Lambda):
@@ -549,6 +686,8 @@ class Ctx:
             if not isinstance(f, Closure):
                 raise EvalError("loop body is not a function")
             lam, lenv = f.lam, f.env
+            if self.counting:
+                self.count_extra(e.func, count - 1)    # run.py:875-882 evaluates it per iteration
         blist = []
         _collect_builders(builders, blist)
         for b in blist:
@@ -591,12 +730,13 @@ class Ctx:
                 if est * 2 > st.cap:
                     self._dict_regrow_(st, 0, want=est)
             rest = [(s0 + SKETCH_ROWS * st_, st_) for s0, st_ in windows]
-            saved = self.idx0
-            self.idx0 = saved + SKETCH_ROWS
+            saved = self.idx0, self.cbase
+            self.idx0 = saved[0] + SKETCH_ROWS
+            self.cbase = saved[1] + SKETCH_ROWS
             try:
                 self._launch_loop(e, lam, specs, datas, rest, count - SKETCH_ROWS, builders, captures, strategy)
             finally:
-                self.idx0 = saved
+                self.idx0, self.cbase = saved
             return builders
         self._launch_loop(e, lam, specs, datas, windows, count, builders, captures, strategy)
         return builders
@@ -605,12 +745,13 @@ class Ctx:
         bstruct, bmap = _bspecs(builders, strategy, count, loop_id=id(e), assume_lowcard=assume_lowcard)
         # The expression identities fix every type in the loop; only the
         # runtime choices (strides, alignment, builder modes, externs) vary.
-        key = (id(e), id(lam), tuple((s.strided, s.aligned) for s in specs), _bsig(bstruct), self._ext_key)
+        counting = self.counting and self._counts_body(lam)
+        key = (id(e), id(lam), tuple((s.strided, s.aligned) for s in specs), _bsig(bstruct), self._ext_key, counting)
         with _plan_lock:
             cached = _plan_cache.get(key)
         if cached is None:
             plan = generate(e if lam is e.func else _with_func(e, lam), specs, bstruct, captures,
-                            self.externs, strategy)
+                            self.externs, strategy, counting=counting)
             plan.key_id = id(e)
             kern = rt.get_kernel(plan.source, plan.name)
             cached = (plan, kern, e, lam)
@@ -635,6 +776,40 @@ class Ctx:
                     _plan_cache[ckey] = cc
             sizes = self._count_pass(cc[0], cc[1], count, datas, windows, bmap, captures)
         self.launch(plan, kern, count, datas, windows, builders, bmap, captures, sizes=sizes)
+
+    def _body_stats(self, plan, bmap):
+        """EvalStats events of the loop body (nested loops' traversals,
+        literal vectors materialised per execution, run.py:781-789, 948):
+        counted on the device, accounted here in the reference's terms.  A
+        literal merged into a vecbuilder[vec[T]] survives in its result."""
+        arr = np.zeros(len(plan.stat_nodes), dtype=np.uint64)
+        rt.d2h(arr.ctypes.data, self._scnt_buf.ptr, arr.nbytes)
+        keep = {}
+        for bid, ids in plan.lit_nodes.items():
+            for i in ids:
+                keep[i] = bmap[bid]
+        for (what, node), c in zip(plan.stat_nodes, arr):
+            c = int(c)
+            if not c:
+                continue
+            if what == "trav":
+                self.traversals += c * len(node.iters)
+                continue
+            nbytes = c * payload_bytes(node.ty, [0] * len(node.items)) if is_flat(node.ty.elem) else None
+            if nbytes is None:
+                raise DeviceUnsupported("vector literal of non-scalar elements in a loop body")
+            self.alloc(nbytes)
+            self.allocs += c
+            owner = keep.get(id(node))
+            if owner is not None:
+                owner.lit_acct = getattr(owner, "lit_acct", (0, 0))
+                owner.lit_acct = (owner.lit_acct[0] + c, owner.lit_acct[1] + nbytes)
+            else:
+                self.registry.append((None, nbytes, c))
+
+    def _counts_body(self, lam):
+        from weldmill.expr import walk
+        return any(id(x) in self._cnt_ord for x in walk(lam.body))
 
     def _count_pass(self, plan, kern, count, datas, windows, bmap, captures):
         """Launch the count-only kernel.  Returns {builder id: appends}."""
@@ -676,23 +851,38 @@ class Ctx:
         self.tasks += grid
         # per-launch builder resources
         res = {}
+        segstats = []
+        segacct = not self._synthetic
         for b in plan.builders:
             st = bmap[b.bid]
             if isinstance(b.kind, (VecBuilder, GroupBuilder)):
+                seg_model = segacct and getattr(st, "segk", None) is not None
                 if b.mode == "direct":
                     per = b.k * b.extra.get("nested_len", 1)
                     if b.extra.get("nested"):
                         st.nested_len = b.extra["nested_len"]
                     seg = st.new_segment(count * per, True)
                     res[b.bid] = seg
-                    self._acct_append(st, count * per)
+                    if seg_model:
+                        self.seg_rows(st, self.cbase, self.cbase + count, b.k, self._claimed)
+                    elif getattr(st, "segk", None) is None:
+                        self._acct_append(st, count * per)
                 elif b.mode == "scan":
                     cap = sizes[b.bid] if (b.k is None or (sizes and b.bid in sizes)) else count * b.k
                     seg = st.new_segment(cap, False)
                     status = rt.alloc(8 * max(ntiles, 1))
                     rt.memset(status.ptr, 0, 8 * max(ntiles, 1))
                     res[b.bid] = (seg, status)
-                    self._acct_append(st, cap)
+                    if b.bid in plan.seg_bids:
+                        g_ = self.cfg.grain_size
+                        c0, c1 = self.cbase // g_, (self.cbase + count - 1) // g_
+                        coff = rt.alloc(8 * (c1 - c0 + 1))
+                        rt.memset(coff.ptr, 0, 8 * (c1 - c0 + 1))
+                        res[("coff", b.bid)] = coff
+                        if seg_model:
+                            segstats.append((st, seg, coff, c0, c1))
+                    elif getattr(st, "segk", None) is None:
+                        self._acct_append(st, cap)
             elif isinstance(b.kind, DictMerger):
                 st.ensure(count * max(1, b.extra.get("maxm", 1)), hint_key=(plan.key_id, b.bid))
                 if b.extra.get("part") and b.extra.get("deferred"):
@@ -703,6 +893,12 @@ class Ctx:
             tilectr = rt.alloc(8)
             rt.memset(tilectr.ptr, 0, 8)
 
+        if plan.count_nodes:
+            self._cnt_buf = rt.alloc(8 * len(plan.count_nodes))
+            rt.memset(self._cnt_buf.ptr, 0, 8 * len(plan.count_nodes))
+        if plan.stat_nodes:
+            self._scnt_buf = rt.alloc(8 * len(plan.stat_nodes))
+            rt.memset(self._scnt_buf.ptr, 0, 8 * len(plan.stat_nodes))
         packer = getattr(plan, "_packer", None)
         if packer is None:
             # every parameter is one 8-byte word (f64 or a masked integer)
@@ -722,6 +918,21 @@ class Ctx:
         kern.launch(grid, plan.block, blob, smem)
         self.launches += 1
         self.dirty = True
+        for st, seg, coff, c0, c1 in segstats:
+            out = rt.alloc(32)
+            rt.call("wg_seg_stats", coff.ptr, c1 - c0 + 1, seg.total_buf.ptr, out.ptr)
+            self.launches += 1
+            if self._claimed:
+                self._seg_pending.append((st, self.step, (self.step, c0), (self.step, c1), out))
+            else:
+                self._seg_pending.append((st, self.step, (self.step, 0), (self.step, 0), out))
+        if plan.count_nodes:
+            arr = np.zeros(len(plan.count_nodes), dtype=np.uint64)
+            rt.d2h(arr.ctypes.data, self._cnt_buf.ptr, arr.nbytes)
+            for node, c in zip(plan.count_nodes, arr):
+                self.count_extra(node, int(c))
+        if plan.stat_nodes and not self._synthetic:
+            self._body_stats(plan, bmap)
         # partitioned dictmergers: fold every bucket, merge into the HBM table
         for b in plan.builders:
             if isinstance(b.kind, DictMerger) and b.extra.get("part") and b.extra.get("deferred"):
@@ -837,6 +1048,17 @@ class Ctx:
             return tilectr.ptr
         if k0 == "pipe_stages":
             return 0
+        if k0 == "cnt":
+            return self._cnt_buf.ptr
+        if k0 == "scnt":
+            return self._scnt_buf.ptr
+        if k0 == "cgrain":
+            return self.cfg.grain_size
+        if k0 == "cgmask":
+            g_ = self.cfg.grain_size
+            return g_ - 1 if g_ & (g_ - 1) == 0 else -1
+        if k0 == "cbase":
+            return self.cbase
         if k0 == "itcol":
             _, k, l = key
             d = datas[k]
@@ -899,6 +1121,8 @@ class Ctx:
                     return r[1].ptr if r[1] is not None else 0
                 if what == "total":
                     return r[0].total_buf.ptr
+                if what == "coff":
+                    return res[("coff", bid)].ptr
             if isinstance(st, VecMergerDev):
                 if what == "len":
                     return st.n
@@ -1028,10 +1252,33 @@ def _slot_bytes(t):
 
 
 def payload_bytes_dvec(ty, v):
-    fixed = _fixed(ty.elem)
-    if fixed is not None:
-        return 16 + v.n * fixed
-    return 16 + v.n * 16
+    """weldmill's payload_bytes (builders.py:59-82) of a device vector:
+    16-byte header plus contents, nested vectors counted with their own
+    headers and elements."""
+    return 16 + _elem_bytes(ty.elem, v.n, v.layout)
+
+
+def _value_bytes(t, v):
+    """payload_bytes of a runtime value that may hold device vectors."""
+    if isinstance(v, DVec):
+        return payload_bytes_dvec(t, v)
+    if isinstance(v, HostVec):
+        if isinstance(v.payload, list):
+            return payload_bytes(t, v.payload)
+        return payload_bytes_dvec(t, v.dev())
+    if isinstance(t, Struct):
+        return sum(_value_bytes(f, x) for f, x in zip(t.fields, v))
+    return payload_bytes(t, v)
+
+
+def _elem_bytes(t, n, lay):
+    if isinstance(t, Scalar):
+        return n * SIZE[t.kind]
+    if isinstance(t, Struct):
+        return sum(_elem_bytes(f, n, l) for f, l in zip(t.fields, lay))
+    if isinstance(t, Vec):
+        return n * 16 + _elem_bytes(t.elem, lay.total, lay.child)
+    raise EvalError(f"no byte accounting for values of type {t}")
 
 
 def _fixed(t):
@@ -1130,6 +1377,10 @@ def _bspecs(builders, strategy, count, loop_id=None, assume_lowcard=False):
                     bs.mode = "global"
             else:
                 bs.mode = "global"
+        if isinstance(v, AppenderDev) and isinstance(v.kind, VecBuilder) and getattr(v, "segk", None) is not None:
+            # unhinted vecbuilder: scan-mode kernels record where each
+            # grain-wide chunk's appends start (reallocation accounting)
+            bs.extra["segstats"] = True
         if isinstance(v, (AppenderDev,)) and v.kinds is None:
             raise DeviceUnsupported(f"vecbuilder[{v.kind.elem}] (nested element types) on the device")
         return bs
@@ -1144,7 +1395,7 @@ def _bsig(bs):
     if isinstance(bs, tuple):
         return tuple(_bsig(x) for x in bs)
     return (bs.mode, bs.extra.get("nbins"), bs.extra.get("smem_slots"), bs.extra.get("lowcard"),
-            bs.extra.get("part"), bs.extra.get("pbits"))
+            bs.extra.get("part"), bs.extra.get("pbits"), bs.extra.get("segstats"))
 
 
 def _type_of(v, lam, name):
@@ -1198,7 +1449,7 @@ def _collect_ids(v, acc):
     if isinstance(v, tuple):
         for x in v:
             _collect_ids(x, acc)
-    elif isinstance(v, (DVec, DDict, DGroups, HostVec)):
+    elif isinstance(v, (DVec, DDict, DGroups, HostVec, np.ndarray)):
         acc.add(id(v))
 
 
@@ -1222,6 +1473,8 @@ def evaluate(e, env=None, config=None, externs=None, *, result="python", idx0=0,
     ctx = Ctx(cfg, externs, idx0=idx0)
     if _ctx_out is not None:
         _ctx_out.append(ctx)
+    if ctx.counting:
+        ctx.count_program(e)
     frame = {}
     for name, v in (env or {}).items():
         payload = v.data if isinstance(v, Value) else v
@@ -1235,44 +1488,116 @@ def evaluate(e, env=None, config=None, externs=None, *, result="python", idx0=0,
             frame[name] = HostVec(t, payload) if isinstance(t, Vec) else payload
         else:
             frame[name] = payload
-    if result == "numpy" and STREAMING:
+    cand = None
+    if result == "numpy" and STREAMING and not ctx.counting:
         cand = _stream_candidate(e, frame)
-        if cand is not None:
-            payload = _stream_evaluate(ctx, e, frame, cand)
-            stats = EvalStats()
-            stats.vector_traversals = ctx.traversals
-            stats.tasks_created = ctx.tasks
-            return Value(e.ty, payload), stats
-    try:
-        val = ctx.ev(e, frame)
-    except _DU as exc:
-        if isinstance(exc, EvalError):
-            raise
-        raise DeviceUnsupported(str(exc)) from None
-    ctx.check_device()
-    if result == "device":
-        payload = val
-    elif result == "numpy":
-        payload = _numpy_tree(val, e.ty)
+    if cand is not None:
+        val = payload = _stream_evaluate(ctx, e, frame, cand)
     else:
-        payload = to_host_payload(val, e.ty)
+        try:
+            val = ctx.ev(e, frame)
+        except _DU as exc:
+            if isinstance(exc, EvalError):
+                raise
+            raise DeviceUnsupported(str(exc)) from None
+        ctx.check_device()
+        if result == "device":
+            payload = val
+        elif result == "numpy":
+            payload = _numpy_tree(val, e.ty)
+        else:
+            payload = to_host_payload(val, e.ty)
 
+    ctx.settle_segs()
     stats = EvalStats()
     stats.vector_traversals = ctx.traversals
     stats.vector_allocations = ctx.allocs
+    stats.vecbuilder_reallocations = ctx.reallocs
     stats.tasks_created = ctx.tasks
+    if ctx.counting:
+        stats.node_evals = ctx.node_evals()
     reachable = set()
     _collect_ids(val, reachable)
     kept = 0
-    for obj, nbytes in ctx.registry:
-        if id(obj) in reachable:
-            kept += 1
+    for obj, nbytes, cnt in ctx.registry:
+        if obj is not None and id(obj) in reachable:
+            kept += cnt
         else:
             ctx.free(nbytes)
     stats.peak_bytes = ctx.peak
     stats.live_bytes = ctx.live
     stats.intermediate_allocations = stats.vector_allocations - kept
     return Value(e.ty, payload), stats
+
+
+def _seg_dbl(k):
+    """Capacity doublings of a segment holding k appends (16, 32, 64, ...)."""
+    return 0 if k <= 16 else (k - 1).bit_length() - 4
+
+
+def _seg_cap(k):
+    return 0 if k <= 0 else 16 << _seg_dbl(k)
+
+
+def _compiled_nodes(root):
+    """Every node weldmill's _compile wraps with a counter (run.py:544-880):
+    all nodes except lambda literals in function position (a loop's body,
+    iterate's update, sort's key), whose bodies are compiled directly."""
+    out = []
+    stack = [root]
+
+    def fn_pos(f):
+        stack.append(f.body if isinstance(f, Lambda) else f)
+
+    while stack:
+        e = stack.pop()
+        out.append(e)
+        if isinstance(e, For):
+            for it in e.iters:
+                stack.extend(x for x in (it.data, it.start, it.end, it.stride) if x is not None)
+            stack.append(e.builders)
+            fn_pos(e.func)
+        elif isinstance(e, Iterate):
+            stack.append(e.init)
+            fn_pos(e.update)
+        elif isinstance(e, Sort):
+            stack.append(e.vec)
+            fn_pos(e.key)
+        elif isinstance(e, Let):
+            stack.extend((e.value, e.body))
+        elif isinstance(e, Lambda):
+            stack.append(e.body)
+        elif isinstance(e, Apply):
+            stack.append(e.func)
+            stack.extend(e.args)
+        elif isinstance(e, BinaryOp):
+            stack.extend((e.lhs, e.rhs))
+        elif isinstance(e, UnaryOp):
+            stack.append(e.operand)
+        elif isinstance(e, (If, BitSelect)):
+            stack.extend((e.cond, e.on_true, e.on_false))
+        elif isinstance(e, Lookup):
+            stack.extend((e.coll, e.index))
+        elif isinstance(e, FieldAccess):
+            stack.append(e.base)
+        elif isinstance(e, Len):
+            stack.append(e.coll)
+        elif isinstance(e, ToVec):
+            stack.append(e.mapping)
+        elif isinstance(e, (MakeStruct, MakeVector)):
+            stack.extend(e.items)
+        elif isinstance(e, NewBuilder):
+            if e.arg is not None:
+                stack.append(e.arg)
+        elif isinstance(e, Merge):
+            stack.extend((e.builder, e.value))
+        elif isinstance(e, Result):
+            stack.append(e.builder)
+        elif isinstance(e, (Broadcast, CastScalar)):
+            stack.append(e.value)
+        elif isinstance(e, ExternCall):
+            stack.extend(e.args)
+    return out
 
 
 def _infer_free_type(e, name):
@@ -1487,7 +1812,7 @@ def _stream_evaluate(ctx, e, frame, cand):
                 f2[it.data.name] = dvec_from_cols(hv.ty.elem, m, [Col(cc.ptr, kk, cc.owner) for cc, kk in zip(cols, ks)])
             f2["__wg_sb"] = bval
             ctx.idx0 = lo // 4 if simd else lo
-            ctx.run_loop(loop2, f2, count_traversal=(c == 0))
+            ctx.run_loop(loop2, f2, part=(ctx.idx0, n // 4 if simd else n, c == 0, c == nch - 1))
             ev_k[c].record()
             # copy out (stream 2): this chunk's appended rows
             rt.stream_select(2)
@@ -1524,14 +1849,23 @@ def _stream_evaluate(ctx, e, frame, cand):
         st.consume()
         if isinstance(st, MergerDev):
             return st.read()
+        # the reference's VecBuilderState.result: release the segments, then
+        # account the materialised vector (builders.py:274-283)
+        ctx.settle_segs()
+        ctx.free(st.acct)
         if outs.get(id(st)) is not None and all(s.n is not None for s in st.segments):
             o = outs[id(st)]
             if id(st) in scan_off:
                 o = [a[:scan_off[id(st)]] for a in o]
-            return o[0] if isinstance(st.kind.elem, Scalar) else tuple(o)
-        cols, tot = st.concat() if st.segments else ([Col.alloc(k, 0) for k in st.kinds], 0)
-        from .columns import to_numpy
-        return to_numpy(dvec_from_cols(st.kind.elem, tot, cols))
+            r = o[0] if isinstance(st.kind.elem, Scalar) else tuple(o)
+            nr = len(o[0])
+        else:
+            cols, tot = st.concat() if st.segments else ([Col.alloc(k, 0) for k in st.kinds], 0)
+            from .columns import to_numpy
+            r = to_numpy(dvec_from_cols(st.kind.elem, tot, cols))
+            nr = tot
+        ctx.materialized(r if not isinstance(r, tuple) else r[0], 16 + nr * st.eb)
+        return r
 
     it_ = iter(blist)
     try:
@@ -1566,7 +1900,7 @@ def _stream_tail(ctx, tail, frame, hvs, kinds, leaves_np, n4, n, bval, blist, ou
             cols.append(Col(buf.ptr - n4 * SIZE[kk], kk, buf))
         f2[it.data.name] = dvec_from_cols(hv.ty.elem, n, cols)
     seen = {id(st): len(st.segments) for st in blist if isinstance(st, AppenderDev)}
-    ctx.run_loop(t[1], f2, count_traversal=False)
+    ctx.run_loop(t[1], f2)
     rt.sync()
     for st in blist:
         if not isinstance(st, AppenderDev) or outs.get(id(st)) is None:

@@ -146,6 +146,30 @@ def test_iterate_in_loop_bodies_lowers_and_compiles():
             assert runtime.compile_check(p.source) > 0
 
 
+def test_stats_instrumented_kernels_compile():
+    """count_evals kernels (a warp-aggregated counter per body node) and the
+    chunk-offset records of unhinted scan appenders (reallocation
+    accounting) lower and compile for sm_100a: corpus sample, flatmap and
+    iterate bodies."""
+    from helpers import load_golden
+    from paper_1709_06416_b200 import codegen, runtime
+    srcs = [(p["source"], p["inputs"]) for p in CORPUS[::11]]
+    srcs += [(c["source"], c["inputs"]) for c in load_golden("flatmap.json")["cases"][::40]]
+    srcs += [(c["source"], c["inputs"]) for c in load_golden("iterate.json")["cases"][::40]]
+    seen = set()
+    n_count = n_seg = 0
+    for src, inputs in srcs:
+        for pl in codegen.static_plans(_tree(src, inputs, "O3"), counting=True, segstats=True):
+            if pl.source in seen:
+                continue
+            seen.add(pl.source)
+            n_count += "wg_count(p.cnt" in pl.source
+            n_seg += bool(pl.seg_bids)
+            assert len(pl.count_nodes) > 0
+            assert runtime.compile_check(pl.source) > 0, src
+    assert n_count > 10 and n_seg >= 3, (n_count, n_seg)
+
+
 def _typed_with_externs(src, inputs, names):
     import paper_1709_06416_b200  # noqa: F401
     from weldmill.optim import OptLevel, optimize
