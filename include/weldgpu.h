@@ -107,6 +107,10 @@ int wg_exclusive_scan_i64(uint64_t src, uint64_t dst, uint64_t n, uint64_t total
  * capacities over interior chunks 1..nch-2, then the first and last chunk's
  * append counts. */
 int wg_seg_stats(uint64_t coff, uint64_t nch, uint64_t total, uint64_t out);
+/* the +0.0 key of a sorted float dictionary key column (width 4 or 8) becomes
+ * -0.0 when a -0.0 key was merged first (DictMergerState._upsert keeps the
+ * first-inserted key object, builders.py:346-351) */
+int wg_neg_zero(uint64_t col, uint64_t n, int width);
 int wg_sort_pairs(uint64_t keys_in, uint64_t vals_in, uint64_t keys_out, uint64_t vals_out, uint64_t n, int begin_bit,
                   int end_bit);
 int wg_gather(uint64_t src, uint64_t perm, uint64_t dst, uint64_t n, int width);

@@ -484,7 +484,14 @@ def finish_groups(g: GroupDev, dict_ty):
         return DGroups(dict_ty, keys, offs, dvec_from_cols(dict_ty.value.elem, 0, vcols))
     words = []
     for c in kcols:
-        if SIZE[c.kind] == 8:
+        if c.kind in (F32, F64):
+            # float keys compare as the reference's dict keys do: -0.0 == 0.0
+            # and NaN with NaN (order_key words); each run keeps its first
+            # row's key, i.e. the first-inserted key object
+            wc = Col.alloc(I64, n)
+            rt.call("wg_order_key", c.ptr, KIND_CODE[c.kind], n, 0, wc.ptr)
+            words.append(wc)
+        elif SIZE[c.kind] == 8:
             words.append(c)
         else:
             wc = Col.alloc(I64, n)

@@ -986,6 +986,11 @@ class Gen:
         key, val = v.items
         kks = leaves(kind.key)
         vks = leaves(kind.value)
+        if len(kks) == 1 and kks[0] in (F32, F64):
+            x = _flat(key)[0].c
+            zr = self.param(f"d{b.bid}_zrow", "unsigned long long*", ("b", b.bid, "zrow"))
+            neg = f"(__double_as_longlong({x}) < 0)" if kks[0] == F64 else f"(__float_as_int({x}) < 0)"
+            self.emit(f"if ({x} == 0) wg_zero_row({zr}, {neg}, i);")
         words = self._key_words(kks, _flat(key))
         if b.extra.get("deferred"):
             # one pending merge per item; applied after the item loop

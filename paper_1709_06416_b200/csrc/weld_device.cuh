@@ -523,10 +523,24 @@ template <> __device__ __forceinline__ u64 wg_okey<double>(double v) {
 }
 template <> __device__ __forceinline__ u64 wg_okey<float>(float v) { return wg_okey<double>((double)v); }
 
+// First row (loop index) merging a -0.0 (z[1]) / +0.0 (z[0]) key into a
+// one-float-field dictmerger: the reference keeps the first-inserted key
+// object of the pair -0.0 == 0.0 (Python dict semantics).
+__device__ __forceinline__ void wg_zero_row(unsigned long long* z, bool neg, i64 row) {
+  unsigned long long* w = z + (neg ? 1 : 0);
+  if ((unsigned long long)row < *(volatile unsigned long long*)w) atomicMin(w, (unsigned long long)row);
+}
+
 // Canonical key words.  -0.0 and 0.0 are one dictionary key in the
 // reference (Python dict semantics); they map to the same word here.
-__device__ __forceinline__ u64 wg_key_f64(double v) { return v == 0.0 ? 0ULL : (u64)__double_as_longlong(v); }
-__device__ __forceinline__ u64 wg_key_f32(float v) { return v == 0.0f ? 0ULL : (u64)(u32)__float_as_int(v); }
+// Every NaN is one key too: the NaNs a program produces (0.0 / 0.0, inf -
+// inf, ...) are one float object in the reference and compare as one key.
+__device__ __forceinline__ u64 wg_key_f64(double v) {
+  return v == 0.0 ? 0ULL : (v != v ? 0x7ff8000000000000ULL : (u64)__double_as_longlong(v));
+}
+__device__ __forceinline__ u64 wg_key_f32(float v) {
+  return v == 0.0f ? 0ULL : (v != v ? 0x7fc00000ULL : (u64)(u32)__float_as_int(v));
+}
 
 // ---------------------------------------------------------------------------
 // Contiguous per-thread column access (ITEMS consecutive elements): 16-byte

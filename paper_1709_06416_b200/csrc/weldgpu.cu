@@ -697,6 +697,14 @@ __global__ void __launch_bounds__(1024) k_exscan_i64(const int64_t* src, int64_t
   }
   if (threadIdx.x == 0) *total = s_carry;
 }
+// The canonical +0.0 key of a float dictionary column becomes -0.0 (the
+// first-inserted key object, builders.py:346-351).
+__global__ void k_neg_zero(void* col, uint64_t n, int width) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    if (width == 8) { uint64_t* c = (uint64_t*)col; if (c[i] == 0) c[i] = 0x8000000000000000ULL; }
+    else { uint32_t* c = (uint32_t*)col; if (c[i] == 0) c[i] = 0x80000000U; }
+  }
+}
 // Reallocation accounting of an unhinted vecbuilder (builders.py:256-272):
 // coff[c] = output position where chunk c of the launch starts (coff[0] = 0),
 // *total = the launch's appends.  A segment of k appends starts at capacity
@@ -1171,6 +1179,14 @@ int wg_order_key(uint64_t src, int kind, uint64_t n, uint64_t perm, uint64_t dst
   if (!n) return 0;
   { WG_PROF("k_order_key"); k_order_key<<<grid_for(n, 256), 256, 0, g_stream>>>((const void*)(uintptr_t)src, kind, n,
                                                        (const uint32_t*)(uintptr_t)perm, (uint64_t*)(uintptr_t)dst); }
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int wg_neg_zero(uint64_t col, uint64_t n, int width) {
+  NEED_INIT();
+  if (!n) return 0;
+  { WG_PROF("k_neg_zero"); k_neg_zero<<<grid_for(n, 256), 256, 0, g_stream>>>((void*)(uintptr_t)col, n, width); }
   CK(cudaGetLastError());
   return 0;
 }

@@ -550,6 +550,7 @@ class Ctx:
             if d is None:
                 self._settle(b)
                 d = finish_dict(b, Dict(kind.key, kind.value))
+            _first_zero_sign(b, d)
             self.materialized(d, 16 + d.n * (16 + _slot_bytes(kind.key) + _slot_bytes(kind.value)))
             return d
         if isinstance(kind, GroupBuilder):
@@ -885,6 +886,14 @@ class Ctx:
                         self._acct_append(st, cap)
             elif isinstance(b.kind, DictMerger):
                 st.ensure(count * max(1, b.extra.get("maxm", 1)), hint_key=(plan.key_id, b.bid))
+                if len(st.kks) == 1 and st.kks[0] in (F32, F64):
+                    # first -0.0 / +0.0 rows of this launch (synthetic replays
+                    # re-insert canonical keys and do not count)
+                    zb = rt.alloc(16)
+                    rt.memset(zb.ptr, 0xFF, 16)
+                    st.zrow_cur = zb
+                    if not self._synthetic:
+                        st.zrows = getattr(st, "zrows", []) + [zb]
                 if b.extra.get("part") and b.extra.get("deferred"):
                     st.ensure_part(count, 1 << b.extra["pbits"])
                     st.pbits = b.extra["pbits"]
@@ -1153,6 +1162,8 @@ class Ctx:
                     return st.pv[key[3]].ptr
                 if what == "oval":
                     return st.over[1][key[3]].ptr
+                if what == "zrow":
+                    return st.zrow_cur.ptr
         raise EvalError(f"internal: no value for kernel parameter {key}")
 
 
@@ -1528,6 +1539,21 @@ def evaluate(e, env=None, config=None, externs=None, *, result="python", idx0=0,
     stats.live_bytes = ctx.live
     stats.intermediate_allocations = stats.vector_allocations - kept
     return Value(e.ty, payload), stats
+
+
+def _first_zero_sign(b, d):
+    """A one-float-field dictmerger keeps the first-inserted key object of
+    the equal pair -0.0 / 0.0 (builders.py:346-351, Python dict semantics):
+    the earliest launch that merged a zero key decides, by its first row."""
+    for zb in getattr(b, "zrows", ()):
+        w = np.zeros(2, dtype=np.uint64)
+        rt.d2h(w.ctypes.data, zb.ptr, 16)
+        pos, neg = int(w[0]), int(w[1])
+        if pos == neg:           # no zero key in this launch
+            continue
+        if neg < pos and d.n:
+            rt.call("wg_neg_zero", d.keys.cols[0].ptr, d.n, SIZE[b.kks[0]])
+        return
 
 
 def _seg_dbl(k):

@@ -65,6 +65,7 @@ _SIGS = {
     "wg_iota_u32": (c_int, [u64, u64]),
     "wg_iota_i64": (c_int, [u64, u64, i64]),
     "wg_seg_stats": (c_int, [u64, u64, u64, u64]),
+    "wg_neg_zero": (c_int, [u64, u64, c_int]),
     "wg_exclusive_scan_i64": (c_int, [u64, u64, u64, u64]),
     "wg_sort_pairs": (c_int, [u64, u64, u64, u64, u64, c_int, c_int]),
     "wg_gather": (c_int, [u64, u64, u64, u64, c_int]),
@@ -350,7 +351,7 @@ def compile_check(src: str, name="weld_loop.cu"):
 # optional hook called around each generated-kernel launch (bench timing).
 LAUNCHES = [0]
 LAUNCH_HOOK = [None]
-_KERNEL_CALLS = {"wg_dict_finish_small": 1, "wg_table_init": 1, "wg_table_compact": 1, "wg_order_key": 1, "wg_iota_u32": 1, "wg_iota_i64": 1, "wg_seg_stats": 1, "wg_exclusive_scan_i64": 1,
+_KERNEL_CALLS = {"wg_dict_finish_small": 1, "wg_table_init": 1, "wg_table_compact": 1, "wg_order_key": 1, "wg_iota_u32": 1, "wg_iota_i64": 1, "wg_seg_stats": 1, "wg_neg_zero": 1, "wg_exclusive_scan_i64": 1,
                  "wg_sort_pairs": 1, "wg_gather": 1, "wg_narrow": 1, "wg_widen": 1, "wg_run_starts": 2, "wg_group_finish1": 12,
                  "wg_gen_column": 1, "wg_mul_inplace_f64": 1, "wg_flush_l2": 1}
 

@@ -115,3 +115,47 @@ def test_partitioned_dictmerger_sentinel_key_full_size():
     gk, gv = out
     assert np.array_equal(np.asarray(gk), uk)
     assert np.array_equal(np.asarray(gv), sums)
+
+
+FLOAT_CASES = [
+    [0.0, -0.0, 1.5, -0.0, 0.0],
+    [-0.0, 0.0, 1.5, 0.0],
+    [1.0, 2.0, -0.0, -0.0],
+    [2.5, float("inf"), -float("inf"), -0.0],
+]
+
+
+@pytest.mark.parametrize("data", FLOAT_CASES, ids=range(len(FLOAT_CASES)))
+@pytest.mark.parametrize("kind", ["f64", "f32"])
+def test_signed_zero_keys_keep_the_first_inserted_key(data, kind):
+    """-0.0 == 0.0 is one key; its sign is that of the first row merging it
+    (Python dict keeps the first-inserted key object)."""
+    import math
+    for src in (f"tovec(result(for(v, dictmerger[{kind}, i64, +], (b, i, x) => merge(b, {{x, i}}))))",
+                f"tovec(result(for(v, groupbuilder[{kind}, i64], (b, i, x) => merge(b, {{x, i}}))))"):
+        got, want = _both(src, {"v": f"vec[{kind}]"}, {"v": data})
+        assert got == want, (src, got, want)
+        assert [math.copysign(1.0, k) for k, _ in got] == [math.copysign(1.0, k) for k, _ in want]
+
+
+@pytest.mark.parametrize("n", [5000, 300_007])
+def test_signed_zero_keys_at_size(n):
+    import math
+    rng = random.Random(n)
+    for first in (0.0, -0.0):
+        data = [first] + [rng.choice([0.0, -0.0, 1.0, 2.0, -3.5]) for _ in range(n - 1)]
+        for src in ("tovec(result(for(v, dictmerger[f64, i64, +], (b, i, x) => merge(b, {x, 1}))))",
+                    "tovec(result(for(v, groupbuilder[f64, i64], (b, i, x) => merge(b, {x, i}))))"):
+            got, want = _both(src, {"v": "vec[f64]"}, {"v": data})
+            assert got == want
+            assert [math.copysign(1.0, k) for k, _ in got] == [math.copysign(1.0, k) for k, _ in want]
+
+
+def test_nan_keys_collapse_like_the_reference():
+    """NaN keys produced by the program (0.0 / 0.0) or passed in as one float
+    object are a single dictionary key in the reference; so on the device."""
+    nan = float("nan")
+    for src in ("tovec(result(for(v, dictmerger[f64, i64, +], (b, i, x) => merge(b, {x / 0.0, 1}))))",
+                "tovec(result(for(v, groupbuilder[f64, i64], (b, i, x) => merge(b, {x, i}))))"):
+        got, want = _both(src, {"v": "vec[f64]"}, {"v": [nan, 1.0, 0.0, nan, -0.0, 2.0, nan]})
+        assert repr(got) == repr(want), (got, want)
