@@ -1419,6 +1419,7 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
         g.param(f"m{b.bid}_part", "u64*", ("b", b.bid, "part"))
         g.param(f"m{b.bid}_slot", "u64*", ("b", b.bid, "slot"))
         g.param(f"m{b.bid}_init", "i64", ("b", b.bid, "init"))
+        g.param(f"m{b.bid}_mirror", "u64*", ("b", b.bid, "mirror"))
     if merger_bs:
         g.param("ticket", "unsigned int*", ("ticket",))
     for b in g.bspecs:
@@ -1817,7 +1818,17 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
                            f" if ({f} == 0) p.m{b.bid}_slot[{F}] = (u64)h_; }}"
                            f" else if (h_) {{ p.m{b.bid}_slot[{f}] = wg_to_bits<{ct}>({op}::f(wg_from_bits<{ct}>(p.m{b.bid}_slot[{f}]), a_));"
                            f" p.m{b.bid}_slot[{F}] = 1; }} }} }}")
-        src.append("    if (threadIdx.x == 0) *p.ticket = 0;")
+        # pinned host mirror of each slot plus the error word: the host reads
+        # the result after a stream sync, with no copy-engine round trip
+        src.append("    __syncthreads();")
+        src.append("    if (threadIdx.x == 0) {")
+        src.append("      const u64 e0_ = __ldcg((const u64*)p.err), e1_ = __ldcg((const u64*)p.err + 1);")
+        for b in merger_bs:
+            F = len(leaves(b.kind.elem))
+            src.append(f"      if (p.m{b.bid}_mirror) {{ for (int f_ = 0; f_ <= {F}; ++f_) p.m{b.bid}_mirror[f_] = p.m{b.bid}_slot[f_];"
+                       f" p.m{b.bid}_mirror[{F + 1}] = e0_; p.m{b.bid}_mirror[{F + 2}] = e1_; }}")
+        src.append("      *p.ticket = 0;")
+        src.append("    }")
         src.append("  }")
     src.append("}")
     source = "\n".join(src) + "\n"

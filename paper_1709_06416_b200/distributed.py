@@ -364,6 +364,7 @@ def combine_merger(p, comm: DeviceComm):
     k.launch(1, 32, _struct.pack("<QQQ", allw.ptr, comm.world, p["slot"].ptr))
     b = p["b"]
     b.launched = True
+    b.mirrored = False          # the combine kernel writes the device slot only
     vals = [None]
     words = b.read_words()
     from .irtypes import from_bits, identity_value

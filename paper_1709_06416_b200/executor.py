@@ -119,6 +119,7 @@ class _Plan:
 
 _plan_cache = {}
 _plan_lock = threading.Lock()
+_TICKET = [None]
 _fv_cache = {}
 
 
@@ -138,6 +139,7 @@ class Ctx:
         self.launches = 0
         self._ticket = None
         self.dirty = False
+        self.rec = []         # launches of a replayable evaluation (see _Replay)
         # the reference's loop step (run.py:958-981): +1 before and after
         # every claimed top-level loop; appender segments are keyed by
         # (step, chunk) and the chunk is the loop row // grain_size
@@ -254,10 +256,19 @@ class Ctx:
         self.allocs += 1
 
     def ticket(self):
-        if self._ticket is None:
-            self._ticket = rt.alloc(8)
-            rt.memset(self._ticket.ptr, 0, 8)
-        return self._ticket.ptr
+        """The last-CTA ticket of merger kernels.  Every such kernel resets it
+        to 0 on exit and all loop kernels run in order on the library's
+        stream, so one process-wide zeroed word serves every launch."""
+        t = _TICKET[0]
+        if t is None:
+            with _plan_lock:
+                if _TICKET[0] is None:
+                    b = rt.alloc(8)
+                    rt.memset(b.ptr, 0, 8)
+                    _TICKET[0] = b
+            t = _TICKET[0]
+        self._ticket = t
+        return t.ptr
 
     # -- device error word ---------------------------------------------------
     def check_device(self):
@@ -740,6 +751,7 @@ class Ctx:
                 self.idx0, self.cbase = saved
             return builders
         self._launch_loop(e, lam, specs, datas, windows, count, builders, captures, strategy)
+        self._last_builders = builders
         return builders
 
     def _launch_loop(self, e, lam, specs, datas, windows, count, builders, captures, strategy, assume_lowcard=False):
@@ -927,6 +939,12 @@ class Ctx:
         kern.launch(grid, plan.block, blob, smem)
         self.launches += 1
         self.dirty = True
+        if self.rec is not None:
+            if sizes is not None or segstats or plan.count_nodes or plan.stat_nodes or \
+                    not all(isinstance(bmap[b.bid], MergerDev) for b in plan.builders):
+                self.rec = None
+            else:
+                self.rec.append((kern, grid, plan.block, blob, smem))
         for st, seg, coff, c0, c1 in segstats:
             out = rt.alloc(32)
             rt.call("wg_seg_stats", coff.ptr, c1 - c0 + 1, seg.total_buf.ptr, out.ptr)
@@ -1119,6 +1137,8 @@ class Ctx:
                     return st.slot.ptr
                 if what == "init":
                     return st.take_init_flag()
+                if what == "mirror":
+                    return st.mirror_ptr()
             if isinstance(st, (AppenderDev, GroupDev)):
                 r = res[bid]
                 if what == "ctotal":
@@ -1480,6 +1500,14 @@ def evaluate(e, env=None, config=None, externs=None, *, result="python", idx0=0,
         raise EvalError("grain_size must be at least 1")
     if e.ty is None:
         raise EvalError("expression must be type-checked before evaluation")
+    rkey = None
+    if (REPLAY and not cfg.count_evals and env and result in ("python", "device") and type(e) is Result
+            and type(e.builder) is For and _ctx_out is None and idx0 == 0):
+        rkey = _replay_key(e, env, externs, result)
+        if rkey is not None:
+            hit = _REPLAYS.get(rkey)
+            if hit is not None and hit.valid(e, env, cfg, externs):
+                return hit.run(e)
     note_evaluation()
     ctx = Ctx(cfg, externs, idx0=idx0)
     if _ctx_out is not None:
@@ -1538,7 +1566,111 @@ def evaluate(e, env=None, config=None, externs=None, *, result="python", idx0=0,
     stats.peak_bytes = ctx.peak
     stats.live_bytes = ctx.live
     stats.intermediate_allocations = stats.vector_allocations - kept
+    if rkey is not None and ctx.rec and len(ctx.rec) == 1 and ctx.launches == 1 and cand is None:
+        bl = []
+        lb = getattr(ctx, "_last_builders", None)
+        if lb is not None:
+            _collect_builders(lb, bl)
+        if bl and all(isinstance(b, MergerDev) for b in bl):
+            _REPLAYS.put(rkey, _Replay(e, env, cfg, externs, ctx, bl, stats))
+            if any(not b.mirrored for b in bl):
+                _REPLAYS.d.pop(rkey, None)
     return Value(e.ty, payload), stats
+
+
+# ---------------------------------------------------------------------------
+# Launch replay for repeated evaluations of one merger loop over the same
+# device-resident inputs (C1 at its 1M-row config size is launch-bound: the
+# host control plane -- tree walk, plan lookup, parameter packing -- costs
+# more than the kernel).  The first evaluation records its single launch;
+# later calls with the same program object, the same input objects, config
+# and externs re-issue it and read the merger slots with the error word in
+# one synchronisation.  The kernel writes the slots from scratch (init flag),
+# resets its last-CTA ticket and reuses its per-CTA partials buffer.
+
+REPLAY = _os.environ.get("WELDGPU_REPLAY", "1") == "1"
+
+
+class _ReplayCache:
+    def __init__(self, cap=32):
+        self.d = {}
+        self.cap = cap
+        self.lock = threading.Lock()
+
+    def get(self, k):
+        return self.d.get(k)
+
+    def put(self, k, v):
+        with self.lock:
+            if len(self.d) >= self.cap:
+                self.d.clear()
+            self.d[k] = v
+
+
+_REPLAYS = _ReplayCache()
+
+
+def _replay_key(e, env, externs, result):
+    ids = []
+    for name, v in env.items():
+        p = v.data if type(v) is Value else v
+        if type(p) is not DVec:
+            return None           # host inputs are uploaded per call
+        ids.append(name)
+        ids.append(id(p))
+    return (id(e), tuple(ids), tuple(map(id, externs.values())) if externs else (), result)
+
+
+class _Replay:
+    __slots__ = ("e", "inputs", "cfg", "externs", "launch", "mergers", "stats", "keep", "lock", "shape")
+
+    def __init__(self, e, env, cfg, externs, ctx, mergers, stats):
+        from dataclasses import replace
+        self.e = e
+        self.inputs = {k: (v.data if isinstance(v, Value) else v) for k, v in env.items()}
+        self.cfg = replace(cfg)
+        self.externs = dict(externs or {})
+        self.launch = ctx.rec[0]
+        self.mergers = list(mergers)
+        self.stats = stats
+        self.keep = (ctx._ticket, ctx._keep)
+        self.lock = threading.Lock()
+        self.shape = ctx._last_builders
+
+    def valid(self, e, env, cfg, externs):
+        if e is not self.e or cfg != self.cfg or len(env) != len(self.inputs):
+            return False
+        for k, v in env.items():
+            p = v.data if isinstance(v, Value) else v
+            if self.inputs.get(k) is not p:
+                return False
+        ext = externs or {}
+        return len(ext) == len(self.externs) and all(self.externs.get(k) is f for k, f in ext.items())
+
+    def run(self, e):
+        note_evaluation()
+        kern, grid, block, blob, smem = self.launch
+        with self.lock:
+            kern.launch(grid, block, blob, smem)
+            vals = []
+            for q, b in enumerate(self.mergers):
+                if q == 0:
+                    err = []
+                    vals.append(b.read(err))
+                    code, info = err[0]
+                    if code:
+                        raise device_error(code, info)
+                else:
+                    vals.append(b.read())
+        if len(vals) == 1 and not isinstance(self.shape, tuple):
+            payload = vals[0]
+        else:
+            it = iter(vals)
+            payload = _shape_like(self.shape, lambda: next(it))
+        st = EvalStats.__new__(EvalStats)
+        st.__dict__.update(self.stats.__dict__)
+        st.node_evals = {}
+        return Value(e.ty, payload), st
 
 
 def _first_zero_sign(b, d):
@@ -1693,6 +1825,7 @@ def evaluate_partials_device(loop, env, config=None, externs=None, idx0=0, rank=
             F = len(b.ks)
             if not b.launched:         # no rows on this rank: merged flag 0
                 rt.memset(b.slot.ptr, 0, 8 * (F + 1))
+                b.mirrored = False
             out.append({"kind": "merger", "op": kind.op, "kinds": b.ks, "slot": b.slot, "b": b})
         elif isinstance(kind, VecBuilder):
             if b.segments:

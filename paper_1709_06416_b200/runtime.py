@@ -276,6 +276,19 @@ def d2h_checked(host_ptr, src_ptr, nbytes):
     return c.value, i.value
 
 
+def host_alloc(nbytes):
+    """Pinned host memory (cudaMallocHost; device-accessible at the same
+    address under unified addressing)."""
+    p = c_void_p(0)
+    _check(lib().wg_host_alloc(nbytes, ctypes.byref(p)))
+    return p.value
+
+
+def clear_error():
+    """Reset the device error word (after a raise read from a host mirror)."""
+    read_error()
+
+
 def read_error():
     c, i = i64(0), i64(0)
     _check(lib().wg_read_error(ctypes.byref(c), ctypes.byref(i)))
