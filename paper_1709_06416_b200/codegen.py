@@ -1607,9 +1607,20 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
                 out.append(f"#pragma unroll\n    for (int q = 0; q < ITEMS; ++q) dkf{b.bid}[q] = false;")
                 for f, kk in enumerate(leaves(b.kind.value)):
                     out.append(f"    {CTYPE[kk]} dkv{b.bid}_{f}[ITEMS];")
+        seg_coarse = seg_bs and not (ITEMS > 32 or any(b.extra.get("segstats") == "fine" for b in seg_bs))
+        if seg_coarse:
+            # the (at most one) item of this thread that starts a grain-wide
+            # chunk; phase A notes the thread-local append count there
+            out.append("    int j0a_ = -1;")
+            out.append("    { i64 r_ = (p.cgmask >= 0) ? ((p.cbase + t0) & p.cgmask) : ((p.cbase + t0) % p.cgrain);")
+            out.append("      r_ = r_ ? p.cgrain - r_ : 0; if (r_ < ITEMS && t0 + r_ < n) j0a_ = (int)r_; }")
+            for b in seg_bs:
+                out.append(f"    int c0s{b.bid} = -1;")
         out.append("#pragma unroll")
         out.append("    for (int j = 0; j < ITEMS; ++j) {")
         out.append("      const i64 li = t0 + j;")
+        if seg_coarse:
+            out.append("      if (j == j0a_) { " + " ".join(f"c0s{b.bid} = (int)cnt{b.bid};" for b in seg_bs) + " }")
         out.append("      if (li < n) {")
         out.append("        const i64 i = p.idx0 + li;")
         out.extend(body_a)
@@ -1638,16 +1649,30 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
             for si, b in enumerate(scan_bs):
                 if not b.extra["staged"]:
                     out.append(f"    wpos{b.bid} += s_toff[{si}];")
+            fine = ITEMS > 32 or any(b.extra.get("segstats") == "fine" for b in seg_bs)
             if seg_bs:
                 # first item of this thread that starts a grain-wide chunk
                 out.append("    i64 sgn_ = (p.cgmask >= 0) ? ((p.cbase + t0) & p.cgmask) : ((p.cbase + t0) % p.cgrain);")
                 out.append("    sgn_ = sgn_ ? p.cgrain - sgn_ : 0;")
+            if seg_bs and not fine:
+                # grain >= ITEMS: at most one chunk start per thread; phase A
+                # noted the thread-local append count there (c0s), so the
+                # slot is written once, before phase B
+                out.append(f"    if (c0s{seg_bs[0].bid} >= 0) {{")
+                out.append("      const i64 g0_ = p.cbase + t0 + sgn_;")
+                out.append("      const i64 ci0_ = (p.cgmask >= 0) ? ((g0_ >> __popcll(p.cgmask)) - (p.cbase >> __popcll(p.cgmask)))"
+                           " : (g0_ / p.cgrain - p.cbase / p.cgrain);")
+                for b in seg_bs:
+                    si = scan_bs.index(b)
+                    pos = f"wpos{b.bid} + s_toff[{si}]" if b.extra["staged"] else f"wpos{b.bid}"
+                    out.append(f"      p.a{b.bid}_coff[ci0_] = {pos} + c0s{b.bid};")
+                out.append("    }")
             out.append("#pragma unroll")
             out.append("    for (int j = 0; j < ITEMS; ++j) {")
             out.append("      const i64 li = t0 + j;")
             out.append("      if (li < n) {")
             out.append("        const i64 i = p.idx0 + li;")
-            if seg_bs:
+            if seg_bs and fine:
                 out.append("        if (j == sgn_) {")
                 out.append("          const i64 ci_ = (p.cbase + li) / p.cgrain - p.cbase / p.cgrain;")
                 for b in seg_bs:

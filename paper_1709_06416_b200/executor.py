@@ -755,7 +755,8 @@ class Ctx:
         return builders
 
     def _launch_loop(self, e, lam, specs, datas, windows, count, builders, captures, strategy, assume_lowcard=False):
-        bstruct, bmap = _bspecs(builders, strategy, count, loop_id=id(e), assume_lowcard=assume_lowcard)
+        bstruct, bmap = _bspecs(builders, strategy, count, loop_id=id(e), assume_lowcard=assume_lowcard,
+                                   grain=self.cfg.grain_size)
         # The expression identities fix every type in the loop; only the
         # runtime choices (strides, alignment, builder modes, externs) vary.
         counting = self.counting and self._counts_body(lam)
@@ -781,7 +782,8 @@ class Ctx:
             with _plan_lock:
                 cc = _plan_cache.get(ckey)
             if cc is None:
-                cbs, _ = _bspecs(builders, strategy, count, loop_id=id(e), assume_lowcard=assume_lowcard)
+                cbs, _ = _bspecs(builders, strategy, count, loop_id=id(e), assume_lowcard=assume_lowcard,
+                                   grain=self.cfg.grain_size)
                 cplan = generate(e if lam is e.func else _with_func(e, lam), specs, cbs, captures, self.externs,
                                  strategy, count_only=True)
                 cc = (cplan, rt.get_kernel(cplan.source, cplan.name))
@@ -1361,7 +1363,7 @@ def _builder_order(builders):
     return out
 
 
-def _bspecs(builders, strategy, count, loop_id=None, assume_lowcard=False):
+def _bspecs(builders, strategy, count, loop_id=None, assume_lowcard=False, grain=1024):
     bmap = {}
     counter = [0]
     single = not isinstance(builders, tuple)
@@ -1410,8 +1412,9 @@ def _bspecs(builders, strategy, count, loop_id=None, assume_lowcard=False):
                 bs.mode = "global"
         if isinstance(v, AppenderDev) and isinstance(v.kind, VecBuilder) and getattr(v, "segk", None) is not None:
             # unhinted vecbuilder: scan-mode kernels record where each
-            # grain-wide chunk's appends start (reallocation accounting)
-            bs.extra["segstats"] = True
+            # grain-wide chunk's appends start (reallocation accounting);
+            # "fine" when a thread's items can hold more than one chunk start
+            bs.extra["segstats"] = "fine" if grain < 32 else True
         if isinstance(v, (AppenderDev,)) and v.kinds is None:
             raise DeviceUnsupported(f"vecbuilder[{v.kind.elem}] (nested element types) on the device")
         return bs
