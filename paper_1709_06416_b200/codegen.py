@@ -74,6 +74,13 @@ SCAN_EARLY_CLAIM = _os.environ.get("WELDGPU_SCAN_EARLY_CLAIM", "1") == "1"
 SCAN_MINBLOCKS = int(_os.environ.get("WELDGPU_SCAN_MINBLOCKS", "4"))   # in 256-thread CTAs per SM
 PART_ITEMS = int(_os.environ.get("WELDGPU_PART_ITEMS", "8"))
 PIPE_STAGES = int(_os.environ.get("WELDGPU_PIPE_STAGES", "4"))
+# warp-specialised scan schedule: the compute warps publish each tile's
+# aggregate and stage its appends, one extra warp resolves the look-back and
+# stores the tile; WS_NBUF staging buffers decouple the two
+SCAN_WS = _os.environ.get("WELDGPU_SCAN_WS", "1") == "1"
+WS_NBUF = int(_os.environ.get("WELDGPU_WS_NBUF", "2"))
+WS_MINB = int(_os.environ.get("WELDGPU_WS_MINB", "4"))
+WS_ITEMS = int(_os.environ.get("WELDGPU_WS_ITEMS", "8"))
 PIPE_MAX_STAGES = 8
 PIPE_SMEM_BUDGET = int(_os.environ.get("WELDGPU_PIPE_SMEM", str(48 * 1024)))
 
@@ -271,6 +278,7 @@ class KernelPlan:
     stat_nodes: list = field(default_factory=list)    # ("alloc" | "trav", node): body EvalStats events
     lit_nodes: dict = field(default_factory=dict)     # nested appender bid -> ids of literals it keeps
     seg_bids: list = field(default_factory=list)      # unhinted scan appenders with chunk offsets
+    threads: int = 0                                  # launch block size (block + the store warp under SCAN_WS)
 
 
 def _hex_f64(v):
@@ -1341,6 +1349,23 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
                 b.extra["staged"] = True
             staged_bytes = need
 
+    # warp-specialised scan schedule: appenders only (every builder of the
+    # loop a scan appender with at most k merges per row), staged in dynamic
+    # shared memory
+    ws = bool(SCAN_WS and scan_bs and not count_only and all(b.mode == "scan" for b in g.bspecs)
+              and all(b.k is not None for b in scan_bs) and ITEMS <= 32
+              and not any(b.extra.get("segstats") == "fine" for b in scan_bs))
+    if ws and not (items or ITEMS_OVERRIDE):
+        ITEMS = min(ITEMS, WS_ITEMS)
+        g.items = ITEMS
+    ws_need = sum(BLOCK * ITEMS * b.k * SIZE[k] for b in scan_bs for k in b.extra["kinds"]) if ws else 0
+    if ws and WS_NBUF * ws_need > 160 * 1024:
+        ws = False
+    if ws:
+        for b in scan_bs:
+            b.extra["staged"] = True
+        staged_bytes = 0
+
     merger_bs = [b for b in g.bspecs if isinstance(b.kind, Merger)]
     schedule = "scan" if scan_bs else "static"
 
@@ -1498,6 +1523,18 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
             fl.append("}")
             smem_flush.append("\n    ".join(fl))
 
+    ws_off = 0
+    ws_boff = {}
+    if ws:
+        ws_off = (dyn_smem + 127) // 128 * 128
+        o_ = 0
+        for b in scan_bs:
+            for f, kk in enumerate(b.extra["kinds"]):
+                ws_boff[(b.bid, f)] = o_
+                o_ += (BLOCK * ITEMS * b.k * SIZE[kk] + 15) // 16 * 16
+        ws_buf = o_
+        dyn_smem = ws_off + WS_NBUF * ws_buf
+
     # bulk-async column pipeline (static schedule, contiguous 16B-aligned
     # columns).  The stage count is a launch parameter: the executor picks
     # the most stages that do not lower the kernel's occupancy.
@@ -1530,6 +1567,8 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
     src.append('#include "weld_device.cuh"')
     src.append(f"#define BLOCK {BLOCK}")
     src.append(f"#define ITEMS {ITEMS}")
+    if ws:
+        src.append(f"#define WS_NBUF {WS_NBUF}")
     src.append("#define TILE (BLOCK * ITEMS)")
     src.append("struct Params {")
     for p_ in g.params:
@@ -1542,6 +1581,8 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
         # CTAs of 256 threads per SM)
         minb = SCAN_MINBLOCKS * 256 // BLOCK
     lb = f"BLOCK, {minb}" if minb else "BLOCK"
+    if ws:
+        lb = f"BLOCK + 32, {WS_MINB}" if WS_MINB else "BLOCK + 32"
     src.append(f'extern "C" __global__ void __launch_bounds__({lb}) {name}(const Params p) {{')
     src.append("  extern __shared__ __align__(16) u64 wg_dyn_smem[];")
     for t in sorted(g.tabs):
@@ -1562,7 +1603,16 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
             src.extend(_regcache_decl(b, b.extra["regcache"]))
     src.append("  const i64 n = p.n;")
     src.append("  const i64 ntiles = (n + TILE - 1) / TILE;")
-    if scan_bs:
+    if ws:
+        src.append("  __shared__ i64 s_scan[33];")
+        src.append("  __shared__ i64 s_wtile;")
+        src.append("  __shared__ i64 s_btile[WS_NBUF];")
+        src.append(f"  __shared__ i64 s_bagg[WS_NBUF][{len(scan_bs)}];")
+        if seg_bs:
+            src.append(f"  __shared__ i64 s_bci[WS_NBUF][BLOCK];")
+            src.append(f"  __shared__ int s_bcp[WS_NBUF][{len(seg_bs)}][BLOCK];")
+        src.append("  __shared__ __align__(8) u64 wg_full[WS_NBUF], wg_empty[WS_NBUF];")
+    elif scan_bs:
         src.append("  __shared__ i64 s_scan[33];")
         src.append(f"  __shared__ i64 s_toff[{len(scan_bs)}];")
         src.append("  __shared__ i64 s_tile[2];")
@@ -1583,6 +1633,121 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
                 out.append(f"{ind}  else {{ for (int q = 0; q < {cnt}; ++q) {{ const i64 e_ = lt0_ * {per} + q; "
                            f"{a}[q] = (e_ < n * {per}) ? {col}[e_] : ({st})0; }} }}")
         out.append(f"{ind}}}")
+        return out
+
+    def ws_lines():
+        """Warp-specialised scan schedule.  Threads [0, BLOCK) claim tiles in
+        order, count, scan, publish the tile aggregate at once and stage the
+        tile's appends in buffer it % WS_NBUF; the extra warp [BLOCK,
+        BLOCK + 32) resolves each staged tile's look-back, stores it and frees
+        the buffer.  A slow predecessor stalls only the store warp while the
+        compute warps fill the other buffer(s)."""
+        def bufptrs(ind, bvar):
+            out = []
+            for b in scan_bs:
+                for f, kk in enumerate(b.extra["kinds"]):
+                    out.append(f"{ind}{STYPE[kk]}* const s_ap{b.bid}_{f} = ({STYPE[kk]}*)((char*)wg_dyn_smem + {ws_off} + "
+                               f"(u64){bvar} * {ws_buf} + {ws_boff[(b.bid, f)]});")
+            return out
+        out = ["  if (threadIdx.x == 0) {",
+               "    for (int b_ = 0; b_ < WS_NBUF; ++b_) { wg_mbar_init(&wg_full[b_], 1); wg_mbar_init(&wg_empty[b_], 1); }",
+               "    wg_fence_mbar_init();",
+               "  }",
+               "  __syncthreads();",
+               "  if (threadIdx.x >= BLOCK) {",
+               "    // look-back + store warp",
+               "    const int lane_ = threadIdx.x & 31;",
+               "    for (i64 it_ = 0; ; ++it_) {",
+               "      const int bf_ = (int)(it_ % WS_NBUF);",
+               "      wg_mbar_wait(&wg_full[bf_], (unsigned)((it_ / WS_NBUF) & 1));",
+               "      const i64 tile = s_btile[bf_];",
+               "      if (tile < 0) break;"]
+        out += bufptrs("      ", "bf_")
+        for si, b in enumerate(scan_bs):
+            out.append(f"      {{ const i64 agg_ = s_bagg[bf_][{si}];")
+            out.append(f"        const i64 pre_ = wg_lookback_resolve(p.a{b.bid}_status, tile, agg_);")
+            out.append(f"        if (lane_ == 0 && tile == ntiles - 1) *p.a{b.bid}_total = pre_ + agg_;")
+            for f, kk in enumerate(b.extra["kinds"]):
+                out.append(f"        for (i64 q = lane_; q < agg_; q += 32) __stcs(p.a{b.bid}_{f} + pre_ + q, s_ap{b.bid}_{f}[q]);")
+            if b in seg_bs:
+                sj = seg_bs.index(b)
+                out.append(f"        for (int q = lane_; q < BLOCK; q += 32) {{ const int lp_ = s_bcp[bf_][{sj}][q];"
+                           f" if (lp_ >= 0) p.a{b.bid}_coff[s_bci[bf_][q]] = pre_ + lp_; }}")
+            out.append("      }")
+        out += ["      __syncwarp();",
+                "      if (lane_ == 0) wg_mbar_arrive(&wg_empty[bf_]);",
+                "    }",
+                "    return;",
+                "  }",
+                "  if (threadIdx.x == 0) s_wtile = (i64)atomicAdd(p.tilectr, 1ULL);",
+                "  wg_bar_group(BLOCK);",
+                "  for (i64 it_ = 0; ; ++it_) {",
+                "    const int bf_ = (int)(it_ % WS_NBUF);",
+                # (claiming the next tile during phase B instead: 1.59 vs 1.46 ms --
+                # a claimed-but-unpublished tile stalls every later look-back)
+                "    if (it_ > 0) { if (threadIdx.x == 0) s_wtile = (i64)atomicAdd(p.tilectr, 1ULL); wg_bar_group(BLOCK); }",
+                "    const i64 tile = s_wtile;",
+                "    if (tile >= ntiles) {",
+                "      if (threadIdx.x == 0) {",
+                "        if (it_ >= WS_NBUF) wg_mbar_wait(&wg_empty[bf_], (unsigned)(((it_ / WS_NBUF) - 1) & 1));",
+                "        s_btile[bf_] = -1;",
+                "        wg_mbar_arrive(&wg_full[bf_]);",
+                "      }",
+                "      break;",
+                "    }"]
+        out += decl_lines("", "    ")
+        out += load_lines("tile", "", "    ")
+        out.append("    const i64 t0 = tile * TILE + (i64)threadIdx.x * ITEMS;")
+        out.append("    const bool full = (t0 + ITEMS <= n);")
+        for b in scan_bs:
+            out.append(f"    i64 cnt{b.bid} = 0;")
+        if seg_bs:
+            out.append("    int j0a_ = -1;")
+            out.append("    { i64 r_ = (p.cgmask >= 0) ? ((p.cbase + t0) & p.cgmask) : ((p.cbase + t0) % p.cgrain);")
+            out.append("      r_ = r_ ? p.cgrain - r_ : 0; if (r_ < ITEMS && t0 + r_ < n) j0a_ = (int)r_; }")
+            for b in seg_bs:
+                out.append(f"    int c0s{b.bid} = -1;")
+        out.append("#pragma unroll")
+        out.append("    for (int j = 0; j < ITEMS; ++j) {")
+        out.append("      const i64 li = t0 + j;")
+        if seg_bs:
+            out.append("      if (j == j0a_) { " + " ".join(f"c0s{b.bid} = (int)cnt{b.bid};" for b in seg_bs) + " }")
+        out.append("      if (li < n) {")
+        out.append("        const i64 i = p.idx0 + li;")
+        out.extend(body_a)
+        out.append("      }")
+        out.append("    }")
+        for si, b in enumerate(scan_bs):
+            out.append(f"    i64 agg{b.bid};")
+            out.append(f"    i64 wpos{b.bid} = wg_group_exclusive_scan(cnt{b.bid}, s_scan, &agg{b.bid}, BLOCK);")
+            out.append(f"    if (threadIdx.x == 0) wg_publish_aggregate(p.a{b.bid}_status, tile, agg{b.bid});")
+        out.append("    if (it_ >= WS_NBUF) wg_mbar_wait(&wg_empty[bf_], (unsigned)(((it_ / WS_NBUF) - 1) & 1));")
+        out += bufptrs("    ", "bf_")
+        if seg_bs:
+            out.append("    {")
+            out.append("      const i64 sgn_ = (j0a_ >= 0) ? j0a_ : 0;")
+            out.append("      const i64 g0_ = p.cbase + t0 + sgn_;")
+            out.append("      s_bci[bf_][threadIdx.x] = (p.cgmask >= 0) ? ((g0_ >> __popcll(p.cgmask)) - (p.cbase >> __popcll(p.cgmask)))"
+                       " : (g0_ / p.cgrain - p.cbase / p.cgrain);")
+            for sj, b in enumerate(seg_bs):
+                out.append(f"      s_bcp[bf_][{sj}][threadIdx.x] = (c0s{b.bid} >= 0) ? (int)(wpos{b.bid} + c0s{b.bid}) : -1;")
+            out.append("    }")
+        out.append("#pragma unroll")
+        out.append("    for (int j = 0; j < ITEMS; ++j) {")
+        out.append("      const i64 li = t0 + j;")
+        out.append("      if (li < n) {")
+        out.append("        const i64 i = p.idx0 + li;")
+        out.extend(body_b)
+        out.append("      }")
+        out.append("    }")
+        out.append("    wg_bar_group(BLOCK);")
+        out.append("    if (threadIdx.x == 0) {")
+        out.append("      s_btile[bf_] = tile;")
+        for si, b in enumerate(scan_bs):
+            out.append(f"      s_bagg[bf_][{si}] = agg{b.bid};")
+        out.append("      wg_mbar_arrive(&wg_full[bf_]);")
+        out.append("    }")
+        out.append("  }")
         return out
 
     def decl_lines(suffix, ind):
@@ -1704,7 +1869,9 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
                 out.append("    __syncthreads();")
         return out
 
-    if scan_bs:
+    if ws:
+        src.extend(ws_lines())
+    elif scan_bs:
         # Dynamic tiles, claimed in order through an atomic counter (so every
         # predecessor a tile's look-back waits on is held by a running CTA).
         if SCAN_EARLY_CLAIM:
@@ -1859,7 +2026,7 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
     source = "\n".join(src) + "\n"
     plan = KernelPlan(source=source, name=name, params=g.params, schedule=schedule, items=ITEMS, block=BLOCK,
                       smem=dyn_smem, builders=g.bspecs, scan_bids=[b.bid for b in scan_bs],
-                      merger_bids=[b.bid for b in merger_bs])
+                      merger_bids=[b.bid for b in merger_bs], threads=BLOCK + 32 if ws else BLOCK)
     plan.pipe_stage_bytes = pipe_stage_bytes if pipe else 0
     plan.count_nodes = g.count_nodes
     plan.stat_nodes = g.stat_nodes

@@ -340,6 +340,75 @@ __device__ __forceinline__ i64 wg_lookback(u64* status, i64 tile, i64 aggregate)
   return excl;
 }
 
+// Warp-specialised scan schedule (codegen SCAN_WS): the compute warps
+// (threads [0, nthreads)) publish each tile's aggregate as soon as it is
+// counted and move on; one extra warp resolves the tile's exclusive prefix
+// later (the aggregate is already in status[tile]) and publishes the
+// inclusive prefix.
+__device__ __forceinline__ void wg_bar_group(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+// Block-wide exclusive scan over the compute group only (named barrier 1).
+__device__ __forceinline__ i64 wg_group_exclusive_scan(i64 x, i64* smem /* >= 33 */, i64* total, int nthreads) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = nthreads >> 5;
+  i64 incl = x;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    i64 o = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += o;
+  }
+  wg_bar_group(nthreads);
+  if (lane == 31) smem[warp] = incl;
+  wg_bar_group(nthreads);
+  if (warp == 0) {
+    i64 w = (lane < nw) ? smem[lane] : 0;
+    i64 wi = w;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      i64 o = __shfl_up_sync(0xffffffffu, wi, d);
+      if (lane >= d) wi += o;
+    }
+    if (lane < nw) smem[lane] = wi - w;
+    if (lane == nw - 1) smem[32] = wi;
+  }
+  wg_bar_group(nthreads);
+  *total = smem[32];
+  return smem[warp] + incl - x;
+}
+__device__ __forceinline__ void wg_publish_aggregate(u64* status, i64 tile, i64 aggregate) {
+  wg_st_volatile(status + tile, (tile == 0 ? WG_ST_PRE : WG_ST_AGG) | (u64)aggregate);
+}
+// The look-back of wg_lookback for a tile whose aggregate is already
+// published (whole warp; returns the exclusive prefix).
+__device__ __forceinline__ i64 wg_lookback_resolve(u64* status, i64 tile, i64 aggregate) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) return 0;
+  i64 excl = 0;
+  i64 t = tile - 1;
+  while (true) {
+    const i64 idx = t - lane;
+    const u64 s = (idx >= 0) ? wg_ld_volatile(status + idx) : WG_ST_PRE;
+    const unsigned mp = __ballot_sync(0xffffffffu, (s >> 62) == 2);
+    const int first = mp ? __ffs(mp) - 1 : 32;
+    const unsigned mx = __ballot_sync(0xffffffffu, (s >> 62) == 0);
+    const unsigned upto = (first >= 31) ? 0xffffffffu : ((2u << first) - 1u);
+    if (mx & upto) {
+#if WG_LB_SLEEP > 0
+      __nanosleep(WG_LB_SLEEP);
+#endif
+      continue;
+    }
+    i64 val = (lane <= first) ? (i64)(s & WG_ST_MASK) : 0;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) val += __shfl_xor_sync(0xffffffffu, val, d);
+    excl += val;
+    if (mp) break;
+    t -= 32;
+  }
+  if (lane == 0) wg_st_volatile(status + tile, WG_ST_PRE | (u64)(excl + aggregate));
+  return excl;
+}
+
 // ---------------------------------------------------------------------------
 // Atomic folds into 8-byte slots (dictmerger values, vecmerger bins).
 template <typename T> __device__ __forceinline__ void wg_atomic_add(T* p, T v);

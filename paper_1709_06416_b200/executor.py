@@ -861,7 +861,8 @@ class Ctx:
                     stages = s_
                     break
             smem = plan.smem + stages * plan.pipe_stage_bytes
-        occ = kern.blocks_per_sm(plan.block, smem)
+        nthr = plan.threads or plan.block
+        occ = kern.blocks_per_sm(nthr, smem)
         grid = max(1, min(ntiles, rt.sm_count() * occ))
         self.tasks += grid
         # per-launch builder resources
@@ -938,7 +939,7 @@ class Ctx:
                     raise EvalError(f"internal: float for {p.ctype} parameter")
                 words.append(int(v) & 0xFFFFFFFFFFFFFFFF)
         blob = packer[0].pack(*words)
-        kern.launch(grid, plan.block, blob, smem)
+        kern.launch(grid, nthr, blob, smem)
         self.launches += 1
         self.dirty = True
         if self.rec is not None:
@@ -946,7 +947,7 @@ class Ctx:
                     not all(isinstance(bmap[b.bid], MergerDev) for b in plan.builders):
                 self.rec = None
             else:
-                self.rec.append((kern, grid, plan.block, blob, smem))
+                self.rec.append((kern, grid, nthr, blob, smem))
         for st, seg, coff, c0, c1 in segstats:
             out = rt.alloc(32)
             rt.call("wg_seg_stats", coff.ptr, c1 - c0 + 1, seg.total_buf.ptr, out.ptr)
