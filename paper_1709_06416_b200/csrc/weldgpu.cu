@@ -43,6 +43,20 @@ std::mutex g_acct_mu;
 std::unordered_map<void*, uint64_t> g_sizes;       // live blocks -> rounded size
 std::multimap<uint64_t, void*> g_free;             // cached blocks by size
 uint64_t g_cached = 0;
+// Blocks freed while more than one stream may be in flight (the streaming
+// host-input path selects the copy streams) are not reused until every
+// stream has drained (wg_sync_all): a copy still pending on stream 1/2
+// must not race with a new owner on stream 0.
+bool g_multi = false;
+std::vector<std::pair<uint64_t, void*>> g_deferred;
+static void release_deferred() {   // caller holds g_acct_mu, every stream drained
+  for (auto& kv : g_deferred) {
+    g_free.emplace(kv.first, kv.second);
+    g_cached += kv.first;
+  }
+  g_deferred.clear();
+}
+
 
 int fail(const std::string& msg) {
   g_err = msg;
@@ -814,9 +828,10 @@ int wg_alloc(uint64_t bytes, uint64_t* dptr) {
     cudaError_t e = cudaMalloc(&p, b);
     if (e != cudaSuccess) {
       cudaGetLastError();
-      CK(cudaStreamSynchronize(g_stream));
+      for (int i = 0; i < 3; ++i) CK(cudaStreamSynchronize(g_streams[i]));
       {
         std::lock_guard<std::mutex> lk(g_acct_mu);
+        release_deferred();
         for (auto& kv : g_free) cudaFree(kv.second);
         g_free.clear();
         g_cached = 0;
@@ -844,16 +859,21 @@ int wg_free(uint64_t dptr) {
   auto it = g_sizes.find(p);
   if (it == g_sizes.end()) return fail("wg_free: unknown device pointer");
   g_live -= it->second;
-  g_free.emplace(it->second, p);
-  g_cached += it->second;
+  if (g_multi) g_deferred.emplace_back(it->second, p);
+  else {
+    g_free.emplace(it->second, p);
+    g_cached += it->second;
+  }
   g_sizes.erase(it);
   return 0;
 }
 
+
 int wg_mem_trim(void) {
   NEED_INIT();
-  CK(cudaStreamSynchronize(g_stream));
+  for (int i = 0; i < 3; ++i) CK(cudaStreamSynchronize(g_streams[i]));
   std::lock_guard<std::mutex> lk(g_acct_mu);
+  release_deferred();
   for (auto& kv : g_free) cudaFree(kv.second);
   g_free.clear();
   g_cached = 0;
@@ -1559,6 +1579,10 @@ int wg_stream_select(int which) {
   NEED_INIT();
   if (which < 0 || which > 2) return fail("wg_stream_select: stream 0, 1 or 2");
   g_stream = g_streams[which];
+  if (which != 0) {
+    std::lock_guard<std::mutex> lk(g_acct_mu);
+    g_multi = true;
+  }
   return 0;
 }
 
@@ -1571,6 +1595,11 @@ int wg_stream_wait_event(uint64_t ev) {
 int wg_sync_all(void) {
   NEED_INIT();
   for (int i = 0; i < 3; ++i) CK(cudaStreamSynchronize(g_streams[i]));
+  {
+    std::lock_guard<std::mutex> lk(g_acct_mu);
+    if (g_stream == g_streams[0]) g_multi = false;
+    release_deferred();
+  }
   return 0;
 }
 

@@ -1488,13 +1488,26 @@ def _collect_ids(v, acc):
         acc.add(id(v))
 
 
+# One evaluation at a time per process: the device runtime's current
+# stream, error word and allocator epoch are process-wide, so concurrent
+# evaluate() calls (allowed by the reference's contract) are serialised
+# here rather than interleaved on the device.
+_EVAL_LOCK = threading.RLock()
+
+
 def evaluate(e, env=None, config=None, externs=None, *, result="python", idx0=0, _ctx_out=None):
     """Run a type-checked core expression on the GPU.  Returns (Value, EvalStats).
 
     Same contract as weldmill.engine.evaluate (run.py:1008-1074).  Extra
     keyword ``result``: "python" (the reference's payload: lists, tuples,
     dicts), "device" (DVec / DDict handles left in HBM) or "numpy".
+    Thread-safe: concurrent calls run one after another.
     """
+    with _EVAL_LOCK:
+        return _evaluate(e, env, config, externs, result=result, idx0=idx0, _ctx_out=_ctx_out)
+
+
+def _evaluate(e, env=None, config=None, externs=None, *, result="python", idx0=0, _ctx_out=None):
     cfg = config or EngineConfig()
     if cfg.threads < 1:
         raise EvalError("threads must be at least 1")

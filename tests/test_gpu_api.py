@@ -92,3 +92,31 @@ def test_reference_cli_runs_on_the_gpu(tmp_path, capsys):
     finally:
         wg.uninstall()
     assert gpu_out.read_bytes() == cpu_out.read_bytes()
+
+
+def test_concurrent_evaluate_calls_match_reference():
+    """The reference allows evaluate() from several threads; the device
+    executor serialises them (one process-wide runtime) and every thread
+    gets its own correct result."""
+    import threading
+    import paper_1709_06416_b200 as wg
+    want = [_run(src, inputs) for src, inputs in PROGRAMS]
+    wg.install()
+    got = [None] * (2 * len(PROGRAMS))
+    errs = []
+
+    def work(j):
+        try:
+            got[j] = _run(*PROGRAMS[j % len(PROGRAMS)])
+        except Exception as ex:       # surfaced below
+            errs.append(ex)
+    try:
+        ts = [threading.Thread(target=work, args=(j,)) for j in range(len(got))]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+    finally:
+        wg.uninstall()
+    assert not errs, errs
+    assert got == want + want
