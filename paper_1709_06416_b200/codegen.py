@@ -2393,7 +2393,7 @@ def _deferred_dict_lines(g, b):
     L.append(f"      u64 h_[ITEMS], c_[ITEMS];")
     L.append("#pragma unroll")
     L.append(f"      for (int j = 0; j < ITEMS; ++j) {{ h_[j] = wg_ht_home(dkk{B}[j], {P['mask']}); "
-             f"c_[j] = dkf{B}[j] ? *(volatile u64*)({P['table']} + h_[j] * {sw}) : 0ULL; }}")
+             f"c_[j] = dkf{B}[j] ? WG_PROBE_LD({P['table']} + h_[j] * {sw}) : 0ULL; }}")
     L.append("#pragma unroll")
     L.append("      for (int j = 0; j < ITEMS; ++j) {")
     L.append(f"        if (!dkf{B}[j]) continue;")

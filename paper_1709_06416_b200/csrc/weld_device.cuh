@@ -521,6 +521,14 @@ __device__ __forceinline__ u64 wg_mix64(u64 x) {
 // table's distinct-key counter at kernel end -- no contended global
 // counter on the insert path).
 #define WG_MAX_PROBE 128
+// Probe read of a single-word key slot: an L2 (cg) load.  A slot moves from
+// EMPTY to its key exactly once (CAS), so a stale EMPTY only costs a failed
+// CAS that returns the key; no system-scope (volatile) load is needed.
+#ifndef WG_PROBE_VOLATILE
+#define WG_PROBE_LD(p) __ldcg((const unsigned long long*)(p))
+#else
+#define WG_PROBE_LD(p) (*(volatile u64*)(p))
+#endif
 __device__ __forceinline__ i64 wg_ht_find1(u64* table, int slot_words, u64 mask, u64 key, int& claims) {
   if (key == WG_EMPTY_KEY) {
     // Dedicated slot for the sentinel value (claim word EMPTY -> 0).
@@ -533,7 +541,7 @@ __device__ __forceinline__ i64 wg_ht_find1(u64* table, int slot_words, u64 mask,
 #pragma unroll 1
   for (int probe = 0; probe < WG_MAX_PROBE; ++probe) {
     u64* s = table + h * (u64)slot_words;
-    u64 cur = *(volatile u64*)s;
+    u64 cur = WG_PROBE_LD(s);
     if (cur == key) return (i64)h;
     if (cur == WG_EMPTY_KEY) {
       u64 prev = atomicCAS((unsigned long long*)s, WG_EMPTY_KEY, key);
@@ -734,7 +742,7 @@ __device__ __forceinline__ i64 wg_ht_resolve1(u64* table, int slot_words, u64 ma
       if (prev == key) return (i64)h;
     }
     h = (h + 1) & mask;
-    cur = *(volatile u64*)(table + h * (u64)slot_words);
+    cur = WG_PROBE_LD(table + h * (u64)slot_words);
   }
   return -1;
 }

@@ -656,20 +656,37 @@ __device__ __forceinline__ uint64_t wg_okey_col(const void* src, int kind, uint6
   }
 }
 
-__global__ void k_okey_minmax(const void* keys, int kind, uint64_t n, unsigned long long* mm, uint64_t* ok) {
-  uint64_t lo = ~0ULL, hi = 0;
+// Order keys of a key column, their min/max (mm[0..1]) and, when vals is
+// given, the min/max of the 8-byte values' flipped bits v ^ 2^63 (mm[4..5]:
+// the payload-narrowing test of the sort).
+__global__ void k_okey_minmax(const void* keys, int kind, uint64_t n, unsigned long long* mm, uint64_t* ok,
+                              const uint64_t* vals) {
+  uint64_t lo = ~0ULL, hi = 0, vlo = ~0ULL, vhi = 0;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t v = wg_okey_col(keys, kind, i);
     ok[i] = v;
     lo = v < lo ? v : lo;
     hi = v > hi ? v : hi;
+    if (vals) {
+      const uint64_t w = __ldcs(vals + i) ^ (1ULL << 63);
+      vlo = w < vlo ? w : vlo;
+      vhi = w > vhi ? w : vhi;
+    }
   }
   for (int d = 16; d > 0; d >>= 1) {
     uint64_t a = __shfl_xor_sync(0xffffffffu, lo, d), b = __shfl_xor_sync(0xffffffffu, hi, d);
     lo = a < lo ? a : lo;
     hi = b > hi ? b : hi;
+    a = __shfl_xor_sync(0xffffffffu, vlo, d);
+    b = __shfl_xor_sync(0xffffffffu, vhi, d);
+    vlo = a < vlo ? a : vlo;
+    vhi = b > vhi ? b : vhi;
   }
-  if ((threadIdx.x & 31) == 0) { atomicMin(mm, lo); atomicMax(mm + 1, hi); }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(mm, lo);
+    atomicMax(mm + 1, hi);
+    if (vals) { atomicMin(mm + 4, vlo); atomicMax(mm + 5, vhi); }
+  }
 }
 
 // order keys relative to the minimum (same order, fewer varying bits)
@@ -1254,6 +1271,37 @@ namespace {
 // (kin, vin); the result lands in (kA, vA); (kB, vB) are ping-pong scratch.
 // Stability is what makes multi-field lexicographic sorts (last field first)
 // and order-preserving grouping correct.
+template <typename K, typename VI, typename VS, typename VO, typename CV>
+int onesweep_pass(const K* ki, const VI* vi, K* ko, VO* vo, uint64_t n, int shift, int wbits, const uint32_t* gofs,
+                  unsigned long long* status, uint32_t* ctr, uint64_t vbase) {
+  constexpr int ITEMS = 8, TILE = 512 * ITEMS;
+  constexpr int SMEM = wgr::onesweep_smem<K, VS, ITEMS>();
+  static bool attr_set = false;   // per template instance
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(wgr::k_onesweep<K, VI, VS, VO, CV, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    attr_set = true;
+  }
+  const uint64_t tiles = (n + TILE - 1) / TILE;
+  CK(cudaMemsetAsync(status, 0, tiles * wgr::RADIX * 8, g_stream));
+  { WG_PROF("k_onesweep"); wgr::k_onesweep<K, VI, VS, VO, CV, ITEMS><<<(unsigned)tiles, 512, SMEM, g_stream>>>(
+      ki, vi, ko, vo, (uint32_t)n, shift, (1u << wbits) - 1u, gofs, status, ctr, vbase); }
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// Histogram + offsets of every pass; *status sized for the tiles of a pass.
+template <typename K>
+int radix_prologue(const K* kin, uint64_t n, int begin_bit, int end_bit, int npass, uint32_t** hist,
+                   unsigned long long** status) {
+  const uint64_t tiles = (n + 4095) / 4096;
+  CK(cudaMallocAsync((void**)hist, (npass * wgr::RADIX + npass) * 4, g_stream));
+  CK(cudaMemsetAsync(*hist, 0, (npass * wgr::RADIX + npass) * 4, g_stream));
+  CK(cudaMallocAsync((void**)status, tiles * wgr::RADIX * 8, g_stream));
+  { WG_PROF("k_radix_hist"); wgr::k_radix_hist<K><<<grid_for(n, 256), 256, 0, g_stream>>>(kin, n, begin_bit, end_bit, npass, *hist); }
+  { WG_PROF("k_radix_offsets"); wgr::k_radix_offsets<<<npass, wgr::RADIX, 0, g_stream>>>(*hist); }
+  return 0;
+}
+
 template <typename K, typename V>
 int radix_sort(const K* kin, const V* vin, K* kA, K* kB, V* vA, V* vB, uint64_t n, int begin_bit, int end_bit) {
   if (n > 0xffffffffULL) return fail("radix sort: more than 2^32 items");
@@ -1264,22 +1312,10 @@ int radix_sort(const K* kin, const V* vin, K* kA, K* kB, V* vA, V* vB, uint64_t 
     if ((const void*)vA != (const void*)vin) CK(cudaMemcpyAsync(vA, vin, n * sizeof(V), cudaMemcpyDeviceToDevice, g_stream));
     return 0;
   }
-  constexpr int ITEMS = 8, TILE = 512 * ITEMS;
-  constexpr int SMEM = wgr::onesweep_smem<K, V, ITEMS>();
-  static bool attr_set = false;   // per template instance
-  if (!attr_set) {
-    CK(cudaFuncSetAttribute(wgr::k_onesweep<K, V, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-    attr_set = true;
-  }
-  const uint64_t tiles = (n + TILE - 1) / TILE;
   uint32_t* hist;
   unsigned long long* status;
-  CK(cudaMallocAsync((void**)&hist, (npass * wgr::RADIX + npass) * 4, g_stream));
+  if (radix_prologue<K>(kin, n, begin_bit, end_bit, npass, &hist, &status)) return -1;
   uint32_t* ctr = hist + npass * wgr::RADIX;
-  CK(cudaMemsetAsync(hist, 0, (npass * wgr::RADIX + npass) * 4, g_stream));
-  CK(cudaMallocAsync((void**)&status, tiles * wgr::RADIX * 8, g_stream));
-  { WG_PROF("k_radix_hist"); wgr::k_radix_hist<K><<<grid_for(n, 256), 256, 0, g_stream>>>(kin, n, begin_bit, end_bit, npass, hist); }
-  { WG_PROF("k_radix_offsets"); wgr::k_radix_offsets<<<npass, wgr::RADIX, 0, g_stream>>>(hist); }
   const K* ki = kin;
   const V* vi = vin;
   for (int p = 0; p < npass; ++p) {
@@ -1288,12 +1324,50 @@ int radix_sort(const K* kin, const V* vin, K* kA, K* kB, V* vA, V* vB, uint64_t 
     V* vo = toA ? vA : vB;
     const int shift = begin_bit + 8 * p;
     const int wbits = end_bit - shift < 8 ? end_bit - shift : 8;
-    CK(cudaMemsetAsync(status, 0, tiles * wgr::RADIX * 8, g_stream));
-    { WG_PROF("k_onesweep"); wgr::k_onesweep<K, V, ITEMS><<<(unsigned)tiles, 512, SMEM, g_stream>>>(
-        ki, vi, ko, vo, (uint32_t)n, shift, (1u << wbits) - 1u, hist + p * wgr::RADIX, status, ctr + p); }
-    CK(cudaGetLastError());
+    if (onesweep_pass<K, V, V, V, wgr::VCopy>(ki, vi, ko, vo, n, shift, wbits, hist + p * wgr::RADIX, status, ctr + p, 0))
+      return -1;
     ki = ko;
     vi = vo;
+  }
+  CK(cudaFreeAsync(status, g_stream));
+  CK(cudaFreeAsync(hist, g_stream));
+  return 0;
+}
+
+// The same sort with a narrowed payload: 8-byte values whose flipped bits
+// (v ^ 2^63) lie in [vbase, vbase + 2^32) travel as u32 offsets (t0/t1
+// scratch, n words each) -- 12 instead of 16 bytes per row per pass for u64
+// keys.  Needs at least two passes; the result lands in (kA, vout).
+template <typename K>
+int radix_sort_narrow(const K* kin, const uint64_t* vin, K* kA, K* kB, uint64_t* vout, uint32_t* t0, uint32_t* t1,
+                      uint64_t n, int begin_bit, int end_bit, uint64_t vbase) {
+  if (n > 0xffffffffULL) return fail("radix sort: more than 2^32 items");
+  const int npass = end_bit > begin_bit ? (end_bit - begin_bit + 7) / 8 : 0;
+  if (npass < 2) return fail("radix_sort_narrow: needs two passes or more");
+  uint32_t* hist;
+  unsigned long long* status;
+  if (radix_prologue<K>(kin, n, begin_bit, end_bit, npass, &hist, &status)) return -1;
+  uint32_t* ctr = hist + npass * wgr::RADIX;
+  const K* ki = kin;
+  const uint32_t* ti = nullptr;
+  for (int p = 0; p < npass; ++p) {
+    const bool toA = ((npass - 1 - p) & 1) == 0;
+    K* ko = toA ? kA : kB;
+    uint32_t* to = (p & 1) ? t1 : t0;
+    const int shift = begin_bit + 8 * p;
+    const int wbits = end_bit - shift < 8 ? end_bit - shift : 8;
+    int rc;
+    if (p == 0)
+      rc = onesweep_pass<K, uint64_t, uint32_t, uint32_t, wgr::VNarrow>(ki, vin, ko, to, n, shift, wbits, hist, status, ctr, vbase);
+    else if (p == npass - 1)
+      rc = onesweep_pass<K, uint32_t, uint32_t, uint64_t, wgr::VWiden>(ki, ti, ko, vout, n, shift, wbits, hist + p * wgr::RADIX,
+                                                                       status, ctr + p, vbase);
+    else
+      rc = onesweep_pass<K, uint32_t, uint32_t, uint32_t, wgr::VCopy>(ki, ti, ko, to, n, shift, wbits, hist + p * wgr::RADIX,
+                                                                      status, ctr + p, 0);
+    if (rc) return -1;
+    ki = ko;
+    ti = to;
   }
   CK(cudaFreeAsync(status, g_stream));
   CK(cudaFreeAsync(hist, g_stream));
@@ -1394,6 +1468,7 @@ int wg_run_starts(const uint64_t* key_words, int kw, uint64_t n, uint64_t starts
 // radix sort on the top 32 varying bits, then a stable insertion sort
 // inside the (small) buckets; skewed data falls back to a full radix sort.
 static bool g_group_u32 = getenv("WELDGPU_GROUP_U32") == nullptr || getenv("WELDGPU_GROUP_U32")[0] != '0';
+static bool g_group_narrow = getenv("WELDGPU_GROUP_NARROW") == nullptr || getenv("WELDGPU_GROUP_NARROW")[0] != '0';
 
 int wg_group_finish1(uint64_t keys, int key_kind, uint64_t vals, int val_width, uint64_t n, uint64_t ukeys_out,
                      uint64_t offs_out, uint64_t vals_out, uint64_t* K_out) {
@@ -1424,15 +1499,20 @@ int wg_group_finish1(uint64_t keys, int key_kind, uint64_t vals, int val_width, 
   CK(cudaMallocAsync((void**)&vB, n * 8, g_stream));
   // the last radix pass writes the values straight into vals_out when they are 8 bytes wide
   if (own_v0) CK(cudaMallocAsync((void**)&vA, n * 8, g_stream)); else vA = (uint64_t*)(uintptr_t)vals_out;
-  CK(cudaMallocAsync((void**)&mm, 32, g_stream));
+  CK(cudaMallocAsync((void**)&mm, 48, g_stream));
   flag = (int*)(mm + 2);
-  uint64_t init[4] = {~0ULL, 0ULL, 0ULL, 0ULL};
-  CK(cudaMemcpyAsync(mm, init, 32, cudaMemcpyHostToDevice, g_stream));
-  { WG_PROF("k_okey_minmax"); k_okey_minmax<<<g, 256, 0, g_stream>>>((const void*)(uintptr_t)keys, key_kind, n, mm, k0); }
+  uint64_t init[6] = {~0ULL, 0ULL, 0ULL, 0ULL, ~0ULL, 0ULL};
+  CK(cudaMemcpyAsync(mm, init, 48, cudaMemcpyHostToDevice, g_stream));
+  const bool try_narrow = !own_v0 && g_group_narrow;
+  { WG_PROF("k_okey_minmax"); k_okey_minmax<<<g, 256, 0, g_stream>>>((const void*)(uintptr_t)keys, key_kind, n, mm, k0,
+                                                                   try_narrow ? v0 : nullptr); }
   if (own_v0) { WG_PROF("k_widen"); k_widen<<<g, 256, 0, g_stream>>>((const void*)(uintptr_t)vals, v0, val_width, n); }
-  unsigned long long hmm[2];
-  CK(cudaMemcpyAsync(hmm, mm, 16, cudaMemcpyDeviceToHost, g_stream));
+  unsigned long long hmm[6];
+  CK(cudaMemcpyAsync(hmm, mm, 48, cudaMemcpyDeviceToHost, g_stream));
   CK(cudaStreamSynchronize(g_stream));
+  // values narrow to u32 offsets when their flipped bits span < 2^32
+  const bool narrow = try_narrow && hmm[5] - hmm[4] <= 0xffffffffULL;
+  const uint64_t vbase = hmm[4];
   const uint64_t diff = hmm[0] ^ hmm[1], span = hmm[1] - hmm[0];
   int vbits = diff ? 64 - __builtin_clzll(diff) : 1;   // bits above vbits are equal in every key
   const int rbits = span ? 64 - __builtin_clzll(span) : 1;
@@ -1459,12 +1539,17 @@ int wg_group_finish1(uint64_t keys, int key_kind, uint64_t vals, int val_width, 
     uint32_t* wA = (uint32_t*)kA;
     uint32_t* wB = w0 + n;                                      // kB holds w0 and wB (2 x 4n bytes)
     { WG_PROF("k_key_u32"); k_key_u32<<<g, 256, 0, g_stream>>>(k0, n, sub, w0); }
-    if (radix_sort<uint32_t, uint64_t>(w0, v0, wA, wB, vA, vB, n, 0, vbits)) return -1;
+    if (narrow && vbits > 8) {
+      if (radix_sort_narrow<uint32_t>(w0, v0, wA, wB, vA, (uint32_t*)vB, (uint32_t*)vB + n, n, 0, vbits, vbase)) return -1;
+    } else if (radix_sort<uint32_t, uint64_t>(w0, v0, wA, wB, vA, vB, n, 0, vbits)) return -1;
     if (run_heads(wgr::EqU32{wA}, n, starts, &hK)) return -1;
     { WG_PROF("k_group_out"); k_group_out<uint32_t><<<grid_for(hK + 1, 256), 256, 0, g_stream>>>(
         starts, hK, n, wA, recon, key_kind, (int64_t*)(uintptr_t)offs_out, (void*)(uintptr_t)ukeys_out); }
   } else {
-    if (radix_sort<uint64_t, uint64_t>(k0, v0, kA, kB, vA, vB, n, begin_bit, vbits)) return -1;
+    if (narrow && vbits - begin_bit > 8) {
+      if (radix_sort_narrow<uint64_t>(k0, v0, kA, kB, vA, (uint32_t*)vB, (uint32_t*)vB + n, n, begin_bit, vbits, vbase))
+        return -1;
+    } else if (radix_sort<uint64_t, uint64_t>(k0, v0, kA, kB, vA, vB, n, begin_bit, vbits)) return -1;
     if (begin_bit > 0) {
       uint64_t cap = n / 8 + 1024;
       uint32_t* pos = starts;             // scratch until the run starts are computed

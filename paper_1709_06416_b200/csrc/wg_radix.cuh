@@ -110,11 +110,28 @@ constexpr int onesweep_smem() {
   return 512 * ITEMS * (int)(sizeof(K) + sizeof(V)) + (512 / 32) * RADIX * 2;
 }
 
-template <typename K, typename V, int ITEMS>
+// Payload conversions of a pass (value in -> staged -> value out).  Narrowed
+// payloads: 8-byte values whose order-flipped bits (v ^ 2^63) span less than
+// 2^32 travel the middle passes as u32 offsets from their minimum.
+struct VCopy {
+  template <typename T> __device__ static T in(T v, uint64_t) { return v; }
+  template <typename T> __device__ static T out(T v, uint64_t) { return v; }
+};
+struct VNarrow {   // first pass: u64 in, u32 staged and out
+  __device__ static uint32_t in(uint64_t v, uint64_t base) { return (uint32_t)((v ^ (1ULL << 63)) - base); }
+  __device__ static uint32_t out(uint32_t v, uint64_t) { return v; }
+};
+struct VWiden {    // last pass: u32 in and staged, u64 out
+  __device__ static uint32_t in(uint32_t v, uint64_t) { return v; }
+  __device__ static uint64_t out(uint32_t v, uint64_t base) { return ((uint64_t)v + base) ^ (1ULL << 63); }
+};
+
+template <typename K, typename VI, typename VS, typename VO, typename CV, int ITEMS>
 __global__ void __launch_bounds__(512, 2)
-k_onesweep(const K* __restrict__ kin, const V* __restrict__ vin, K* __restrict__ kout, V* __restrict__ vout,
+k_onesweep(const K* __restrict__ kin, const VI* __restrict__ vin, K* __restrict__ kout, VO* __restrict__ vout,
            uint32_t n, int shift, uint32_t dmask, const uint32_t* __restrict__ gofs, unsigned long long* status,
-           uint32_t* tile_ctr) {
+           uint32_t* tile_ctr, uint64_t vbase) {
+  using V = VS;
   constexpr int BLOCK = 512, WARPS = BLOCK / 32, TILE = BLOCK * ITEMS;
   extern __shared__ __align__(16) unsigned char s_dyn[];
   K* s_k = reinterpret_cast<K*>(s_dyn);
@@ -140,7 +157,7 @@ k_onesweep(const K* __restrict__ kin, const V* __restrict__ vin, K* __restrict__
     const uint32_t row = wbase + i * 32 + lane;
     const bool ok = row < n;
     k[i] = ok ? kin[row] : (K)0;
-    v[i] = ok ? vin[row] : (V)0;
+    v[i] = ok ? CV::in(vin[row], vbase) : (V)0;
   }
   const unsigned lt = lanemask_lt();
   // peer masks of every round first (independent, pipelined), then the
@@ -256,7 +273,7 @@ k_onesweep(const K* __restrict__ kin, const V* __restrict__ vin, K* __restrict__
       const K kk = s_k[idx];
       const uint32_t dst = s_dbase[digit_of(kk, shift, dmask)] + idx;
       kout[dst] = kk;
-      vout[dst] = s_v[idx];
+      vout[dst] = CV::out(s_v[idx], vbase);
     }
   }
 }

@@ -31,7 +31,7 @@ int ours(const K* kin, const V* vin, K* kA, K* kB, V* vA, V* vB, uint32_t n, int
 #endif
   constexpr int ITEMS = AB_ITEMS, TILE = 512 * ITEMS;
   constexpr int SMEM = wgr::onesweep_smem<K, V, ITEMS>();
-  cudaFuncSetAttribute(wgr::k_onesweep<K, V, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  cudaFuncSetAttribute(wgr::k_onesweep<K, V, V, V, wgr::VCopy, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
   const uint64_t tiles = (n + TILE - 1) / TILE;
   static uint32_t* hist = nullptr; static unsigned long long* status = nullptr;
   if (!hist) { cudaMalloc(&hist, 9 * 256 * 4); cudaMalloc(&status, tiles * 256 * 8); }
@@ -44,8 +44,8 @@ int ours(const K* kin, const V* vin, K* kA, K* kB, V* vA, V* vB, uint32_t n, int
     K* ko = toA ? kA : kB; V* vo = toA ? vA : vB;
     const int shift = begin + 8 * p, wb = std::min(8, end - shift);
     cudaMemsetAsync(status, 0, tiles * 256 * 8, s);
-    wgr::k_onesweep<K, V, ITEMS><<<(unsigned)tiles, 512, SMEM, s>>>(ki, vi, ko, vo, n, shift, (1u << wb) - 1u,
-                                                                  hist + p * 256, status, hist + npass * 256 + p);
+    wgr::k_onesweep<K, V, V, V, wgr::VCopy, ITEMS><<<(unsigned)tiles, 512, SMEM, s>>>(ki, vi, ko, vo, n, shift, (1u << wb) - 1u,
+                                                                  hist + p * 256, status, hist + npass * 256 + p, 0);
     ki = ko; vi = vo;
   }
   return 0;
