@@ -29,21 +29,33 @@ __version__ = "0.1.0"
 _installed = {}
 
 
-def install():
+def install(zero_copy=True):
     """Rebind the reference API's executor (api.py:23 imports `evaluate` by
     name; api.py:374 calls it) so evaluate_object, the CLI and the foreign
-    surface run on the GPU."""
+    surface run on the GPU.  zero_copy=True (default) also binds data
+    leaves straight to HBM and encodes flat-vector results from the device
+    columns (api_bridge: no per-leaf encode/decode round trip, api.py:224-226)."""
     import weldmill.api as api
-    if "api" not in _installed:
+    uninstall()
+    if zero_copy:
+        from . import api_bridge
+        api_bridge.install()
+        _installed["bridge"] = True
+    else:
         _installed["api"] = api.evaluate
-    api.evaluate = evaluate
+        api.evaluate = evaluate
 
 
 def uninstall():
     import weldmill.api as api
+    if _installed.pop("bridge", None):
+        from . import api_bridge
+        api_bridge.uninstall()
     if "api" in _installed:
         api.evaluate = _installed.pop("api")
 
 
-__all__ = ["evaluate", "install", "uninstall", "EngineConfig", "EvalStats", "Value", "DeviceUnsupported", "DVec",
+from .api_bridge import column_encoder  # noqa: E402,F401
+
+__all__ = ["evaluate", "install", "uninstall", "column_encoder", "EngineConfig", "EvalStats", "Value", "DeviceUnsupported", "DVec",
            "to_device", "to_numpy", "to_payload", "to_boundary_bytes"]

@@ -4,6 +4,7 @@ WeldResult, api.py:113-404) with install() routing its executor seam
 (api.py:23 import, :374 call) to the B200 executor.  Results must be the
 same boundary bytes as the reference CPU engine's; staged errors must carry
 the same stage and error class (api.py:373-376)."""
+import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
@@ -120,3 +121,104 @@ def test_concurrent_evaluate_calls_match_reference():
         wg.uninstall()
     assert not errs, errs
     assert got == want + want
+
+
+ZC_PROGRAMS = [
+    ("result(for(zip(v0, v1), merger[f64, +], (b, i, x) => if (x.0 > 10, merge(b, x.1 * 2.0), b)))",
+     [("vec[i32]", np.arange(-50, 2000, dtype=np.int32)), ("vec[f64]", np.arange(2050) * 0.25)]),
+    ("filter(v0, (x) => x.0 % 3 == 0)",
+     [("vec[{i64,f64}]", (np.arange(5000, dtype=np.int64), np.arange(5000) * 0.25))]),
+    ("tovec(result(for(v0, dictmerger[i64, i64, +], (b, i, x) => merge(b, {x % 97, x}))))",
+     [("vec[i64]", np.arange(100000, dtype=np.int64) * 7919)]),
+    ("map(v0, (x) => x * 3 + 1)", [("vec[i64]", np.arange(-3000, 3000, dtype=np.int64))]),
+    ("sort(v0, (x) => 0.0 - x)", [("vec[f64]", np.sin(np.arange(3000.0)))]),
+]
+
+
+def _lists(data):
+    if isinstance(data, tuple):
+        return [tuple(r) for r in zip(*(c.tolist() for c in data))]
+    return data.tolist()
+
+
+@pytest.mark.parametrize("src,inputs", ZC_PROGRAMS, ids=[p[0][:40] for p in ZC_PROGRAMS])
+def test_zero_copy_leaves_bypass_the_codec(src, inputs):
+    """install() binds numpy-column leaves straight to HBM: after the leaf's
+    creation-time validation, evaluate_object makes no encode/decode call on
+    it (the reference's build_program would round-trip every leaf through
+    boundary bytes, api.py:224-226) -- and the result bytes equal the
+    reference engine's over the same values given as lists."""
+    import paper_1709_06416_b200 as wg
+    from weldmill.api import Encoder, evaluate_object, free_result, new_computed_object, new_data_object
+    from weldmill.parser import parse_type_text
+    want = _run(src, [(t, _lists(d)) for t, d in inputs])
+    calls = [0]
+
+    def enc(d, t):
+        calls[0] += 1
+        return wg.column_encoder.encode(d, t)
+
+    def dec(b, t):
+        calls[0] += 1
+        return wg.column_encoder.decode(b, t)
+    counting = Encoder("counting", enc, dec)
+    objs = [new_data_object(d, parse_type_text(t), counting) for t, d in inputs]
+    created = calls[0]
+    wg.install()
+    try:
+        r = evaluate_object(new_computed_object(objs, src))
+        got = (r.ok, r.result_bytes() if r.ok else None)
+        free_result(r)
+    finally:
+        wg.uninstall()
+    assert calls[0] == created
+    assert got == want
+
+
+def test_zero_copy_foreign_bytes_leaf():
+    """foreign.weld_new_data(type, boundary bytes) keeps the bytes as the
+    leaf (no decode to lists) under install(); results match the reference."""
+    import paper_1709_06416_b200 as wg
+    from weldmill import foreign
+    from weldmill.boundary import encode_value
+    from weldmill.parser import parse_type_text
+
+    def run():
+        h = foreign.weld_new_data("vec[{i64,f64}]", encode_value([(i, i * 0.5) for i in range(4000)],
+                                                                  parse_type_text("vec[{i64,f64}]")))
+        c = foreign.weld_new_computed([h], "result(for(v0, merger[f64, +], (b, i, x) => merge(b, x.1 * cast(x.0, f64))))")
+        r = foreign.weld_evaluate(c)
+        return foreign.weld_result_error(r), foreign.weld_result_bytes(r)
+    want = run()
+    wg.install()
+    try:
+        got = run()
+    finally:
+        wg.uninstall()
+    assert want[0] is None and got == want
+
+
+def test_zero_copy_cli_manifest_path_input(tmp_path, capsys):
+    """A manifest 'path' input (boundary bytes file, cli.py:150-153) reaches
+    the device as bytes; stdout and --out bytes equal the CPU engine's."""
+    import json
+    import paper_1709_06416_b200 as wg
+    from weldmill import cli
+    from weldmill.boundary import encode_value
+    from weldmill.parser import parse_type_text
+    (tmp_path / "v.bin").write_bytes(encode_value(list(range(-500, 70000)), parse_type_text("vec[i64]")))
+    (tmp_path / "p.ir").write_text("filter(v0, (x) => x % 7 == 3)")
+    (tmp_path / "m.json").write_text(json.dumps([{"name": "v0", "type": "vec[i64]", "path": "v.bin"}]))
+
+    def run(out):
+        capsys.readouterr()
+        assert cli.main(["run", str(tmp_path / "p.ir"), "--inputs", str(tmp_path / "m.json"), "--out", str(out)]) == 0
+        return capsys.readouterr().out
+    want = run(tmp_path / "cpu.bin")
+    wg.install()
+    try:
+        got = run(tmp_path / "gpu.bin")
+    finally:
+        wg.uninstall()
+    assert got == want
+    assert (tmp_path / "gpu.bin").read_bytes() == (tmp_path / "cpu.bin").read_bytes()
