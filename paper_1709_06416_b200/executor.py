@@ -33,7 +33,7 @@ from weldmill.expr import (Apply, BinaryOp, BitSelect, Broadcast, CastScalar, Ex
 from . import runtime as rt
 from . import semantics as sem
 from .builders_dev import (_finish_small, AppenderDev, DDict, DGroups, DictDev, GroupDev, MergerDev, VecMergerDev,
-                           dict_payload, finish_dict, finish_groups, gather_cols, sort_perm, tovec)
+                           Segment, dict_payload, finish_dict, finish_groups, gather_cols, sort_perm, tovec)
 from .codegen import DEFER_DICT, PIPE_STAGES, BSpec, IterSpec, generate
 from .columns import Col, DVec, to_device, to_payload, dvec_from_cols
 from .irtypes import (BOOL, F32, F64, I64, SIZE, identity_value, Builder, DeviceUnsupported as _DU, Dict, DictMerger, Function,
@@ -943,11 +943,28 @@ class Ctx:
         self.launches += 1
         self.dirty = True
         if self.rec is not None:
-            if sizes is not None or segstats or plan.count_nodes or plan.stat_nodes or \
-                    not all(isinstance(bmap[b.bid], MergerDev) for b in plan.builders):
+            outs = {}
+            ok = not (sizes is not None or segstats or plan.count_nodes or plan.stat_nodes)
+            for b in plan.builders:
+                st = bmap[b.bid]
+                if isinstance(st, MergerDev):
+                    continue
+                if (isinstance(st, AppenderDev) and isinstance(b.kind, VecBuilder) and b.mode == "direct"
+                        and not b.extra.get("nested") and len(st.segments) == 1):
+                    # replayed with fresh output columns patched into the blob
+                    idx = [next((i for i, p in enumerate(plan.params) if p.key == ("b", b.bid, "col", f)), None)
+                           for f in range(len(st.kinds))]
+                    if None in idx:
+                        ok = False
+                        break
+                    outs[id(st)] = (idx, st.segments[0].cap)
+                    continue
+                ok = False
+                break
+            if not ok:
                 self.rec = None
             else:
-                self.rec.append((kern, grid, nthr, blob, smem))
+                self.rec.append((kern, grid, nthr, blob, smem, outs))
         for st, seg, coff, c0, c1 in segstats:
             out = rt.alloc(32)
             rt.call("wg_seg_stats", coff.ptr, c1 - c0 + 1, seg.total_buf.ptr, out.ptr)
@@ -1588,9 +1605,10 @@ def _evaluate(e, env=None, config=None, externs=None, *, result="python", idx0=0
         lb = getattr(ctx, "_last_builders", None)
         if lb is not None:
             _collect_builders(lb, bl)
-        if bl and all(isinstance(b, MergerDev) for b in bl):
-            _REPLAYS.put(rkey, _Replay(e, env, cfg, externs, ctx, bl, stats))
-            if any(not b.mirrored for b in bl):
+        outs = ctx.rec[0][5]
+        if bl and all(isinstance(b, MergerDev) or id(b) in outs for b in bl):
+            _REPLAYS.put(rkey, _Replay(e, env, cfg, externs, ctx, bl, stats, result))
+            if any(isinstance(b, MergerDev) and not b.mirrored for b in bl):
                 _REPLAYS.d.pop(rkey, None)
     return Value(e.ty, payload), stats
 
@@ -1639,20 +1657,33 @@ def _replay_key(e, env, externs, result):
 
 
 class _Replay:
-    __slots__ = ("e", "inputs", "cfg", "externs", "launch", "mergers", "stats", "keep", "lock", "shape")
+    """One recorded single-launch evaluation: merger slots are re-read from
+    their pinned mirrors; DIRECT vecbuilder outputs get fresh columns patched
+    into the parameter blob (the recorded run's outputs belong to its caller
+    and are not kept)."""
+    __slots__ = ("e", "inputs", "cfg", "externs", "launch", "builders", "stats", "keep", "lock", "shape", "result",
+                 "mergers")
 
-    def __init__(self, e, env, cfg, externs, ctx, mergers, stats):
+    def __init__(self, e, env, cfg, externs, ctx, builders, stats, result="python"):
         from dataclasses import replace
         self.e = e
         self.inputs = {k: (v.data if isinstance(v, Value) else v) for k, v in env.items()}
         self.cfg = replace(cfg)
         self.externs = dict(externs or {})
-        self.launch = ctx.rec[0]
-        self.mergers = list(mergers)
+        kern, grid, nthr, blob, smem, outs = ctx.rec[0]
+        self.launch = (kern, grid, nthr, blob, smem)
+        # per builder, in result order: the merger, or (elem type, leaf kinds,
+        # rows, blob word index of each leaf column)
+        self.builders = [b if isinstance(b, MergerDev) else (b.kind.elem, list(b.kinds), outs[id(b)][1], outs[id(b)][0])
+                         for b in builders]
+        self.mergers = [b for b in builders if isinstance(b, MergerDev)]
         self.stats = stats
-        self.keep = (ctx._ticket, ctx._keep)
+        res = ctx._keep[1] if ctx._keep else None
+        keep_res = {k: v for k, v in res.items() if not isinstance(v, Segment)} if isinstance(res, dict) else None
+        self.keep = (ctx._ticket, ctx._keep[0] if ctx._keep else None, keep_res)
         self.lock = threading.Lock()
         self.shape = ctx._last_builders
+        self.result = result
 
     def valid(self, e, env, cfg, externs):
         if e is not self.e or cfg != self.cfg or len(env) != len(self.inputs):
@@ -1667,23 +1698,44 @@ class _Replay:
     def run(self, e):
         note_evaluation()
         kern, grid, block, blob, smem = self.launch
+        vals = []
         with self.lock:
+            if len(self.mergers) < len(self.builders):
+                blob = bytearray(blob)
+                for b in self.builders:
+                    if isinstance(b, MergerDev):
+                        continue
+                    elem, kinds, rows, idx = b
+                    cols = [Col.alloc(k, rows) for k in kinds]
+                    for i, c in zip(idx, cols):
+                        _struct.pack_into("<Q", blob, 8 * i, c.ptr)
+                    vals.append(dvec_from_cols(elem, rows, cols))
+                blob = bytes(blob)
             kern.launch(grid, block, blob, smem)
-            vals = []
-            for q, b in enumerate(self.mergers):
-                if q == 0:
-                    err = []
-                    vals.append(b.read(err))
-                    code, info = err[0]
-                    if code:
-                        raise device_error(code, info)
-                else:
-                    vals.append(b.read())
-        if len(vals) == 1 and not isinstance(self.shape, tuple):
-            payload = vals[0]
+            if self.mergers:
+                mv = []
+                for q, b in enumerate(self.mergers):
+                    if q == 0:
+                        err = []
+                        mv.append(b.read(err))
+                        code, info = err[0]
+                        if code:
+                            raise device_error(code, info)
+                    else:
+                        mv.append(b.read())
+            else:
+                code, info = rt.read_error()
+                if code:
+                    raise device_error(code, info)
+        mi, ai = iter(mv if self.mergers else ()), iter(vals)
+        leaf = lambda b: next(mi) if isinstance(b, MergerDev) else next(ai)
+        order = iter(self.builders)
+        if len(self.builders) == 1 and not isinstance(self.shape, tuple):
+            payload = leaf(self.builders[0])
         else:
-            it = iter(vals)
-            payload = _shape_like(self.shape, lambda: next(it))
+            payload = _shape_like(self.shape, lambda: leaf(next(order)))
+        if self.result == "python":
+            payload = to_host_payload(payload, e.ty)
         st = EvalStats.__new__(EvalStats)
         st.__dict__.update(self.stats.__dict__)
         st.node_evals = {}

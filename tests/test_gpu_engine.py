@@ -399,3 +399,38 @@ def test_streaming_path_stats_match_reference(monkeypatch):
                     assert getattr(got, f) == getattr(want, f), (src, level, grain, f, getattr(got, f),
                                                                  getattr(want, f))
     assert len(calls) >= 8
+
+
+def test_replayed_appender_evaluations_get_fresh_results():
+    """Launch replay of a single-launch DIRECT vecbuilder program (the C2
+    shape): every evaluate() returns its own output columns (earlier results
+    stay intact), values equal the first, non-replayed run's, and stats are
+    the same."""
+    import numpy as np
+    import paper_1709_06416_b200 as wg
+    from paper_1709_06416_b200 import executor
+    from paper_1709_06416_b200.columns import to_device, to_numpy
+    from weldmill.engine import EngineConfig, Value
+    from weldmill.parser import parse_type_text
+    tree = _front("result(for({a, b}, {vecbuilder[f64], vecbuilder[i64]}, (bs, i, x) => "
+                  "{merge(bs.0, x.0 * 2.0 + 1.0), merge(bs.1, x.1 * 3 + i)}))",
+                  _types(a="vec[f64]", b="vec[i64]"))
+    a = np.linspace(-5.0, 5.0, 100_003)
+    b = np.arange(100_003, dtype=np.int64)
+    env = {"a": Value(parse_type_text("vec[f64]"), to_device(parse_type_text("vec[f64]"), a)),
+           "b": Value(parse_type_text("vec[i64]"), to_device(parse_type_text("vec[i64]"), b))}
+    executor._REPLAYS.d.clear()
+    outs = [wg.evaluate(tree, env, EngineConfig(), result="device") for _ in range(4)]
+    assert len(executor._REPLAYS.d) == 1
+    first = [to_numpy(v) for v in outs[0][0].data]
+    assert np.array_equal(first[0], a * 2.0 + 1.0)
+    assert np.array_equal(first[1], b * 3 + np.arange(b.size))
+    ptrs = set()
+    for val, st in outs:
+        got = [to_numpy(v) for v in val.data]
+        assert all(np.array_equal(x, y) for x, y in zip(got, first))
+        ptrs.update(c.ptr for v in val.data for c in v.cols)
+        assert st.vector_traversals == outs[0][1].vector_traversals
+    assert len(ptrs) == 8           # fresh columns every call
+    py, _ = wg.evaluate(tree, env, EngineConfig())
+    assert py.data[1][:3] == [0, 4, 8]
