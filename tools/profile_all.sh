@@ -20,4 +20,10 @@ for w in blackscholes q6 q1 dict group hist filter map; do
 done
 timeout 900 ncu -f --set full --clock-control none --import-source on -k regex:wg_dagg -s 2 -c 1 -o gpurun_out/prof/full_dict_dagg \
    python bench.py --workload dict --steps 1 --warmup 3 --no-cpu --no-e2e --no-kernel-timing > gpurun_out/prof/ncu_dict_dagg.log 2>&1
+# the group step's dominant kernel is the library's onesweep radix pass
+timeout 900 ncu -f --set full --clock-control none --import-source on -k regex:k_onesweep -s 13 -c 1 -o gpurun_out/prof/full_group_onesweep \
+   python bench.py --workload group --steps 1 --warmup 3 --no-cpu --no-e2e --no-kernel-timing > gpurun_out/prof/ncu_group_onesweep.log 2>&1
+# L2 RED ceiling (C5)
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/red_peak tools/red_peak.cu && ./tools/red_peak > gpurun_out/prof/red_peak.txt 2>&1
 timeout 600 python bench.py --workload q6 --steps 20 --warmup 5 --no-cpu 2>&1 | tail -1 > gpurun_out/prof/bench_q6_1M.json
+timeout 600 python tools/api_e2e.py 1000000 > gpurun_out/prof/api_e2e.txt 2>&1

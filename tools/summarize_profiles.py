@@ -21,7 +21,12 @@ os.makedirs(OUT, exist_ok=True)
 RAW = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
        "dram__cycles_active.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
        "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread", "launch__grid_size",
-       "launch__shared_mem_per_block_dynamic", "lts__t_sectors_op_red.sum", "lts__t_sectors_op_atom.sum",
+       "launch__shared_mem_per_block_dynamic",
+       # L2 reduction / atomic traffic from the SMs (the metric names the --set full capture holds)
+       "lts__t_sectors_srcunit_tex_op_red.sum", "lts__t_sectors_srcunit_tex_op_red.sum.pct_of_peak_sustained_elapsed",
+       "lts__t_sectors_srcunit_tex_op_red_lookup_miss.sum",
+       "lts__t_sectors_srcunit_tex_op_atom.sum", "lts__t_sectors_srcunit_tex_op_atom.sum.pct_of_peak_sustained_elapsed",
+       "lts__throughput.avg.pct_of_peak_sustained_elapsed",
        "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "sm__issue_active.avg.pct_of_peak_sustained_elapsed",
        "lts__t_sector_hit_rate.pct"]
 
@@ -32,7 +37,7 @@ def raw(rep):
     if len(rows) < 3:
         return {}
     h, units, vals = rows[0], rows[1], rows[2]
-    d = {}
+    d = {"Kernel Name": (vals[h.index("Kernel Name")], "")} if "Kernel Name" in h else {}
     stalls = []
     for i, c in enumerate(h):
         if c in RAW:
@@ -74,7 +79,7 @@ for rep in sorted(glob.glob(os.path.join(SRC, "full_*.ncu-rep"))):
             bench = {}
     rows = (bench.get("config") or {}).get("rows_per_gpu")
     summary[w] = {
-        "kernel": "wg_loop (NVRTC, sm_100a)",
+        "kernel": (r.get("Kernel Name", ("wg_loop",))[0][:60] + (" (NVRTC, sm_100a)" if r.get("Kernel Name", ("wg_",))[0].startswith("wg_") else " (libweldgpu, sm_100a)")),
         "n": rows,
         "ncu_duration_ms": round(dur, 4),
         "dram_bytes": dram,
@@ -88,8 +93,12 @@ for rep in sorted(glob.glob(os.path.join(SRC, "full_*.ncu-rep"))):
         "registers": int(float(r["launch__registers_per_thread"][0])),
         "grid": int(float(r["launch__grid_size"][0])),
         "dyn_smem_bytes": r.get("launch__shared_mem_per_block_dynamic", ("0",))[0],
-        "l2_red_sectors": r.get("lts__t_sectors_op_red.sum", ("0",))[0],
-        "l2_atom_sectors": r.get("lts__t_sectors_op_atom.sum", ("0",))[0],
+        "l2_red_sectors": r.get("lts__t_sectors_srcunit_tex_op_red.sum", ("0",))[0],
+        "l2_red_pct_of_peak": r.get("lts__t_sectors_srcunit_tex_op_red.sum.pct_of_peak_sustained_elapsed", ("0",))[0],
+        "l2_red_lookup_miss_sectors": r.get("lts__t_sectors_srcunit_tex_op_red_lookup_miss.sum", ("0",))[0],
+        "l2_atom_sectors": r.get("lts__t_sectors_srcunit_tex_op_atom.sum", ("0",))[0],
+        "l2_atom_pct_of_peak": r.get("lts__t_sectors_srcunit_tex_op_atom.sum.pct_of_peak_sustained_elapsed", ("0",))[0],
+        "l2_throughput_pct": r.get("lts__throughput.avg.pct_of_peak_sustained_elapsed", ("0",))[0],
         "top_stalls": r["stalls"],
         "bench_roofline": bench.get("roofline"),
         "bench_value_rows_per_s": bench.get("value"),
@@ -101,12 +110,19 @@ with open(os.path.join(OUT, f"ncu_summary_{RND}.json"), "w") as f:
 
 lines = [f"# ncu summary ({RND}) -- one `ncu --set full --clock-control none` capture of each workload's loop kernel",
          "", "Device: B200 (sm_100a). ncu times are cold-cache and serialised (replay); bench times are live CUDA events.",
-         "", "| workload | rows | ncu ms | DRAM GB (r+w) | DRAM % | SM % | FP64 % | warps % | regs | bench kernel ms | roofline frac | top stalls |",
-         "|---|---|---|---|---|---|---|---|---|---|---|---|"]
+         "", "| workload | kernel | rows | ncu ms | DRAM GB (r+w) | DRAM % | SM % | FP64 % | L2 RED sectors (% peak) | L2 ATOM sectors (% peak) | warps % | regs | bench kernel ms | roofline frac | top stalls |",
+         "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
 for w, s in summary.items():
     rf = s["bench_roofline"] or {}
-    lines.append(f"| {w} | {s['n']} | {s['ncu_duration_ms']:.3f} | {s['dram_bytes']/1e9:.2f} | {s['dram_throughput_pct']:.0f} | "
-                 f"{s['sm_throughput_pct']:.0f} | {s['fp64_pipe_pct']:.0f} | {s['warps_active_pct']:.0f} | {s['registers']} | "
+    def _f(x):
+        try:
+            return float(str(x).replace(",", ""))
+        except ValueError:
+            return 0.0
+    lines.append(f"| {w} | `{s['kernel'].split(' (')[0][:28]}` | {s['n']} | {s['ncu_duration_ms']:.3f} | {s['dram_bytes']/1e9:.2f} | "
+                 f"{s['dram_throughput_pct']:.0f} | {s['sm_throughput_pct']:.0f} | {s['fp64_pipe_pct']:.0f} | "
+                 f"{_f(s['l2_red_sectors']):.3g} ({_f(s['l2_red_pct_of_peak']):.0f}%) | {_f(s['l2_atom_sectors']):.3g} ({_f(s['l2_atom_pct_of_peak']):.0f}%) | "
+                 f"{s['warps_active_pct']:.0f} | {s['registers']} | "
                  f"{(rf.get('kernel_ms') or 0):.3f} | {(rf.get('frac') or 0):.3f} | "
                  + ", ".join(f"{n}={v}" for n, v in s["top_stalls"][:3]) + " |")
 
