@@ -7,7 +7,7 @@ timeout 1500 python -m pytest tests -q -m gpu 2>&1 | tail -5 > gpurun_out/prof/p
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/prof/smoke.log 2>&1
 timeout 900 python bench.py 2>&1 | tail -1 > gpurun_out/prof/bench_default.json
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches_default.csv \
-  python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e --no-kernel-timing > /dev/null 2>&1
+  python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e --no-kernel-timing --per-config none > /dev/null 2>&1
 for w in blackscholes q6 q1 dict group hist filter map; do
   extra=""
   [ $w = q6 ] && extra="--n 600000000"
@@ -15,7 +15,7 @@ for w in blackscholes q6 q1 dict group hist filter map; do
   timeout 900 ncu -f --set full --clock-control none --import-source on -k regex:wg_loop -s $skip -c 1 -o gpurun_out/prof/full_$w \
      python bench.py --workload $w --steps 1 --warmup 3 --no-cpu --no-e2e --no-kernel-timing $extra > gpurun_out/prof/ncu_$w.log 2>&1
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches_$w.csv \
-     python bench.py --workload $w --steps 1 --warmup 3 --no-cpu --no-e2e --no-kernel-timing $extra > /dev/null 2>&1
+     python bench.py --workload $w --steps 1 --warmup 3 --no-cpu --no-e2e --no-kernel-timing --per-config none $extra > /dev/null 2>&1
   timeout 600 python bench.py --workload $w --steps 10 --warmup 3 --no-cpu $extra 2>&1 | tail -1 > gpurun_out/prof/bench_$w.json
 done
 timeout 900 ncu -f --set full --clock-control none --import-source on -k regex:wg_dagg -s 2 -c 1 -o gpurun_out/prof/full_dict_dagg \
