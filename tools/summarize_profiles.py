@@ -135,7 +135,7 @@ if os.path.exists(ll):
     tot = {}
     for r in rows[1:]:
         tot.setdefault(r[ki][:60], []).append(to_ms(r[vi], r[ui]))
-    lines += ["", "## Launch list of the default bench (`bench.py --steps 3 --warmup 3`, all launches)", "",
+    lines += ["", "## Launch list of the headline bench (`bench.py --steps 3 --warmup 3 --per-config none`: input generation + 3 warm-up + 3 timed steps)", "",
               "| kernel | launches | total ms | share |", "|---|---|---|---|"]
     allt = sum(sum(v) for v in tot.values())
     for k, v in sorted(tot.items(), key=lambda kv: -sum(kv[1])):
