@@ -68,6 +68,10 @@ PER_CONFIG = [
 ]
 
 
+# scattered 8-byte L2 REDs per second on B200 into an L2-resident target (profiles/red_peak_r02.txt)
+RED_PEAK = 1.86e11
+
+
 def _dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -354,6 +358,13 @@ class Runner:
                 "basis": "algorithmic bytes / device time of every kernel in the step (wg_prof events)",
                 "algorithmic_bytes": alg, "step_kernel_ms": step_kern_ms,
                 "step_frac": alg / (ms / 1e3) / 1e9 / peak}
+        if name == "hist" and step_kern_ms:
+            # C5 is bound by the L2 reduction units, not HBM: one scattered
+            # RED per row at the measured ceiling (tools/red_peak.cu,
+            # profiles/red_peak_r02.txt)
+            floor = n_total / RED_PEAK * 1e3
+            roof["ceiling"] = {"bound": "l2-red", "peak": RED_PEAK, "unit": "RED/s", "floor_ms": floor,
+                               "frac": floor / step_kern_ms, "source": "profiles/red_peak_r02.txt"}
         if dom:
             roof["kernel"] = dom[0]
             roof["kernel_ms"] = dom[1][0] / steps
