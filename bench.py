@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Benchmark: the Weld IR programs of BASELINE.json on N B200s (one process per GPU).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--n ROWS]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--rows ROWS]
     python bench.py --impl reference ...      # the reference's CPU engine arm
 
 A "step" is one evaluate() of a workload's IR program (BASELINE.json
@@ -459,7 +459,8 @@ def _relaunch(args):
     ranks (one process per GPU) and pass rank 0's JSON line through."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
            "--master-addr=127.0.0.1", f"--master-port={29500 + os.getpid() % 1000}", os.path.abspath(__file__)]
-    cmd += [a for a in sys.argv[1:]]
+    # (torchrun's parser would read "--n" as an abbreviation of its own options)
+    cmd += ["--rows" + a[3:] if a == "--n" or a.startswith("--n=") else a for a in sys.argv[1:]]
     rc = subprocess.call(cmd)
     sys.exit(rc)
 
@@ -470,7 +471,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="blackscholes")
-    ap.add_argument("--n", type=int, default=0, help="global rows (default: the config's size)")
+    ap.add_argument("--rows", "--n", dest="n", type=int, default=0, help="global rows (default: the config's size)")
     ap.add_argument("--impl", default="weldgpu")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
