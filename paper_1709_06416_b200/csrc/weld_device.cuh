@@ -292,6 +292,7 @@ __device__ __forceinline__ void wg_st_volatile(u64* p, u64 v) {
 #ifndef WG_LB_SLEEP
 #define WG_LB_SLEEP 0
 #endif
+__device__ __forceinline__ i64 wg_lookback_core(u64* status, i64 tile, i64 aggregate);
 __device__ __forceinline__ i64 wg_lookback(u64* status, i64 tile, i64 aggregate) {
   const int lane = threadIdx.x & 31;
   if (tile == 0) {
@@ -299,6 +300,12 @@ __device__ __forceinline__ i64 wg_lookback(u64* status, i64 tile, i64 aggregate)
     return 0;
   }
   if (lane == 0) wg_st_volatile(status + tile, WG_ST_AGG | (u64)aggregate);
+  return wg_lookback_core(status, tile, aggregate);
+}
+// The look-back proper (tile > 0, its aggregate already published): each
+// lane reads WG_LB_PER consecutive predecessors per round trip.
+__device__ __forceinline__ i64 wg_lookback_core(u64* status, i64 tile, i64 aggregate) {
+  const int lane = threadIdx.x & 31;
   i64 excl = 0;
   i64 t = tile - 1;
   while (true) {
@@ -381,32 +388,8 @@ __device__ __forceinline__ void wg_publish_aggregate(u64* status, i64 tile, i64 
 // The look-back of wg_lookback for a tile whose aggregate is already
 // published (whole warp; returns the exclusive prefix).
 __device__ __forceinline__ i64 wg_lookback_resolve(u64* status, i64 tile, i64 aggregate) {
-  const int lane = threadIdx.x & 31;
   if (tile == 0) return 0;
-  i64 excl = 0;
-  i64 t = tile - 1;
-  while (true) {
-    const i64 idx = t - lane;
-    const u64 s = (idx >= 0) ? wg_ld_volatile(status + idx) : WG_ST_PRE;
-    const unsigned mp = __ballot_sync(0xffffffffu, (s >> 62) == 2);
-    const int first = mp ? __ffs(mp) - 1 : 32;
-    const unsigned mx = __ballot_sync(0xffffffffu, (s >> 62) == 0);
-    const unsigned upto = (first >= 31) ? 0xffffffffu : ((2u << first) - 1u);
-    if (mx & upto) {
-#if WG_LB_SLEEP > 0
-      __nanosleep(WG_LB_SLEEP);
-#endif
-      continue;
-    }
-    i64 val = (lane <= first) ? (i64)(s & WG_ST_MASK) : 0;
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) val += __shfl_xor_sync(0xffffffffu, val, d);
-    excl += val;
-    if (mp) break;
-    t -= 32;
-  }
-  if (lane == 0) wg_st_volatile(status + tile, WG_ST_PRE | (u64)(excl + aggregate));
-  return excl;
+  return wg_lookback_core(status, tile, aggregate);
 }
 
 // ---------------------------------------------------------------------------
