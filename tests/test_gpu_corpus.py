@@ -126,3 +126,51 @@ def test_corpus_second_seed_parity(front, level):
                 failures.append(f"{p['name']}: {first_diff(got, want, F64_TOL)}")
             checked += 1
     assert not failures, f"{len(failures)} failures ({checked} ok):\n" + "\n".join(failures[:40])
+
+
+def _load_gz(name):
+    import gzip
+    import json
+    import os
+    with gzip.open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", name), "rt") as f:
+        return json.load(f)
+
+
+CORPUS3 = _load_gz("corpus_s3.json.gz")["programs"]
+
+
+@pytest.mark.parametrize("level", LEVELS)
+def test_corpus_long_inputs_parity(front, level):
+    """The generator with vectors of 2049-2600 elements (tests/golden/
+    make_corpus3.py, seed 20261018): every loop spans several 2048-row tiles
+    of the device schedules -- look-back chains across tiles, the
+    warp-specialised scan's buffer hand-offs, partial last tiles, dictionaries
+    and groups built from thousands of rows -- at every optimizer level."""
+    from weldmill.engine import Value
+    from weldmill.optim import optimize
+    import paper_1709_06416_b200 as wg
+
+    failures = []
+    checked = 0
+    for p in CORPUS3:
+        typed, env = front(p["source"], p["inputs"])
+        tree = optimize(typed, _level(level))[0]
+        for case in p["cases"]:
+            vals = {k: Value(env[k], v) for k, v in case["inputs"].items()}
+            try:
+                got = norm(wg.evaluate(tree, vals)[0].data)
+            except Exception as exc:
+                if "error" in case and type(exc).__name__ == case["error"]:
+                    checked += 1
+                    continue
+                failures.append(f"{p['name']}: {type(exc).__name__}: {str(exc)[:200]}")
+                continue
+            if "error" in case:
+                failures.append(f"{p['name']}: expected {case['error']}, got a value")
+                continue
+            want = case["expected"]
+            ok = approx_equal(got, want, F64_TOL) if p["is_float"] else got == want
+            if not ok:
+                failures.append(f"{p['name']}: {first_diff(got, want, F64_TOL)}")
+            checked += 1
+    assert not failures, f"{len(failures)} failures ({checked} ok):\n" + "\n".join(failures[:40])
