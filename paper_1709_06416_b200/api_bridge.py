@@ -26,6 +26,7 @@ length, no decode to lists) under ``column_encoder``.
 from __future__ import annotations
 
 import struct as _struct
+import threading
 
 import numpy as np
 
@@ -164,9 +165,18 @@ class _Bound:
 
 
 _orig = {}
+# build_program calls swap the encoders of shared leaf nodes for their
+# duration: one at a time, so a concurrent call never saves another call's
+# stand-in as a leaf's encoder
+_BUILD_LOCK = threading.Lock()
 
 
 def _build_program(root):
+    with _BUILD_LOCK:
+        return _build_program_locked(root)
+
+
+def _build_program_locked(root):
     order, _ = _dag_order(root)
     swapped = []
     try:
