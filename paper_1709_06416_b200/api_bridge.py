@@ -172,7 +172,10 @@ _BUILD_LOCK = threading.Lock()
 
 
 def _build_program(root):
-    with _BUILD_LOCK:
+    from .executor import _EVAL_LOCK
+    # binding leaves copies to the device: under the executor's lock too, so
+    # the copies never interleave with another thread's evaluation
+    with _EVAL_LOCK, _BUILD_LOCK:
         return _build_program_locked(root)
 
 
