@@ -54,6 +54,8 @@ int wg_host_unregister(void* p);
  *      run.py:411-425, 693-710; builders.py:413-417) ------------------------ */
 int wg_error_ptr(uint64_t* p);
 int wg_read_error(int64_t* code, int64_t* info);
+/* the error word captured by the last wg_dict_finish_small (same sync as its count), then cleared */
+int wg_last_sync_error(int64_t* code, int64_t* info);
 /* device -> host copy plus the error-word check, one stream synchronisation */
 int wg_d2h_checked(void* dst, uint64_t src, uint64_t bytes, int64_t* code, int64_t* info);
 

@@ -467,8 +467,8 @@ def _finish_small(d: DictDev, dict_ty):
     if nkl > 6 or nvl > 16 or (d.hint_key is not None and _SIZE_HINTS.get(d.hint_key, 0) > SMALL_DICT):
         return None
     n = SMALL_DICT
-    kcols = [Col.alloc(k, max(n, 1)) for k in d.kks]
-    vcols = [Col.alloc(k, max(n, 1)) for k in d.vks]
+    cols = Col.alloc_many(list(d.kks) + list(d.vks), n)
+    kcols, vcols = cols[:nkl], cols[nkl:]
     desc = []
     for (wi, sh, width), k in zip(d.lay, d.kks):
         desc += [wi, sh, width, KIND_CODE[k]]
@@ -479,6 +479,8 @@ def _finish_small(d: DictDev, dict_ty):
     mode = 1 if d.nw == 1 else 2
     rt.call("wg_dict_finish_small", d.table.ptr, d.cap, d.slot_words, mode, d.nw, nkl, kd, nvl, vk, outs,
             d.counters.ptr, ctypes.byref(cnt))
+    # the error word came back with the count (same sync); the caller raises it
+    d.sync_err = rt.last_sync_error()
     n = cnt.value
     if n > SMALL_DICT:          # too many entries, or spilled merges to replay first
         return None

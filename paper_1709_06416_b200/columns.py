@@ -35,6 +35,17 @@ class Col:
         buf = rt.alloc(max(n, 1) * SIZE[kind])
         return cls(buf.ptr, kind, buf)
 
+    @classmethod
+    def alloc_many(cls, kinds, n):
+        """Columns of n elements for each kind, carved from ONE device
+        buffer (256-byte aligned): one allocator call instead of len(kinds)."""
+        offs, total = [], 0
+        for k in kinds:
+            offs.append(total)
+            total += (max(n, 1) * SIZE[k] + 255) // 256 * 256
+        buf = rt.alloc(max(total, 1))
+        return [cls(buf.ptr + o, k, buf) for o, k in zip(offs, kinds)]
+
     def offset(self, k):
         """A view starting k elements in."""
         return Col(self.ptr + k * SIZE[self.kind], self.kind, self.owner)

@@ -38,6 +38,7 @@ cudaStream_t g_streams[3] = {nullptr, nullptr, nullptr};  // 0 compute, 1 host->
 int g_sm_count = 0;
 int64_t* g_err_word = nullptr;      // device {code, info}
 int64_t* g_err_host = nullptr;      // pinned mirror
+int64_t g_sync_err[2] = {0, 0};     // error word captured by wg_dict_finish_small's sync
 uint64_t g_live = 0, g_peak = 0;    // device bytes handed out by wg_alloc
 std::mutex g_acct_mu;
 std::unordered_map<void*, uint64_t> g_sizes;       // live blocks -> rounded size
@@ -1204,10 +1205,23 @@ int wg_dict_finish_small(uint64_t table, uint64_t nslots, int slot_words, int mo
   { WG_PROF("k_dict_finish_small"); k_dict_finish_small<<<1, 1024, smem, g_stream>>>((const uint64_t*)(uintptr_t)table, nslots, d,
                                                    (const unsigned long long*)(uintptr_t)counters, d_cnt); }
   CK(cudaGetLastError());
-  unsigned long long h = 0;
-  CK(cudaMemcpyAsync(&h, d_cnt, 8, cudaMemcpyDeviceToHost, g_stream));
+  // the entry count and the error word (its neighbour) in one copy and one
+  // synchronisation; the error word is kept for wg_last_sync_error
+  CK(cudaMemcpyAsync(g_err_host + 4, g_err_word, 24, cudaMemcpyDeviceToHost, g_stream));
   CK(cudaStreamSynchronize(g_stream));
-  *count_out = h;
+  *count_out = (uint64_t)g_err_host[6];
+  g_sync_err[0] = g_err_host[4];
+  g_sync_err[1] = g_err_host[5];
+  if (g_sync_err[0] != 0) CK(cudaMemsetAsync(g_err_word, 0, 16, g_stream));
+  return 0;
+}
+
+// The error word as read by the last synchronising call that captures it
+// (wg_dict_finish_small), then forgotten: the host needs no second copy.
+int wg_last_sync_error(int64_t* code, int64_t* info) {
+  *code = g_sync_err[0];
+  *info = g_sync_err[1];
+  g_sync_err[0] = g_sync_err[1] = 0;
   return 0;
 }
 

@@ -558,9 +558,13 @@ class Ctx:
             if b.table is None:
                 b.ensure(1)
             d = _finish_small(b, Dict(kind.key, kind.value))
+            self._raise_sync_err(b)
             if d is None:
                 self._settle(b)
                 d = finish_dict(b, Dict(kind.key, kind.value))
+                self._raise_sync_err(b)
+            else:
+                self.dirty = False        # the finish synchronised after every launch and read the error word
             _first_zero_sign(b, d)
             self.materialized(d, 16 + d.n * (16 + _slot_bytes(kind.key) + _slot_bytes(kind.value)))
             return d
@@ -570,6 +574,13 @@ class Ctx:
             self.materialized(g, 16 + g.n * (16 + _slot_bytes(kind.key) + 16) + g.vals.n * _slot_bytes(kind.value))
             return g
         raise EvalError(f"unknown builder kind {kind!r}")
+
+    def _raise_sync_err(self, b):
+        code, info = getattr(b, "sync_err", (0, 0))
+        b.sync_err = (0, 0)
+        if code:
+            self.dirty = False
+            raise device_error(code, info)
 
     def ev_ToVec(self, e, env):
         d = self.ev(e.mapping, env)

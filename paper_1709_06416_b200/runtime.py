@@ -46,6 +46,7 @@ _SIGS = {
     "wg_host_unregister": (c_int, [c_void_p]),
     "wg_error_ptr": (c_int, [ctypes.POINTER(u64)]),
     "wg_read_error": (c_int, [ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+    "wg_last_sync_error": (c_int, [ctypes.POINTER(i64), ctypes.POINTER(i64)]),
     "wg_d2h_checked": (c_int, [c_void_p, u64, u64, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
     "wg_compile": (c_int, [c_char_p, c_char_p, c_int, ctypes.POINTER(c_char_p), ctypes.POINTER(c_char_p), c_int,
                            ctypes.POINTER(c_char_p), ctypes.POINTER(u64), c_char_p, u64]),
@@ -292,6 +293,13 @@ def clear_error():
 def read_error():
     c, i = i64(0), i64(0)
     _check(lib().wg_read_error(ctypes.byref(c), ctypes.byref(i)))
+    return c.value, i.value
+
+
+def last_sync_error():
+    """Error word captured by the last wg_dict_finish_small (no device sync)."""
+    c, i = i64(0), i64(0)
+    _check(lib().wg_last_sync_error(ctypes.byref(c), ctypes.byref(i)))
     return c.value, i.value
 
 

@@ -76,6 +76,16 @@ class TestRuntimeErrors:
             run("result(for(v, merger[i64, +], (b, i, x) => merge(b, 10 / x)))",
                 types=_types(v=VI64), values={"v": [3, 2, 0, 1]})
 
+    def test_divide_by_zero_in_dictmerger_loop(self):
+        """The error word comes back with the small-dictionary finish's count
+        (one sync): the error is raised, and the next evaluation is clean."""
+        from weldmill.errors import DivideByZero
+        src = "tovec(result(for(v, dictmerger[i64, i64, +], (b, i, x) => merge(b, {x % 3, 10 / x}))))"
+        with pytest.raises(DivideByZero):
+            run(src, types=_types(v=VI64), values={"v": [3, 2, 0, 1] * 50})
+        got = run(src, types=_types(v=VI64), values={"v": [3, 2, 5, 1] * 50})[0].data
+        assert got == [(0, 150), (1, 500), (2, 350)]
+
     def test_lookup_out_of_bounds(self):
         from weldmill.errors import IndexOutOfBounds
         with pytest.raises(IndexOutOfBounds):
