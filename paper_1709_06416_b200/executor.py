@@ -12,6 +12,7 @@ the device path does not lower raises ``DeviceUnsupported`` (an EvalError).
 """
 from __future__ import annotations
 
+import ctypes
 import math
 import struct as _struct
 import threading
@@ -36,7 +37,7 @@ from .builders_dev import (_finish_small, AppenderDev, DDict, DGroups, DictDev, 
                            Segment, dict_payload, finish_dict, finish_groups, gather_cols, sort_perm, tovec)
 from .codegen import DEFER_DICT, PIPE_STAGES, BSpec, IterSpec, generate
 from .columns import Col, DVec, to_device, to_payload, dvec_from_cols
-from .irtypes import (BOOL, F32, F64, I64, SIZE, identity_value, Builder, DeviceUnsupported as _DU, Dict, DictMerger, Function,
+from .irtypes import (BOOL, F32, F64, I32, I64, SIZE, identity_value, Builder, DeviceUnsupported as _DU, Dict, DictMerger, Function,
                       GroupBuilder, Merger, NPTYPE, Scalar, Simd, Struct, Vec, VecBuilder, VecMerger, is_flat, leaves,
                       to_bits)
 
@@ -559,6 +560,7 @@ class Ctx:
                 b.ensure(1)
             d = _finish_small(b, Dict(kind.key, kind.value))
             self._raise_sync_err(b)
+            b.small = d is not None
             if d is None:
                 self._settle(b)
                 d = finish_dict(b, Dict(kind.key, kind.value))
@@ -959,6 +961,12 @@ class Ctx:
             for b in plan.builders:
                 st = bmap[b.bid]
                 if isinstance(st, MergerDev):
+                    continue
+                if (isinstance(st, DictDev) and not b.extra.get("part") and len(plan.builders) == 1
+                        and all(k in (BOOL, I32, I64) for k in st.kks)):
+                    # replayed with its table re-initialised (the buffers
+                    # the blob points at stay owned by the replay)
+                    outs[id(st)] = "dict"
                     continue
                 if (isinstance(st, AppenderDev) and isinstance(b.kind, VecBuilder) and b.mode == "direct"
                         and not b.extra.get("nested") and len(st.segments) == 1):
@@ -1546,13 +1554,17 @@ def _evaluate(e, env=None, config=None, externs=None, *, result="python", idx0=0
     if e.ty is None:
         raise EvalError("expression must be type-checked before evaluation")
     rkey = None
-    if (REPLAY and not cfg.count_evals and env and result in ("python", "device") and type(e) is Result
-            and type(e.builder) is For and _ctx_out is None and idx0 == 0):
+    if (REPLAY and not cfg.count_evals and env and result in ("python", "device") and _ctx_out is None and idx0 == 0
+            and ((type(e) is Result and type(e.builder) is For)
+                 or (type(e) is ToVec and type(e.mapping) is Result and type(e.mapping.builder) is For))):
         rkey = _replay_key(e, env, externs, result)
         if rkey is not None:
             hit = _REPLAYS.get(rkey)
             if hit is not None and hit.valid(e, env, cfg, externs):
-                return hit.run(e)
+                out = hit.run(e)
+                if out is not None:
+                    return out
+                _REPLAYS.d.pop(rkey, None)       # the replayed dictionary outgrew its recorded finish
     note_evaluation()
     ctx = Ctx(cfg, externs, idx0=idx0)
     if _ctx_out is not None:
@@ -1617,6 +1629,9 @@ def _evaluate(e, env=None, config=None, externs=None, *, result="python", idx0=0
         if lb is not None:
             _collect_builders(lb, bl)
         outs = ctx.rec[0][5]
+        dicts = [b for b in bl if isinstance(b, DictDev)]
+        if dicts and not (len(bl) == 1 and type(e) is ToVec and getattr(dicts[0], "small", False)):
+            bl = []            # dictionaries replay as the one builder of a tovec(result(...)) with a small result
         if bl and all(isinstance(b, MergerDev) or id(b) in outs for b in bl):
             _REPLAYS.put(rkey, _Replay(e, env, cfg, externs, ctx, bl, stats, result))
             if any(isinstance(b, MergerDev) and not b.mirrored for b in bl):
@@ -1685,8 +1700,8 @@ class _Replay:
         self.launch = (kern, grid, nthr, blob, smem)
         # per builder, in result order: the merger, or (elem type, leaf kinds,
         # rows, blob word index of each leaf column)
-        self.builders = [b if isinstance(b, MergerDev) else (b.kind.elem, list(b.kinds), outs[id(b)][1], outs[id(b)][0])
-                         for b in builders]
+        self.builders = [b if isinstance(b, (MergerDev, DictDev)) else
+                         (b.kind.elem, list(b.kinds), outs[id(b)][1], outs[id(b)][0]) for b in builders]
         self.mergers = [b for b in builders if isinstance(b, MergerDev)]
         self.stats = stats
         res = ctx._keep[1] if ctx._keep else None
@@ -1707,6 +1722,8 @@ class _Replay:
         return len(ext) == len(self.externs) and all(self.externs.get(k) is f for k, f in ext.items())
 
     def run(self, e):
+        if isinstance(self.builders[0], DictDev):
+            return self._run_dict(e)
         note_evaluation()
         kern, grid, block, blob, smem = self.launch
         vals = []
@@ -1751,6 +1768,39 @@ class _Replay:
         st.__dict__.update(self.stats.__dict__)
         st.node_evals = {}
         return Value(e.ty, payload), st
+
+
+def _replay_run_dict(self, e):
+    """tovec(result(for(..., dictmerger, ...))) with a small result: the
+    table and counters the recorded blob points at are re-initialised, the
+    loop kernel relaunched, and the one-launch finish writes fresh result
+    columns.  None when the result no longer fits the small finish (the
+    caller then evaluates normally)."""
+    b = self.builders[0]
+    kern, grid, block, blob, smem = self.launch
+    kind = b.kind
+    with self.lock:
+        note_evaluation()
+        pat = (ctypes.c_uint64 * b.slot_words)(*b.pattern())
+        rt.call("wg_table_init", b.table.ptr, b.cap + 1, b.slot_words, pat)
+        rt.memset(b.counters.ptr, 0, 16)
+        kern.launch(grid, block, blob, smem)
+        d = _finish_small(b, Dict(kind.key, kind.value))
+        code, info = getattr(b, "sync_err", (0, 0))
+        b.sync_err = (0, 0)
+        if code:
+            raise device_error(code, info)
+        if d is None:
+            return None
+    out = tovec(d, e.ty.elem)
+    payload = out if self.result == "device" else to_host_payload(out, e.ty)
+    st = EvalStats.__new__(EvalStats)
+    st.__dict__.update(self.stats.__dict__)
+    st.node_evals = {}
+    return Value(e.ty, payload), st
+
+
+_Replay._run_dict = _replay_run_dict
 
 
 def _first_zero_sign(b, d):

@@ -444,3 +444,30 @@ def test_replayed_appender_evaluations_get_fresh_results():
     assert len(ptrs) == 8           # fresh columns every call
     py, _ = wg.evaluate(tree, env, EngineConfig())
     assert py.data[1][:3] == [0, 4, 8]
+
+
+def test_replayed_dictmerger_evaluations():
+    """Launch replay of tovec(result(for(..., dictmerger, ...))) with a small
+    result (the C3 shape): the table is re-initialised each call and the
+    results equal the reference's."""
+    import numpy as np
+    import paper_1709_06416_b200 as wg
+    from paper_1709_06416_b200 import executor
+    from paper_1709_06416_b200.columns import to_device
+    from weldmill.engine import EngineConfig, Value, evaluate as ref_evaluate
+    from weldmill.parser import parse_type_text
+    T = parse_type_text
+    tree = _front("tovec(result(for({a, b}, dictmerger[{i32, i64}, {i64, f64}, +], (d, i, x) => "
+                  "merge(d, {{x.0 % 7, x.1 % 3}, {x.1, 0.5 * f64(x.0)}}))))".replace("f64(x.0)", "cast(x.0, f64)"),
+                  _types(a="vec[i32]", b="vec[i64]"))
+    a = (np.arange(300_001) % 1000).astype(np.int32)
+    b = np.arange(300_001, dtype=np.int64)
+    env = {"a": Value(T("vec[i32]"), to_device(T("vec[i32]"), a)), "b": Value(T("vec[i64]"), to_device(T("vec[i64]"), b))}
+    want = ref_evaluate(tree, {"a": Value(T("vec[i32]"), a.tolist()), "b": Value(T("vec[i64]"), b.tolist())})[0].data
+    executor._REPLAYS.d.clear()
+    for _ in range(4):
+        got = wg.evaluate(tree, env, EngineConfig())[0].data
+        assert [k for k, _ in got] == [k for k, _ in want]
+        for (_, gv), (_, wv) in zip(got, want):
+            assert gv[0] == wv[0] and abs(gv[1] - wv[1]) <= 1e-9 * max(1.0, abs(wv[1]))
+    assert len(executor._REPLAYS.d) == 1
