@@ -326,7 +326,12 @@ def device_comm(group=None):
     if not dist.is_initialized():
         return SoloComm()
     if dist.get_backend(group) == "nccl" and torch.cuda.device_count() >= dist.get_world_size(group):
-        return NcclComm(group)
+        try:
+            return NcclComm(group)
+        except Exception as exc:            # e.g. libnccl.so.2 missing: same results, host-staged
+            import sys
+            print(f"paper_1709_06416_b200: NCCL combine unavailable ({exc}); using the host-staged combine",
+                  file=sys.stderr)
     return StagedComm(group)
 
 
