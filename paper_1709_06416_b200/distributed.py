@@ -332,6 +332,7 @@ def device_comm(group=None):
             import sys
             print(f"paper_1709_06416_b200: NCCL combine unavailable ({exc}); using the host-staged combine",
                   file=sys.stderr)
+            return StagedComm(dist.new_group(backend="gloo"))   # host tensors need a gloo group
     return StagedComm(group)
 
 
