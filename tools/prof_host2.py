@@ -26,4 +26,4 @@ pr.enable()
 for _ in range(N):
     wg.evaluate(tree, env, cfg, ext, result="device")
 pr.disable()
-pstats.Stats(pr).sort_stats("tottime").print_stats(25)
+pstats.Stats(pr).sort_stats(sys.argv[3] if len(sys.argv) > 3 else "tottime").print_stats(40)
