@@ -1992,8 +1992,9 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
                 src.append(f"  {{ int h_ = m{b.bid}_h; wg_block_fold<{ct}, {OPSTRUCT[b.kind.op]}<{ct}>>(m{b.bid}_{f}, h_, {ident}, ({ct}*)s_red, s_redh);")
                 src.append(f"    if (threadIdx.x == 0) {{ p.m{b.bid}_part[(u64)blockIdx.x * {F + 1} + {f}] = wg_to_bits<{ct}>(m{b.bid}_{f});"
                            f" if ({f} == 0) p.m{b.bid}_part[(u64)blockIdx.x * {F + 1} + {F}] = (u64)h_; }} }}")
-        src.append("  __threadfence();")
-        src.append("  if (threadIdx.x == 0) s_last = (atomicAdd(p.ticket, 1u) == gridDim.x - 1);")
+        # only thread 0 wrote this CTA's partials: it alone fences them
+        # before taking the ticket (a CTA-wide fence stalled every warp)
+        src.append("  if (threadIdx.x == 0) { __threadfence(); s_last = (atomicAdd(p.ticket, 1u) == gridDim.x - 1); }")
         src.append("  __syncthreads();")
         src.append("  if (s_last) {")
         src.append("    __threadfence();")
