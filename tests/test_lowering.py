@@ -225,3 +225,30 @@ def test_extern_error_text_matches_the_reference_form():
     assert codegen.extern_error_text(2 * i) == "extern 'log' failed: math domain error"
     i = codegen.EXTERN_IDS["exp"]
     assert codegen.extern_error_text(2 * i + 1) == "extern 'exp' failed: math range error"
+
+
+@pytest.mark.parametrize("src,types,want_ws", [
+    ("filter(v, (x) => x > 0)", {"v": "vec[i64]"}, True),
+    ("result(for({a, b}, {vecbuilder[{f64, i64}], vecbuilder[i32]}, (bs, i, x) => "
+     "{if (x.0 > 0.5, merge(bs.0, {x.0, i}), bs.0), if (x.1 % 7 == 3, merge(bs.1, x.1), bs.1)}))",
+     {"a": "vec[f64]", "b": "vec[i32]"}, True),
+    # an appender next to a merger: the non-specialised scan schedule
+    ("result(for(v, {vecbuilder[i64], merger[i64, +]}, (bs, i, x) => "
+     "{if (x > 0, merge(bs.0, x), bs.0), merge(bs.1, x)}))", {"v": "vec[i64]"}, False),
+    # data-dependent fan-out (flatmap): unbounded appends stay on the count pre-pass path
+    ("result(for(v, vecbuilder[i64], (b, i, x) => for(rng, b, (c, j, y) => if (y < x, merge(c, x * 10 + y), c))))",
+     {"v": "vec[i64]", "rng": "vec[i64]"}, False),
+])
+def test_warp_specialised_scan_selection(src, types, want_ws):
+    """The warp-specialised scan schedule (SCAN_WS) is chosen
+    exactly for loops whose builders are all bounded order-preserving
+    appenders; its kernels carry the store warp and compile for sm_100a."""
+    from paper_1709_06416_b200 import codegen, runtime
+    plans = codegen.static_plans(_tree(src, types, "none"))
+    scans = [pl for pl in plans if pl.schedule == "scan"]
+    assert scans
+    ws = [pl for pl in scans if pl.threads == pl.block + 32]
+    assert bool(ws) == want_ws
+    for pl in ws:
+        assert "wg_lookback_resolve" in pl.source and "wg_mbar_wait(&wg_full" in pl.source
+        runtime.compile_check(pl.source)
