@@ -797,7 +797,7 @@ int wg_init(int device) {
   CK(cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, device));
   cudaMemPool_t pool;
   CK(cudaDeviceGetDefaultMemPool(&pool, device));
-  uint64_t thr = UINT64_MAX;  // temporaries (CUB scratch) use the stream-ordered pool
+  uint64_t thr = UINT64_MAX;  // temporaries (sort scratch) use the stream-ordered pool
   CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
   CK(cudaMalloc((void**)&g_err_word, 64));
   CK(cudaMemset(g_err_word, 0, 64));
