@@ -79,7 +79,8 @@ PIPE_STAGES = int(_os.environ.get("WELDGPU_PIPE_STAGES", "4"))
 # stores the tile; WS_NBUF staging buffers decouple the two
 SCAN_WS = _os.environ.get("WELDGPU_SCAN_WS", "1") == "1"
 WS_NBUF = int(_os.environ.get("WELDGPU_WS_NBUF", "2"))
-WS_MINB = int(_os.environ.get("WELDGPU_WS_MINB", "4"))
+WS_MINB = int(_os.environ.get("WELDGPU_WS_MINB", "3"))
+WS_BLOCK = int(_os.environ.get("WELDGPU_WS_BLOCK", "384"))     # compute threads (+ the store warp)
 WS_ITEMS = int(_os.environ.get("WELDGPU_WS_ITEMS", "8"))
 PIPE_NOGUARD = _os.environ.get("WELDGPU_PIPE_NOGUARD", "1") == "1"
 PIPE_MAX_STAGES = 8
@@ -1359,6 +1360,8 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
     if ws and not (items or ITEMS_OVERRIDE):
         ITEMS = min(ITEMS, WS_ITEMS)
         g.items = ITEMS
+    if ws and "WELDGPU_BLOCK" not in _os.environ:
+        BLOCK = WS_BLOCK
     ws_need = sum(BLOCK * ITEMS * b.k * SIZE[k] for b in scan_bs for k in b.extra["kinds"]) if ws else 0
     if ws and WS_NBUF * ws_need > 160 * 1024:
         ws = False
