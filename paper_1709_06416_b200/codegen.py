@@ -79,6 +79,9 @@ PIPE_STAGES = int(_os.environ.get("WELDGPU_PIPE_STAGES", "4"))
 # stores the tile; WS_NBUF staging buffers decouple the two
 SCAN_WS = _os.environ.get("WELDGPU_SCAN_WS", "1") == "1"
 WS_NBUF = int(_os.environ.get("WELDGPU_WS_NBUF", "2"))
+# 256-bit (sm_100) per-thread column loads / stores in wg_load_contig / wg_store_contig
+LD256 = int(_os.environ.get("WELDGPU_LD256", "1"))
+ST256 = int(_os.environ.get("WELDGPU_ST256", "1"))
 WS_MINB = int(_os.environ.get("WELDGPU_WS_MINB", "3"))
 WS_BLOCK = int(_os.environ.get("WELDGPU_WS_BLOCK", "384"))     # compute threads (+ the store warp)
 WS_ITEMS = int(_os.environ.get("WELDGPU_WS_ITEMS", "8"))
@@ -1566,6 +1569,8 @@ def generate(loop: For, iters, bstruct, captures, externs, strategy, name="wg_lo
 
     # ---- assemble ----------------------------------------------------------
     src = []
+    src.append(f"#define WG_LD256 {LD256}")
+    src.append(f"#define WG_ST256 {ST256}")
     src.append(f"#define WG_LB_PER {LB_PER}")
     src.append(f"#define WG_LB_SLEEP {LB_SLEEP}")
     src.append('#include "weld_device.cuh"')

@@ -603,13 +603,42 @@ __device__ __forceinline__ u64 wg_key_f32(float v) {
 }
 
 // ---------------------------------------------------------------------------
-// Contiguous per-thread column access (ITEMS consecutive elements): 16-byte
+#ifndef WG_LD256
+#define WG_LD256 1
+#endif
+#ifndef WG_ST256
+#define WG_ST256 1
+#endif
+// 256-bit vector ld/st need PTX 8.8 (CUDA 12.9); an older NVRTC (e.g. torch's
+// bundled 12.8, when torch loaded its libnvrtc first) gets the 16-byte path.
+#if !defined(__CUDACC_VER_MAJOR__) || __CUDACC_VER_MAJOR__ < 12 || (__CUDACC_VER_MAJOR__ == 12 && __CUDACC_VER_MINOR__ < 9)
+#undef WG_LD256
+#define WG_LD256 0
+#undef WG_ST256
+#define WG_ST256 0
+#endif
+// Contiguous per-thread column access (ITEMS consecutive elements): 32-byte
+// (sm_100 LDG.256 / STG.256) or 16-byte
 // vector loads/stores when the address allows, streaming cache hints so the
 // single-use column traffic does not evict hash tables or bins from L2.
 template <typename T, int N>
 __device__ __forceinline__ void wg_load_contig(const T* __restrict__ src, T (&dst)[N]) {
   constexpr int B = N * (int)sizeof(T);
   const unsigned long long a = (unsigned long long)src;
+#if WG_LD256
+  // sm_100 256-bit loads: each lane reads whole 32-byte sectors
+  if constexpr (B % 32 == 0) {
+    if ((a & 31) == 0) {
+#pragma unroll
+      for (int c = 0; c < B / 32; ++c) {
+        unsigned long long* d = reinterpret_cast<unsigned long long*>(&dst[0]) + 4 * c;
+        asm volatile("ld.global.cs.v4.u64 {%0,%1,%2,%3}, [%4];"
+                     : "=l"(d[0]), "=l"(d[1]), "=l"(d[2]), "=l"(d[3]) : "l"(src + c * (32 / (int)sizeof(T))));
+      }
+      return;
+    }
+  }
+#endif
   if constexpr (B % 16 == 0) {
     if ((a & 15) == 0) {
 #pragma unroll
@@ -639,6 +668,19 @@ template <typename T, int N>
 __device__ __forceinline__ void wg_store_contig(T* __restrict__ dst, const T (&src)[N]) {
   constexpr int B = N * (int)sizeof(T);
   const unsigned long long a = (unsigned long long)dst;
+#if WG_ST256
+  if constexpr (B % 32 == 0) {
+    if ((a & 31) == 0) {
+#pragma unroll
+      for (int c = 0; c < B / 32; ++c) {
+        const unsigned long long* d = reinterpret_cast<const unsigned long long*>(&src[0]) + 4 * c;
+        asm volatile("st.global.cs.v4.u64 [%0], {%1,%2,%3,%4};"
+                     :: "l"(dst + c * (32 / (int)sizeof(T))), "l"(d[0]), "l"(d[1]), "l"(d[2]), "l"(d[3]) : "memory");
+      }
+      return;
+    }
+  }
+#endif
   if constexpr (B % 16 == 0) {
     if ((a & 15) == 0) {
 #pragma unroll
