@@ -478,7 +478,27 @@ __global__ void k_flush(uint4* buf, uint64_t n16, uint32_t salt) {
 // stable insertion sort (most buckets hold a single distinct key).
 __global__ void k_disorder(const uint64_t* k, uint64_t n, int shift, uint32_t* pos, unsigned long long* npos,
                            uint64_t cap) {
-  for (uint64_t i = 1 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, stride = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t i0 = 1;
+  if ((((uintptr_t)k) & 31) == 0) {
+    // rows 4q..4q+3 against their predecessors: one 256-bit load + the row before
+    const uint64_t n4 = n / 4;
+    for (uint64_t q = tid; q < n4; q += stride) {
+      uint64_t c[5];
+      asm volatile("ld.global.cs.v4.u64 {%0,%1,%2,%3}, [%4];"
+                   : "=l"(c[1]), "=l"(c[2]), "=l"(c[3]), "=l"(c[4]) : "l"(k + 4 * q));
+      c[0] = q ? k[4 * q - 1] : c[1];
+#pragma unroll
+      for (int j = 1; j <= 4; ++j) {
+        if ((c[j - 1] >> shift) == (c[j] >> shift) && c[j - 1] > c[j]) {
+          unsigned long long p = atomicAdd(npos, 1ULL);
+          if (p < cap) pos[p] = (uint32_t)(4 * q + j - 1);
+        }
+      }
+    }
+    i0 = n4 * 4 > 1 ? n4 * 4 : 1;
+  }
+  for (uint64_t i = i0 + tid; i < n; i += stride) {
     uint64_t a = k[i - 1], b = k[i];
     if ((a >> shift) == (b >> shift) && a > b) {
       unsigned long long q = atomicAdd(npos, 1ULL);
@@ -663,7 +683,38 @@ __device__ __forceinline__ uint64_t wg_okey_col(const void* src, int kind, uint6
 __global__ void k_okey_minmax(const void* keys, int kind, uint64_t n, unsigned long long* mm, uint64_t* ok,
                               const uint64_t* vals) {
   uint64_t lo = ~0ULL, hi = 0, vlo = ~0ULL, vhi = 0;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+  uint64_t i0 = 0;
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, stride = (uint64_t)gridDim.x * blockDim.x;
+  if (kind == 2 && ((((uintptr_t)keys) | ((uintptr_t)ok) | ((uintptr_t)vals)) & 31) == 0) {
+    // 8-byte keys: four rows per thread with 256-bit loads/stores (sm_100)
+    const uint64_t n4 = n / 4;
+    for (uint64_t q = tid; q < n4; q += stride) {
+      uint64_t k[4];
+      asm volatile("ld.global.cs.v4.u64 {%0,%1,%2,%3}, [%4];"
+                   : "=l"(k[0]), "=l"(k[1]), "=l"(k[2]), "=l"(k[3]) : "l"((const uint64_t*)keys + 4 * q));
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        k[c] ^= 0x8000000000000000ULL;
+        lo = k[c] < lo ? k[c] : lo;
+        hi = k[c] > hi ? k[c] : hi;
+      }
+      asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(ok + 4 * q), "l"(k[0]), "l"(k[1]), "l"(k[2]), "l"(k[3])
+                   : "memory");
+      if (vals) {
+        uint64_t w[4];
+        asm volatile("ld.global.cs.v4.u64 {%0,%1,%2,%3}, [%4];"
+                     : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3]) : "l"(vals + 4 * q));
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint64_t x = w[c] ^ (1ULL << 63);
+          vlo = x < vlo ? x : vlo;
+          vhi = x > vhi ? x : vhi;
+        }
+      }
+    }
+    i0 = n4 * 4;
+  }
+  for (uint64_t i = i0 + tid; i < n; i += stride) {
     const uint64_t v = wg_okey_col(keys, kind, i);
     ok[i] = v;
     lo = v < lo ? v : lo;
