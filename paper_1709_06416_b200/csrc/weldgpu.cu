@@ -680,8 +680,16 @@ __device__ __forceinline__ uint64_t wg_okey_col(const void* src, int kind, uint6
 // Order keys of a key column, their min/max (mm[0..1]) and, when vals is
 // given, the min/max of the 8-byte values' flipped bits v ^ 2^63 (mm[4..5]:
 // the payload-narrowing test of the sort).
+// With `spec`, also the 256-bin counts of the four top bytes of the order key
+// (bits 32..63): the radix histogram of a sort over the top 32 of 64 varying
+// bits, taken in the same read (used when min/max confirm that window).
 __global__ void k_okey_minmax(const void* keys, int kind, uint64_t n, unsigned long long* mm, uint64_t* ok,
-                              const uint64_t* vals) {
+                              const uint64_t* vals, uint32_t* spec) {
+  __shared__ uint32_t sh[4][256];
+  if (spec) {
+    for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
+    __syncthreads();
+  }
   uint64_t lo = ~0ULL, hi = 0, vlo = ~0ULL, vhi = 0;
   uint64_t i0 = 0;
   const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, stride = (uint64_t)gridDim.x * blockDim.x;
@@ -697,6 +705,10 @@ __global__ void k_okey_minmax(const void* keys, int kind, uint64_t n, unsigned l
         k[c] ^= 0x8000000000000000ULL;
         lo = k[c] < lo ? k[c] : lo;
         hi = k[c] > hi ? k[c] : hi;
+        if (spec) {
+#pragma unroll
+          for (int d = 0; d < 4; ++d) atomicAdd(&sh[d][(unsigned)(k[c] >> (32 + 8 * d)) & 255u], 1u);
+        }
       }
       asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(ok + 4 * q), "l"(k[0]), "l"(k[1]), "l"(k[2]), "l"(k[3])
                    : "memory");
@@ -717,6 +729,10 @@ __global__ void k_okey_minmax(const void* keys, int kind, uint64_t n, unsigned l
   for (uint64_t i = i0 + tid; i < n; i += stride) {
     const uint64_t v = wg_okey_col(keys, kind, i);
     ok[i] = v;
+    if (spec) {
+#pragma unroll
+      for (int d = 0; d < 4; ++d) atomicAdd(&sh[d][(unsigned)(v >> (32 + 8 * d)) & 255u], 1u);
+    }
     lo = v < lo ? v : lo;
     hi = v > hi ? v : hi;
     if (vals) {
@@ -738,6 +754,13 @@ __global__ void k_okey_minmax(const void* keys, int kind, uint64_t n, unsigned l
     atomicMin(mm, lo);
     atomicMax(mm + 1, hi);
     if (vals) { atomicMin(mm + 4, vlo); atomicMax(mm + 5, vhi); }
+  }
+  if (spec) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) {
+      const uint32_t c = (&sh[0][0])[i];
+      if (c) atomicAdd(spec + i, c);
+    }
   }
 }
 
@@ -1354,6 +1377,10 @@ int onesweep_pass(const K* ki, const VI* vi, K* ko, VO* vo, uint64_t n, int shif
   return 0;
 }
 
+// Radix histogram of the top 32 of 64 order-key bits taken by k_okey_minmax
+// (wg_group_finish1 sets it around its sort when that is the sort's window).
+static const uint32_t* g_pre_hist = nullptr;
+
 // Histogram + offsets of every pass; *status sized for the tiles of a pass.
 template <typename K>
 int radix_prologue(const K* kin, uint64_t n, int begin_bit, int end_bit, int npass, uint32_t** hist,
@@ -1362,7 +1389,9 @@ int radix_prologue(const K* kin, uint64_t n, int begin_bit, int end_bit, int npa
   CK(cudaMallocAsync((void**)hist, (npass * wgr::RADIX + npass) * 4, g_stream));
   CK(cudaMemsetAsync(*hist, 0, (npass * wgr::RADIX + npass) * 4, g_stream));
   CK(cudaMallocAsync((void**)status, tiles * wgr::RADIX * 8, g_stream));
-  { WG_PROF("k_radix_hist"); wgr::k_radix_hist<K><<<grid_for(n, 256), 256, 0, g_stream>>>(kin, n, begin_bit, end_bit, npass, *hist); }
+  if (g_pre_hist && sizeof(K) == 8 && npass == 4 && begin_bit == 32 && end_bit == 64)
+    CK(cudaMemcpyAsync(*hist, g_pre_hist, 4 * wgr::RADIX * 4, cudaMemcpyDeviceToDevice, g_stream));
+  else { WG_PROF("k_radix_hist"); wgr::k_radix_hist<K><<<grid_for(n, 256), 256, 0, g_stream>>>(kin, n, begin_bit, end_bit, npass, *hist); }
   { WG_PROF("k_radix_offsets"); wgr::k_radix_offsets<<<npass, wgr::RADIX, 0, g_stream>>>(*hist); }
   return 0;
 }
@@ -1534,6 +1563,7 @@ int wg_run_starts(const uint64_t* key_words, int kw, uint64_t n, uint64_t starts
 // inside the (small) buckets; skewed data falls back to a full radix sort.
 static bool g_group_u32 = getenv("WELDGPU_GROUP_U32") == nullptr || getenv("WELDGPU_GROUP_U32")[0] != '0';
 static bool g_group_narrow = getenv("WELDGPU_GROUP_NARROW") == nullptr || getenv("WELDGPU_GROUP_NARROW")[0] != '0';
+static bool g_group_spec_hist = getenv("WELDGPU_GROUP_SPEC_HIST") == nullptr || getenv("WELDGPU_GROUP_SPEC_HIST")[0] != '0';
 
 int wg_group_finish1(uint64_t keys, int key_kind, uint64_t vals, int val_width, uint64_t n, uint64_t ukeys_out,
                      uint64_t offs_out, uint64_t vals_out, uint64_t* K_out) {
@@ -1564,13 +1594,15 @@ int wg_group_finish1(uint64_t keys, int key_kind, uint64_t vals, int val_width, 
   CK(cudaMallocAsync((void**)&vB, n * 8, g_stream));
   // the last radix pass writes the values straight into vals_out when they are 8 bytes wide
   if (own_v0) CK(cudaMallocAsync((void**)&vA, n * 8, g_stream)); else vA = (uint64_t*)(uintptr_t)vals_out;
-  CK(cudaMallocAsync((void**)&mm, 48, g_stream));
+  CK(cudaMallocAsync((void**)&mm, 48 + 4 * 256 * 4, g_stream));
   flag = (int*)(mm + 2);
+  uint32_t* spec = g_group_spec_hist && key_kind == 2 ? (uint32_t*)(mm + 6) : nullptr;
   uint64_t init[6] = {~0ULL, 0ULL, 0ULL, 0ULL, ~0ULL, 0ULL};
   CK(cudaMemcpyAsync(mm, init, 48, cudaMemcpyHostToDevice, g_stream));
+  if (spec) CK(cudaMemsetAsync(spec, 0, 4 * 256 * 4, g_stream));
   const bool try_narrow = !own_v0 && g_group_narrow;
   { WG_PROF("k_okey_minmax"); k_okey_minmax<<<g, 256, 0, g_stream>>>((const void*)(uintptr_t)keys, key_kind, n, mm, k0,
-                                                                   try_narrow ? v0 : nullptr); }
+                                                                   try_narrow ? v0 : nullptr, spec); }
   if (own_v0) { WG_PROF("k_widen"); k_widen<<<g, 256, 0, g_stream>>>((const void*)(uintptr_t)vals, v0, val_width, n); }
   unsigned long long hmm[6];
   CK(cudaMemcpyAsync(hmm, mm, 48, cudaMemcpyDeviceToHost, g_stream));
@@ -1611,10 +1643,14 @@ int wg_group_finish1(uint64_t keys, int key_kind, uint64_t vals, int val_width, 
     { WG_PROF("k_group_out"); k_group_out<uint32_t><<<grid_for(hK + 1, 256), 256, 0, g_stream>>>(
         starts, hK, n, wA, recon, key_kind, (int64_t*)(uintptr_t)offs_out, (void*)(uintptr_t)ukeys_out); }
   } else {
-    if (narrow && vbits - begin_bit > 8) {
-      if (radix_sort_narrow<uint64_t>(k0, v0, kA, kB, vA, (uint32_t*)vB, (uint32_t*)vB + n, n, begin_bit, vbits, vbase))
-        return -1;
-    } else if (radix_sort<uint64_t, uint64_t>(k0, v0, kA, kB, vA, vB, n, begin_bit, vbits)) return -1;
+    g_pre_hist = (spec && kbase == 0) ? spec : nullptr;   // the window is bits 32..63 exactly when vbits == 64
+    int rc_;
+    if (narrow && vbits - begin_bit > 8)
+      rc_ = radix_sort_narrow<uint64_t>(k0, v0, kA, kB, vA, (uint32_t*)vB, (uint32_t*)vB + n, n, begin_bit, vbits, vbase);
+    else
+      rc_ = radix_sort<uint64_t, uint64_t>(k0, v0, kA, kB, vA, vB, n, begin_bit, vbits);
+    g_pre_hist = nullptr;
+    if (rc_) return -1;
     if (begin_bit > 0) {
       uint64_t cap = n / 8 + 1024;
       uint32_t* pos = starts;             // scratch until the run starts are computed
